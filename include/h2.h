@@ -1,0 +1,153 @@
+/*
+ * h2.h — C ABI of the B200-native H^2-matrix hot path (arXiv 1402.5056).
+ *
+ * Citations: P:n = line n of the paper's text, SURVEY §8 = the build's scope table.
+ * All floating point is IEEE double (FP64).  All dense arrays are column-major.
+ *
+ * Index conventions:
+ *   - cluster ids are DFS preorder (root 0, son0 before son1);
+ *   - perm[i] is the ORIGINAL index of tree position i;
+ *   - low-rank factors X, Y passed to h2_lowrank_update are in TREE order restricted to the
+ *     contiguous ranges of t0 / s0;
+ *   - vectors passed to h2_matvec / h2_solve are in ORIGINAL order (the library applies perm).
+ *
+ * Ownership: handles are library-owned and freed by the matching *_destroy.  Host inputs are
+ * copied before the call returns.  Device pointers are borrowed for the stream-ordered duration
+ * of the call (do not free or overwrite them until the stream has passed the call).  An h2_mat
+ * lives in device memory allocated by the library (cudaMalloc) on the current device.
+ *
+ * Errors: every call validates its arguments before mutating anything and returns an
+ * h2_status; h2_last_error() returns a thread-local message for the last non-OK status.
+ * Calls on one h2_mat must be ordered on one stream (h2_matvec uses per-matrix device
+ * workspace); different matrices are independent.
+ */
+#ifndef H2_B200_H
+#define H2_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct h2_tree_* h2_tree;   /* cluster tree + permutation, immutable      */
+typedef struct h2_btree_* h2_btree; /* block tree (rows, cols, eta), immutable   */
+typedef struct h2_mat_* h2_mat;     /* H^2 matrix resident on one GPU, mutable    */
+typedef void* h2_stream;            /* a cudaStream_t (0 = legacy default stream)             */
+
+typedef enum {
+  H2_OK = 0,
+  H2_ERR_ARG = 1,       /* invalid argument (e.g. (t0,s0) not a block, n/dim/leaf <= 0)        */
+  H2_ERR_SHAPE = 2,     /* shape or rank mismatch, rank above the matrix's capacity             */
+  H2_ERR_STRUCTURE = 3, /* a CSR nonzero lands in an admissible block (message names the entry) */
+  H2_ERR_NONFINITE = 4, /* NaN/Inf in a host input                                              */
+  H2_ERR_BREAKDOWN = 5, /* dense leaf pivot breakdown (message names the cluster and pivot)     */
+  H2_ERR_NOMEM = 6,     /* device allocation failed / capacity exceeded                         */
+  H2_ERR_CUDA = 7,      /* a CUDA runtime error                                                 */
+  H2_ERR_UNSUPPORTED = 8 /* operation not available in this build                               */
+} h2_status;
+
+/* TruncationControl (reading SURVEY R5): a cluster keeps
+ *   r = #{ sigma_i > max(rel_tol * sigma_1, abs_tol) },  r <= max_rank (max_rank <= 0: unbounded),
+ * of the singular values of its weighted basis V~_t B~_t^T. sigma_1 = 0 gives r = 0. */
+typedef struct {
+  double rel_tol;
+  double abs_tol;
+  int32_t max_rank;
+} h2_trunc;
+
+typedef enum { H2_FULL = 0, H2_LOWER = 1 } h2_storage; /* LOWER: blocks with t-range >= s-range */
+typedef enum { H2_LR = 0, H2_CHOLESKY = 1 } h2_factor_kind;
+
+/* ---- structure (host, exact integer/FP predicates) -------------------------------------- */
+
+/* Cluster tree by geometric bisection (binary P:331-332; reading SURVEY R2):
+ * tight bounding box, split the longest extent (lowest axis on ties) at its midpoint, points with
+ * coord < mid go to son0 (stable), stop at <= leaf_size points.
+ * pts: host, n x dim, row-major (point i at pts[i*dim .. i*dim+dim-1]); dim in {1,2,3}. */
+h2_status h2_cluster_tree(const double* pts, int64_t n, int32_t dim, int32_t leaf_size, h2_tree* out);
+
+/* Export: perm[n]; lo/hi/son0/son1/level[nclusters] (son = -1 for leaves); any pointer may be
+ * NULL.  *nclusters receives the count (call once with NULL arrays to size them). */
+h2_status h2_tree_export(h2_tree tree, int64_t* perm, int32_t* lo, int32_t* hi, int32_t* son0,
+                         int32_t* son1, int32_t* level, int32_t* nclusters);
+void h2_tree_destroy(h2_tree tree);
+
+/* Block tree, sons(b) = sons+(t) x sons+(s) t-son-major; admissible
+ * iff dist > 0 and max(diam_t, diam_s) <= eta * dist on tight point boxes (reading SURVEY R1).
+ * The handle keeps references to both trees: destroy it before them. */
+h2_status h2_block_tree(h2_tree rows, h2_tree cols, double eta, h2_btree* out);
+
+/* Export blocks in DFS preorder: t[], s[], kind[] (0 subdivided, 1 admissible leaf,
+ * 2 inadmissible leaf); arrays may be NULL; *nblocks receives the count.  *csp (may be NULL)
+ * receives the sparsity constant C_sp. */
+h2_status h2_btree_export(h2_btree bt, int32_t* t, int32_t* s, int8_t* kind, int64_t* nblocks,
+                          int32_t* csp);
+void h2_btree_destroy(h2_btree bt);
+
+/* ---- H^2 matrix on the device ------------------------------------------------------------ */
+
+/* h2_from_sparse: all cluster bases of rank 0, the CSR (host arrays, ORIGINAL
+ * order, n x n) scattered into dense nearfield tiles.  A nonzero falling in an
+ * admissible block -> H2_ERR_STRUCTURE.  storage = H2_LOWER keeps only blocks whose row range
+ * starts at or after the column range (the Cholesky factor layout).
+ * rank_cap: capacity of stored ranks per cluster (e.g. 32); update_cap: the largest update rank
+ * k a later h2_lowrank_update may pass (extended rank capacity = rank_cap + update_cap <= 64). */
+h2_status h2_from_sparse(h2_btree bt, int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                         const double* val, h2_storage storage, int32_t rank_cap, int32_t update_cap,
+                         h2_stream stream, h2_mat* out);
+
+/* Local low-rank update Z|_{t0 x s0} += alpha X Y^T keeping Z globally H^2 (Thm 1):
+ * exact nearfield part, basis extension (eq. 4a-c), weights, truncated nested bases
+ * (P:769-872), coupling re-projection, transfer fix-up.
+ * X: device, |t0| x k, leading dimension ldx >= |t0|; Y: device, |s0| x k, ldy >= |s0|; rows in
+ * tree order within t0 / s0.  0 <= k <= update_cap.  (t0,s0) must be a node of the block tree
+ * (H2_ERR_ARG otherwise).  An inadmissible-leaf target gets the exact dense add only.
+ * Ranks are chosen on the device by *trunc; nothing is copied back to the host. */
+h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t k, double alpha,
+                            const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                            const h2_trunc* trunc, h2_stream stream);
+
+/* y <- alpha op(Z) x + beta y (op = transpose ? Z^T : Z), x/y device vectors in ORIGINAL order
+ * (forward transform, couplings, backward transform, nearfield). */
+h2_status h2_matvec(h2_mat Z, int32_t transpose, double alpha, const double* x, double beta, double* y,
+                    h2_stream stream);
+
+/* Z <- Z + alpha X Y (recursive product over the triple tree).
+ * Not available in this build: returns H2_ERR_UNSUPPORTED. */
+h2_status h2_addmul(h2_mat Z, double alpha, h2_mat X, h2_mat Y, const h2_trunc* trunc, h2_stream stream);
+
+/* In-place LR / Cholesky factorization.
+ * Not available in this build: returns H2_ERR_UNSUPPORTED. */
+h2_status h2_lr_factor(h2_mat A, h2_factor_kind kind, const h2_trunc* trunc, h2_stream stream);
+
+/* x <- F^{-1} x for a factored matrix (P:392-450 vector case).  Not available in this build. */
+h2_status h2_solve(h2_mat F, double* x, int32_t nrhs, int64_t ldx, h2_stream stream);
+
+/* ---- inspection (synchronous: these synchronize the given stream) -------------------------- */
+
+/* Row ranks k_t and column ranks l_s per cluster (arrays of nclusters, host). */
+h2_status h2_ranks(h2_mat Z, int32_t* row_rank, int32_t* col_rank);
+
+/* Stored scalars at the current ranks: [nearfield, leaf bases, transfers, couplings]. */
+h2_status h2_storage_report(h2_mat Z, int64_t scalars[4]);
+
+/* Test hook: copy the whole representation to host buffers (each may be NULL), tight layouts:
+ *   V: per leaf cluster in id order |t| x k_t;  E: per non-root cluster k_t x k_parent;
+ *   W, F: the same for the column basis;  S: per stored admissible block (DFS order) k_t x l_s;
+ *   N: per stored inadmissible block (DFS order) |t| x |s|.   sizes[6] receives the number of
+ * doubles of each array (call with NULL buffers first to size them). */
+h2_status h2_export(h2_mat Z, double* V, double* E, double* W, double* F, double* S, double* N,
+                    int64_t sizes[6]);
+
+/* Device-side status word: nonzero if a device kernel hit a rank above rank_cap (clamped) since
+ * the last call; the flag is cleared.  Synchronizes the stream. */
+h2_status h2_check_device_flags(h2_mat Z, int32_t* flags);
+
+void h2_mat_destroy(h2_mat Z);
+const char* h2_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H2_B200_H */

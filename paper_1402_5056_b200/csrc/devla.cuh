@@ -1,0 +1,196 @@
+// CTA-level dense FP64 kernels for the small matrices of the local update.
+// One CTA owns one small matrix staged in shared memory; all routines must be called by every
+// thread of the block (they contain __syncthreads()).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+
+namespace h2 {
+namespace la {
+
+__device__ __forceinline__ int pow2floor(int x) {
+  int p = 1;
+  while (p * 2 <= x) p *= 2;
+  return p;
+}
+
+__device__ __forceinline__ unsigned group_mask(int S) {
+  if (S >= 32) return 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  return ((1u << S) - 1u) << (lane & ~(S - 1));
+}
+
+// In-place Householder QR of the m x n column-major matrix A (lda) in shared memory; on return
+// the first min(m,n) rows hold R (upper trapezoidal, strictly-lower part zeroed).  Only the
+// R-factor is needed by the method ("P_t ... are not computed").
+// One reduction per column: all dots d_c = a_j[j:]^T a_c[j:] are formed together, and with
+// v = a_j[j:] - alpha e_1:  v^T a_c = d_c - alpha a_jc,  v^T v / 2 = |a_j|^2 - alpha a_jj.
+// red: >= 1 double of shared scratch; diag: >= min(m,n) doubles of shared scratch.
+__device__ void cta_qr_R(double* A, int lda, int m, int n, double* diag, double* red) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  int npow = 1;
+  while (npow < n) npow *= 2;
+  int S = nt / npow;
+  if (S > 32) S = 32;
+  if (S < 1) S = 1;
+  const int c = tid / S, sl = tid % S;
+  const unsigned gm = group_mask(S);
+  const int jmax = m < n ? m : n;
+  for (int j = 0; j < jmax; ++j) {
+    double part = 0.0;
+    if (c >= j && c < n)
+      for (int i = j + sl; i < m; i += S) part += A[i + j * lda] * A[i + c * lda];
+    for (int o = S / 2; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (c == j && sl == 0) red[0] = part;
+    __syncthreads();
+    const double nrm2 = red[0];
+    const double ajj = A[j + j * lda];
+    if (nrm2 > 0.0) {
+      const double nrm = sqrt(nrm2);
+      const double alpha = ajj > 0.0 ? -nrm : nrm;
+      const double half_vtv = nrm2 - alpha * ajj;
+      if (c > j && c < n) {
+        const double ajc = A[j + c * lda];
+        __syncwarp(gm);
+        const double f = (part - alpha * ajc) / half_vtv;
+        for (int i = j + sl; i < m; i += S) {
+          const double vi = (i == j) ? (ajj - alpha) : A[i + j * lda];
+          A[i + c * lda] -= f * vi;
+        }
+      }
+      if (tid == 0) diag[j] = alpha;
+    } else if (tid == 0) {
+      diag[j] = 0.0;
+    }
+    __syncthreads();
+  }
+  // write R: rows < jmax
+  for (int e = tid; e < jmax * n; e += nt) {
+    const int i = e % jmax, cc = e / jmax;
+    if (cc < i) A[i + cc * lda] = 0.0;
+    else if (cc == i) A[i + cc * lda] = diag[i];
+  }
+  __syncthreads();
+}
+
+// C (m x n, ldc) = op(A) op(B) (+ C if accumulate); A: m x kk (or kk x m if ta), B: kk x n (or n x kk if tb).
+// Any pointers (shared or global).  Every thread of the CTA participates.
+__device__ void cta_gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb,
+                         int m, int n, int kk, bool accumulate) {
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int i = e % m, j = e / m;
+    double acc = accumulate ? C[i + j * ldc] : 0.0;
+    for (int q = 0; q < kk; ++q) {
+      const double a = ta ? A[q + i * lda] : A[i + q * lda];
+      const double b = tb ? B[j + q * ldb] : B[q + j * ldb];
+      acc += a * b;
+    }
+    C[i + j * ldc] = acc;
+  }
+}
+
+__device__ __forceinline__ void cta_fill(double* A, int lda, int m, int n, double v) {
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) A[(e % m) + (e / m) * lda] = v;
+}
+
+__device__ __forceinline__ void cta_copy(double* D, int ldd, const double* Sx, int lds, int m, int n) {
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) D[(e % m) + (e / m) * ldd] = Sx[(e % m) + (e / m) * lds];
+}
+
+// One-sided (Hestenes) Jacobi SVD of the m x p matrix M (ldm, shared memory): orthogonalises the
+// columns by plane rotations until |a_i^T a_j| <= tol sqrt(|a_i|^2 |a_j|^2) for every pair (cyclic
+// round-robin ordering, p/2 disjoint pairs per round).  On return column j of M is sigma_j u_j
+// (unsorted); sig[j] = |M(:,j)|; order[q] = index of the q-th largest sigma (ties by index).
+// scratch: >= 2 ints of shared memory.
+__device__ void cta_jacobi(double* M, int ldm, int m, int p, double* sig, int* order, int* scratch) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int pp = p + (p & 1);
+  const int npairs = pp / 2;
+  int G = npairs > 0 ? pow2floor(nt / npairs) : 32;
+  if (G > 32) G = 32;
+  if (G < 1) G = 1;
+  const int q = tid / G, g = tid % G;
+  const double tol = 1e-15;
+  const int nr = pp - 1;  // rounds per sweep
+  for (int sweep = 0; sweep < 60 && p > 1; ++sweep) {
+    if (tid == 0) scratch[0] = 0;
+    __syncthreads();
+    for (int r = 0; r < nr; ++r) {
+      int a = -1, b = -1;
+      if (q < npairs) {
+        if (q == 0) {
+          a = 0;
+          b = (r % nr) + 1;
+        } else {
+          a = ((r + q) % nr) + 1;
+          b = ((r - q + nr) % nr) + 1;
+        }
+        if (a >= p || b >= p) a = b = -1;
+      }
+      double al = 0.0, be = 0.0, ga = 0.0;
+      if (a >= 0)
+        for (int i = g; i < m; i += G) {
+          const double x = M[i + a * ldm], y = M[i + b * ldm];
+          al += x * x;
+          be += y * y;
+          ga += x * y;
+        }
+      for (int o = G / 2; o; o >>= 1) {
+        al += __shfl_xor_sync(0xffffffffu, al, o);
+        be += __shfl_xor_sync(0xffffffffu, be, o);
+        ga += __shfl_xor_sync(0xffffffffu, ga, o);
+      }
+      if (a >= 0 && ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+        const double zeta = (be - al) / (2.0 * ga);
+        double t;
+        if (fabs(zeta) > 1e150) t = 0.5 / zeta;
+        else t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int i = g; i < m; i += G) {
+          const double x = M[i + a * ldm], y = M[i + b * ldm];
+          M[i + a * ldm] = cs * x - sn * y;
+          M[i + b * ldm] = sn * x + cs * y;
+        }
+        if (g == 0) scratch[0] = 1;
+      }
+      __syncthreads();
+    }
+    const int changed = scratch[0];
+    __syncthreads();
+    if (!changed) break;
+  }
+  // column norms
+  for (int j = tid; j < p; j += nt) {
+    double s = 0.0;
+    for (int i = 0; i < m; ++i) s += M[i + j * ldm] * M[i + j * ldm];
+    sig[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < p; j += nt) {
+    int pos = 0;
+    const double sj = sig[j];
+    for (int i = 0; i < p; ++i) pos += (sig[i] > sj) || (sig[i] == sj && i < j);
+    order[pos] = j;
+  }
+  __syncthreads();
+}
+
+// Rank rule of the truncation: r = #{sigma_q > max(rel sigma_1, abs)}, <= max_rank, <= cap.
+__device__ __forceinline__ int trunc_rank(const double* sig, const int* order, int p, double rel, double abs_tol,
+                                          int max_rank, int cap, int* clamped) {
+  if (p == 0) return 0;
+  const double s1 = sig[order[0]];
+  if (!(s1 > 0.0)) return 0;
+  const double thr = fmax(rel * s1, abs_tol);
+  int r = 0;
+  for (int q = 0; q < p; ++q) r += sig[order[q]] > thr;
+  if (max_rank > 0 && r > max_rank) r = max_rank;
+  if (r > cap) {
+    r = cap;
+    *clamped = 1;
+  }
+  return r;
+}
+
+}  // namespace la
+}  // namespace h2

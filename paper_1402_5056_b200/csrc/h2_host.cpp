@@ -1,0 +1,638 @@
+// Host side of the B200 H^2 library: structure (cluster/block trees), device storage, C ABI.
+//
+// Structure work is exact: integer-valued coordinates give exact box predicates,
+// and this file is compiled with -ffp-contract=off.  All FP64 arithmetic of the method runs in
+// the CUDA kernels (h2_matvec.cu, h2_update.cu); the host only builds index structures and
+// schedules launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "h2_internal.h"
+
+using namespace h2;
+
+static thread_local std::string g_last_error;
+
+void h2::set_error(const std::string& msg) { g_last_error = msg; }
+
+extern "C" const char* h2_last_error(void) { return g_last_error.c_str(); }
+
+#define H2_FAIL(code, msg)  \
+  do {                      \
+    h2::set_error(msg);     \
+    return code;            \
+  } while (0)
+
+#define CUDA_TRY(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      h2::set_error(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #expr); \
+      return e_ == cudaErrorMemoryAllocation ? H2_ERR_NOMEM : H2_ERR_CUDA;                  \
+    }                                                                                       \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------------
+// Cluster tree (binary P:331-332), geometric bisection per SURVEY R2.
+// ------------------------------------------------------------------------------------------------
+extern "C" h2_status h2_cluster_tree(const double* pts, int64_t n, int32_t dim, int32_t leaf_size,
+                                     h2_tree* out) {
+  if (!out) H2_FAIL(H2_ERR_ARG, "h2_cluster_tree: out is NULL");
+  *out = nullptr;
+  if (!pts || n <= 0 || dim < 1 || dim > 3 || leaf_size < 1)
+    H2_FAIL(H2_ERR_ARG, "h2_cluster_tree: need pts != NULL, n > 0, 1 <= dim <= 3, leaf_size >= 1");
+  for (int64_t i = 0; i < n * dim; ++i)
+    if (!std::isfinite(pts[i])) H2_FAIL(H2_ERR_NONFINITE, "h2_cluster_tree: non-finite coordinate");
+  h2_tree_* T = new (std::nothrow) h2_tree_();
+  if (!T) H2_FAIL(H2_ERR_NOMEM, "h2_cluster_tree: host allocation failed");
+  T->n = n;
+  T->dim = dim;
+  T->leaf = leaf_size;
+  T->perm.resize(n);
+  std::vector<int64_t> idx(n);
+  for (int64_t i = 0; i < n; ++i) idx[i] = i;
+
+  std::function<int(std::vector<int64_t>&, int64_t, int, int)> build =
+      [&](std::vector<int64_t>& ids, int64_t start, int par, int lev) -> int {
+    int cid = (int)T->lo.size();
+    T->lo.push_back((int32_t)start);
+    T->hi.push_back((int32_t)(start + (int64_t)ids.size()));
+    T->son0.push_back(-1);
+    T->son1.push_back(-1);
+    T->parent.push_back(par);
+    T->level.push_back(lev);
+    double bmin[3], bmax[3];
+    for (int d = 0; d < dim; ++d) {
+      bmin[d] = pts[ids[0] * dim + d];
+      bmax[d] = bmin[d];
+    }
+    for (int64_t q : ids)
+      for (int d = 0; d < dim; ++d) {
+        bmin[d] = std::min(bmin[d], pts[q * dim + d]);
+        bmax[d] = std::max(bmax[d], pts[q * dim + d]);
+      }
+    for (int d = 0; d < dim; ++d) {
+      T->bmin.push_back(bmin[d]);
+      T->bmax.push_back(bmax[d]);
+    }
+    auto make_leaf = [&]() {
+      for (size_t i = 0; i < ids.size(); ++i) T->perm[start + (int64_t)i] = ids[i];
+      return cid;
+    };
+    if ((int64_t)ids.size() <= leaf_size) return make_leaf();
+    int ax = 0;
+    for (int d = 1; d < dim; ++d)
+      if (bmax[d] - bmin[d] > bmax[ax] - bmin[ax]) ax = d;  // strict: lowest axis on ties
+    const double twomid = bmin[ax] + bmax[ax];
+    std::vector<int64_t> left, right;
+    for (int64_t q : ids) (2.0 * pts[q * dim + ax] < twomid ? left : right).push_back(q);
+    if (left.empty() || right.empty()) return make_leaf();
+    ids.clear();
+    ids.shrink_to_fit();
+    int64_t nl = (int64_t)left.size();
+    int c0 = build(left, start, cid, lev + 1);
+    int c1 = build(right, start + nl, cid, lev + 1);
+    T->son0[cid] = c0;
+    T->son1[cid] = c1;
+    return cid;
+  };
+  build(idx, 0, -1, 0);
+  const int nc = (int)T->lo.size();
+  T->nclusters = nc;
+  T->depth = *std::max_element(T->level.begin(), T->level.end());
+  T->tsize.assign(nc, 1);
+  for (int t = nc - 1; t >= 0; --t)
+    if (T->son0[t] >= 0) T->tsize[t] = 1 + T->tsize[T->son0[t]] + T->tsize[T->son1[t]];
+  // BFS order: sorted by (level, id)
+  T->level_ptr.assign(T->depth + 2, 0);
+  for (int t = 0; t < nc; ++t) T->level_ptr[T->level[t] + 1]++;
+  for (int L = 0; L <= T->depth; ++L) T->level_ptr[L + 1] += T->level_ptr[L];
+  T->bfs.assign(nc, 0);
+  {
+    std::vector<int32_t> fill(T->level_ptr.begin(), T->level_ptr.end() - 1);
+    for (int t = 0; t < nc; ++t) T->bfs[fill[T->level[t]]++] = t;
+  }
+  T->leaf_index.assign(nc, -1);
+  for (int t = 0; t < nc; ++t)
+    if (T->son0[t] < 0) {
+      T->leaf_index[t] = (int32_t)T->leaves.size();
+      T->leaves.push_back(t);
+    }
+  *out = T;
+  return H2_OK;
+}
+
+extern "C" h2_status h2_tree_export(h2_tree tree, int64_t* perm, int32_t* lo, int32_t* hi, int32_t* son0,
+                                    int32_t* son1, int32_t* level, int32_t* nclusters) {
+  if (!tree) H2_FAIL(H2_ERR_ARG, "h2_tree_export: NULL tree");
+  const h2_tree_* T = tree;
+  if (nclusters) *nclusters = T->nclusters;
+  if (perm) std::copy(T->perm.begin(), T->perm.end(), perm);
+  if (lo) std::copy(T->lo.begin(), T->lo.end(), lo);
+  if (hi) std::copy(T->hi.begin(), T->hi.end(), hi);
+  if (son0) std::copy(T->son0.begin(), T->son0.end(), son0);
+  if (son1) std::copy(T->son1.begin(), T->son1.end(), son1);
+  if (level) std::copy(T->level.begin(), T->level.end(), level);
+  return H2_OK;
+}
+
+extern "C" void h2_tree_destroy(h2_tree tree) { delete tree; }
+
+// ------------------------------------------------------------------------------------------------
+// Block tree (sons+ P:1031-1037), admissibility per SURVEY R1.
+// ------------------------------------------------------------------------------------------------
+static double diam2(const h2_tree_* T, int t) {
+  double s = 0;
+  for (int d = 0; d < T->dim; ++d) {
+    double e = T->bmax[t * T->dim + d] - T->bmin[t * T->dim + d];
+    s += e * e;
+  }
+  return s;
+}
+
+static double dist2(const h2_tree_* R, int t, const h2_tree_* C, int s) {
+  double acc = 0;
+  for (int d = 0; d < R->dim; ++d) {
+    double g = std::max(0.0, std::max(C->bmin[s * C->dim + d] - R->bmax[t * R->dim + d],
+                                      R->bmin[t * R->dim + d] - C->bmax[s * C->dim + d]));
+    acc += g * g;
+  }
+  return acc;
+}
+
+extern "C" h2_status h2_block_tree(h2_tree rows, h2_tree cols, double eta, h2_btree* out) {
+  if (!out) H2_FAIL(H2_ERR_ARG, "h2_block_tree: out is NULL");
+  *out = nullptr;
+  if (!rows || !cols) H2_FAIL(H2_ERR_ARG, "h2_block_tree: NULL tree");
+  if (!(eta > 0) || !std::isfinite(eta)) H2_FAIL(H2_ERR_ARG, "h2_block_tree: eta must be finite and > 0");
+  if (rows->dim != cols->dim) H2_FAIL(H2_ERR_ARG, "h2_block_tree: trees of different dimension");
+  h2_btree_* B = new (std::nothrow) h2_btree_();
+  if (!B) H2_FAIL(H2_ERR_NOMEM, "h2_block_tree: host allocation failed");
+  B->rt = rows;
+  B->ct = cols;
+  B->eta = eta;
+  const double eta2 = eta * eta;
+  std::function<int(int, int, int)> build = [&](int t, int s, int par) -> int {
+    int b = (int)B->t.size();
+    B->t.push_back(t);
+    B->s.push_back(s);
+    B->parent.push_back(par);
+    B->sons.push_back({-1, -1, -1, -1});
+    B->nsons.push_back(0);
+    B->kind.push_back(SUBDIV);
+    const double d2 = dist2(rows, t, cols, s);
+    if (d2 > 0.0 && std::max(diam2(rows, t), diam2(cols, s)) <= eta2 * d2) {
+      B->kind[b] = ADM;
+      return b;
+    }
+    const bool tl = rows->son0[t] < 0, sl = cols->son0[s] < 0;
+    if (tl && sl) {
+      B->kind[b] = INADM;
+      return b;
+    }
+    int ts[2], ss[2], nt = 0, ns = 0;
+    if (tl) ts[nt++] = t; else { ts[nt++] = rows->son0[t]; ts[nt++] = rows->son1[t]; }
+    if (sl) ss[ns++] = s; else { ss[ns++] = cols->son0[s]; ss[ns++] = cols->son1[s]; }
+    int q = 0;
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j < ns; ++j) {
+        int c = build(ts[i], ss[j], b);
+        B->sons[b][q++] = c;
+      }
+    B->nsons[b] = (int8_t)q;
+    return b;
+  };
+  build(0, 0, -1);
+  const int nb = (int)B->t.size();
+  B->bsize.assign(nb, 1);
+  for (int b = nb - 1; b >= 0; --b)
+    for (int q = 0; q < B->nsons[b]; ++q) B->bsize[b] += B->bsize[B->sons[b][q]];
+  B->index.reserve(nb * 2);
+  std::vector<int> cr(rows->nclusters, 0), cc(cols->nclusters, 0);
+  for (int b = 0; b < nb; ++b) {
+    B->index[(int64_t)B->t[b] * cols->nclusters + B->s[b]] = b;
+    cr[B->t[b]]++;
+    cc[B->s[b]]++;
+  }
+  B->csp = std::max(*std::max_element(cr.begin(), cr.end()), *std::max_element(cc.begin(), cc.end()));
+  *out = B;
+  return H2_OK;
+}
+
+extern "C" h2_status h2_btree_export(h2_btree bt, int32_t* t, int32_t* s, int8_t* kind, int64_t* nblocks,
+                                     int32_t* csp) {
+  if (!bt) H2_FAIL(H2_ERR_ARG, "h2_btree_export: NULL block tree");
+  if (nblocks) *nblocks = (int64_t)bt->t.size();
+  if (csp) *csp = bt->csp;
+  if (t) std::copy(bt->t.begin(), bt->t.end(), t);
+  if (s) std::copy(bt->s.begin(), bt->s.end(), s);
+  if (kind) std::copy(bt->kind.begin(), bt->kind.end(), kind);
+  return H2_OK;
+}
+
+extern "C" void h2_btree_destroy(h2_btree bt) { delete bt; }
+
+// ------------------------------------------------------------------------------------------------
+// Device storage
+// ------------------------------------------------------------------------------------------------
+template <class T>
+static cudaError_t dalloc(h2_mat_* Z, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e == cudaSuccess) Z->allocs.push_back((void*)*p);
+  return e;
+}
+
+template <class T>
+static cudaError_t dupload(h2_mat_* Z, T** p, const std::vector<T>& v) {
+  cudaError_t e = dalloc(Z, p, v.size());
+  if (e != cudaSuccess) return e;
+  if (!v.empty()) e = cudaMemcpy(*p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+static void free_mat(h2_mat_* Z) {
+  if (!Z) return;
+  for (void* p : Z->allocs) cudaFree(p);
+  delete Z;
+}
+
+extern "C" void h2_mat_destroy(h2_mat Z) { free_mat(Z); }
+
+static h2_status setup_side(h2_mat_* Z, DevSide& D, const h2_tree_* T, bool row_side) {
+  const h2_btree_* B = Z->bt;
+  const MatDev& M = Z->d;
+  D.tree = T;
+  D.nclusters = T->nclusters;
+  D.nleaves = (int)T->leaves.size();
+  CUDA_TRY(dupload(Z, &D.lo, T->lo));
+  CUDA_TRY(dupload(Z, &D.hi, T->hi));
+  CUDA_TRY(dupload(Z, &D.son0, T->son0));
+  CUDA_TRY(dupload(Z, &D.son1, T->son1));
+  CUDA_TRY(dupload(Z, &D.parent, T->parent));
+  CUDA_TRY(dupload(Z, &D.tsize, T->tsize));
+  CUDA_TRY(dupload(Z, &D.leafidx, T->leaf_index));
+  CUDA_TRY(dupload(Z, &D.bfs, T->bfs));
+  CUDA_TRY(dupload(Z, &D.leaves, T->leaves));
+  CUDA_TRY(dupload(Z, &D.level, T->level));
+  CUDA_TRY(dupload(Z, &D.perm, T->perm));
+  // admissible stored blocks per cluster (adm slots in DFS order)
+  std::vector<int32_t> ptr(T->nclusters + 1, 0), idx;
+  for (size_t a = 0; a < Z->adm_blk.size(); ++a) {
+    int b = Z->adm_blk[a];
+    ptr[(row_side ? B->t[b] : B->s[b]) + 1]++;
+  }
+  for (int t = 0; t < T->nclusters; ++t) ptr[t + 1] += ptr[t];
+  idx.assign(ptr.back(), 0);
+  {
+    std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
+    for (size_t a = 0; a < Z->adm_blk.size(); ++a) {
+      int b = Z->adm_blk[a];
+      idx[fill[row_side ? B->t[b] : B->s[b]]++] = (int32_t)a;
+    }
+  }
+  CUDA_TRY(dupload(Z, &D.bptr, ptr));
+  CUDA_TRY(dupload(Z, &D.bidx, idx));
+  CUDA_TRY(dalloc(Z, &D.rank, T->nclusters));
+  CUDA_TRY(cudaMemset(D.rank, 0, sizeof(int32_t) * T->nclusters));
+  const size_t r2 = (size_t)M.rcap * M.rcap;
+  CUDA_TRY(dalloc(Z, &D.leafb, (size_t)D.nleaves * M.lmax * M.rcap));
+  CUDA_TRY(cudaMemset(D.leafb, 0, sizeof(double) * (size_t)D.nleaves * M.lmax * M.rcap));
+  CUDA_TRY(dalloc(Z, &D.tr, (size_t)T->nclusters * r2));
+  CUDA_TRY(cudaMemset(D.tr, 0, sizeof(double) * (size_t)T->nclusters * r2));
+  CUDA_TRY(dalloc(Z, &D.rc, (size_t)T->nclusters * r2));
+  CUDA_TRY(cudaMemset(D.rc, 0, sizeof(double) * (size_t)T->nclusters * r2));
+  CUDA_TRY(dalloc(Z, &D.xh, (size_t)T->nclusters * M.rcap));
+  return H2_OK;
+}
+
+static h2_status alloc_update_workspace(h2_mat_* Z, DevSide& D) {
+  if (D.re) return H2_OK;
+  const MatDev& M = Z->d;
+  const size_t nc = D.nclusters, k2 = (size_t)M.kcap * M.kcap;
+  CUDA_TRY(dalloc(Z, &D.re, nc * k2));
+  CUDA_TRY(dalloc(Z, &D.bw, nc * k2));
+  CUDA_TRY(dalloc(Z, &D.rn, nc * k2));
+  CUDA_TRY(dalloc(Z, &D.qn, nc * (size_t)M.ldq * M.rcap));
+  CUDA_TRY(dalloc(Z, &D.rnew, nc));
+  return H2_OK;
+}
+
+extern "C" h2_status h2_from_sparse(h2_btree bt, int64_t n, const int64_t* rowptr, const int32_t* colidx,
+                                    const double* val, h2_storage storage, int32_t rank_cap,
+                                    int32_t update_cap, h2_stream stream, h2_mat* out) {
+  if (!out) H2_FAIL(H2_ERR_ARG, "h2_from_sparse: out is NULL");
+  *out = nullptr;
+  if (!bt) H2_FAIL(H2_ERR_ARG, "h2_from_sparse: NULL block tree");
+  const h2_tree_* R = bt->rt;
+  const h2_tree_* C = bt->ct;
+  if (n != R->n || n != C->n) H2_FAIL(H2_ERR_SHAPE, "h2_from_sparse: n does not match the cluster trees");
+  if (!rowptr || (n > 0 && rowptr[n] > 0 && (!colidx || !val)))
+    H2_FAIL(H2_ERR_ARG, "h2_from_sparse: NULL CSR array");
+  if (storage != H2_FULL && storage != H2_LOWER) H2_FAIL(H2_ERR_ARG, "h2_from_sparse: bad storage");
+  if (storage == H2_LOWER && R != C) H2_FAIL(H2_ERR_ARG, "h2_from_sparse: H2_LOWER needs one shared tree");
+  if (rank_cap < 1 || update_cap < 0 || rank_cap + update_cap > KCAP_MAX)
+    H2_FAIL(H2_ERR_ARG, "h2_from_sparse: need rank_cap >= 1, update_cap >= 0, rank_cap + update_cap <= 64");
+  int lmax = 0;
+  for (int t : R->leaves) lmax = std::max(lmax, R->hi[t] - R->lo[t]);
+  for (int t : C->leaves) lmax = std::max(lmax, C->hi[t] - C->lo[t]);
+  if (lmax > LMAX_MAX) H2_FAIL(H2_ERR_ARG, "h2_from_sparse: leaf clusters larger than 64 are not supported");
+  for (int64_t i = 0; i < n; ++i)
+    if (rowptr[i + 1] < rowptr[i]) H2_FAIL(H2_ERR_ARG, "h2_from_sparse: rowptr not monotone");
+  const int64_t nnz = rowptr[n] - rowptr[0];
+  for (int64_t q = rowptr[0]; q < rowptr[0] + nnz; ++q) {
+    if (colidx[q] < 0 || colidx[q] >= n) H2_FAIL(H2_ERR_ARG, "h2_from_sparse: column index out of range");
+    if (!std::isfinite(val[q])) H2_FAIL(H2_ERR_NONFINITE, "h2_from_sparse: non-finite value");
+  }
+  h2_mat_* Z = new (std::nothrow) h2_mat_();
+  if (!Z) H2_FAIL(H2_ERR_NOMEM, "h2_from_sparse: host allocation failed");
+  Z->bt = bt;
+  Z->lower = storage == H2_LOWER;
+  MatDev& M = Z->d;
+  M.rcap = rank_cap;
+  M.ucap = update_cap;
+  M.kcap = rank_cap + update_cap;
+  M.lmax = lmax;
+  M.ldq = std::max(lmax, 2 * rank_cap);
+  const int nb = (int)bt->t.size();
+  auto stored = [&](int b) { return !Z->lower || R->lo[bt->t[b]] >= C->lo[bt->s[b]]; };
+  Z->blk2adm.assign(nb, -1);
+  Z->blk2inad.assign(nb, -1);
+  Z->inad_range.assign(2 * nb, 0);
+  for (int b = 0; b < nb; ++b) {
+    if (bt->kind[b] == ADM && stored(b)) {
+      Z->blk2adm[b] = (int32_t)Z->adm_blk.size();
+      Z->adm_blk.push_back(b);
+    } else if (bt->kind[b] == INADM && stored(b)) {
+      Z->blk2inad[b] = (int32_t)Z->inad_blk.size();
+      Z->inad_blk.push_back(b);
+    }
+  }
+  // [first,last) inadmissible slots inside each block subtree (subtrees are contiguous in DFS order)
+  {
+    std::vector<int32_t> before(nb + 1, 0);
+    for (int b = 0; b < nb; ++b) before[b + 1] = before[b] + (Z->blk2inad[b] >= 0 ? 1 : 0);
+    for (int b = 0; b < nb; ++b) {
+      Z->inad_range[2 * b] = before[b];
+      Z->inad_range[2 * b + 1] = before[b + bt->bsize[b]];
+    }
+  }
+  M.nadm = (int)Z->adm_blk.size();
+  M.ninad = (int)Z->inad_blk.size();
+  // scatter the CSR into nearfield tiles on the host (tree order), then upload
+  std::vector<int64_t> iperm_r(n), iperm_c(n);
+  for (int64_t i = 0; i < n; ++i) {
+    iperm_r[R->perm[i]] = i;
+    iperm_c[C->perm[i]] = i;
+  }
+  std::vector<int32_t> rleaf(n), cleaf(n);
+  for (int t : R->leaves)
+    for (int i = R->lo[t]; i < R->hi[t]; ++i) rleaf[i] = t;
+  for (int s : C->leaves)
+    for (int i = C->lo[s]; i < C->hi[s]; ++i) cleaf[i] = s;
+  std::vector<double> tiles((size_t)M.ninad * lmax * lmax, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t q = rowptr[i]; q < rowptr[i + 1]; ++q) {
+      const double v = val[q];
+      if (v == 0.0) continue;
+      const int64_t pi = iperm_r[i], pj = iperm_c[colidx[q]];
+      const int t = rleaf[pi], s = cleaf[pj];
+      const int b = bt->find(t, s);
+      if (b < 0 || bt->kind[b] != INADM) {
+        free_mat(Z);
+        char msg[200];
+        snprintf(msg, sizeof msg, "h2_from_sparse: nonzero (%lld,%lld) lies in an admissible block",
+                 (long long)i, (long long)colidx[q]);
+        H2_FAIL(H2_ERR_STRUCTURE, msg);
+      }
+      const int slot = Z->blk2inad[b];
+      if (slot < 0) continue;  // upper part of a symmetric matrix in H2_LOWER storage
+      tiles[(size_t)slot * lmax * lmax + (pi - R->lo[t]) + (size_t)(pj - C->lo[s]) * lmax] += v;
+    }
+  }
+  h2_status st;
+  cudaError_t e;
+  std::vector<int32_t> at(M.nadm), as(M.nadm), it(M.ninad), is(M.ninad);
+  for (int a = 0; a < M.nadm; ++a) {
+    at[a] = bt->t[Z->adm_blk[a]];
+    as[a] = bt->s[Z->adm_blk[a]];
+  }
+  for (int a = 0; a < M.ninad; ++a) {
+    it[a] = bt->t[Z->inad_blk[a]];
+    is[a] = bt->s[Z->inad_blk[a]];
+  }
+  // nearfield CSR per row leaf and per column leaf
+  std::vector<int32_t> nptr(R->nclusters + 1, 0), nidx(M.ninad), ntptr(C->nclusters + 1, 0), ntidx(M.ninad);
+  for (int a = 0; a < M.ninad; ++a) {
+    nptr[it[a] + 1]++;
+    ntptr[is[a] + 1]++;
+  }
+  for (int t = 0; t < R->nclusters; ++t) nptr[t + 1] += nptr[t];
+  for (int t = 0; t < C->nclusters; ++t) ntptr[t + 1] += ntptr[t];
+  {
+    std::vector<int32_t> f1(nptr.begin(), nptr.end() - 1), f2(ntptr.begin(), ntptr.end() - 1);
+    for (int a = 0; a < M.ninad; ++a) {
+      nidx[f1[it[a]]++] = a;
+      ntidx[f2[is[a]]++] = a;
+    }
+  }
+#define TRY_ALLOC(expr)        \
+  do {                         \
+    e = (expr);                \
+    if (e != cudaSuccess) {    \
+      free_mat(Z);             \
+      CUDA_TRY(e);             \
+    }                          \
+  } while (0)
+  TRY_ALLOC(dupload(Z, &M.adm_t, at));
+  TRY_ALLOC(dupload(Z, &M.adm_s, as));
+  TRY_ALLOC(dupload(Z, &M.in_t, it));
+  TRY_ALLOC(dupload(Z, &M.in_s, is));
+  TRY_ALLOC(dupload(Z, &M.nptr, nptr));
+  TRY_ALLOC(dupload(Z, &M.nidx, nidx));
+  TRY_ALLOC(dupload(Z, &M.ntptr, ntptr));
+  TRY_ALLOC(dupload(Z, &M.ntidx, ntidx));
+  TRY_ALLOC(dupload(Z, &M.N, tiles));
+  TRY_ALLOC(dalloc(Z, &M.S, (size_t)M.nadm * M.rcap * M.rcap));
+  TRY_ALLOC(cudaMemset(M.S, 0, sizeof(double) * (size_t)M.nadm * M.rcap * M.rcap));
+  TRY_ALLOC(dalloc(Z, &M.flags, 4));
+  TRY_ALLOC(cudaMemset(M.flags, 0, 4 * sizeof(int32_t)));
+  TRY_ALLOC(dalloc(Z, &M.xt, n));
+  TRY_ALLOC(dalloc(Z, &M.yt, n));
+#undef TRY_ALLOC
+  if ((st = setup_side(Z, M.row, R, true)) != H2_OK) { free_mat(Z); return st; }
+  if ((st = setup_side(Z, M.col, C, false)) != H2_OK) { free_mat(Z); return st; }
+  e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) { free_mat(Z); CUDA_TRY(e); }
+  *out = Z;
+  return H2_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Operations
+// ------------------------------------------------------------------------------------------------
+extern "C" h2_status h2_matvec(h2_mat Z, int32_t transpose, double alpha, const double* x, double beta,
+                               double* y, h2_stream stream) {
+  if (!Z || !x || !y) H2_FAIL(H2_ERR_ARG, "h2_matvec: NULL argument");
+  if (!std::isfinite(alpha) || !std::isfinite(beta)) H2_FAIL(H2_ERR_NONFINITE, "h2_matvec: non-finite scalar");
+  CUDA_TRY(launch_matvec(Z, transpose ? 1 : 0, alpha, x, beta, y, (cudaStream_t)stream));
+  return H2_OK;
+}
+
+extern "C" h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t k, double alpha,
+                                       const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                                       const h2_trunc* trunc, h2_stream stream) {
+  if (!Z) H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: NULL matrix");
+  const h2_btree_* B = Z->bt;
+  if (t0 < 0 || t0 >= B->rt->nclusters || s0 < 0 || s0 >= B->ct->nclusters)
+    H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: cluster id out of range");
+  const int b0 = B->find(t0, s0);
+  if (b0 < 0) H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: (t0,s0) is not a block of the block tree");
+  if (k < 0 || k > Z->d.ucap) H2_FAIL(H2_ERR_SHAPE, "h2_lowrank_update: k outside [0, update_cap]");
+  if (!std::isfinite(alpha)) H2_FAIL(H2_ERR_NONFINITE, "h2_lowrank_update: non-finite alpha");
+  if (k > 0 && (!X || !Y)) H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: NULL factor");
+  const int mt = B->rt->hi[t0] - B->rt->lo[t0], ms = B->ct->hi[s0] - B->ct->lo[s0];
+  if (k > 0 && (ldx < mt || ldy < ms)) H2_FAIL(H2_ERR_SHAPE, "h2_lowrank_update: leading dimension too small");
+  h2_trunc tc = trunc ? *trunc : h2_trunc{1e-4, 0.0, 0};
+  if (!(tc.rel_tol >= 0) || !(tc.abs_tol >= 0)) H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: negative tolerance");
+  if (Z->lower && B->rt->lo[t0] < B->ct->lo[s0])
+    H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: target block is not stored in H2_LOWER storage");
+  if (k == 0) return H2_OK;  // bit-identical
+  h2_status st;
+  if ((st = alloc_update_workspace(Z, Z->d.row)) != H2_OK) return st;
+  if ((st = alloc_update_workspace(Z, Z->d.col)) != H2_OK) return st;
+  UpdArgs a;
+  a.t0 = t0;
+  a.s0 = s0;
+  a.k = k;
+  a.X = X;
+  a.ldx = ldx;
+  a.Y = Y;
+  a.ldy = ldy;
+  a.alpha = alpha;
+  a.rel_tol = tc.rel_tol;
+  a.abs_tol = tc.abs_tol;
+  a.max_rank = tc.max_rank;
+  CUDA_TRY(launch_update(Z, a, (cudaStream_t)stream));
+  return H2_OK;
+}
+
+extern "C" h2_status h2_addmul(h2_mat, double, h2_mat, h2_mat, const h2_trunc*, h2_stream) {
+  H2_FAIL(H2_ERR_UNSUPPORTED, "h2_addmul: not available in this build");
+}
+
+extern "C" h2_status h2_lr_factor(h2_mat, h2_factor_kind, const h2_trunc*, h2_stream) {
+  H2_FAIL(H2_ERR_UNSUPPORTED, "h2_lr_factor: not available in this build");
+}
+
+extern "C" h2_status h2_solve(h2_mat, double*, int32_t, int64_t, h2_stream) {
+  H2_FAIL(H2_ERR_UNSUPPORTED, "h2_solve: not available in this build");
+}
+
+// ------------------------------------------------------------------------------------------------
+// Inspection
+// ------------------------------------------------------------------------------------------------
+extern "C" h2_status h2_ranks(h2_mat Z, int32_t* row_rank, int32_t* col_rank) {
+  if (!Z) H2_FAIL(H2_ERR_ARG, "h2_ranks: NULL matrix");
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (row_rank)
+    CUDA_TRY(cudaMemcpy(row_rank, Z->d.row.rank, sizeof(int32_t) * Z->d.row.nclusters, cudaMemcpyDeviceToHost));
+  if (col_rank)
+    CUDA_TRY(cudaMemcpy(col_rank, Z->d.col.rank, sizeof(int32_t) * Z->d.col.nclusters, cudaMemcpyDeviceToHost));
+  return H2_OK;
+}
+
+extern "C" h2_status h2_check_device_flags(h2_mat Z, int32_t* flags) {
+  if (!Z || !flags) H2_FAIL(H2_ERR_ARG, "h2_check_device_flags: NULL argument");
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(flags, Z->d.flags, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemset(Z->d.flags, 0, sizeof(int32_t)));
+  return H2_OK;
+}
+
+extern "C" h2_status h2_storage_report(h2_mat Z, int64_t scalars[4]) {
+  if (!Z || !scalars) H2_FAIL(H2_ERR_ARG, "h2_storage_report: NULL argument");
+  const h2_btree_* B = Z->bt;
+  std::vector<int32_t> kr(Z->d.row.nclusters), kc(Z->d.col.nclusters);
+  h2_status st = h2_ranks(Z, kr.data(), kc.data());
+  if (st != H2_OK) return st;
+  const h2_tree_* R = B->rt;
+  const h2_tree_* C = B->ct;
+  int64_t near = 0, leaf = 0, tr = 0, cp = 0;
+  for (int b : Z->inad_blk) near += (int64_t)(R->hi[B->t[b]] - R->lo[B->t[b]]) * (C->hi[B->s[b]] - C->lo[B->s[b]]);
+  for (int t : R->leaves) leaf += (int64_t)(R->hi[t] - R->lo[t]) * kr[t];
+  for (int s : C->leaves) leaf += (int64_t)(C->hi[s] - C->lo[s]) * kc[s];
+  for (int t = 1; t < R->nclusters; ++t) tr += (int64_t)kr[t] * kr[R->parent[t]];
+  for (int s = 1; s < C->nclusters; ++s) tr += (int64_t)kc[s] * kc[C->parent[s]];
+  for (int b : Z->adm_blk) cp += (int64_t)kr[B->t[b]] * kc[B->s[b]];
+  scalars[0] = near;
+  scalars[1] = leaf;
+  scalars[2] = tr;
+  scalars[3] = cp;
+  return H2_OK;
+}
+
+extern "C" h2_status h2_export(h2_mat Z, double* V, double* E, double* W, double* F, double* S, double* N,
+                               int64_t sizes[6]) {
+  if (!Z || !sizes) H2_FAIL(H2_ERR_ARG, "h2_export: NULL argument");
+  const h2_btree_* B = Z->bt;
+  const h2_tree_* R = B->rt;
+  const h2_tree_* C = B->ct;
+  const MatDev& M = Z->d;
+  std::vector<int32_t> kr(M.row.nclusters), kc(M.col.nclusters);
+  h2_status st = h2_ranks(Z, kr.data(), kc.data());
+  if (st != H2_OK) return st;
+  const size_t r2 = (size_t)M.rcap * M.rcap;
+  std::vector<double> hleafr((size_t)M.row.nleaves * M.lmax * M.rcap), hleafc((size_t)M.col.nleaves * M.lmax * M.rcap);
+  std::vector<double> htrr((size_t)R->nclusters * r2), htrc((size_t)C->nclusters * r2);
+  std::vector<double> hS((size_t)M.nadm * r2), hN((size_t)M.ninad * M.lmax * M.lmax);
+  CUDA_TRY(cudaMemcpy(hleafr.data(), M.row.leafb, hleafr.size() * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(hleafc.data(), M.col.leafb, hleafc.size() * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(htrr.data(), M.row.tr, htrr.size() * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(htrc.data(), M.col.tr, htrc.size() * 8, cudaMemcpyDeviceToHost));
+  if (!hS.empty()) CUDA_TRY(cudaMemcpy(hS.data(), M.S, hS.size() * 8, cudaMemcpyDeviceToHost));
+  if (!hN.empty()) CUDA_TRY(cudaMemcpy(hN.data(), M.N, hN.size() * 8, cudaMemcpyDeviceToHost));
+  int64_t nV = 0, nE = 0, nW = 0, nF = 0, nS = 0, nN = 0;
+  auto put = [](double* dst, int64_t& pos, const double* src, int rows, int cols, int ld) {
+    for (int j = 0; j < cols; ++j)
+      for (int i = 0; i < rows; ++i) {
+        if (dst) dst[pos] = src[i + (size_t)j * ld];
+        ++pos;
+      }
+  };
+  for (size_t q = 0; q < R->leaves.size(); ++q) {
+    int t = R->leaves[q];
+    put(V, nV, &hleafr[q * M.lmax * M.rcap], R->hi[t] - R->lo[t], kr[t], M.lmax);
+  }
+  for (size_t q = 0; q < C->leaves.size(); ++q) {
+    int s = C->leaves[q];
+    put(W, nW, &hleafc[q * M.lmax * M.rcap], C->hi[s] - C->lo[s], kc[s], M.lmax);
+  }
+  for (int t = 1; t < R->nclusters; ++t) put(E, nE, &htrr[t * r2], kr[t], kr[R->parent[t]], M.rcap);
+  for (int s = 1; s < C->nclusters; ++s) put(F, nF, &htrc[s * r2], kc[s], kc[C->parent[s]], M.rcap);
+  for (int a = 0; a < M.nadm; ++a) {
+    int b = Z->adm_blk[a];
+    put(S, nS, &hS[a * r2], kr[B->t[b]], kc[B->s[b]], M.rcap);
+  }
+  for (int a = 0; a < M.ninad; ++a) {
+    int b = Z->inad_blk[a];
+    put(N, nN, &hN[(size_t)a * M.lmax * M.lmax], R->hi[B->t[b]] - R->lo[B->t[b]], C->hi[B->s[b]] - C->lo[B->s[b]],
+        M.lmax);
+  }
+  sizes[0] = nV;
+  sizes[1] = nE;
+  sizes[2] = nW;
+  sizes[3] = nF;
+  sizes[4] = nS;
+  sizes[5] = nN;
+  return H2_OK;
+}

@@ -1,0 +1,126 @@
+// Internal structures of the B200 H^2 library (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <array>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/h2.h"
+
+namespace h2 {
+
+constexpr int KCAP_MAX = 64;  // extended rank capacity (rank_cap + update_cap) handled by the kernels
+constexpr int LMAX_MAX = 64;  // largest leaf cluster handled by the kernels
+constexpr int NTHREADS = 256; // threads per CTA of the small-matrix kernels
+
+enum { SUBDIV = 0, ADM = 1, INADM = 2 };
+
+}  // namespace h2
+
+struct h2_tree_ {
+  int64_t n = 0;
+  int dim = 0, leaf = 0;
+  int nclusters = 0, depth = 0;
+  std::vector<int64_t> perm;
+  std::vector<int32_t> lo, hi, son0, son1, parent, level, tsize;
+  std::vector<double> bmin, bmax;       // nclusters * dim
+  std::vector<int32_t> bfs, level_ptr;  // clusters sorted by (level, id); level_ptr[depth+2]
+  std::vector<int32_t> leaf_index;      // cluster -> leaf ordinal (or -1)
+  std::vector<int32_t> leaves;          // leaf ordinal -> cluster
+  bool in_subtree(int t, int root) const { return t >= root && t < root + tsize[root]; }
+};
+
+struct h2_btree_ {
+  h2_tree_* rt = nullptr;
+  h2_tree_* ct = nullptr;
+  double eta = 0;
+  std::vector<int32_t> t, s, parent, bsize;
+  std::vector<int8_t> kind;
+  std::vector<std::array<int32_t, 4>> sons;
+  std::vector<int8_t> nsons;
+  std::unordered_map<int64_t, int32_t> index;  // key t * ct->nclusters + s
+  int csp = 0;
+  int32_t find(int a, int b) const {
+    auto it = index.find((int64_t)a * ct->nclusters + b);
+    return it == index.end() ? -1 : it->second;
+  }
+};
+
+namespace h2 {
+
+// One cluster-basis family (row: V/E, column: W/F) resident on the device.
+struct DevSide {
+  const h2_tree_* tree = nullptr;
+  int nclusters = 0, nleaves = 0;
+  // structure
+  int32_t *lo = nullptr, *hi = nullptr, *son0 = nullptr, *son1 = nullptr, *parent = nullptr,
+          *tsize = nullptr, *leafidx = nullptr, *bfs = nullptr, *level = nullptr, *leaves = nullptr;
+  int32_t *bptr = nullptr, *bidx = nullptr;  // admissible stored blocks per cluster (CSR of adm slots)
+  int64_t* perm = nullptr;
+  // data
+  int32_t* rank = nullptr;  // k_t
+  double* leafb = nullptr;  // nleaves * lmax * rcap        (V_t, |t| x k_t, ld lmax)
+  double* tr = nullptr;     // nclusters * rcap * rcap       (E_t, k_t x k_parent, ld rcap)
+  double* rc = nullptr;     // nclusters * rcap * rcap       (R-factor of V_t, k_t x k_t padded, ld rcap)
+  // update workspace (indexed by cluster id), ld kcap
+  double* re = nullptr;     // R-factor of the extended basis V~_t         (kcap x kcap)
+  double* bw = nullptr;     // weight B~_t (square padded)                   (kcap x kcap)
+  double* rn = nullptr;     // basis change R_t = Q_t^T V~_t (r_t x K_t)      (kcap x kcap)
+  double* qn = nullptr;     // new leaf basis (lmax x rcap) or Qhat_t (2rcap x rcap), ld max(lmax,2rcap)
+  int32_t* rnew = nullptr;  // new ranks
+  // matvec workspace
+  double* xh = nullptr;     // nclusters * rcap coefficients
+};
+
+// Everything a device kernel needs for one local update (passed by value).
+struct UpdArgs {
+  // row side (A) and column side (B) roots and update rank
+  int t0, s0, k;
+  const double* X;
+  int64_t ldx;
+  const double* Y;
+  int64_t ldy;
+  double alpha;
+  double rel_tol, abs_tol;
+  int max_rank;
+};
+
+struct MatDev {
+  int rcap, ucap, kcap, lmax, ldq;
+  DevSide row, col;
+  int nadm, ninad;
+  int32_t *adm_t = nullptr, *adm_s = nullptr;
+  double* S = nullptr;  // nadm * rcap * rcap (k_t x l_s, ld rcap)
+  int32_t *in_t = nullptr, *in_s = nullptr;
+  double* N = nullptr;  // ninad * lmax * lmax (|t| x |s|, ld lmax)
+  int32_t *nptr = nullptr, *nidx = nullptr;    // inadmissible stored blocks per row leaf (CSR)
+  int32_t *ntptr = nullptr, *ntidx = nullptr;  // inadmissible stored blocks per column leaf (CSR)
+  int32_t* flags = nullptr;
+  double *xt = nullptr, *yt = nullptr;  // tree-order vectors
+};
+
+}  // namespace h2
+
+struct h2_mat_ {
+  h2_btree_* bt = nullptr;
+  bool lower = false;
+  h2::MatDev d;
+  std::vector<int32_t> adm_blk, inad_blk;  // slot -> block id (DFS order)
+  std::vector<int32_t> blk2adm, blk2inad;  // block id -> slot or -1
+  std::vector<int32_t> inad_range;         // per block: [first,last) inadmissible slot in its subtree
+  std::vector<void*> allocs;
+};
+
+namespace h2 {
+void set_error(const std::string& msg);
+
+// launchers (h2_matvec.cu)
+cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const double* x, double beta,
+                          double* y, cudaStream_t st);
+// launchers (h2_update.cu)
+cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a, cudaStream_t st);
+cudaError_t update_init_attributes();
+}  // namespace h2

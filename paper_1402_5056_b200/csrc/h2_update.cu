@@ -1,0 +1,542 @@
+// Local low-rank update Z|_{t0 x s0} += alpha X Y^T on the device (Theorem 1).
+//
+// One update = a short sequence of launches, each covering every cluster of one phase/level of
+// BOTH sides (row basis V/E with subtree root t0, column basis W/F with root s0):
+//   k_upd_ext_leaf     U0 exact nearfield add + U1/U2 leaf R-factors of V~_t = [V_t, X|t]
+//   k_upd_ext_level    U2 R-factors of the extended nested basis, bottom-up ([BO10 Alg.16])
+//   k_upd_weights_path U3 weights B~_t along pred(t0) (root first), TSQR of the stacked
+//                      [R_{W,s} S~_{t,s}^T ; B~_{t+} E~_t^T]
+//   k_upd_weights_level U3 below t0, top-down
+//   k_upd_svd_leaf     U4 leaf SVD of V~_t B~_t^T, rank choice, Q_t, R_t = Q_t^T V~_t
+//   k_upd_svd_level    U4 internal SVD of V^_t B~_t^T, V^_t = [R_{t1}E~_{t1}; R_{t2}E~_{t2}]
+//   k_upd_couple       U5 S_b <- R_t S~_b R_s^T (three cases)
+//   k_upd_install      U6 V_t <- Q_t, E <- F, E_{t0} <- R_{t0}[E_{t0};0], R-cache reset
+//   k_upd_rcache_path  refresh the memoised R-factors of the current bases on pred(t0)
+// Ranks are decided on the device and consumed from device memory (capacity-padded slots), so the
+// host never synchronises inside an update.  One CTA owns one small matrix in shared memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "devla.cuh"
+#include "h2_internal.h"
+
+namespace h2 {
+namespace {
+
+constexpr int NT = NTHREADS;
+constexpr int KC = KCAP_MAX;      // 64
+constexpr int PR = 192;           // TSQR panel rows (>= KC + largest chunk)
+constexpr int LD2 = 2 * KC;       // rows of a stacked pair of KC x KC factors
+
+__device__ __forceinline__ bool inside(const DevSide& D, int t, int root) {
+  return t >= root && t < root + D.tsize[root];
+}
+
+// ---- U0 + U1/U2 leaves -------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_upd_ext_leaf(MatDev M, UpdArgs a, int rl0, int nrl, int cl0, int ncl,
+                                                     int in0, int nin) {
+  extern __shared__ double sm[];
+  const int b = blockIdx.x;
+  if (b < nrl + ncl) {
+    const bool rs = b < nrl;
+    const DevSide& D = rs ? M.row : M.col;
+    const int t = D.leaves[rs ? rl0 + b : cl0 + b - nrl];
+    const int root = rs ? a.t0 : a.s0;
+    const double* Xf = rs ? a.X : a.Y;
+    const int64_t ldx = rs ? a.ldx : a.ldy;
+    const double al = rs ? a.alpha : 1.0;
+    const int m = D.hi[t] - D.lo[t], kt = D.rank[t], K = kt + a.k;
+    const int lda = M.lmax;
+    double* A = sm;                 // lmax x KC
+    double* diag = A + lda * KC;    // KC
+    double* red = diag + KC;        // 1
+    const double* Vb = D.leafb + (size_t)D.leafidx[t] * M.lmax * M.rcap;
+    const int off = D.lo[t] - D.lo[root];
+    for (int e = threadIdx.x; e < m * K; e += NT) {
+      const int i = e % m, j = e / m;
+      A[i + j * lda] = j < kt ? Vb[i + (size_t)j * M.lmax] : al * Xf[off + i + (size_t)(j - kt) * ldx];
+    }
+    __syncthreads();
+    la::cta_qr_R(A, lda, m, K, diag, red);
+    double* RE = D.re + (size_t)t * M.kcap * M.kcap;
+    const int mk = m < K ? m : K;
+    for (int e = threadIdx.x; e < K * K; e += NT) {
+      const int i = e % K, j = e / K;
+      RE[i + j * M.kcap] = i < mk ? A[i + j * lda] : 0.0;
+    }
+    return;
+  }
+  // U0: exact nearfield part N_b += alpha X|t Y|s^T for the inadmissible leaves of T_{b0}
+  const int slot = in0 + (b - nrl - ncl);
+  if (slot >= in0 + nin) return;
+  const int t = M.in_t[slot], s = M.in_s[slot];
+  const int mt = M.row.hi[t] - M.row.lo[t], ms = M.col.hi[s] - M.col.lo[s];
+  const int ot = M.row.lo[t] - M.row.lo[a.t0], os = M.col.lo[s] - M.col.lo[a.s0];
+  double* Na = M.N + (size_t)slot * M.lmax * M.lmax;
+  for (int e = threadIdx.x; e < mt * ms; e += NT) {
+    const int i = e % mt, j = e / mt;
+    double acc = 0.0;
+    for (int q = 0; q < a.k; ++q) acc += a.X[ot + i + (size_t)q * a.ldx] * a.Y[os + j + (size_t)q * a.ldy];
+    Na[i + (size_t)j * M.lmax] += a.alpha * acc;
+  }
+}
+
+// ---- U2 internal, bottom-up ------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_upd_ext_level(MatDev M, UpdArgs a, int bA, int nA, int bB, int nB) {
+  extern __shared__ double sm[];
+  const bool rs = (int)blockIdx.x < nA;
+  const DevSide& D = rs ? M.row : M.col;
+  const int t = D.bfs[rs ? bA + blockIdx.x : bB + blockIdx.x - nA];
+  if (D.son0[t] < 0) return;
+  const int k = a.k, kt = D.rank[t], K = kt + k;
+  double* A = sm;              // LD2 x KC
+  double* diag = A + LD2 * KC;
+  double* red = diag + KC;
+  int row0 = 0;
+  for (int q = 0; q < 2; ++q) {
+    const int c = q ? D.son1[t] : D.son0[t];
+    const int kc = D.rank[c], Kc = kc + k;
+    const double* RE = D.re + (size_t)c * M.kcap * M.kcap;
+    const double* E = D.tr + (size_t)c * M.rcap * M.rcap;  // kc x kt
+    // rows row0..row0+Kc-1:  [ RE[:, :kc] E_c , RE[:, kc:kc+k] ]
+    for (int e = threadIdx.x; e < Kc * K; e += NT) {
+      const int i = e % Kc, j = e / Kc;
+      double v;
+      if (j < kt) {
+        v = 0.0;
+        for (int p = i; p < kc; ++p) v += RE[i + p * M.kcap] * E[p + j * M.rcap];  // RE upper triangular
+      } else {
+        v = RE[i + (kc + j - kt) * M.kcap];
+      }
+      A[row0 + i + j * LD2] = v;
+    }
+    row0 += Kc;
+  }
+  __syncthreads();
+  la::cta_qr_R(A, LD2, row0, K, diag, red);
+  double* RE = D.re + (size_t)t * M.kcap * M.kcap;
+  const int mk = row0 < K ? row0 : K;
+  for (int e = threadIdx.x; e < K * K; e += NT) {
+    const int i = e % K, j = e / K;
+    RE[i + j * M.kcap] = i < mk ? A[i + j * LD2] : 0.0;
+  }
+}
+
+// ---- U3 weights for one cluster t of side A (partner side B) --------------------------------
+__device__ void weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm) {
+  const DevSide& A = rs ? M.row : M.col;
+  const DevSide& B = rs ? M.col : M.row;
+  const int a0 = rs ? a.t0 : a.s0, b0 = rs ? a.s0 : a.t0;
+  const int k = a.k;
+  const bool in_t = inside(A, t, a0);
+  const int kt = A.rank[t];
+  const int K = kt + (in_t ? k : 0);
+  double* P = sm;                 // PR x KC panel
+  double* diag = P + PR * KC;
+  double* red = diag + KC;
+  int rows = 0;
+  auto flush = [&]() {
+    if (rows > 0) {
+      la::cta_qr_R(P, PR, rows, K, diag, red);
+      rows = rows < K ? rows : K;
+    }
+  };
+  for (int q = A.bptr[t]; q < A.bptr[t + 1]; ++q) {
+    const int slot = A.bidx[q];
+    const int s = rs ? M.adm_s[slot] : M.adm_t[slot];
+    const double* Sa = M.S + (size_t)slot * M.rcap * M.rcap;
+    const bool in_s = inside(B, s, b0);
+    const int ls = B.rank[s];
+    const int rc = in_s ? ls + k : ls;
+    if (rc == 0) continue;
+    if (rows + rc > PR) flush();
+    const double* RB = in_s ? B.re + (size_t)s * M.kcap * M.kcap : B.rc + (size_t)s * M.rcap * M.rcap;
+    const int ldR = in_s ? M.kcap : M.rcap;
+    for (int e = threadIdx.x; e < rc * K; e += NT) {
+      const int i = e % rc, c = e / rc;
+      double v = 0.0;
+      if (c < kt) {
+        // (R_B S~^T)(i,c) = sum_j R_B(i,j) S_or(c,j),   S_or = S (row side) or S^T (column side)
+        for (int j = i; j < ls; ++j) v += RB[i + j * ldR] * (rs ? Sa[c + j * M.rcap] : Sa[j + c * M.rcap]);
+      } else if (in_s) {
+        v = RB[i + (ls + c - kt) * ldR];  // identity block of S~ = diag(S, I)
+      }
+      P[rows + i + c * PR] = v;
+    }
+    rows += rc;
+    __syncthreads();
+  }
+  const int p = A.parent[t];
+  if (p >= 0) {
+    const bool in_p = inside(A, p, a0);
+    const int kp = A.rank[p];
+    const int Kp = kp + (in_p ? k : 0);
+    if (Kp > 0) {
+      if (rows + Kp > PR) flush();
+      const double* Bp = A.bw + (size_t)p * M.kcap * M.kcap;
+      const double* E = A.tr + (size_t)t * M.rcap * M.rcap;  // kt x kp
+      for (int e = threadIdx.x; e < Kp * K; e += NT) {
+        const int i = e % Kp, c = e / Kp;
+        double v = 0.0;
+        if (c < kt) {
+          for (int j = 0; j < kp; ++j) v += Bp[i + j * M.kcap] * E[c + j * M.rcap];
+        } else if (in_p) {
+          v = Bp[i + (kp + c - kt) * M.kcap];  // E~_t = diag(E_t, I) inside T_{t0}
+        }                                      // E~_{t0} = [E_{t0}; 0]: zero columns
+        P[rows + i + c * PR] = v;
+      }
+      rows += Kp;
+      __syncthreads();
+    }
+  }
+  flush();
+  double* Bt = A.bw + (size_t)t * M.kcap * M.kcap;
+  for (int e = threadIdx.x; e < K * K; e += NT) {
+    const int i = e % K, j = e / K;
+    Bt[i + j * M.kcap] = i < rows ? P[i + j * PR] : 0.0;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(NT) k_upd_weights_path(MatDev M, UpdArgs a) {
+  extern __shared__ double sm[];
+  const bool rs = blockIdx.x == 0;
+  const DevSide& A = rs ? M.row : M.col;
+  int path[64];
+  int np = 0;
+  for (int t = rs ? a.t0 : a.s0; t >= 0 && np < 64; t = A.parent[t]) path[np++] = t;
+  for (int q = np - 1; q >= 0; --q) weights_cluster(M, a, rs, path[q], sm);
+}
+
+__global__ void __launch_bounds__(NT) k_upd_weights_level(MatDev M, UpdArgs a, int bA, int nA, int bB, int nB) {
+  extern __shared__ double sm[];
+  const bool rs = (int)blockIdx.x < nA;
+  const DevSide& A = rs ? M.row : M.col;
+  const int t = A.bfs[rs ? bA + blockIdx.x : bB + blockIdx.x - nA];
+  weights_cluster(M, a, rs, t, sm);
+}
+
+// ---- U4 truncated nested basis --------------------------------------------------------------
+// Given V (m x K, ldv) in shared memory and B~_t, compute M = V B~^T, its SVD, the rank, Q and R_t.
+__device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, int t, double* V, int ldv, int m,
+                         int K, double* sm_rest) {
+  double* Bt = sm_rest;             // KC x KC
+  double* Mm = Bt + KC * KC;        // 64 x KC (ld 64)
+  double* Q = Mm + 64 * KC;         // 64 x KC (ld 64)
+  double* sig = Q + 64 * KC;        // KC
+  int* order = (int*)(sig + KC);    // KC ints
+  int* scr = order + KC;            // 4 ints
+  const double* Bg = D.bw + (size_t)t * M.kcap * M.kcap;
+  la::cta_copy(Bt, KC, Bg, M.kcap, K, K);
+  __syncthreads();
+  // Mm = V Bt^T  (m x K)
+  la::cta_gemm(Mm, 64, V, ldv, false, Bt, KC, true, m, K, K, false);
+  __syncthreads();
+  la::cta_jacobi(Mm, 64, m, K, sig, order, scr);
+  __shared__ int clamped;
+  if (threadIdx.x == 0) clamped = 0;
+  __syncthreads();
+  const int r = la::trunc_rank(sig, order, K, a.rel_tol, a.abs_tol, a.max_rank, M.rcap, &clamped);
+  // Q(:, q) = Mm(:, order[q]) / sigma
+  for (int e = threadIdx.x; e < m * r; e += NT) {
+    const int i = e % m, q = e / m;
+    const int j = order[q];
+    Q[i + q * 64] = Mm[i + j * 64] / sig[j];
+  }
+  __syncthreads();
+  double* qn = D.qn + (size_t)t * M.ldq * M.rcap;
+  for (int e = threadIdx.x; e < m * r; e += NT) qn[(e % m) + (e / m) * M.ldq] = Q[(e % m) + (e / m) * 64];
+  // R_t = Q^T V  (r x K)
+  double* rn = D.rn + (size_t)t * M.kcap * M.kcap;
+  la::cta_gemm(rn, M.kcap, Q, 64, true, V, ldv, false, r, K, m, false);
+  if (threadIdx.x == 0) {
+    D.rnew[t] = r;
+    if (clamped) atomicOr(M.flags, 1);
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_upd_svd_leaf(MatDev M, UpdArgs a, int rl0, int nrl, int cl0, int ncl) {
+  extern __shared__ double sm[];
+  const bool rs = (int)blockIdx.x < nrl;
+  const DevSide& D = rs ? M.row : M.col;
+  const int t = D.leaves[rs ? rl0 + blockIdx.x : cl0 + blockIdx.x - nrl];
+  const int root = rs ? a.t0 : a.s0;
+  const double* Xf = rs ? a.X : a.Y;
+  const int64_t ldx = rs ? a.ldx : a.ldy;
+  const double al = rs ? a.alpha : 1.0;
+  const int m = D.hi[t] - D.lo[t], kt = D.rank[t], K = kt + a.k;
+  double* V = sm;  // 64 x KC
+  const double* Vb = D.leafb + (size_t)D.leafidx[t] * M.lmax * M.rcap;
+  const int off = D.lo[t] - D.lo[root];
+  for (int e = threadIdx.x; e < m * K; e += NT) {
+    const int i = e % m, j = e / m;
+    V[i + j * 64] = j < kt ? Vb[i + (size_t)j * M.lmax] : al * Xf[off + i + (size_t)(j - kt) * ldx];
+  }
+  __syncthreads();
+  svd_core(M, a, D, t, V, 64, m, K, V + 64 * KC);
+}
+
+__global__ void __launch_bounds__(NT) k_upd_svd_level(MatDev M, UpdArgs a, int bA, int nA, int bB, int nB) {
+  extern __shared__ double sm[];
+  const bool rs = (int)blockIdx.x < nA;
+  const DevSide& D = rs ? M.row : M.col;
+  const int t = D.bfs[rs ? bA + blockIdx.x : bB + blockIdx.x - nA];
+  if (D.son0[t] < 0) return;
+  const int k = a.k, kt = D.rank[t], K = kt + k;
+  double* V = sm;  // 64 x KC : V^_t = [R_{t1} E~_{t1}; R_{t2} E~_{t2}]
+  int row0 = 0;
+  for (int q = 0; q < 2; ++q) {
+    const int c = q ? D.son1[t] : D.son0[t];
+    const int rc = D.rnew[c], kc = D.rank[c];
+    const double* RN = D.rn + (size_t)c * M.kcap * M.kcap;  // rc x (kc + k)
+    const double* E = D.tr + (size_t)c * M.rcap * M.rcap;   // kc x kt
+    for (int e = threadIdx.x; e < rc * K; e += NT) {
+      const int i = e % rc, j = e / rc;
+      double v;
+      if (j < kt) {
+        v = 0.0;
+        for (int p = 0; p < kc; ++p) v += RN[i + p * M.kcap] * E[p + j * M.rcap];
+      } else {
+        v = RN[i + (kc + j - kt) * M.kcap];
+      }
+      V[row0 + i + j * 64] = v;
+    }
+    row0 += rc;
+  }
+  __syncthreads();
+  svd_core(M, a, D, t, V, 64, row0, K, V + 64 * KC);
+}
+
+// ---- U5 couplings ------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_upd_couple(MatDev M, UpdArgs a, int nA, int nB) {
+  extern __shared__ double sm[];
+  double* T1 = sm;             // KC x KC (ld KC)
+  double* Out = T1 + KC * KC;  // KC x KC (ld KC)
+  const int k = a.k;
+  const bool rs = (int)blockIdx.x < nA;
+  if (rs) {
+    const int t = a.t0 + blockIdx.x;
+    const int kt = M.row.rank[t], Kt = kt + k, rt = M.row.rnew[t];
+    const double* RNt = M.row.rn + (size_t)t * M.kcap * M.kcap;  // rt x Kt
+    for (int q = M.row.bptr[t]; q < M.row.bptr[t + 1]; ++q) {
+      const int slot = M.row.bidx[q];
+      const int s = M.adm_s[slot];
+      double* Sa = M.S + (size_t)slot * M.rcap * M.rcap;  // kt x ls
+      const int ls = M.col.rank[s];
+      if (inside(M.col, s, a.s0)) {
+        const int Ls = ls + k, rsn = M.col.rnew[s];
+        const double* RNs = M.col.rn + (size_t)s * M.kcap * M.kcap;  // rsn x Ls
+        // T1 = R_t diag(S, I)  (rt x Ls)
+        for (int e = threadIdx.x; e < rt * Ls; e += NT) {
+          const int i = e % rt, j = e / rt;
+          double v;
+          if (j < ls) {
+            v = 0.0;
+            for (int p = 0; p < kt; ++p) v += RNt[i + p * M.kcap] * Sa[p + j * M.rcap];
+          } else {
+            v = RNt[i + (kt + j - ls) * M.kcap];
+          }
+          T1[i + j * KC] = v;
+        }
+        __syncthreads();
+        la::cta_gemm(Out, KC, T1, KC, false, RNs, M.kcap, true, rt, rsn, Ls, false);
+        __syncthreads();
+        la::cta_copy(Sa, M.rcap, Out, KC, rt, rsn);
+      } else {
+        // S <- R_t [S; 0] = R_t(:, :kt) S
+        la::cta_gemm(Out, KC, RNt, M.kcap, false, Sa, M.rcap, false, rt, ls, kt, false);
+        __syncthreads();
+        la::cta_copy(Sa, M.rcap, Out, KC, rt, ls);
+      }
+      __syncthreads();
+    }
+  } else {
+    const int s = a.s0 + (blockIdx.x - nA);
+    const int ls = M.col.rank[s], rsn = M.col.rnew[s];
+    const double* RNs = M.col.rn + (size_t)s * M.kcap * M.kcap;  // rsn x (ls + k)
+    for (int q = M.col.bptr[s]; q < M.col.bptr[s + 1]; ++q) {
+      const int slot = M.col.bidx[q];
+      const int t = M.adm_t[slot];
+      if (inside(M.row, t, a.t0)) continue;  // handled by the row-side CTA
+      double* Sa = M.S + (size_t)slot * M.rcap * M.rcap;
+      const int kt = M.row.rank[t];
+      // S <- [S, 0] R_s^T = S R_s(:, :ls)^T
+      la::cta_gemm(Out, KC, Sa, M.rcap, false, RNs, M.kcap, true, kt, rsn, ls, false);
+      __syncthreads();
+      la::cta_copy(Sa, M.rcap, Out, KC, kt, rsn);
+      __syncthreads();
+    }
+  }
+}
+
+// ---- U6 install --------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_upd_install(MatDev M, UpdArgs a, int nA, int nB) {
+  extern __shared__ double sm[];
+  const bool rs = (int)blockIdx.x < nA;
+  const DevSide& D = rs ? M.row : M.col;
+  const int root = rs ? a.t0 : a.s0;
+  const int t = root + (rs ? blockIdx.x : blockIdx.x - nA);
+  const int r = D.rnew[t];
+  const double* qn = D.qn + (size_t)t * M.ldq * M.rcap;
+  if (D.son0[t] < 0) {
+    const int m = D.hi[t] - D.lo[t];
+    double* Vb = D.leafb + (size_t)D.leafidx[t] * M.lmax * M.rcap;
+    la::cta_copy(Vb, M.lmax, qn, M.ldq, m, r);
+  } else {
+    const int c0 = D.son0[t], c1 = D.son1[t];
+    const int r0 = D.rnew[c0], r1 = D.rnew[c1];
+    la::cta_copy(D.tr + (size_t)c0 * M.rcap * M.rcap, M.rcap, qn, M.ldq, r0, r);
+    la::cta_copy(D.tr + (size_t)c1 * M.rcap * M.rcap, M.rcap, qn + r0, M.ldq, r1, r);
+  }
+  if (t == root && D.parent[t] >= 0) {
+    // E_{t0} <- R_{t0} [E_{t0}; 0] = R_{t0}(:, :k_{t0}) E_{t0}
+    const int kold = D.rank[t], kp = D.rank[D.parent[t]];
+    double* E = D.tr + (size_t)t * M.rcap * M.rcap;
+    const double* RN = D.rn + (size_t)t * M.kcap * M.kcap;
+    la::cta_gemm(sm, KC, RN, M.kcap, false, E, M.rcap, false, r, kp, kold, false);
+    __syncthreads();
+    la::cta_copy(E, M.rcap, sm, KC, r, kp);
+  }
+  // the new basis is orthonormal: its R-factor is the identity
+  double* rc = D.rc + (size_t)t * M.rcap * M.rcap;
+  for (int e = threadIdx.x; e < r * r; e += NT) rc[(e % r) + (e / r) * M.rcap] = (e % r) == (e / r) ? 1.0 : 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) D.rank[t] = r;
+}
+
+// ---- memoised R-factors on pred(t0) ----------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_upd_rcache_path(MatDev M, UpdArgs a) {
+  extern __shared__ double sm[];
+  const bool rs = blockIdx.x == 0;
+  const DevSide& D = rs ? M.row : M.col;
+  double* A = sm;  // LD2 x KC
+  double* diag = A + LD2 * KC;
+  double* red = diag + KC;
+  for (int t = D.parent[rs ? a.t0 : a.s0]; t >= 0; t = D.parent[t]) {
+    const int kt = D.rank[t];
+    int row0 = 0;
+    for (int q = 0; q < 2; ++q) {
+      const int c = q ? D.son1[t] : D.son0[t];
+      const int kc = D.rank[c];
+      const double* RC = D.rc + (size_t)c * M.rcap * M.rcap;
+      const double* E = D.tr + (size_t)c * M.rcap * M.rcap;
+      for (int e = threadIdx.x; e < kc * kt; e += NT) {
+        const int i = e % kc, j = e / kc;
+        double v = 0.0;
+        for (int p = i; p < kc; ++p) v += RC[i + p * M.rcap] * E[p + j * M.rcap];
+        A[row0 + i + j * LD2] = v;
+      }
+      row0 += kc;
+    }
+    __syncthreads();
+    if (kt > 0) la::cta_qr_R(A, LD2, row0, kt, diag, red);
+    double* RC = D.rc + (size_t)t * M.rcap * M.rcap;
+    const int mk = row0 < kt ? row0 : kt;
+    for (int e = threadIdx.x; e < kt * kt; e += NT) {
+      const int i = e % kt, j = e / kt;
+      RC[i + j * M.rcap] = i < mk ? A[i + j * LD2] : 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+constexpr size_t SM_EXT_LEAF = (size_t)(LMAX_MAX * KC + KC + 8) * 8;
+constexpr size_t SM_EXT_LEVEL = (size_t)(LD2 * KC + KC + 8) * 8;
+constexpr size_t SM_WEIGHTS = (size_t)(PR * KC + KC + 8) * 8;
+constexpr size_t SM_SVD = (size_t)(64 * KC + KC * KC + 64 * KC + 64 * KC + KC + KC) * 8 + 64;
+constexpr size_t SM_COUPLE = (size_t)(2 * KC * KC) * 8;
+constexpr size_t SM_INSTALL = (size_t)(KC * KC) * 8;
+
+bool g_attr_done = false;
+
+// clusters of `T` at level L inside the subtree of root: contiguous segment of the BFS list
+void level_segment(const h2_tree_* T, int root, int L, int* begin, int* count) {
+  *begin = 0;
+  *count = 0;
+  if (L > T->depth || L < T->level[root]) return;
+  const int* b = T->bfs.data() + T->level_ptr[L];
+  const int* e = T->bfs.data() + T->level_ptr[L + 1];
+  const int* lo = std::lower_bound(b, e, root);
+  const int* hi = std::lower_bound(b, e, root + T->tsize[root]);
+  *begin = (int)(lo - T->bfs.data());
+  *count = (int)(hi - lo);
+}
+
+void leaf_range(const h2_tree_* T, int root, int* begin, int* count) {
+  const auto b = T->leaves.begin(), e = T->leaves.end();
+  const auto lo = std::lower_bound(b, e, root);
+  const auto hi = std::lower_bound(b, e, root + T->tsize[root]);
+  *begin = (int)(lo - b);
+  *count = (int)(hi - lo);
+}
+
+}  // namespace
+
+cudaError_t update_init_attributes() {
+  if (g_attr_done) return cudaSuccess;
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_upd_ext_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXT_LEAF))) return e;
+  if ((e = cudaFuncSetAttribute(k_upd_ext_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXT_LEVEL))) return e;
+  if ((e = cudaFuncSetAttribute(k_upd_weights_path, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_WEIGHTS))) return e;
+  if ((e = cudaFuncSetAttribute(k_upd_weights_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_WEIGHTS))) return e;
+  if ((e = cudaFuncSetAttribute(k_upd_svd_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_SVD))) return e;
+  if ((e = cudaFuncSetAttribute(k_upd_svd_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_SVD))) return e;
+  if ((e = cudaFuncSetAttribute(k_upd_couple, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_COUPLE))) return e;
+  if ((e = cudaFuncSetAttribute(k_upd_install, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_INSTALL))) return e;
+  if ((e = cudaFuncSetAttribute(k_upd_rcache_path, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXT_LEVEL))) return e;
+  g_attr_done = true;
+  return cudaSuccess;
+}
+
+cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a, cudaStream_t st) {
+  cudaError_t e = update_init_attributes();
+  if (e != cudaSuccess) return e;
+  const MatDev& M = Z->d;
+  const h2_btree_* B = Z->bt;
+  const h2_tree_* R = B->rt;
+  const h2_tree_* C = B->ct;
+  const int b0 = B->find(a.t0, a.s0);
+  const int in0 = Z->inad_range[2 * b0], nin = Z->inad_range[2 * b0 + 1] - in0;
+  if (B->kind[b0] == INADM) {  // dense add only
+    if (nin > 0) k_upd_ext_leaf<<<nin, NT, SM_EXT_LEAF, st>>>(M, a, 0, 0, 0, 0, in0, nin);
+    return cudaGetLastError();
+  }
+  int rl0, nrl, cl0, ncl;
+  leaf_range(R, a.t0, &rl0, &nrl);
+  leaf_range(C, a.s0, &cl0, &ncl);
+  k_upd_ext_leaf<<<nrl + ncl + nin, NT, SM_EXT_LEAF, st>>>(M, a, rl0, nrl, cl0, ncl, in0, nin);
+  const int Lr = R->level[a.t0], Lc = C->level[a.s0];
+  const int Lmax = std::max(R->depth, C->depth), Lmin = std::min(Lr, Lc);
+  // U2 bottom-up (internal clusters)
+  for (int L = Lmax - 1; L >= Lmin; --L) {
+    int bA, nA, bB, nB;
+    level_segment(R, a.t0, L, &bA, &nA);
+    level_segment(C, a.s0, L, &bB, &nB);
+    if (nA + nB > 0) k_upd_ext_level<<<nA + nB, NT, SM_EXT_LEVEL, st>>>(M, a, bA, nA, bB, nB);
+  }
+  // U3 weights: path (root .. t0), then the subtree top-down
+  k_upd_weights_path<<<2, NT, SM_WEIGHTS, st>>>(M, a);
+  for (int L = Lmin + 1; L <= Lmax; ++L) {
+    int bA = 0, nA = 0, bB = 0, nB = 0;
+    if (L > Lr) level_segment(R, a.t0, L, &bA, &nA);
+    if (L > Lc) level_segment(C, a.s0, L, &bB, &nB);
+    if (nA + nB > 0) k_upd_weights_level<<<nA + nB, NT, SM_WEIGHTS, st>>>(M, a, bA, nA, bB, nB);
+  }
+  // U4 bottom-up
+  k_upd_svd_leaf<<<nrl + ncl, NT, SM_SVD, st>>>(M, a, rl0, nrl, cl0, ncl);
+  for (int L = Lmax - 1; L >= Lmin; --L) {
+    int bA, nA, bB, nB;
+    level_segment(R, a.t0, L, &bA, &nA);
+    level_segment(C, a.s0, L, &bB, &nB);
+    if (nA + nB > 0) k_upd_svd_level<<<nA + nB, NT, SM_SVD, st>>>(M, a, bA, nA, bB, nB);
+  }
+  // U5, U6, R-cache refresh
+  const int nA = R->tsize[a.t0], nB = C->tsize[a.s0];
+  k_upd_couple<<<nA + nB, NT, SM_COUPLE, st>>>(M, a, nA, nB);
+  k_upd_install<<<nA + nB, NT, SM_INSTALL, st>>>(M, a, nA, nB);
+  k_upd_rcache_path<<<2, NT, SM_EXT_LEVEL, st>>>(M, a);
+  return cudaGetLastError();
+}
+
+}  // namespace h2

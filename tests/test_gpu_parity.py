@@ -1,0 +1,142 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Bars (north_star / SURVEY §8(c).4):
+  * structure and ranks chosen: bit-exact (ranks compared after every update);
+  * operators on 16 seeded probe vectors: relative 2-norm difference <= 1e-9 for fixed-rank
+    runs, <= 10 * eps_trunc for adaptive runs (both sides also agree far tighter in practice; the
+    measured value is printed);
+  * matvec of an exactly represented matrix (h2_from_sparse, rank 0): <= 1e-13 (pure rounding of
+    the same dot products in a different order).
+"""
+import numpy as np
+import pytest
+
+from inputs.updates import c1_stream, c0_global_factors, mixed_stream
+from oracle.update import Updater, Trunc as OTrunc
+from oracle.dense import densify
+from h2util import setup, adm_targets, all_targets, operator_rel_diff, gpu_apply
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+import paper_1402_5056_b200 as P  # noqa: E402
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("name,N", [("C0", None), ("C1", None), ("C2", 128), ("C3", 16)])
+def test_matvec_from_sparse(name, N):
+    s = setup(name, N)
+    A = s["c"]["A"]
+    n = A.shape[0]
+    X = np.random.default_rng(1).standard_normal((n, 4))
+    Y = gpu_apply(s["Z"], X)
+    ref = A @ X
+    assert np.linalg.norm(Y - ref) / np.linalg.norm(ref) < 1e-13
+    # transpose + alpha/beta
+    x = _t(X[:, 0])
+    y = _t(X[:, 1])
+    P.h2_matvec(s["Z"], x, y, alpha=2.0, beta=-0.5, transpose=True)
+    ref = 2.0 * (A.T @ X[:, 0]) - 0.5 * X[:, 1]
+    assert np.linalg.norm(y.cpu().numpy() - ref) / np.linalg.norm(ref) < 1e-13
+    kr, kc = P.h2_ranks(s["Z"])
+    assert kr.sum() == 0 and kc.sum() == 0
+
+
+def _run_pair(s, updates, trunc, check_every=1, tol=None, alpha=1.0):
+    """Apply the same update sequence to the oracle and the GPU; compare ranks and operators."""
+    OZ, ot, Z = s["OZ"], s["ot"], s["Z"]
+    up = Updater(OZ, OTrunc(trunc.rel_tol, trunc.abs_tol, trunc.max_rank))
+    worst = 0.0
+    keep = []
+    for i, (t0, s0, X, Y) in enumerate(updates):
+        up(t0, s0, X, Y, alpha=alpha)
+        keep.append(P.h2_lowrank_update(Z, t0, s0, _t(X), _t(Y), alpha=alpha, trunc=trunc))
+        if (i + 1) % check_every == 0 or i + 1 == len(updates):
+            kr, kc = P.h2_ranks(Z)
+            np.testing.assert_array_equal(kr, OZ.k, err_msg=f"row ranks differ after update {i}")
+            np.testing.assert_array_equal(kc, OZ.l, err_msg=f"col ranks differ after update {i}")
+            d = operator_rel_diff(Z, OZ, ot.n)
+            worst = max(worst, d)
+            if tol is not None:
+                assert d <= tol, f"operator differs by {d:.3e} after update {i}"
+            keep.clear()
+    assert P.h2_check_device_flags(Z) == 0
+    return worst
+
+
+def test_update_mixed_targets_c0_adaptive():
+    s = setup("C0")
+    ups = mixed_stream(all_targets(s["ot"], s["ob"]), 40, kmax=8, seed=3)
+    w = _run_pair(s, ups, P.Trunc(1e-4), tol=10 * 1e-4)
+    print("C0 mixed adaptive worst rel diff", w)
+    assert w < 1e-9  # observed agreement (the bar above is 10 eps)
+
+
+def test_update_exact_no_truncation():
+    s = setup("C0")
+    ups = mixed_stream(all_targets(s["ot"], s["ob"]), 12, kmax=3, seed=5)
+    w = _run_pair(s, ups, P.Trunc(0.0, 0.0, 0), tol=1e-9)
+    print("C0 exact worst rel diff", w)
+
+
+def test_c0_exact_rank8_pin_gpu():
+    """SURVEY R15 pin on the GPU: rank 8 wherever row*/col* is non-empty, operator = A + P_adm(XY^T)/n."""
+    s = setup("C0")
+    ot, ob = s["ot"], s["ob"]
+    n = ot.n
+    X, Y = c0_global_factors(n)
+    Xt, Yt = X[ot.perm], Y[ot.perm]
+    ups = [(int(ob.t[b]), int(ob.s[b]), Xt[ot.lo[ob.t[b]]:ot.hi[ob.t[b]]], Yt[ot.lo[ob.s[b]]:ot.hi[ob.s[b]]])
+           for b in ob.adm]
+    w = _run_pair(s, ups, P.Trunc(1e-4), check_every=66, tol=1e-12, alpha=1.0 / n)
+    kr, kc = P.h2_ranks(s["Z"])
+    for t in range(ot.nclusters):
+        has_row = any(ob.row[p] for p in ot.pred(t))
+        assert kr[t] == (8 if has_row else 0)
+    print("C0 rank-8 pin worst rel diff", w)
+
+
+@pytest.mark.parametrize("ku", [4, 8, 16, 32])
+def test_c1_fixed_rank_chain(ku):
+    """C1 protocol (R16) at fixed rank 16, shortened to 150 updates per k_u for the test."""
+    s = setup("C1")
+    ups = c1_stream(adm_targets(s["ot"], s["ob"]), 150, ku, seed=0)
+    w = _run_pair(s, ups, P.Trunc(1e-12, 0.0, 16), check_every=25, tol=1e-9)
+    print(f"C1 k_u={ku} worst rel diff", w)
+
+
+def test_update_global_root_and_edge_cases():
+    s = setup("C0")
+    Z, ot = s["Z"], s["ot"]
+    n = ot.n
+    rng = np.random.default_rng(8)
+    # k = 0 is a no-op; invalid block / capacity errors leave Z untouched
+    before = gpu_apply(Z, np.eye(n)[:, :3])
+    P.h2_lowrank_update(Z, 0, 0, _t(np.zeros((n, 0))), _t(np.zeros((n, 0))))
+    with pytest.raises(P.H2Error) as e:
+        P.h2_lowrank_update(Z, 1, 40, _t(np.zeros((ot.size(1), 1))), _t(np.zeros((ot.size(40), 1))))
+    assert e.value.status == "H2_ERR_ARG"
+    with pytest.raises(P.H2Error) as e:
+        P.h2_lowrank_update(Z, 0, 0, _t(np.zeros((n, 40))), _t(np.zeros((n, 40))))
+    assert e.value.status == "H2_ERR_SHAPE"
+    np.testing.assert_array_equal(before, gpu_apply(Z, np.eye(n)[:, :3]))
+    # global update t0 = s0 = root followed by local ones
+    ups = [(0, 0, rng.standard_normal((n, 6)), rng.standard_normal((n, 6)))]
+    ups += mixed_stream(all_targets(ot, s["ob"]), 10, kmax=5, seed=11)
+    w = _run_pair(s, ups, P.Trunc(1e-6), tol=1e-5)
+    print("global+local worst", w)
+
+
+def test_mutation_is_detected():
+    """The parity checker must fail on a corrupted coupling."""
+    s = setup("C0")
+    ups = mixed_stream(all_targets(s["ot"], s["ob"]), 6, kmax=4, seed=2)
+    _run_pair(s, ups, P.Trunc(1e-4))
+    OZ = s["OZ"]
+    b = next(iter(k for k, v in OZ.S.items() if v.size))
+    OZ.S[b] = OZ.S[b] + 1e-3
+    assert operator_rel_diff(s["Z"], OZ, s["ot"].n) > 1e-9
