@@ -144,6 +144,16 @@ h2_status h2_export(h2_mat Z, double* V, double* E, double* W, double* F, double
  * the last call; the flag is cleared.  Synchronizes the stream. */
 h2_status h2_check_device_flags(h2_mat Z, int32_t* flags);
 
+/* Profiling hook (bench/test only; off by default).  h2_profile_enable(1) synchronizes the
+ * device, clears the counters and brackets every later library launch with cudaEventRecord on
+ * the launch stream; kernels also add their algorithmic flops and bytes (fixed formulas,
+ * SURVEY §8(d)) to device counters.  h2_profile_read synchronizes and returns, per kernel kind
+ * (*count entries): a 32-byte NUL-terminated name in names[32*i], the number of launches, the
+ * summed event time in ms, and the counted flops and bytes.  Any output pointer may be NULL. */
+h2_status h2_profile_enable(int32_t on);
+h2_status h2_profile_read(char* names, int64_t* launches, double* ms_total, double* flops, double* bytes,
+                          int32_t* count);
+
 void h2_mat_destroy(h2_mat Z);
 const char* h2_last_error(void);
 

@@ -23,6 +23,8 @@ from .h2 import (  # noqa: F401
     h2_storage_report,
     h2_export,
     h2_check_device_flags,
+    h2_profile_enable,
+    h2_profile_read,
     library_path,
     EXPORTED_SYMBOLS,
 )

@@ -1,6 +1,6 @@
 """Build the in-tree C-ABI shared library libh2b200.so for sm_100a (B200).
 
-    python -m paper_1402_5056_b200.build
+    python paper_1402_5056_b200/build.py
 
 nvcc cross-compiles without a GPU.  Host code is compiled with -ffp-contract=off so that the
 structure predicates are evaluated exactly as written.
@@ -12,8 +12,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libh2b200.so")
-SOURCES = ["h2_host.cpp", "h2_matvec.cu", "h2_update.cu"]
-HEADERS = ["h2_internal.h", "devla.cuh", os.path.join("..", "..", "include", "h2.h")]
+SOURCES = ["h2_host.cpp", "h2_prof.cpp", "h2_matvec.cu", "h2_update.cu"]
+HEADERS = ["h2_internal.h", "h2_prof.h", "devla.cuh", os.path.join("..", "..", "include", "h2.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -20,12 +20,99 @@ __device__ __forceinline__ unsigned group_mask(int S) {
   return ((1u << S) - 1u) << (lane & ~(S - 1));
 }
 
+// Warp-level Householder QR (one warp, no block barriers): lanes own rows (row i = lane + 32 q,
+// q < ceil(m/32) <= 6), so every dot product is one 5-step butterfly; the Householder vector
+// v = a_j[j:] - alpha e_1 stays in registers.  a_c <- a_c - (v^T a_c / (|a_j|^2 - alpha a_jj)) v.
+// Leaves R in the upper triangle of the first min(m,n) rows, except the diagonal which is
+// written to diag[] (strictly-lower part keeps the reflector data).  m <= 192.
+__device__ __forceinline__ double warp_allsum(double p) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+  return p;
+}
+
+__device__ void warp_qr_R(double* A, int lda, int m, int n, double* diag) {
+  const int lane = threadIdx.x & 31;
+  const int RP = (m + 31) >> 5;
+  const int jmax = m < n ? m : n;
+  for (int j = 0; j < jmax; ++j) {
+    double v[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      const int i = lane + 32 * q;
+      v[q] = (q < RP && i >= j && i < m) ? A[i + j * lda] : 0.0;
+    }
+    double p = 0.0;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) p += v[q] * v[q];
+    const double nrm2 = warp_allsum(p);
+    const double ajj = A[j + j * lda];
+    if (!(nrm2 > 0.0)) {
+      if (lane == 0) diag[j] = 0.0;
+      __syncwarp();
+      continue;
+    }
+    const double nrm = sqrt(nrm2);
+    const double alpha = ajj > 0.0 ? -nrm : nrm;
+    const double inv_h = 1.0 / (nrm2 - alpha * ajj);
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+      if (lane + 32 * q == j) v[q] = ajj - alpha;
+    int c = j + 1;
+    for (; c + 1 < n; c += 2) {
+      double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        if (q < RP) {
+          const int i = lane + 32 * q;
+          if (i < m) {
+            p0 += v[q] * A[i + c * lda];
+            p1 += v[q] * A[i + (c + 1) * lda];
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+        p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+      }
+      const double f0 = p0 * inv_h, f1 = p1 * inv_h;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        if (q < RP) {
+          const int i = lane + 32 * q;
+          if (i < m && i >= j) {
+            A[i + c * lda] -= f0 * v[q];
+            A[i + (c + 1) * lda] -= f1 * v[q];
+          }
+        }
+      }
+    }
+    if (c < n) {
+      double p0 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+        if (q < RP && lane + 32 * q < m) p0 += v[q] * A[lane + 32 * q + c * lda];
+      p0 = warp_allsum(p0);
+      const double f0 = p0 * inv_h;
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int i = lane + 32 * q;
+        if (q < RP && i < m && i >= j) A[i + c * lda] -= f0 * v[q];
+      }
+    }
+    if (lane == 0) diag[j] = alpha;
+    __syncwarp();
+  }
+}
+
 // In-place Householder QR of the m x n column-major matrix A (lda) in shared memory; on return
 // the first min(m,n) rows hold R (upper trapezoidal, strictly-lower part zeroed).  Only the
 // R-factor is needed by the method ("P_t ... are not computed").
-// One reduction per column: all dots d_c = a_j[j:]^T a_c[j:] are formed together, and with
-// v = a_j[j:] - alpha e_1:  v^T a_c = d_c - alpha a_jc,  v^T v / 2 = |a_j|^2 - alpha a_jj.
-// red: >= 1 double of shared scratch; diag: >= min(m,n) doubles of shared scratch.
+// One reduction per column: all dots d_c = a_j[j:]^T a_c[j:] are formed together (S lanes per
+// column, butterfly within the lane group), and with v = a_j[j:] - alpha e_1:
+// v^T a_c = d_c - alpha a_jc,  v^T v / 2 = |a_j|^2 - alpha a_jj.
+// (A one-warp variant, warp_qr_R above, measured ~2x slower on B200: serial shuffle chains.)
 __device__ void cta_qr_R(double* A, int lda, int m, int n, double* diag, double* red) {
   const int tid = threadIdx.x, nt = blockDim.x;
   int npow = 1;
@@ -36,6 +123,7 @@ __device__ void cta_qr_R(double* A, int lda, int m, int n, double* diag, double*
   const int c = tid / S, sl = tid % S;
   const unsigned gm = group_mask(S);
   const int jmax = m < n ? m : n;
+  __syncthreads();
   for (int j = 0; j < jmax; ++j) {
     double part = 0.0;
     if (c >= j && c < n)
@@ -64,7 +152,6 @@ __device__ void cta_qr_R(double* A, int lda, int m, int n, double* diag, double*
     }
     __syncthreads();
   }
-  // write R: rows < jmax
   for (int e = tid; e < jmax * n; e += nt) {
     const int i = e % jmax, cc = e / jmax;
     if (cc < i) A[i + cc * lda] = 0.0;
@@ -110,9 +197,11 @@ __device__ void cta_jacobi(double* M, int ldm, int m, int p, double* sig, int* o
   if (G > 32) G = 32;
   if (G < 1) G = 1;
   const int q = tid / G, g = tid % G;
-  const double tol = 1e-15;
+  // stop when every pair satisfies |a_i^T a_j| <= m eps |a_i| |a_j| (compared in squares)
+  const double tol = (m > 8 ? m : 8) * 2.220446049250313e-16;
+  const double tol2 = tol * tol;
   const int nr = pp - 1;  // rounds per sweep
-  for (int sweep = 0; sweep < 60 && p > 1; ++sweep) {
+  for (int sweep = 0; sweep < 40 && p > 1; ++sweep) {
     if (tid == 0) scratch[0] = 0;
     __syncthreads();
     for (int r = 0; r < nr; ++r) {
@@ -140,7 +229,7 @@ __device__ void cta_jacobi(double* M, int ldm, int m, int p, double* sig, int* o
         be += __shfl_xor_sync(0xffffffffu, be, o);
         ga += __shfl_xor_sync(0xffffffffu, ga, o);
       }
-      if (a >= 0 && ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+      if (a >= 0 && ga != 0.0 && ga * ga > tol2 * al * be) {
         const double zeta = (be - al) / (2.0 * ga);
         double t;
         if (fabs(zeta) > 1e150) t = 0.5 / zeta;

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/h2.h"
+#include "h2_prof.h"
 
 namespace h2 {
 
@@ -86,6 +87,7 @@ struct UpdArgs {
   double alpha;
   double rel_tol, abs_tol;
   int max_rank;
+  double* prof;  // device flop/byte counters (profiling) or nullptr
 };
 
 struct MatDev {

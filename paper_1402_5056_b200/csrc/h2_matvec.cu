@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) k_leaf_out(
     const int32_t* __restrict__ npartner, const int32_t* __restrict__ lo_s, const int32_t* __restrict__ hi_s,
     const double* __restrict__ N, int lmax, int rcap, int transpose, const double* __restrict__ yh,
     const double* __restrict__ xt, const int64_t* __restrict__ perm_d, double alpha, double beta,
-    double* __restrict__ y) {
+    double* __restrict__ y, double* __restrict__ prof) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= nleaves) return;
@@ -172,6 +172,16 @@ __global__ void __launch_bounds__(256) k_leaf_out(
       }
     }
   }
+  if (prof && lane == 0) {
+    // algorithmic bytes: leaf basis m x k_t, every nearfield tile, x|t (read once), y|t written (+read)
+    double bytes = 8.0 * ((double)m * kt + m * (beta == 0.0 ? 1 : 2) + m);
+    for (int q = nptr[t]; q < nptr[t + 1]; ++q) {
+      const int s = npartner[nidx[q]];
+      bytes += 8.0 * m * (hi_s[s] - lo_s[s]);
+    }
+    atomicAdd(prof + 2 * K_MV_LEAF_OUT + 1, bytes);
+    atomicAdd(prof + 2 * K_MV_LEAF_OUT, 2.0 * bytes / 8.0);
+  }
   if (lane < m) {
     const int64_t o = perm_d[lo_d[t] + lane];
     y[o] = beta == 0.0 ? alpha * a0 : alpha * a0 + beta * y[o];
@@ -194,34 +204,41 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   const h2_tree_* Ts = src.tree;
   const h2_tree_* Td = dst.tree;
   const int64_t n = Ts->n;
-  k_gather<<<cdiv(n, 256), 256, 0, st>>>(x, src.perm, M.xt, n);
+  double* prof = prof_dev();
+  H2_LAUNCH(K_MV_GATHER, st, k_gather<<<cdiv(n, 256), 256, 0, st>>>(x, src.perm, M.xt, n));
   // forward transform: leaves (all levels), then internal clusters deepest level first
-  k_fwd_leaf<<<cdiv((long long)src.nleaves * 32, 256), 256, 0, st>>>(
-      src.leaves, src.nleaves, src.lo, src.hi, src.leafidx, src.rank, src.leafb, M.lmax, M.rcap, M.xt, src.xh);
+  H2_LAUNCH(K_MV_FWD_LEAF, st,
+            k_fwd_leaf<<<cdiv((long long)src.nleaves * 32, 256), 256, 0, st>>>(
+                src.leaves, src.nleaves, src.lo, src.hi, src.leafidx, src.rank, src.leafb, M.lmax, M.rcap, M.xt,
+                src.xh));
   for (int L = Ts->depth - 1; L >= 0; --L) {
     const int b = Ts->level_ptr[L], e = Ts->level_ptr[L + 1];
     if (e > b)
-      k_fwd_level<<<cdiv((long long)(e - b) * M.rcap, 256), 256, 0, st>>>(src.bfs + b, e - b, src.son0, src.son1,
-                                                                          src.rank, src.tr, M.rcap, src.xh);
+      H2_LAUNCH(K_MV_FWD_LEVEL, st,
+                k_fwd_level<<<cdiv((long long)(e - b) * M.rcap, 256), 256, 0, st>>>(
+                    src.bfs + b, e - b, src.son0, src.son1, src.rank, src.tr, M.rcap, src.xh));
   }
   // couplings
-  k_couple<<<cdiv((long long)Td->nclusters * 32, 256), 256, 0, st>>>(
-      Td->nclusters, dst.bptr, dst.bidx, transpose ? M.adm_t : M.adm_s, dst.rank, src.rank, M.S, M.rcap, transpose,
-      src.xh, dst.xh);
+  H2_LAUNCH(K_MV_COUPLE, st,
+            k_couple<<<cdiv((long long)Td->nclusters * 32, 256), 256, 0, st>>>(
+                Td->nclusters, dst.bptr, dst.bidx, transpose ? M.adm_t : M.adm_s, dst.rank, src.rank, M.S, M.rcap,
+                transpose, src.xh, dst.xh));
   // backward transform
   for (int L = 1; L <= Td->depth; ++L) {
     const int b = Td->level_ptr[L], e = Td->level_ptr[L + 1];
     if (e > b)
-      k_bwd_level<<<cdiv((long long)(e - b) * M.rcap, 256), 256, 0, st>>>(dst.bfs + b, e - b, dst.parent, dst.rank,
-                                                                          dst.tr, M.rcap, dst.xh);
+      H2_LAUNCH(K_MV_BWD_LEVEL, st,
+                k_bwd_level<<<cdiv((long long)(e - b) * M.rcap, 256), 256, 0, st>>>(
+                    dst.bfs + b, e - b, dst.parent, dst.rank, dst.tr, M.rcap, dst.xh));
   }
   // leaves + nearfield + scatter
   const int32_t* np = transpose ? M.ntptr : M.nptr;
   const int32_t* ni = transpose ? M.ntidx : M.nidx;
   const int32_t* npart = transpose ? M.in_t : M.in_s;
-  k_leaf_out<<<cdiv((long long)dst.nleaves * 32, 256), 256, 0, st>>>(
-      dst.leaves, dst.nleaves, dst.lo, dst.hi, dst.leafidx, dst.rank, dst.leafb, np, ni, npart, src.lo, src.hi, M.N,
-      M.lmax, M.rcap, transpose, dst.xh, M.xt, dst.perm, alpha, beta, y);
+  H2_LAUNCH(K_MV_LEAF_OUT, st,
+            k_leaf_out<<<cdiv((long long)dst.nleaves * 32, 256), 256, 0, st>>>(
+                dst.leaves, dst.nleaves, dst.lo, dst.hi, dst.leafidx, dst.rank, dst.leafb, np, ni, npart, src.lo,
+                src.hi, M.N, M.lmax, M.rcap, transpose, dst.xh, M.xt, dst.perm, alpha, beta, y, prof));
   return cudaGetLastError();
 }
 

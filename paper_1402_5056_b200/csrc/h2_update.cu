@@ -33,11 +33,25 @@ __device__ __forceinline__ bool inside(const DevSide& D, int t, int root) {
   return t >= root && t < root + D.tsize[root];
 }
 
-// ---- U0 + U1/U2 leaves -------------------------------------------------------------------------
+__device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm, int mode);
+
+// ---- U0 + U1/U2 leaves + local weight stacks of the ancestors (all independent) ---------------
 __global__ void __launch_bounds__(NT) k_upd_ext_leaf(MatDev M, UpdArgs a, int rl0, int nrl, int cl0, int ncl,
-                                                     int in0, int nin) {
+                                                     int in0, int nin, int npA, int npB) {
   extern __shared__ double sm[];
   const int b = blockIdx.x;
+  if (b >= nrl + ncl + nin) {
+    // U3 (part): C_a = R(local stack) for the proper ancestors a of t0 (side A) / s0 (side B)
+    const int j = b - (nrl + ncl + nin);
+    const bool rs = j < npA;
+    const DevSide& D = rs ? M.row : M.col;
+    int t = rs ? a.t0 : a.s0;
+    const int lev = rs ? j : j - npA;  // ancestor at this level
+    for (int up = (rs ? npA : npB) - lev; up > 0; --up) t = D.parent[t];
+    const double fl = weights_cluster(M, a, rs, t, sm, 1 /*W_LOCAL*/);
+    if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_W_PATH, fl);
+    return;
+  }
   if (b < nrl + ncl) {
     const bool rs = b < nrl;
     const DevSide& D = rs ? M.row : M.col;
@@ -65,6 +79,7 @@ __global__ void __launch_bounds__(NT) k_upd_ext_leaf(MatDev M, UpdArgs a, int rl
       const int i = e % K, j = e / K;
       RE[i + j * M.kcap] = i < mk ? A[i + j * lda] : 0.0;
     }
+    if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_EXT_LEAF, hh_flops(m, K));
     return;
   }
   // U0: exact nearfield part N_b += alpha X|t Y|s^T for the inadmissible leaves of T_{b0}
@@ -80,6 +95,7 @@ __global__ void __launch_bounds__(NT) k_upd_ext_leaf(MatDev M, UpdArgs a, int rl
     for (int q = 0; q < a.k; ++q) acc += a.X[ot + i + (size_t)q * a.ldx] * a.Y[os + j + (size_t)q * a.ldy];
     Na[i + (size_t)j * M.lmax] += a.alpha * acc;
   }
+  if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_EXT_LEAF, 2.0 * mt * ms * a.k);
 }
 
 // ---- U2 internal, bottom-up ------------------------------------------------------------------
@@ -121,10 +137,23 @@ __global__ void __launch_bounds__(NT) k_upd_ext_level(MatDev M, UpdArgs a, int b
     const int i = e % K, j = e / K;
     RE[i + j * M.kcap] = i < mk ? A[i + j * LD2] : 0.0;
   }
+  if (a.prof && threadIdx.x == 0) {
+    double f = hh_flops(row0, K);
+    for (int q = 0; q < 2; ++q) {
+      const int c = q ? D.son1[t] : D.son0[t];
+      f += (double)(D.rank[c] + k) * D.rank[c] * kt;  // upper-triangular RE times E
+    }
+    atomicAdd(a.prof + 2 * K_EXT_LEVEL, f);
+  }
 }
 
 // ---- U3 weights for one cluster t of side A (partner side B) --------------------------------
-__device__ void weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm) {
+// mode W_FULL: B~_t = R([local stack; B~_{t+} E~_t^T]) -> bw[t]
+// mode W_LOCAL: C_t = R(local stack) -> re[t]   (proper ancestors of t0 only: their re slot is free)
+// mode W_CHAIN: B~_t = R([C_t; B~_{t+} E_t^T])   -> bw[t]  (C_t from re[t])
+enum { W_FULL = 0, W_LOCAL = 1, W_CHAIN = 2 };
+
+__device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm, int mode) {
   const DevSide& A = rs ? M.row : M.col;
   const DevSide& B = rs ? M.col : M.row;
   const int a0 = rs ? a.t0 : a.s0, b0 = rs ? a.s0 : a.t0;
@@ -136,13 +165,20 @@ __device__ void weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int 
   double* diag = P + PR * KC;
   double* red = diag + KC;
   int rows = 0;
+  double fl = 0.0;
   auto flush = [&]() {
     if (rows > 0) {
       la::cta_qr_R(P, PR, rows, K, diag, red);
+      fl += hh_flops(rows, K);
       rows = rows < K ? rows : K;
     }
   };
-  for (int q = A.bptr[t]; q < A.bptr[t + 1]; ++q) {
+  if (mode == W_CHAIN) {
+    la::cta_copy(P, PR, A.re + (size_t)t * M.kcap * M.kcap, M.kcap, K, K);
+    rows = K;
+    __syncthreads();
+  }
+  for (int q = A.bptr[t]; mode != W_CHAIN && q < A.bptr[t + 1]; ++q) {
     const int slot = A.bidx[q];
     const int s = rs ? M.adm_s[slot] : M.adm_t[slot];
     const double* Sa = M.S + (size_t)slot * M.rcap * M.rcap;
@@ -164,11 +200,12 @@ __device__ void weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int 
       }
       P[rows + i + c * PR] = v;
     }
+    fl += (double)rc * ls * kt;  // triangular R_B times S^T
     rows += rc;
     __syncthreads();
   }
   const int p = A.parent[t];
-  if (p >= 0) {
+  if (p >= 0 && mode != W_LOCAL) {
     const bool in_p = inside(A, p, a0);
     const int kp = A.rank[p];
     const int Kp = kp + (in_p ? k : 0);
@@ -186,17 +223,19 @@ __device__ void weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int 
         }                                      // E~_{t0} = [E_{t0}; 0]: zero columns
         P[rows + i + c * PR] = v;
       }
+      fl += 2.0 * Kp * kp * kt;
       rows += Kp;
       __syncthreads();
     }
   }
   flush();
-  double* Bt = A.bw + (size_t)t * M.kcap * M.kcap;
+  double* Bt = (mode == W_LOCAL ? A.re : A.bw) + (size_t)t * M.kcap * M.kcap;
   for (int e = threadIdx.x; e < K * K; e += NT) {
     const int i = e % K, j = e / K;
     Bt[i + j * M.kcap] = i < rows ? P[i + j * PR] : 0.0;
   }
   __syncthreads();
+  return fl;
 }
 
 __global__ void __launch_bounds__(NT) k_upd_weights_path(MatDev M, UpdArgs a) {
@@ -206,7 +245,10 @@ __global__ void __launch_bounds__(NT) k_upd_weights_path(MatDev M, UpdArgs a) {
   int path[64];
   int np = 0;
   for (int t = rs ? a.t0 : a.s0; t >= 0 && np < 64; t = A.parent[t]) path[np++] = t;
-  for (int q = np - 1; q >= 0; --q) weights_cluster(M, a, rs, path[q], sm);
+  double fl = 0.0;
+  // proper ancestors: chain on their local stacks (computed in parallel by k_upd_ext_leaf); t0: full
+  for (int q = np - 1; q >= 0; --q) fl += weights_cluster(M, a, rs, path[q], sm, q == 0 ? W_FULL : W_CHAIN);
+  if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_W_PATH, fl);
 }
 
 __global__ void __launch_bounds__(NT) k_upd_weights_level(MatDev M, UpdArgs a, int bA, int nA, int bB, int nB) {
@@ -214,13 +256,14 @@ __global__ void __launch_bounds__(NT) k_upd_weights_level(MatDev M, UpdArgs a, i
   const bool rs = (int)blockIdx.x < nA;
   const DevSide& A = rs ? M.row : M.col;
   const int t = A.bfs[rs ? bA + blockIdx.x : bB + blockIdx.x - nA];
-  weights_cluster(M, a, rs, t, sm);
+  const double fl = weights_cluster(M, a, rs, t, sm, W_FULL);
+  if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_W_LEVEL, fl);
 }
 
 // ---- U4 truncated nested basis --------------------------------------------------------------
 // Given V (m x K, ldv) in shared memory and B~_t, compute M = V B~^T, its SVD, the rank, Q and R_t.
 __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, int t, double* V, int ldv, int m,
-                         int K, double* sm_rest) {
+                         int K, double* sm_rest, int kid, double extra_flops) {
   double* Bt = sm_rest;             // KC x KC
   double* Mm = Bt + KC * KC;        // 64 x KC (ld 64)
   double* Q = Mm + 64 * KC;         // 64 x KC (ld 64)
@@ -253,6 +296,7 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
   if (threadIdx.x == 0) {
     D.rnew[t] = r;
     if (clamped) atomicOr(M.flags, 1);
+    if (a.prof) atomicAdd(a.prof + 2 * kid, extra_flops + 2.0 * m * K * K + svd_flops(m, K) + 2.0 * r * K * m);
   }
 }
 
@@ -274,7 +318,7 @@ __global__ void __launch_bounds__(NT) k_upd_svd_leaf(MatDev M, UpdArgs a, int rl
     V[i + j * 64] = j < kt ? Vb[i + (size_t)j * M.lmax] : al * Xf[off + i + (size_t)(j - kt) * ldx];
   }
   __syncthreads();
-  svd_core(M, a, D, t, V, 64, m, K, V + 64 * KC);
+  svd_core(M, a, D, t, V, 64, m, K, V + 64 * KC, K_SVD_LEAF, 0.0);
 }
 
 __global__ void __launch_bounds__(NT) k_upd_svd_level(MatDev M, UpdArgs a, int bA, int nA, int bB, int nB) {
@@ -305,7 +349,12 @@ __global__ void __launch_bounds__(NT) k_upd_svd_level(MatDev M, UpdArgs a, int b
     row0 += rc;
   }
   __syncthreads();
-  svd_core(M, a, D, t, V, 64, row0, K, V + 64 * KC);
+  double fv = 0.0;
+  for (int q = 0; q < 2; ++q) {
+    const int c = q ? D.son1[t] : D.son0[t];
+    fv += 2.0 * D.rnew[c] * D.rank[c] * kt;
+  }
+  svd_core(M, a, D, t, V, 64, row0, K, V + 64 * KC, K_SVD_LEVEL, fv);
 }
 
 // ---- U5 couplings ------------------------------------------------------------------------------
@@ -315,9 +364,10 @@ __global__ void __launch_bounds__(NT) k_upd_couple(MatDev M, UpdArgs a, int nA, 
   double* Out = T1 + KC * KC;  // KC x KC (ld KC)
   const int k = a.k;
   const bool rs = (int)blockIdx.x < nA;
+  double fl = 0.0;
   if (rs) {
     const int t = a.t0 + blockIdx.x;
-    const int kt = M.row.rank[t], Kt = kt + k, rt = M.row.rnew[t];
+    const int kt = M.row.rank[t], rt = M.row.rnew[t];
     const double* RNt = M.row.rn + (size_t)t * M.kcap * M.kcap;  // rt x Kt
     for (int q = M.row.bptr[t]; q < M.row.bptr[t + 1]; ++q) {
       const int slot = M.row.bidx[q];
@@ -343,11 +393,13 @@ __global__ void __launch_bounds__(NT) k_upd_couple(MatDev M, UpdArgs a, int nA, 
         la::cta_gemm(Out, KC, T1, KC, false, RNs, M.kcap, true, rt, rsn, Ls, false);
         __syncthreads();
         la::cta_copy(Sa, M.rcap, Out, KC, rt, rsn);
+        fl += 2.0 * rt * kt * ls + 2.0 * rt * Ls * rsn;
       } else {
         // S <- R_t [S; 0] = R_t(:, :kt) S
         la::cta_gemm(Out, KC, RNt, M.kcap, false, Sa, M.rcap, false, rt, ls, kt, false);
         __syncthreads();
         la::cta_copy(Sa, M.rcap, Out, KC, rt, ls);
+        fl += 2.0 * rt * kt * ls;
       }
       __syncthreads();
     }
@@ -365,9 +417,11 @@ __global__ void __launch_bounds__(NT) k_upd_couple(MatDev M, UpdArgs a, int nA, 
       la::cta_gemm(Out, KC, Sa, M.rcap, false, RNs, M.kcap, true, kt, rsn, ls, false);
       __syncthreads();
       la::cta_copy(Sa, M.rcap, Out, KC, kt, rsn);
+      fl += 2.0 * kt * ls * rsn;
       __syncthreads();
     }
   }
+  if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_COUPLE, fl);
 }
 
 // ---- U6 install --------------------------------------------------------------------------------
@@ -397,6 +451,7 @@ __global__ void __launch_bounds__(NT) k_upd_install(MatDev M, UpdArgs a, int nA,
     la::cta_gemm(sm, KC, RN, M.kcap, false, E, M.rcap, false, r, kp, kold, false);
     __syncthreads();
     la::cta_copy(E, M.rcap, sm, KC, r, kp);
+    if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_INSTALL, 2.0 * r * kold * kp);
   }
   // the new basis is orthonormal: its R-factor is the identity
   double* rc = D.rc + (size_t)t * M.rcap * M.rcap;
@@ -431,6 +486,7 @@ __global__ void __launch_bounds__(NT) k_upd_rcache_path(MatDev M, UpdArgs a) {
     }
     __syncthreads();
     if (kt > 0) la::cta_qr_R(A, LD2, row0, kt, diag, red);
+    if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_RCACHE, hh_flops(row0, kt) + (double)row0 * row0 * kt);
     double* RC = D.rc + (size_t)t * M.rcap * M.rcap;
     const int mk = row0 < kt ? row0 : kt;
     for (int e = threadIdx.x; e < kt * kt; e += NT) {
@@ -441,9 +497,9 @@ __global__ void __launch_bounds__(NT) k_upd_rcache_path(MatDev M, UpdArgs a) {
   }
 }
 
-constexpr size_t SM_EXT_LEAF = (size_t)(LMAX_MAX * KC + KC + 8) * 8;
-constexpr size_t SM_EXT_LEVEL = (size_t)(LD2 * KC + KC + 8) * 8;
 constexpr size_t SM_WEIGHTS = (size_t)(PR * KC + KC + 8) * 8;
+constexpr size_t SM_EXT_LEAF = SM_WEIGHTS;  // also runs the ancestors' local weight stacks
+constexpr size_t SM_EXT_LEVEL = (size_t)(LD2 * KC + KC + 8) * 8;
 constexpr size_t SM_SVD = (size_t)(64 * KC + KC * KC + 64 * KC + 64 * KC + KC + KC) * 8 + 64;
 constexpr size_t SM_COUPLE = (size_t)(2 * KC * KC) * 8;
 constexpr size_t SM_INSTALL = (size_t)(KC * KC) * 8;
@@ -489,7 +545,9 @@ cudaError_t update_init_attributes() {
   return cudaSuccess;
 }
 
-cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a, cudaStream_t st) {
+cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a_in, cudaStream_t st) {
+  UpdArgs a = a_in;
+  a.prof = prof_dev();
   cudaError_t e = update_init_attributes();
   if (e != cudaSuccess) return e;
   const MatDev& M = Z->d;
@@ -499,43 +557,45 @@ cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a, cudaStream_t st) {
   const int b0 = B->find(a.t0, a.s0);
   const int in0 = Z->inad_range[2 * b0], nin = Z->inad_range[2 * b0 + 1] - in0;
   if (B->kind[b0] == INADM) {  // dense add only
-    if (nin > 0) k_upd_ext_leaf<<<nin, NT, SM_EXT_LEAF, st>>>(M, a, 0, 0, 0, 0, in0, nin);
+    if (nin > 0) H2_LAUNCH(K_EXT_LEAF, st, k_upd_ext_leaf<<<nin, NT, SM_EXT_LEAF, st>>>(M, a, 0, 0, 0, 0, in0, nin, 0, 0));
     return cudaGetLastError();
   }
   int rl0, nrl, cl0, ncl;
   leaf_range(R, a.t0, &rl0, &nrl);
   leaf_range(C, a.s0, &cl0, &ncl);
-  k_upd_ext_leaf<<<nrl + ncl + nin, NT, SM_EXT_LEAF, st>>>(M, a, rl0, nrl, cl0, ncl, in0, nin);
   const int Lr = R->level[a.t0], Lc = C->level[a.s0];
+  H2_LAUNCH(K_EXT_LEAF, st,
+            k_upd_ext_leaf<<<nrl + ncl + nin + Lr + Lc, NT, SM_EXT_LEAF, st>>>(M, a, rl0, nrl, cl0, ncl, in0, nin, Lr,
+                                                                               Lc));
   const int Lmax = std::max(R->depth, C->depth), Lmin = std::min(Lr, Lc);
   // U2 bottom-up (internal clusters)
   for (int L = Lmax - 1; L >= Lmin; --L) {
     int bA, nA, bB, nB;
     level_segment(R, a.t0, L, &bA, &nA);
     level_segment(C, a.s0, L, &bB, &nB);
-    if (nA + nB > 0) k_upd_ext_level<<<nA + nB, NT, SM_EXT_LEVEL, st>>>(M, a, bA, nA, bB, nB);
+    if (nA + nB > 0) H2_LAUNCH(K_EXT_LEVEL, st, k_upd_ext_level<<<nA + nB, NT, SM_EXT_LEVEL, st>>>(M, a, bA, nA, bB, nB));
   }
   // U3 weights: path (root .. t0), then the subtree top-down
-  k_upd_weights_path<<<2, NT, SM_WEIGHTS, st>>>(M, a);
+  H2_LAUNCH(K_W_PATH, st, k_upd_weights_path<<<2, NT, SM_WEIGHTS, st>>>(M, a));
   for (int L = Lmin + 1; L <= Lmax; ++L) {
     int bA = 0, nA = 0, bB = 0, nB = 0;
     if (L > Lr) level_segment(R, a.t0, L, &bA, &nA);
     if (L > Lc) level_segment(C, a.s0, L, &bB, &nB);
-    if (nA + nB > 0) k_upd_weights_level<<<nA + nB, NT, SM_WEIGHTS, st>>>(M, a, bA, nA, bB, nB);
+    if (nA + nB > 0) H2_LAUNCH(K_W_LEVEL, st, k_upd_weights_level<<<nA + nB, NT, SM_WEIGHTS, st>>>(M, a, bA, nA, bB, nB));
   }
   // U4 bottom-up
-  k_upd_svd_leaf<<<nrl + ncl, NT, SM_SVD, st>>>(M, a, rl0, nrl, cl0, ncl);
+  H2_LAUNCH(K_SVD_LEAF, st, k_upd_svd_leaf<<<nrl + ncl, NT, SM_SVD, st>>>(M, a, rl0, nrl, cl0, ncl));
   for (int L = Lmax - 1; L >= Lmin; --L) {
     int bA, nA, bB, nB;
     level_segment(R, a.t0, L, &bA, &nA);
     level_segment(C, a.s0, L, &bB, &nB);
-    if (nA + nB > 0) k_upd_svd_level<<<nA + nB, NT, SM_SVD, st>>>(M, a, bA, nA, bB, nB);
+    if (nA + nB > 0) H2_LAUNCH(K_SVD_LEVEL, st, k_upd_svd_level<<<nA + nB, NT, SM_SVD, st>>>(M, a, bA, nA, bB, nB));
   }
   // U5, U6, R-cache refresh
   const int nA = R->tsize[a.t0], nB = C->tsize[a.s0];
-  k_upd_couple<<<nA + nB, NT, SM_COUPLE, st>>>(M, a, nA, nB);
-  k_upd_install<<<nA + nB, NT, SM_INSTALL, st>>>(M, a, nA, nB);
-  k_upd_rcache_path<<<2, NT, SM_EXT_LEVEL, st>>>(M, a);
+  H2_LAUNCH(K_COUPLE, st, k_upd_couple<<<nA + nB, NT, SM_COUPLE, st>>>(M, a, nA, nB));
+  H2_LAUNCH(K_INSTALL, st, k_upd_install<<<nA + nB, NT, SM_INSTALL, st>>>(M, a, nA, nB));
+  H2_LAUNCH(K_RCACHE, st, k_upd_rcache_path<<<2, NT, SM_EXT_LEVEL, st>>>(M, a));
   return cudaGetLastError();
 }
 

@@ -18,11 +18,12 @@ EXPORTED_SYMBOLS = [
     "h2_block_tree", "h2_btree_export", "h2_btree_destroy",
     "h2_from_sparse", "h2_lowrank_update", "h2_matvec", "h2_addmul", "h2_lr_factor", "h2_solve",
     "h2_ranks", "h2_storage_report", "h2_export", "h2_check_device_flags",
+    "h2_profile_enable", "h2_profile_read",
     "h2_mat_destroy", "h2_last_error",
 ]
 
 if not os.path.exists(_LIBPATH):
-    raise ImportError(f"libh2b200.so not built ({_LIBPATH}); run `python -m paper_1402_5056_b200.build` "
+    raise ImportError(f"libh2b200.so not built ({_LIBPATH}); run `python paper_1402_5056_b200/build.py` "
                       "(there is no CPU fallback)")
 _lib = C.CDLL(_LIBPATH)
 
@@ -50,6 +51,8 @@ _sig = {
     "h2_storage_report": [_p, _p],
     "h2_export": [_p, _p, _p, _p, _p, _p, _p, _p],
     "h2_check_device_flags": [_p, _p],
+    "h2_profile_enable": [_i32],
+    "h2_profile_read": [_p, _p, _p, _p, _p, _p],
     "h2_mat_destroy": [_p],
     "h2_last_error": [],
 }
@@ -266,3 +269,24 @@ def h2_export(Z: Mat):
     _check(_lib.h2_export(Z.h, *[_ptr(b) for b in bufs], _ptr(sizes)))
     kr, kc = h2_ranks(Z)
     return dict(zip(["V", "E", "W", "F", "S", "N"], bufs), k=kr, l=kc)
+
+
+def h2_profile_enable(on: bool = True):
+    _check(_lib.h2_profile_enable(1 if on else 0))
+
+
+def h2_profile_read():
+    """{kernel name: dict(launches, ms, flops, bytes)} for every kernel kind launched."""
+    cnt = _i32()
+    _check(_lib.h2_profile_read(None, None, None, None, None, C.byref(cnt)))
+    n = cnt.value
+    names = C.create_string_buffer(32 * n)
+    la = np.zeros(n, dtype=np.int64)
+    ms, fl, by = (np.zeros(n) for _ in range(3))
+    _check(_lib.h2_profile_read(names, _ptr(la), _ptr(ms), _ptr(fl), _ptr(by), C.byref(cnt)))
+    out = {}
+    for i in range(n):
+        name = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
+        if la[i]:
+            out[name] = dict(launches=int(la[i]), ms=float(ms[i]), flops=float(fl[i]), bytes=float(by[i]))
+    return out
