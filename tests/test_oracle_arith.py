@@ -1,0 +1,149 @@
+"""Pins for the oracle's product, substitutions, LR/Cholesky, solves and PCG (CPU only).
+
+Held to: the dense Cholesky / no-pivot LU factors (unique, tree order) when truncation is
+(nearly) off; the exactness of A*A for a sparse A (far field exactly zero); X = I and
+alpha = 0 special cases; random H^2 products against dense products; the
+factorization error bound ||LL^T - A|| <= 10 eps ||A||; PCG/power-iteration special
+cases."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from inputs import config
+from inputs.updates import c0_global_factors, mixed_stream
+from oracle.structure import ClusterTree, BlockTree, ADM
+from oracle.h2 import from_sparse
+from oracle.update import Updater, Trunc
+from oracle.dense import densify
+from oracle.arith import Arith, Op, dense_factor_product, pcg, power_error
+
+
+def _c0(lower=False, A=None):
+    c = config("C0")
+    rt = ClusterTree(c["points"], c["leaf"])
+    bt = BlockTree(rt, rt, c["eta"])
+    Z = from_sparse(bt, c["A"] if A is None else A, lower=lower)
+    return c, rt, bt, Z
+
+
+def test_cholesky_exact_equals_dense_cholesky():
+    c, rt, bt, Z = _c0(lower=True)
+    Ad = c["A"].toarray()[rt.perm][:, rt.perm]
+    ar = Arith(Z, Trunc(1e-13))
+    ar.chol()
+    L = np.tril(densify(Z))
+    Lref = np.linalg.cholesky(Ad)
+    assert np.abs(L - Lref).max() / np.abs(Lref).max() < 1e-9
+    assert ar.stats["updates"] > 100 and ar.stats["temporaries"] > 0
+
+
+def test_cholesky_truncated_error_bound_and_pcg():
+    c, rt, bt, Z = _c0(lower=True)
+    A = c["A"]
+    Ad = A.toarray()[rt.perm][:, rt.perm]
+    eps = 1e-4
+    ar = Arith(Z, Trunc(eps))
+    ar.chol()
+    E = dense_factor_product(Z, True) - Ad
+    assert np.linalg.norm(E, 2) <= 10 * eps * np.linalg.norm(Ad, 2)
+    b = np.random.default_rng(4).standard_normal(A.shape[0])
+    x, m, rel = pcg(lambda v: A @ v, lambda v: ar.solve(v), b)
+    assert rel < 1e-8 and m <= 10
+    err = power_error(lambda v: A @ v, lambda v: ar.solve(v), np.random.default_rng(5).standard_normal(A.shape[0]))
+    assert err < 0.2
+
+
+def test_lr_exact_equals_dense_lu_after_rank8_update():
+    """C0 protocol (R15): rank-8 update (alpha = 1/n) on every admissible leaf, then LR vs dense
+    no-pivot LU in tree order."""
+    c, rt, bt, Z = _c0()
+    n = rt.n
+    X, Y = c0_global_factors(n)
+    Xt, Yt = X[rt.perm], Y[rt.perm]
+    up = Updater(Z, Trunc(1e-4))
+    for b in bt.adm:
+        t0, s0 = int(bt.t[b]), int(bt.s[b])
+        up(t0, s0, Xt[rt.lo[t0]:rt.hi[t0]], Yt[rt.lo[s0]:rt.hi[s0]], alpha=1.0 / n)
+    M = densify(Z)
+    ar = Arith(Z, Trunc(1e-13))
+    ar.lr()
+    D = densify(Z)
+    # dense Doolittle LU without pivoting
+    U = M.copy()
+    Lr = np.eye(n)
+    for j in range(n):
+        Lr[j + 1:, j] = U[j + 1:, j] / U[j, j]
+        U[j + 1:, j:] -= np.outer(Lr[j + 1:, j], U[j, j:])
+    assert np.abs(np.tril(D, -1) - np.tril(Lr, -1)).max() < 1e-8
+    assert np.abs(np.triu(D) - np.triu(U)).max() / np.abs(U).max() < 1e-8
+    # truncated LR error bound (<= 10 eps for alpha = 1/n)
+    c, rt, bt, Z = _c0()
+    up = Updater(Z, Trunc(1e-4))
+    for b in bt.adm:
+        t0, s0 = int(bt.t[b]), int(bt.s[b])
+        up(t0, s0, Xt[rt.lo[t0]:rt.hi[t0]], Yt[rt.lo[s0]:rt.hi[s0]], alpha=1.0 / n)
+    M = densify(Z)
+    ar = Arith(Z, Trunc(1e-4))
+    ar.lr()
+    E = dense_factor_product(Z, False) - M
+    assert np.linalg.norm(E, 2) <= 10 * 1e-4 * np.linalg.norm(M, 2)
+
+
+def test_product_sparse_squared_is_exact():
+    """for a sparse A (rank-0 bases) every far-field contribution of A*A is zero."""
+    c, rt, bt, A = _c0()
+    Zc, _, _, Z = _c0(A=c["A"] * 0.0)
+    ar = Arith(Z, Trunc(1e-4))
+    ar.addmul(1.0, Op(A), Op(A), 0, 0, 0)
+    Ad = c["A"].toarray()[rt.perm][:, rt.perm]
+    assert np.abs(densify(Z) - Ad @ Ad).max() < 1e-12
+    assert Z.k.sum() == 0
+
+
+def test_product_identity_and_alpha_zero():
+    c, rt, bt, Y = _c0()
+    n = rt.n
+    Updater(Y, Trunc(1e-10))
+    for t0, s0, X_, Y_ in mixed_stream([(int(bt.t[b]), int(bt.s[b]), rt.size(bt.t[b]), rt.size(bt.s[b]))
+                                        for b in bt.adm], 6, 4, seed=3):
+        Updater(Y, Trunc(1e-10))(t0, s0, X_, Y_)
+    _, _, _, I = _c0(A=sp.identity(n, format="csr"))
+    _, _, _, Z = _c0(A=c["A"] * 0.0)
+    ar = Arith(Z, Trunc(1e-10))
+    ar.addmul(1.0, Op(I), Op(Y), 0, 0, 0)  # S:404  X = I -> Z = Y
+    Dy = densify(Y)
+    assert np.linalg.norm(densify(Z) - Dy) / np.linalg.norm(Dy) < 1e-9
+    before = densify(Z)
+    ar.addmul(0.0, Op(Y), Op(Y), 0, 0, 0)  # S:403  alpha = 0 -> unchanged
+    assert np.linalg.norm(densify(Z) - before) <= 1e-9 * np.linalg.norm(before)
+
+
+def test_product_random_h2_against_dense():
+    c, rt, bt, X = _c0()
+    targets = [(int(bt.t[b]), int(bt.s[b]), rt.size(bt.t[b]), rt.size(bt.s[b])) for b in range(bt.nblocks)]
+    ux = Updater(X, Trunc(1e-12))
+    for t0, s0, a, b in mixed_stream(targets, 8, 4, seed=1):
+        ux(t0, s0, a, b)
+    _, _, _, Y = _c0()
+    uy = Updater(Y, Trunc(1e-12))
+    for t0, s0, a, b in mixed_stream(targets, 8, 4, seed=2):
+        uy(t0, s0, a, b)
+    _, _, _, Z = _c0()
+    D0 = densify(Z)
+    ar = Arith(Z, Trunc(1e-12))
+    ar.addmul(-0.5, Op(X), Op(Y, True), 0, 0, 0)
+    ref = D0 - 0.5 * densify(X) @ densify(Y).T
+    assert np.linalg.norm(densify(Z) - ref) / np.linalg.norm(ref) < 1e-8
+
+
+def test_pcg_and_power_special_cases():
+    n = 50
+    b = np.random.default_rng(0).standard_normal(n)
+    x, m, rel = pcg(lambda v: v, lambda v: v, b)  # A = I, M = I -> 1 iteration
+    assert m == 1 and rel < 1e-14
+    A = np.diag(np.linspace(1, 10, n))
+    x, m, rel = pcg(lambda v: A @ v, lambda v: np.linalg.solve(A, v), b)  # exact preconditioner
+    assert m <= 2
+    D = np.diag([1.0, 2.0])  # A = diag(1,2), M = I -> ||I - A|| = 1
+    assert abs(power_error(lambda v: D @ v, lambda v: v, np.array([0.3, 1.0])) - 1.0) < 1e-3
+    assert power_error(lambda v: A @ v, lambda v: np.linalg.solve(A, v), b) < 1e-8
