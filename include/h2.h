@@ -92,7 +92,7 @@ void h2_btree_destroy(h2_btree bt);
  * admissible block -> H2_ERR_STRUCTURE.  storage = H2_LOWER keeps only blocks whose row range
  * starts at or after the column range (the Cholesky factor layout).
  * rank_cap: capacity of stored ranks per cluster (e.g. 32); update_cap: the largest update rank
- * k a later h2_lowrank_update may pass (extended rank capacity = rank_cap + update_cap <= 64). */
+ * k a later h2_lowrank_update may pass (rank_cap <= 48, rank_cap + update_cap <= 96). */
 h2_status h2_from_sparse(h2_btree bt, int64_t n, const int64_t* rowptr, const int32_t* colidx,
                          const double* val, h2_storage storage, int32_t rank_cap, int32_t update_cap,
                          h2_stream stream, h2_mat* out);
@@ -113,16 +113,32 @@ h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t k, double 
 h2_status h2_matvec(h2_mat Z, int32_t transpose, double alpha, const double* x, double beta, double* y,
                     h2_stream stream);
 
-/* Z <- Z + alpha X Y (recursive product over the triple tree).
- * Not available in this build: returns H2_ERR_UNSUPPORTED. */
+/* Z <- Z + alpha X Y: recursive product over the triple tree.  Case 1
+ * recursion over sons+ in the printed order; an admissible-leaf target receives its
+ * sub-products in low-rank temporaries (SVD-truncated) merged by 4 zero-extended local
+ * updates; Case 2 builds low-rank factors and performs a local update
+ * (or a dense add into an inadmissible target).  X, Y: H2_FULL storage; Z, X, Y share the cluster
+ * trees; Z must not alias X or Y.  Truncation of every update and temporary by *trunc. */
 h2_status h2_addmul(h2_mat Z, double alpha, h2_mat X, h2_mat Y, const h2_trunc* trunc, h2_stream stream);
 
-/* In-place LR / Cholesky factorization.
- * Not available in this build: returns H2_ERR_UNSUPPORTED. */
+/* In-place factorization:
+ *   H2_CHOLESKY: A in H2_LOWER storage, symmetric positive definite; on return the
+ *     stored lower triangle holds L (diagonal tiles lower-triangular) with A ~ L L^T;
+ *   H2_LR: A in H2_FULL storage; unit-lower L (strict lower part) and R (upper part), no pivoting.
+ * Block substitutions P:392-450; an admissible-leaf block X = V S (L^{-1} W)^T is re-entered by
+ * S <- 0 and a local update (reading R8).  A non-positive (Cholesky) or |p| <= 1e-14 ||tile||_F
+ * (LR) leaf pivot is reported by h2_check_device_flags as H2_ERR_BREAKDOWN (the call itself only
+ * enqueues work; the matrix is then partially factored). */
 h2_status h2_lr_factor(h2_mat A, h2_factor_kind kind, const h2_trunc* trunc, h2_stream stream);
 
-/* x <- F^{-1} x for a factored matrix (P:392-450 vector case).  Not available in this build. */
+/* x <- F^{-1} x for a factored matrix: (L L^T)^{-1} x (Cholesky) or (L R)^{-1} x (LR), by H^2
+ * forward/backward substitution (the preconditioner of P:1440-1444).  x: device, n x nrhs,
+ * column-major with leading dimension ldx >= n, ORIGINAL order; 1 <= nrhs <= 64. */
 h2_status h2_solve(h2_mat F, double* x, int32_t nrhs, int64_t ldx, h2_stream stream);
+
+/* Counters of the work the product/factorization driver issued on this matrix:
+ * out[0] local low-rank updates, out[1] dense nearfield adds, out[2] temporaries, out[3] 0. */
+h2_status h2_stats(h2_mat Z, int64_t out[4]);
 
 /* ---- inspection (synchronous: these synchronize the given stream) -------------------------- */
 

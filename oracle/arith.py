@@ -212,7 +212,7 @@ class Arith:
     def addmul(self, alpha, X: Op, Y: Op, t, s, r, target=None):
         """Z|_{t x r} += alpha X|_{t x s} Y|_{s x r}; target None = the H^2 matrix Z itself."""
         rt = self.rt
-        if not (X.stored(t, s) and Y.stored(s, r)):
+        if alpha == 0.0 or not (X.stored(t, s) and Y.stored(s, r)):
             return
         kx, ky = X.kind(t, s), Y.kind(s, r)
         if kx == SUBDIV and ky == SUBDIV:
@@ -410,7 +410,7 @@ class Arith:
             b = Z.bt.index[(t, t)]
             N = Z.N[b].copy()
             m = N.shape[0]
-            nrm = np.linalg.norm(N, 2)
+            nrm = np.linalg.norm(N)  # Frobenius (reading: breakdown threshold |p| <= 1e-14 ||tile||_F)
             for j in range(m):
                 if abs(N[j, j]) <= 1e-14 * nrm:
                     raise BreakdownError(f"H2_ERR_BREAKDOWN: leaf {t} pivot {j}")

@@ -31,7 +31,7 @@ __device__ __forceinline__ double warp_allsum(double p) {
   return p;
 }
 
-__device__ void warp_qr_R(double* A, int lda, int m, int n, double* diag) {
+static __device__ void warp_qr_R(double* A, int lda, int m, int n, double* diag) {
   const int lane = threadIdx.x & 31;
   const int RP = (m + 31) >> 5;
   const int jmax = m < n ? m : n;
@@ -113,7 +113,7 @@ __device__ void warp_qr_R(double* A, int lda, int m, int n, double* diag) {
 // column, butterfly within the lane group), and with v = a_j[j:] - alpha e_1:
 // v^T a_c = d_c - alpha a_jc,  v^T v / 2 = |a_j|^2 - alpha a_jj.
 // (A one-warp variant, warp_qr_R above, measured ~2x slower on B200: serial shuffle chains.)
-__device__ void cta_qr_R(double* A, int lda, int m, int n, double* diag, double* red) {
+static __device__ void cta_qr_R(double* A, int lda, int m, int n, double* diag, double* red) {
   const int tid = threadIdx.x, nt = blockDim.x;
   int npow = 1;
   while (npow < n) npow *= 2;
@@ -162,7 +162,7 @@ __device__ void cta_qr_R(double* A, int lda, int m, int n, double* diag, double*
 
 // C (m x n, ldc) = op(A) op(B) (+ C if accumulate); A: m x kk (or kk x m if ta), B: kk x n (or n x kk if tb).
 // Any pointers (shared or global).  Every thread of the CTA participates.
-__device__ void cta_gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb,
+static __device__ void cta_gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb,
                          int m, int n, int kk, bool accumulate) {
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int i = e % m, j = e / m;
@@ -189,7 +189,7 @@ __device__ __forceinline__ void cta_copy(double* D, int ldd, const double* Sx, i
 // round-robin ordering, p/2 disjoint pairs per round).  On return column j of M is sigma_j u_j
 // (unsorted); sig[j] = |M(:,j)|; order[q] = index of the q-th largest sigma (ties by index).
 // scratch: >= 2 ints of shared memory.
-__device__ void cta_jacobi(double* M, int ldm, int m, int p, double* sig, int* order, int* scratch) {
+static __device__ void cta_jacobi(double* M, int ldm, int m, int p, double* sig, int* order, int* scratch) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int pp = p + (p & 1);
   const int npairs = pp / 2;

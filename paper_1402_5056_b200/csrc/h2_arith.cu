@@ -1,0 +1,624 @@
+// Device primitives of the H^2 product / substitution / factorization (see h2_arith.cuh).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "devla.cuh"
+#include "h2_arith.cuh"
+
+namespace h2 {
+namespace {
+
+constexpr int NT = NTHREADS;
+constexpr int KC = KCAP_MAX;
+constexpr int PR = 192;
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// ---- basis expansion ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_expand(MatDev M, DevSide D, int t, int l0, double* out, int ld) {
+  extern __shared__ double smx[];
+  double* P[2] = {smx, smx + KC * KC};
+  const int q = D.leaves[l0 + blockIdx.x];
+  const int kt = D.rank[t];
+  int cur = 0;
+  int kq = D.rank[q];
+  // P = I (kq x kq)
+  for (int e = threadIdx.x; e < kq * kq; e += NT) P[0][(e % kq) + (e / kq) * KC] = (e % kq) == (e / kq) ? 1.0 : 0.0;
+  int rows = kq, cols = kq;
+  __syncthreads();
+  for (int a = q; a != t; a = D.parent[a]) {
+    const int kp = D.rank[D.parent[a]];
+    const double* E = D.tr + (size_t)a * M.rcap * M.rcap;  // k_a x k_p
+    for (int e = threadIdx.x; e < rows * kp; e += NT) {
+      const int i = e % rows, j = e / rows;
+      double acc = 0.0;
+      for (int p = 0; p < cols; ++p) acc += P[cur][i + p * KC] * E[p + j * M.rcap];
+      P[cur ^ 1][i + j * KC] = acc;
+    }
+    cols = kp;
+    cur ^= 1;
+    __syncthreads();
+  }
+  (void)kt;
+  const int m = D.hi[q] - D.lo[q];
+  const int off = D.lo[q] - D.lo[t];
+  const double* V = D.leafb + (size_t)D.leafidx[q] * M.lmax * M.rcap;
+  for (int e = threadIdx.x; e < m * cols; e += NT) {
+    const int i = e % m, j = e / m;
+    double acc = 0.0;
+    for (int p = 0; p < rows; ++p) acc += V[i + p * M.lmax] * P[cur][p + j * KC];
+    out[off + i + (size_t)j * ld] = acc;
+  }
+}
+
+// ---- GEMMs with device dims -------------------------------------------------------------------
+__global__ void k_gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb,
+                       Dim md, Dim nd, Dim kd, double alpha, double beta) {
+  const int m = md.v(), n = nd.v(), kk = kd.v();
+  const long long tot = (long long)m * n;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    double acc = 0.0;
+    for (int q = 0; q < kk; ++q) {
+      const double a = ta ? A[q + (size_t)i * lda] : A[i + (size_t)q * lda];
+      const double b = tb ? B[j + (size_t)q * ldb] : B[q + (size_t)j * ldb];
+      acc += a * b;
+    }
+    const size_t o = i + (size_t)j * ldc;
+    C[o] = beta == 0.0 ? alpha * acc : alpha * acc + beta * C[o];
+  }
+}
+
+// long inner dimension: partial sums per chunk, then a deterministic fixed-order reduction
+__global__ void k_gemm_inner_part(double* part, const double* A, int lda, bool ta, const double* B, int ldb, bool tb,
+                                  Dim md, Dim nd, Dim kd, int chunk) {
+  const int m = md.v(), n = nd.v(), kk = kd.v();
+  const int q0 = blockIdx.x * chunk, q1 = min(kk, q0 + chunk);
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    const int i = e % m, j = e / m;
+    double acc = 0.0;
+    for (int q = q0; q < q1; ++q) {
+      const double a = ta ? A[q + (size_t)i * lda] : A[i + (size_t)q * lda];
+      const double b = tb ? B[j + (size_t)q * ldb] : B[q + (size_t)j * ldb];
+      acc += a * b;
+    }
+    part[(size_t)blockIdx.x * KC * KC + e] = acc;
+  }
+}
+
+__global__ void k_gemm_inner_sum(double* C, int ldc, const double* part, int nparts, Dim md, Dim nd, double alpha,
+                                 double beta) {
+  const int m = md.v(), n = nd.v();
+  for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
+    double acc = 0.0;
+    for (int p = 0; p < nparts; ++p) acc += part[(size_t)p * KC * KC + e];
+    const int i = e % m, j = e / m;
+    const size_t o = i + (size_t)j * ldc;
+    C[o] = beta == 0.0 ? alpha * acc : alpha * acc + beta * C[o];
+  }
+}
+
+double* g_part = nullptr;
+constexpr int NPART = 64;
+
+// ---- H^2 block times dense --------------------------------------------------------------------
+// forward transform over T_b: leaves
+__global__ void __launch_bounds__(NT) k_hm_fwd_leaf(MatDev M, DevSide S, int l0, int base_lo, const double* D, int ldd,
+                                                    Dim md, double* xh) {
+  const int q = S.leaves[l0 + blockIdx.x];
+  const int m = md.v();
+  const int rows = S.hi[q] - S.lo[q], kq = S.rank[q];
+  const double* W = S.leafb + (size_t)S.leafidx[q] * M.lmax * M.rcap;
+  const int off = S.lo[q] - base_lo;
+  double* x = xh + (size_t)q * M.rcap * KC;
+  for (int e = threadIdx.x; e < kq * m; e += NT) {
+    const int j = e % kq, c = e / kq;
+    double acc = 0.0;
+    for (int i = 0; i < rows; ++i) acc += W[i + j * M.lmax] * D[off + i + (size_t)c * ldd];
+    x[j + c * M.rcap] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_hm_fwd_level(MatDev M, DevSide S, int b0, Dim md, double* xh) {
+  const int s = S.bfs[b0 + blockIdx.x];
+  if (S.son0[s] < 0) return;
+  const int m = md.v(), ks = S.rank[s];
+  double* x = xh + (size_t)s * M.rcap * KC;
+  for (int e = threadIdx.x; e < ks * m; e += NT) {
+    const int j = e % ks, c = e / ks;
+    double acc = 0.0;
+    for (int q = 0; q < 2; ++q) {
+      const int sq = q ? S.son1[s] : S.son0[s];
+      const int kq = S.rank[sq];
+      const double* F = S.tr + (size_t)sq * M.rcap * M.rcap;
+      const double* xq = xh + (size_t)sq * M.rcap * KC;
+      for (int i = 0; i < kq; ++i) acc += F[i + j * M.rcap] * xq[i + c * M.rcap];
+    }
+    x[j + c * M.rcap] = acc;
+  }
+}
+
+// couplings: CTA per cluster a' of T_a (dst side): yhat_{a'} = sum_{(a',b') adm, b' in T_b} S_op xhat_{b'}
+__global__ void __launch_bounds__(NT) k_hm_couple(MatDev M, DevSide Dd, DevSide Ds, int a, int b, int trans, Dim md,
+                                                  const double* xh, double* yh) {
+  const int ap = a + blockIdx.x;
+  const int m = md.v(), ka = Dd.rank[ap];
+  const int bsz = Ds.tsize[b];
+  double* y = yh + (size_t)ap * M.rcap * KC;
+  for (int e = threadIdx.x; e < ka * m; e += NT) {
+    const int i = e % ka, c = e / ka;
+    double acc = 0.0;
+    for (int q = Dd.bptr[ap]; q < Dd.bptr[ap + 1]; ++q) {
+      const int slot = Dd.bidx[q];
+      const int bp = trans ? M.adm_t[slot] : M.adm_s[slot];
+      if (bp < b || bp >= b + bsz) continue;
+      const int kb = Ds.rank[bp];
+      const double* Sa = M.S + (size_t)slot * M.rcap * M.rcap;
+      const double* x = xh + (size_t)bp * M.rcap * KC + c * M.rcap;
+      if (!trans)
+        for (int j = 0; j < kb; ++j) acc += Sa[i + j * M.rcap] * x[j];
+      else
+        for (int j = 0; j < kb; ++j) acc += Sa[j + i * M.rcap] * x[j];
+    }
+    y[i + c * M.rcap] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_hm_bwd_level(MatDev M, DevSide D, int b0, Dim md, double* yh) {
+  const int t = D.bfs[b0 + blockIdx.x];
+  const int p = D.parent[t];
+  const int m = md.v(), kt = D.rank[t], kp = D.rank[p];
+  const double* E = D.tr + (size_t)t * M.rcap * M.rcap;
+  double* y = yh + (size_t)t * M.rcap * KC;
+  const double* yp = yh + (size_t)p * M.rcap * KC;
+  for (int e = threadIdx.x; e < kt * m; e += NT) {
+    const int i = e % kt, c = e / kt;
+    double acc = y[i + c * M.rcap];
+    for (int j = 0; j < kp; ++j) acc += E[i + j * M.rcap] * yp[j + c * M.rcap];
+    y[i + c * M.rcap] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_hm_leaf(MatDev M, DevSide Dd, DevSide Ds, int l0, int a, int b, int trans,
+                                                const double* D, int ldd, Dim md, const double* yh, double* out,
+                                                int ldo, double alpha, double beta) {
+  const int ap = Dd.leaves[l0 + blockIdx.x];
+  const int m = md.v();
+  const int rows = Dd.hi[ap] - Dd.lo[ap], ka = Dd.rank[ap];
+  const int offo = Dd.lo[ap] - Dd.lo[a];
+  const int bsz = Ds.tsize[b];
+  const double* V = Dd.leafb + (size_t)Dd.leafidx[ap] * M.lmax * M.rcap;
+  const double* y = yh + (size_t)ap * M.rcap * KC;
+  const int32_t* np = trans ? M.ntptr : M.nptr;
+  const int32_t* ni = trans ? M.ntidx : M.nidx;
+  const int32_t* part = trans ? M.in_t : M.in_s;
+  for (int e = threadIdx.x; e < rows * m; e += NT) {
+    const int i = e % rows, c = e / rows;
+    double acc = 0.0;
+    for (int j = 0; j < ka; ++j) acc += V[i + j * M.lmax] * y[j + c * M.rcap];
+    for (int q = np[ap]; q < np[ap + 1]; ++q) {
+      const int slot = ni[q];
+      const int bp = part[slot];
+      if (bp < b || bp >= b + bsz) continue;
+      const int rb = Ds.hi[bp] - Ds.lo[bp];
+      const double* Na = M.N + (size_t)slot * M.lmax * M.lmax;
+      const double* x = D + (Ds.lo[bp] - Ds.lo[b]) + (size_t)c * ldd;
+      if (!trans)
+        for (int j = 0; j < rb; ++j) acc += Na[i + j * M.lmax] * x[j];
+      else
+        for (int j = 0; j < rb; ++j) acc += Na[j + i * M.lmax] * x[j];
+    }
+    double* o = out + offo + i + (size_t)c * ldo;
+    *o = beta == 0.0 ? alpha * acc : beta * *o + alpha * acc;
+  }
+}
+
+// ---- dense tiles ------------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_potrf(MatDev M, int slot, int t) {
+  __shared__ double T[64 * 65];
+  double* N = M.N + (size_t)slot * M.lmax * M.lmax;
+  const int m = M.row.hi[t] - M.row.lo[t];
+  const int ld = 65;
+  for (int e = threadIdx.x; e < m * m; e += NT) {
+    const int i = e % m, j = e / m;
+    T[i + j * ld] = i >= j ? N[i + j * M.lmax] : N[j + i * M.lmax];  // symmetric from the lower triangle
+  }
+  __syncthreads();
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = T[j + j * ld];
+      if (!(d > 0.0)) bad = 1;
+      T[j + j * ld] = sqrt(fmax(d, 0.0));
+    }
+    __syncthreads();
+    const double djj = T[j + j * ld];
+    for (int i = j + 1 + threadIdx.x; i < m; i += NT) T[i + j * ld] /= djj;
+    __syncthreads();
+    for (int e = threadIdx.x; e < (m - j - 1) * (m - j - 1); e += NT) {
+      const int i = j + 1 + e % (m - j - 1), c = j + 1 + e / (m - j - 1);
+      if (i >= c) T[i + c * ld] -= T[i + j * ld] * T[c + j * ld];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < m * m; e += NT) {
+    const int i = e % m, j = e / m;
+    N[i + j * M.lmax] = i >= j ? T[i + j * ld] : 0.0;
+  }
+  if (threadIdx.x == 0 && bad) {
+    atomicExch(M.flags + 1, 1);
+    atomicExch(M.flags + 2, t);
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_getrf(MatDev M, int slot, int t) {
+  __shared__ double T[64 * 65];
+  __shared__ double nrm;
+  __shared__ int bad;
+  double* N = M.N + (size_t)slot * M.lmax * M.lmax;
+  const int m = M.row.hi[t] - M.row.lo[t];
+  const int ld = 65;
+  for (int e = threadIdx.x; e < m * m; e += NT) T[(e % m) + (e / m) * ld] = N[(e % m) + (e / m) * M.lmax];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int e = 0; e < m * m; ++e) s += T[(e % m) + (e / m) * ld] * T[(e % m) + (e / m) * ld];
+    nrm = sqrt(s);
+    bad = 0;
+  }
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    const double p = T[j + j * ld];
+    if (threadIdx.x == 0 && !(fabs(p) > 1e-14 * nrm)) bad = 1;
+    for (int i = j + 1 + threadIdx.x; i < m; i += NT) T[i + j * ld] /= p;
+    __syncthreads();
+    for (int e = threadIdx.x; e < (m - j - 1) * (m - j - 1); e += NT) {
+      const int i = j + 1 + e % (m - j - 1), c = j + 1 + e / (m - j - 1);
+      T[i + c * ld] -= T[i + j * ld] * T[j + c * ld];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < m * m; e += NT) N[(e % m) + (e / m) * M.lmax] = T[(e % m) + (e / m) * ld];
+  if (threadIdx.x == 0 && bad) {
+    atomicExch(M.flags + 1, 1);
+    atomicExch(M.flags + 2, t);
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_trsm(MatDev M, int slot, int m, int mode, double* B, int ldb, int brows,
+                                             Dim bcols) {
+  __shared__ double T[64 * 65];
+  const int ld = 65;
+  const double* N = M.N + (size_t)slot * M.lmax * M.lmax;
+  for (int e = threadIdx.x; e < m * m; e += NT) T[(e % m) + (e / m) * ld] = N[(e % m) + (e / m) * M.lmax];
+  __syncthreads();
+  const bool rowwise = (mode == RLT || mode == RUN);
+  const int nvec = rowwise ? brows : bcols.v();
+  for (int v = blockIdx.x * NT + threadIdx.x; v < nvec; v += gridDim.x * NT) {
+    // rowwise: x = row v of B (length m, stride ldb); columnwise: x = column v (length m, stride 1)
+    double* x = rowwise ? B + v : B + (size_t)v * ldb;
+    const int st = rowwise ? ldb : 1;
+    switch (mode) {
+      case RLT:  // x L^T = b  <=>  L x^T = b^T  forward
+      case LLN:
+      case LLU:
+        for (int j = 0; j < m; ++j) {
+          double acc = x[j * st];
+          for (int i = 0; i < j; ++i) acc -= T[j + i * ld] * x[i * st];
+          x[j * st] = mode == LLU ? acc : acc / T[j + j * ld];
+        }
+        break;
+      case LLT:  // L^T x = b  backward
+        for (int j = m - 1; j >= 0; --j) {
+          double acc = x[j * st];
+          for (int i = j + 1; i < m; ++i) acc -= T[i + j * ld] * x[i * st];
+          x[j * st] = acc / T[j + j * ld];
+        }
+        break;
+      case RUN:  // x U = b  <=>  U^T x^T = b^T  forward
+      case LUT:
+        for (int j = 0; j < m; ++j) {
+          double acc = x[j * st];
+          for (int i = 0; i < j; ++i) acc -= T[i + j * ld] * x[i * st];
+          x[j * st] = acc / T[j + j * ld];
+        }
+        break;
+      case LUN:  // U x = b  backward
+        for (int j = m - 1; j >= 0; --j) {
+          double acc = x[j * st];
+          for (int i = j + 1; i < m; ++i) acc -= T[j + i * ld] * x[i * st];
+          x[j * st] = acc / T[j + j * ld];
+        }
+        break;
+    }
+  }
+}
+
+// ---- tall R-factor by streaming TSQR (one CTA) --------------------------------------------------
+__global__ void __launch_bounds__(NT) k_tsqr_r(const double* A, int lda, int rows, Dim Kd, double* R, int ldr) {
+  extern __shared__ double sm[];
+  double* P = sm;  // PR x KC
+  double* diag = P + PR * KC;
+  double* red = diag + KC;
+  const int K = Kd.v();
+  int r = 0;  // rows currently in the panel
+  for (int r0 = 0; r0 < rows;) {
+    const int take = min(rows - r0, PR - r);
+    for (int e = threadIdx.x; e < take * K; e += NT) {
+      const int i = e % take, j = e / take;
+      P[r + i + j * PR] = A[r0 + i + (size_t)j * lda];
+    }
+    r += take;
+    r0 += take;
+    la::cta_qr_R(P, PR, r, K, diag, red);
+    r = min(r, K);
+  }
+  for (int e = threadIdx.x; e < K * K; e += NT) {
+    const int i = e % K, j = e / K;
+    R[i + j * ldr] = i < r ? P[i + j * PR] : 0.0;
+  }
+}
+
+// ---- temporary truncation core ----------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_temp_core(const double* Ra, const double* Rb, int ldr, Dim Kd, double* Ma,
+                                                  double* Mb, int ldm, int* rout, double rel, double abs_tol,
+                                                  int max_rank, int cap, int* flags) {
+  extern __shared__ double smt[];
+  double* Mm = smt;
+  double* M0 = Mm + KC * KC;
+  double* U = M0 + KC * KC;
+  double* sig = U + KC * KC;
+  int* order = (int*)(sig + KC);
+  int* scr = order + KC;
+  __shared__ int clamped;
+  const int K = Kd.v();
+  // M = Ra Rb^T
+  for (int e = threadIdx.x; e < K * K; e += NT) {
+    const int i = e % K, j = e / K;
+    double acc = 0.0;
+    for (int q = 0; q < K; ++q) acc += Ra[i + q * ldr] * Rb[j + q * ldr];
+    Mm[i + j * KC] = acc;
+    M0[i + j * KC] = acc;
+  }
+  if (threadIdx.x == 0) clamped = 0;
+  __syncthreads();
+  la::cta_jacobi(Mm, KC, K, K, sig, order, scr);
+  const int r = K > 0 ? la::trunc_rank(sig, order, K, rel, abs_tol, max_rank, cap, &clamped) : 0;
+  // U_r
+  for (int e = threadIdx.x; e < K * r; e += NT) {
+    const int i = e % K, q = e / K;
+    U[i + q * KC] = Mm[i + order[q] * KC] / sig[order[q]];
+  }
+  __syncthreads();
+  // V_r = M0^T U_r / sigma   (stored in Mm)
+  for (int e = threadIdx.x; e < K * r; e += NT) {
+    const int i = e % K, q = e / K;
+    double acc = 0.0;
+    for (int p = 0; p < K; ++p) acc += M0[p + i * KC] * U[p + q * KC];
+    Mm[i + q * KC] = acc / sig[order[q]];
+  }
+  __syncthreads();
+  // Ma = Rb^T V_r ; Mb = Ra^T U_r / sigma
+  for (int e = threadIdx.x; e < K * r; e += NT) {
+    const int i = e % K, q = e / K;
+    double a = 0.0, b = 0.0;
+    for (int p = 0; p < K; ++p) {
+      a += Rb[p + i * ldr] * Mm[p + q * KC];
+      b += Ra[p + i * ldr] * U[p + q * KC];
+    }
+    Ma[i + q * ldm] = a;
+    Mb[i + q * ldm] = b / sig[order[q]];
+  }
+  if (threadIdx.x == 0) {
+    *rout = r;
+    if (clamped) atomicOr(flags, 1);
+  }
+}
+
+__global__ void k_copy_cols(double* dst, int ldd, const double* src, int lds, int rows, Dim cols) {
+  const int c = cols.v();
+  const long long tot = (long long)rows * c;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % rows), j = (int)(e / rows);
+    dst[i + (size_t)j * ldd] = src[i + (size_t)j * lds];
+  }
+}
+
+__global__ void k_set_int(int* p, Dim v) { *p = v.v(); }
+__global__ void k_gather_cols(double* Bt, const double* x, const int64_t* perm, int n, int nrhs, int64_t ldx) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)n * nrhs; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n), c = (int)(e / n);
+    Bt[e] = x[perm[i] + c * ldx];
+  }
+}
+__global__ void k_scatter_cols(double* x, const double* Bt, const int64_t* perm, int n, int nrhs, int64_t ldx) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)n * nrhs; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n), c = (int)(e / n);
+    x[perm[i] + c * ldx] = Bt[e];
+  }
+}
+__global__ void k_rank_if(int* p, const int* a, const int* b) { *p = (*a > 0 && *b > 0) ? *b : 0; }
+// stack [T (rows x kT), zero-extended N (rows_new at row_off, knew cols)] -> dst (rows x (kT+knew))
+__global__ void k_stack(double* dst, int ldd, int rows, const double* T, int ldt, const int* kT, const double* Nw,
+                        int ldn, int row_off, int rows_new, Dim knew) {
+  const int kt = kT ? *kT : 0, kn = knew.v();
+  const long long tot = (long long)rows * (kt + kn);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e % rows), j = (int)(e / rows);
+    double v;
+    if (j < kt) v = T[i + (size_t)j * ldt];
+    else {
+      const int ii = i - row_off;
+      v = (ii >= 0 && ii < rows_new) ? Nw[ii + (size_t)(j - kt) * ldn] : 0.0;
+    }
+    dst[i + (size_t)j * ldd] = v;
+  }
+}
+// choose the Case-2 factorisation of C = S^X G S^Y (k1 x k2), reading R23:
+// k1 <= k2: A = V^X (Ca = I), B = W^Y C^T (Cb = C^T); else A = V^X C (Ca = C), B = W^Y (Cb = I)
+__global__ void k_choose(const double* Cm, int ldc, const int* k1p, const int* k2p, double* Ca, double* Cb, int ldo,
+                         int* kout) {
+  const int k1 = *k1p, k2 = *k2p;
+  const bool first = k1 <= k2;
+  const int kk = first ? k1 : k2;
+  for (int e = threadIdx.x; e < KC * KC; e += blockDim.x) {
+    const int i = e % KC, j = e / KC;
+    if (j < kk) {
+      if (i < k1) Ca[i + j * ldo] = first ? (i == j ? 1.0 : 0.0) : Cm[i + j * ldc];
+      if (i < k2) Cb[i + j * ldo] = first ? Cm[j + i * ldc] : (i == j ? 1.0 : 0.0);
+    }
+  }
+  if (threadIdx.x == 0) *kout = kk;
+}
+__global__ void k_identity(double* I, int ld, int m) {
+  for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < m * m; e += blockDim.x * gridDim.x)
+    I[(e % m) + (e / m) * ld] = (e % m) == (e / m) ? 1.0 : 0.0;
+}
+__global__ void k_transpose_tile(double* dst, int ldd, const double* src, int lds, int rows, int cols) {
+  for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < rows * cols; e += blockDim.x * gridDim.x) {
+    const int i = e % rows, j = e / rows;  // dst (rows x cols) = src^T
+    dst[i + j * ldd] = src[j + i * lds];
+  }
+}
+__global__ void k_add_int(int* p, Dim a, Dim b) { *p = a.v() + b.v(); }
+
+void level_seg(const h2_tree_* T, int root, int L, int* begin, int* count) {
+  *begin = 0;
+  *count = 0;
+  if (L > T->depth || L < T->level[root]) return;
+  const int* b = T->bfs.data() + T->level_ptr[L];
+  const int* e = T->bfs.data() + T->level_ptr[L + 1];
+  const int* lo = std::lower_bound(b, e, root);
+  const int* hi = std::lower_bound(b, e, root + T->tsize[root]);
+  *begin = (int)(lo - T->bfs.data());
+  *count = (int)(hi - lo);
+}
+
+void leaf_rng(const h2_tree_* T, int root, int* begin, int* count) {
+  const auto lo = std::lower_bound(T->leaves.begin(), T->leaves.end(), root);
+  const auto hi = std::lower_bound(T->leaves.begin(), T->leaves.end(), root + T->tsize[root]);
+  *begin = (int)(lo - T->leaves.begin());
+  *count = (int)(hi - lo);
+}
+
+constexpr size_t SM_TSQR = (size_t)(PR * KC + KC + 8) * 8;
+constexpr size_t SM_EXPAND = (size_t)(2 * KC * KC) * 8;
+constexpr size_t SM_TEMP = (size_t)(3 * KC * KC + KC) * 8 + (KC + 8) * 4;
+bool g_attr = false;
+void init_attr() {
+  if (g_attr) return;
+  cudaFuncSetAttribute(k_tsqr_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_TSQR);
+  cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXPAND);
+  cudaFuncSetAttribute(k_temp_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_TEMP);
+  g_attr = true;
+}
+
+}  // namespace
+
+void expand_basis(const MatDev& M, const DevSide& D, int t, double* out, int ld, cudaStream_t st) {
+  int l0, nl;
+  leaf_rng(D.tree, t, &l0, &nl);
+  init_attr();
+  k_expand<<<nl, NT, SM_EXPAND, st>>>(M, D, t, l0, out, ld);
+}
+
+void gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb, Dim m, Dim n,
+          Dim k, int mcap, int ncap, int kcap, double alpha, double beta, cudaStream_t st) {
+  if (mcap <= 0 || ncap <= 0) return;
+  if (kcap > 512 && mcap <= KC && ncap <= KC) {
+    if (!g_part) cudaMalloc(&g_part, sizeof(double) * NPART * KC * KC);
+    const int chunk = (kcap + NPART - 1) / NPART;
+    k_gemm_inner_part<<<NPART, NT, 0, st>>>(g_part, A, lda, ta, B, ldb, tb, m, n, k, chunk);
+    k_gemm_inner_sum<<<1, NT, 0, st>>>(C, ldc, g_part, NPART, m, n, alpha, beta);
+    return;
+  }
+  const long long tot = (long long)mcap * ncap;
+  k_gemm<<<std::max(1, std::min(cdiv(tot, NT), 4 * 148)), NT, 0, st>>>(C, ldc, A, lda, ta, B, ldb, tb, m, n, k,
+                                                                       alpha, beta);
+}
+
+void hmul_dense(const MatDev& M, bool trans, int a, int b, int b_blk, const double* D, int ldd, Dim m, int mcap,
+                double* out, int ldo, double alpha, double beta, cudaStream_t st) {
+  (void)b_blk;
+  (void)mcap;
+  const DevSide& Dd = trans ? M.col : M.row;  // rows of op(Z)
+  const DevSide& Ds = trans ? M.row : M.col;  // columns of op(Z)
+  const h2_tree_* Td = Dd.tree;
+  const h2_tree_* Ts = Ds.tree;
+  double* xh = Ds.hx;
+  double* yh = Dd.hy;
+  int l0, nl;
+  leaf_rng(Ts, b, &l0, &nl);
+  k_hm_fwd_leaf<<<nl, NT, 0, st>>>(M, Ds, l0, Ts->lo[b], D, ldd, m, xh);
+  for (int L = Ts->depth - 1; L >= Ts->level[b]; --L) {
+    int s0, ns;
+    level_seg(Ts, b, L, &s0, &ns);
+    if (ns) k_hm_fwd_level<<<ns, NT, 0, st>>>(M, Ds, s0, m, xh);
+  }
+  k_hm_couple<<<Td->tsize[a], NT, 0, st>>>(M, Dd, Ds, a, b, trans ? 1 : 0, m, xh, yh);
+  for (int L = Td->level[a] + 1; L <= Td->depth; ++L) {
+    int s0, ns;
+    level_seg(Td, a, L, &s0, &ns);
+    if (ns) k_hm_bwd_level<<<ns, NT, 0, st>>>(M, Dd, s0, m, yh);
+  }
+  int la0, nla;
+  leaf_rng(Td, a, &la0, &nla);
+  k_hm_leaf<<<nla, NT, 0, st>>>(M, Dd, Ds, la0, a, b, trans ? 1 : 0, D, ldd, m, yh, out, ldo, alpha, beta);
+}
+
+void tile_potrf(const MatDev& M, int slot, int t, cudaStream_t st) { k_potrf<<<1, NT, 0, st>>>(M, slot, t); }
+void tile_getrf(const MatDev& M, int slot, int t, cudaStream_t st) { k_getrf<<<1, NT, 0, st>>>(M, slot, t); }
+
+void tile_trsm(const MatDev& M, int slot, int m, int mode, double* B, int ldb, int brows, Dim bcols, int bcolcap,
+               cudaStream_t st) {
+  const bool rowwise = (mode == RLT || mode == RUN);
+  const int nvec = rowwise ? brows : bcolcap;
+  k_trsm<<<std::max(1, cdiv(nvec, NT)), NT, 0, st>>>(M, slot, m, mode, B, ldb, brows, bcols);
+}
+
+void tsqr_r(const double* A, int lda, int rows, Dim K, double* R, int ldr, cudaStream_t st) {
+  init_attr();
+  k_tsqr_r<<<1, NT, SM_TSQR, st>>>(A, lda, rows, K, R, ldr);
+}
+
+void temp_core(const double* Ra, const double* Rb, int ldr, Dim K, double* Ma, double* Mb, int ldm, int* rout,
+               double rel, double abs_tol, int max_rank, int cap, int* flags, cudaStream_t st) {
+  init_attr();
+  k_temp_core<<<1, NT, SM_TEMP, st>>>(Ra, Rb, ldr, K, Ma, Mb, ldm, rout, rel, abs_tol, max_rank, cap, flags);
+}
+
+void copy_cols(double* dst, int ldd, const double* src, int lds, int rows, Dim cols, int colcap, cudaStream_t st) {
+  const long long tot = (long long)rows * colcap;
+  if (tot <= 0) return;
+  k_copy_cols<<<std::max(1, std::min(cdiv(tot, NT), 4 * 148)), NT, 0, st>>>(dst, ldd, src, lds, rows, cols);
+}
+
+void set_int(int* p, Dim v, cudaStream_t st) { k_set_int<<<1, 1, 0, st>>>(p, v); }
+void gather_cols(double* Bt, const double* x, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t st) {
+  k_gather_cols<<<std::max(1, std::min(cdiv((long long)n * nrhs, NT), 8 * 148)), NT, 0, st>>>(Bt, x, perm, n, nrhs, ldx);
+}
+void scatter_cols(double* x, const double* Bt, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t st) {
+  k_scatter_cols<<<std::max(1, std::min(cdiv((long long)n * nrhs, NT), 8 * 148)), NT, 0, st>>>(x, Bt, perm, n, nrhs, ldx);
+}
+void rank_if(int* p, const int* a, const int* b, cudaStream_t st) { k_rank_if<<<1, 1, 0, st>>>(p, a, b); }
+void stack_cols(double* dst, int ldd, int rows, const double* T, int ldt, const int* kT, const double* Nw, int ldn,
+                int row_off, int rows_new, Dim knew, int colcap, cudaStream_t st) {
+  const long long tot = (long long)rows * colcap;
+  k_stack<<<std::max(1, std::min(cdiv(tot, NT), 4 * 148)), NT, 0, st>>>(dst, ldd, rows, T, ldt, kT, Nw, ldn, row_off,
+                                                                        rows_new, knew);
+}
+void choose_case2(const double* Cm, int ldc, const int* k1, const int* k2, double* Ca, double* Cb, int ldo, int* kout,
+                  cudaStream_t st) {
+  k_choose<<<1, NT, 0, st>>>(Cm, ldc, k1, k2, Ca, Cb, ldo, kout);
+}
+void identity(double* I, int ld, int m, cudaStream_t st) { k_identity<<<std::max(1, cdiv(m * m, NT)), NT, 0, st>>>(I, ld, m); }
+void transpose_tile(double* dst, int ldd, const double* src, int lds, int rows, int cols, cudaStream_t st) {
+  k_transpose_tile<<<std::max(1, cdiv(rows * cols, NT)), NT, 0, st>>>(dst, ldd, src, lds, rows, cols);
+}
+void add_int(int* p, Dim a, Dim b, cudaStream_t st) { k_add_int<<<1, 1, 0, st>>>(p, a, b); }
+
+}  // namespace h2

@@ -1,0 +1,65 @@
+// Device primitives of the H^2 product / substitution / factorization.
+// Every shape that depends on a rank lives in device memory (Dim), so the host recursion never
+// synchronises on the device.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "h2_internal.h"
+
+namespace h2 {
+
+// a dimension: (p ? *p : 0) + c, resolved on the device
+struct Dim {
+  const int* p;
+  int c;
+#ifdef __CUDACC__
+  __device__ __forceinline__ int v() const { return (p ? *p : 0) + c; }
+#endif
+};
+inline Dim dimc(int c) { return Dim{nullptr, c}; }
+inline Dim dimp(const int* p, int c = 0) { return Dim{p, c}; }
+
+// An operand op(Z) (Z or Z^T) of the product: "rows" basis / "cols" basis / coupling orientation.
+struct DevOp {
+  const MatDev* M;  // host copy of the device descriptor
+  bool trans;
+};
+
+// ---- launchers (h2_arith.cu) -------------------------------------------------------------------
+// out (|t| x k_t, ld) = full nested basis of cluster t of one side (eq. (1))
+void expand_basis(const MatDev& M, const DevSide& D, int t, double* out, int ld, cudaStream_t st);
+// C (m x n) = alpha op(A) op(B) + beta C, dims on the device (caps on the host for grid sizes)
+void gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb, Dim m, Dim n,
+          Dim k, int mcap, int ncap, int kcap, double alpha, double beta, cudaStream_t st);
+// out (|a| x m) = beta out + op(Z)|_{a x b} D,  D: |b| x m  (H^2 block times dense, [BO10 Thm 3.42])
+void hmul_dense(const MatDev& M, bool trans, int a, int b, int b_blk, const double* D, int ldd, Dim m, int mcap,
+                double* out, int ldo, double alpha, double beta, cudaStream_t st);
+// dense tiles (nearfield slots): Cholesky / no-pivot LU in place; breakdown -> flags[1], flags[2] = cluster
+void tile_potrf(const MatDev& M, int slot, int t, cudaStream_t st);
+void tile_getrf(const MatDev& M, int slot, int t, cudaStream_t st);
+// triangular solves with a diagonal tile T (m x m, ld lmax):
+enum TrsmMode { RLT = 0, LLN, LLU, LLT, RUN, LUN, LUT };
+void tile_trsm(const MatDev& M, int slot, int m, int mode, double* B, int ldb, int brows, Dim bcols, int bcolcap,
+               cudaStream_t st);
+// R-factor (K x K, ld kc) of the tall matrix A (rows x K, K on the device <= 64)
+void tsqr_r(const double* A, int lda, int rows, Dim K, double* R, int ldr, cudaStream_t st);
+// temporary truncation core: from Ra, Rb (K x K) -> Ma = Rb^T V_r, Mb = Ra^T U_r S_r^-1 (K x r), r -> *rout
+void temp_core(const double* Ra, const double* Rb, int ldr, Dim K, double* Ma, double* Mb, int ldm, int* rout,
+               double rel, double abs_tol, int max_rank, int cap, int* flags, cudaStream_t st);
+// copy a (rows x cols) block with device column count into dst (zero-extended rows are the caller's)
+void copy_cols(double* dst, int ldd, const double* src, int lds, int rows, Dim cols, int colcap, cudaStream_t st);
+void set_int(int* p, Dim v, cudaStream_t st);
+void rank_if(int* p, const int* a, const int* b, cudaStream_t st);  // *p = (*a>0 && *b>0) ? *b : 0
+void stack_cols(double* dst, int ldd, int rows, const double* T, int ldt, const int* kT, const double* Nw, int ldn,
+                int row_off, int rows_new, Dim knew, int colcap, cudaStream_t st);
+void choose_case2(const double* Cm, int ldc, const int* k1, const int* k2, double* Ca, double* Cb, int ldo, int* kout,
+                  cudaStream_t st);
+void identity(double* I, int ld, int m, cudaStream_t st);
+void transpose_tile(double* dst, int ldd, const double* src, int lds, int rows, int cols, cudaStream_t st);
+void add_int(int* p, Dim a, Dim b, cudaStream_t st);
+// tree-order <-> original-order for n x nrhs blocks: Bt[i, c] = x[perm[i] + c ldx], x[perm[i] + c ldx] = Bt[i, c]
+void gather_cols(double* Bt, const double* x, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t st);
+void scatter_cols(double* x, const double* Bt, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t st);
+
+}  // namespace h2

@@ -340,8 +340,8 @@ extern "C" h2_status h2_from_sparse(h2_btree bt, int64_t n, const int64_t* rowpt
     H2_FAIL(H2_ERR_ARG, "h2_from_sparse: NULL CSR array");
   if (storage != H2_FULL && storage != H2_LOWER) H2_FAIL(H2_ERR_ARG, "h2_from_sparse: bad storage");
   if (storage == H2_LOWER && R != C) H2_FAIL(H2_ERR_ARG, "h2_from_sparse: H2_LOWER needs one shared tree");
-  if (rank_cap < 1 || update_cap < 0 || rank_cap + update_cap > KCAP_MAX)
-    H2_FAIL(H2_ERR_ARG, "h2_from_sparse: need rank_cap >= 1, update_cap >= 0, rank_cap + update_cap <= 64");
+  if (rank_cap < 1 || rank_cap > RCAP_MAX || update_cap < 0 || rank_cap + update_cap > KCAP_MAX)
+    H2_FAIL(H2_ERR_ARG, "h2_from_sparse: need 1 <= rank_cap <= 48, update_cap >= 0, rank_cap + update_cap <= 96");
   int lmax = 0;
   for (int t : R->leaves) lmax = std::max(lmax, R->hi[t] - R->lo[t]);
   for (int t : C->leaves) lmax = std::max(lmax, C->hi[t] - C->lo[t]);
@@ -522,20 +522,10 @@ extern "C" h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t
   a.rel_tol = tc.rel_tol;
   a.abs_tol = tc.abs_tol;
   a.max_rank = tc.max_rank;
+  a.kdev = nullptr;
+  a.prof = nullptr;
   CUDA_TRY(launch_update(Z, a, (cudaStream_t)stream));
   return H2_OK;
-}
-
-extern "C" h2_status h2_addmul(h2_mat, double, h2_mat, h2_mat, const h2_trunc*, h2_stream) {
-  H2_FAIL(H2_ERR_UNSUPPORTED, "h2_addmul: not available in this build");
-}
-
-extern "C" h2_status h2_lr_factor(h2_mat, h2_factor_kind, const h2_trunc*, h2_stream) {
-  H2_FAIL(H2_ERR_UNSUPPORTED, "h2_lr_factor: not available in this build");
-}
-
-extern "C" h2_status h2_solve(h2_mat, double*, int32_t, int64_t, h2_stream) {
-  H2_FAIL(H2_ERR_UNSUPPORTED, "h2_solve: not available in this build");
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -554,8 +544,22 @@ extern "C" h2_status h2_ranks(h2_mat Z, int32_t* row_rank, int32_t* col_rank) {
 extern "C" h2_status h2_check_device_flags(h2_mat Z, int32_t* flags) {
   if (!Z || !flags) H2_FAIL(H2_ERR_ARG, "h2_check_device_flags: NULL argument");
   CUDA_TRY(cudaDeviceSynchronize());
-  CUDA_TRY(cudaMemcpy(flags, Z->d.flags, sizeof(int32_t), cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemset(Z->d.flags, 0, sizeof(int32_t)));
+  int32_t f[3];
+  CUDA_TRY(cudaMemcpy(f, Z->d.flags, sizeof(f), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemset(Z->d.flags, 0, 3 * sizeof(int32_t)));
+  flags[0] = f[0] | (f[1] ? 2 : 0);
+  if (f[1]) {
+    char msg[160];
+    snprintf(msg, sizeof msg, "dense leaf breakdown (non-positive / tiny pivot) in the diagonal tile of cluster %d", f[2]);
+    h2::set_error(msg);
+    return H2_ERR_BREAKDOWN;
+  }
+  return H2_OK;
+}
+
+extern "C" h2_status h2_stats(h2_mat Z, int64_t out[4]) {
+  if (!Z || !out) H2_FAIL(H2_ERR_ARG, "h2_stats: NULL argument");
+  for (int i = 0; i < 4; ++i) out[i] = Z->stats[i];
   return H2_OK;
 }
 

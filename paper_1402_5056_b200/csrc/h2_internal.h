@@ -13,7 +13,8 @@
 
 namespace h2 {
 
-constexpr int KCAP_MAX = 64;  // extended rank capacity (rank_cap + update_cap) handled by the kernels
+constexpr int KCAP_MAX = 96;  // extended rank capacity (rank_cap + update_cap) handled by the kernels
+constexpr int RCAP_MAX = 48;  // stored rank capacity (2 * rank_cap <= KCAP_MAX rows of V^_t)
 constexpr int LMAX_MAX = 64;  // largest leaf cluster handled by the kernels
 constexpr int NTHREADS = 256; // threads per CTA of the small-matrix kernels
 
@@ -74,6 +75,8 @@ struct DevSide {
   int32_t* rnew = nullptr;  // new ranks
   // matvec workspace
   double* xh = nullptr;     // nclusters * rcap coefficients
+  double* hx = nullptr;     // H^2-block x dense workspace: nclusters * rcap * 64 (forward coefficients)
+  double* hy = nullptr;     // nclusters * rcap * 64 (coupling/backward coefficients)
 };
 
 // Everything a device kernel needs for one local update (passed by value).
@@ -88,6 +91,7 @@ struct UpdArgs {
   double rel_tol, abs_tol;
   int max_rank;
   double* prof;  // device flop/byte counters (profiling) or nullptr
+  const int* kdev;  // if set, the update rank is read from device memory (internal callers)
 };
 
 struct MatDev {
@@ -114,6 +118,13 @@ struct h2_mat_ {
   std::vector<int32_t> blk2adm, blk2inad;  // block id -> slot or -1
   std::vector<int32_t> inad_range;         // per block: [first,last) inadmissible slot in its subtree
   std::vector<void*> allocs;
+  // product / factorization state
+  double* ws = nullptr;
+  size_t ws_cap = 0;
+  int* iws = nullptr;
+  size_t iws_cap = 0;
+  int factored = 0;              // 0 no, 1 Cholesky, 2 LR
+  long long stats[4] = {0, 0, 0, 0};  // local updates, dense adds, temporaries issued by the driver
 };
 
 namespace h2 {

@@ -25,7 +25,8 @@ namespace h2 {
 namespace {
 
 constexpr int NT = NTHREADS;
-constexpr int KC = KCAP_MAX;      // 64
+constexpr int KC = KCAP_MAX;      // 96
+constexpr int RM = KC;            // row capacity of V~_t / V^_t in the SVD kernels: max(lmax, 2 rank_cap) <= 96
 constexpr int PR = 192;           // TSQR panel rows (>= KC + largest chunk)
 constexpr int LD2 = 2 * KC;       // rows of a stacked pair of KC x KC factors
 
@@ -36,8 +37,11 @@ __device__ __forceinline__ bool inside(const DevSide& D, int t, int root) {
 __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm, int mode);
 
 // ---- U0 + U1/U2 leaves + local weight stacks of the ancestors (all independent) ---------------
-__global__ void __launch_bounds__(NT) k_upd_ext_leaf(MatDev M, UpdArgs a, int rl0, int nrl, int cl0, int ncl,
+__global__ void __launch_bounds__(NT) k_upd_ext_leaf(MatDev M, UpdArgs a_, int rl0, int nrl, int cl0, int ncl,
                                                      int in0, int nin, int npA, int npB) {
+  UpdArgs a = a_;
+  if (a.kdev) a.k = *a.kdev;
+  if (a.k <= 0) return;
   extern __shared__ double sm[];
   const int b = blockIdx.x;
   if (b >= nrl + ncl + nin) {
@@ -99,7 +103,10 @@ __global__ void __launch_bounds__(NT) k_upd_ext_leaf(MatDev M, UpdArgs a, int rl
 }
 
 // ---- U2 internal, bottom-up ------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_upd_ext_level(MatDev M, UpdArgs a, int bA, int nA, int bB, int nB) {
+__global__ void __launch_bounds__(NT) k_upd_ext_level(MatDev M, UpdArgs a_, int bA, int nA, int bB, int nB) {
+  UpdArgs a = a_;
+  if (a.kdev) a.k = *a.kdev;
+  if (a.k <= 0) return;
   extern __shared__ double sm[];
   const bool rs = (int)blockIdx.x < nA;
   const DevSide& D = rs ? M.row : M.col;
@@ -238,7 +245,10 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
   return fl;
 }
 
-__global__ void __launch_bounds__(NT) k_upd_weights_path(MatDev M, UpdArgs a) {
+__global__ void __launch_bounds__(NT) k_upd_weights_path(MatDev M, UpdArgs a_) {
+  UpdArgs a = a_;
+  if (a.kdev) a.k = *a.kdev;
+  if (a.k <= 0) return;
   extern __shared__ double sm[];
   const bool rs = blockIdx.x == 0;
   const DevSide& A = rs ? M.row : M.col;
@@ -251,7 +261,10 @@ __global__ void __launch_bounds__(NT) k_upd_weights_path(MatDev M, UpdArgs a) {
   if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_W_PATH, fl);
 }
 
-__global__ void __launch_bounds__(NT) k_upd_weights_level(MatDev M, UpdArgs a, int bA, int nA, int bB, int nB) {
+__global__ void __launch_bounds__(NT) k_upd_weights_level(MatDev M, UpdArgs a_, int bA, int nA, int bB, int nB) {
+  UpdArgs a = a_;
+  if (a.kdev) a.k = *a.kdev;
+  if (a.k <= 0) return;
   extern __shared__ double sm[];
   const bool rs = (int)blockIdx.x < nA;
   const DevSide& A = rs ? M.row : M.col;
@@ -265,18 +278,18 @@ __global__ void __launch_bounds__(NT) k_upd_weights_level(MatDev M, UpdArgs a, i
 __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, int t, double* V, int ldv, int m,
                          int K, double* sm_rest, int kid, double extra_flops) {
   double* Bt = sm_rest;             // KC x KC
-  double* Mm = Bt + KC * KC;        // 64 x KC (ld 64)
-  double* Q = Mm + 64 * KC;         // 64 x KC (ld 64)
-  double* sig = Q + 64 * KC;        // KC
+  double* Mm = Bt + KC * KC;        // RM x KC (ld RM)
+  double* Q = Bt;                   // RM x KC (ld RM), reuses Bt once M = V B~^T is formed
+  double* sig = Mm + RM * KC;       // KC
   int* order = (int*)(sig + KC);    // KC ints
   int* scr = order + KC;            // 4 ints
   const double* Bg = D.bw + (size_t)t * M.kcap * M.kcap;
   la::cta_copy(Bt, KC, Bg, M.kcap, K, K);
   __syncthreads();
   // Mm = V Bt^T  (m x K)
-  la::cta_gemm(Mm, 64, V, ldv, false, Bt, KC, true, m, K, K, false);
+  la::cta_gemm(Mm, RM, V, ldv, false, Bt, KC, true, m, K, K, false);
   __syncthreads();
-  la::cta_jacobi(Mm, 64, m, K, sig, order, scr);
+  la::cta_jacobi(Mm, RM, m, K, sig, order, scr);
   __shared__ int clamped;
   if (threadIdx.x == 0) clamped = 0;
   __syncthreads();
@@ -285,14 +298,14 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
   for (int e = threadIdx.x; e < m * r; e += NT) {
     const int i = e % m, q = e / m;
     const int j = order[q];
-    Q[i + q * 64] = Mm[i + j * 64] / sig[j];
+    Q[i + q * RM] = Mm[i + j * RM] / sig[j];
   }
   __syncthreads();
   double* qn = D.qn + (size_t)t * M.ldq * M.rcap;
-  for (int e = threadIdx.x; e < m * r; e += NT) qn[(e % m) + (e / m) * M.ldq] = Q[(e % m) + (e / m) * 64];
+  for (int e = threadIdx.x; e < m * r; e += NT) qn[(e % m) + (e / m) * M.ldq] = Q[(e % m) + (e / m) * RM];
   // R_t = Q^T V  (r x K)
   double* rn = D.rn + (size_t)t * M.kcap * M.kcap;
-  la::cta_gemm(rn, M.kcap, Q, 64, true, V, ldv, false, r, K, m, false);
+  la::cta_gemm(rn, M.kcap, Q, RM, true, V, ldv, false, r, K, m, false);
   if (threadIdx.x == 0) {
     D.rnew[t] = r;
     if (clamped) atomicOr(M.flags, 1);
@@ -300,7 +313,10 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
   }
 }
 
-__global__ void __launch_bounds__(NT) k_upd_svd_leaf(MatDev M, UpdArgs a, int rl0, int nrl, int cl0, int ncl) {
+__global__ void __launch_bounds__(NT) k_upd_svd_leaf(MatDev M, UpdArgs a_, int rl0, int nrl, int cl0, int ncl) {
+  UpdArgs a = a_;
+  if (a.kdev) a.k = *a.kdev;
+  if (a.k <= 0) return;
   extern __shared__ double sm[];
   const bool rs = (int)blockIdx.x < nrl;
   const DevSide& D = rs ? M.row : M.col;
@@ -310,25 +326,28 @@ __global__ void __launch_bounds__(NT) k_upd_svd_leaf(MatDev M, UpdArgs a, int rl
   const int64_t ldx = rs ? a.ldx : a.ldy;
   const double al = rs ? a.alpha : 1.0;
   const int m = D.hi[t] - D.lo[t], kt = D.rank[t], K = kt + a.k;
-  double* V = sm;  // 64 x KC
+  double* V = sm;  // RM x KC
   const double* Vb = D.leafb + (size_t)D.leafidx[t] * M.lmax * M.rcap;
   const int off = D.lo[t] - D.lo[root];
   for (int e = threadIdx.x; e < m * K; e += NT) {
     const int i = e % m, j = e / m;
-    V[i + j * 64] = j < kt ? Vb[i + (size_t)j * M.lmax] : al * Xf[off + i + (size_t)(j - kt) * ldx];
+    V[i + j * RM] = j < kt ? Vb[i + (size_t)j * M.lmax] : al * Xf[off + i + (size_t)(j - kt) * ldx];
   }
   __syncthreads();
-  svd_core(M, a, D, t, V, 64, m, K, V + 64 * KC, K_SVD_LEAF, 0.0);
+  svd_core(M, a, D, t, V, RM, m, K, V + RM * KC, K_SVD_LEAF, 0.0);
 }
 
-__global__ void __launch_bounds__(NT) k_upd_svd_level(MatDev M, UpdArgs a, int bA, int nA, int bB, int nB) {
+__global__ void __launch_bounds__(NT) k_upd_svd_level(MatDev M, UpdArgs a_, int bA, int nA, int bB, int nB) {
+  UpdArgs a = a_;
+  if (a.kdev) a.k = *a.kdev;
+  if (a.k <= 0) return;
   extern __shared__ double sm[];
   const bool rs = (int)blockIdx.x < nA;
   const DevSide& D = rs ? M.row : M.col;
   const int t = D.bfs[rs ? bA + blockIdx.x : bB + blockIdx.x - nA];
   if (D.son0[t] < 0) return;
   const int k = a.k, kt = D.rank[t], K = kt + k;
-  double* V = sm;  // 64 x KC : V^_t = [R_{t1} E~_{t1}; R_{t2} E~_{t2}]
+  double* V = sm;  // RM x KC : V^_t = [R_{t1} E~_{t1}; R_{t2} E~_{t2}]
   int row0 = 0;
   for (int q = 0; q < 2; ++q) {
     const int c = q ? D.son1[t] : D.son0[t];
@@ -344,7 +363,7 @@ __global__ void __launch_bounds__(NT) k_upd_svd_level(MatDev M, UpdArgs a, int b
       } else {
         v = RN[i + (kc + j - kt) * M.kcap];
       }
-      V[row0 + i + j * 64] = v;
+      V[row0 + i + j * RM] = v;
     }
     row0 += rc;
   }
@@ -354,11 +373,14 @@ __global__ void __launch_bounds__(NT) k_upd_svd_level(MatDev M, UpdArgs a, int b
     const int c = q ? D.son1[t] : D.son0[t];
     fv += 2.0 * D.rnew[c] * D.rank[c] * kt;
   }
-  svd_core(M, a, D, t, V, 64, row0, K, V + 64 * KC, K_SVD_LEVEL, fv);
+  svd_core(M, a, D, t, V, RM, row0, K, V + RM * KC, K_SVD_LEVEL, fv);
 }
 
 // ---- U5 couplings ------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_upd_couple(MatDev M, UpdArgs a, int nA, int nB) {
+__global__ void __launch_bounds__(NT) k_upd_couple(MatDev M, UpdArgs a_, int nA, int nB) {
+  UpdArgs a = a_;
+  if (a.kdev) a.k = *a.kdev;
+  if (a.k <= 0) return;
   extern __shared__ double sm[];
   double* T1 = sm;             // KC x KC (ld KC)
   double* Out = T1 + KC * KC;  // KC x KC (ld KC)
@@ -425,7 +447,10 @@ __global__ void __launch_bounds__(NT) k_upd_couple(MatDev M, UpdArgs a, int nA, 
 }
 
 // ---- U6 install --------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_upd_install(MatDev M, UpdArgs a, int nA, int nB) {
+__global__ void __launch_bounds__(NT) k_upd_install(MatDev M, UpdArgs a_, int nA, int nB) {
+  UpdArgs a = a_;
+  if (a.kdev) a.k = *a.kdev;
+  if (a.k <= 0) return;
   extern __shared__ double sm[];
   const bool rs = (int)blockIdx.x < nA;
   const DevSide& D = rs ? M.row : M.col;
@@ -461,7 +486,10 @@ __global__ void __launch_bounds__(NT) k_upd_install(MatDev M, UpdArgs a, int nA,
 }
 
 // ---- memoised R-factors on pred(t0) ----------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_upd_rcache_path(MatDev M, UpdArgs a) {
+__global__ void __launch_bounds__(NT) k_upd_rcache_path(MatDev M, UpdArgs a_) {
+  UpdArgs a = a_;
+  if (a.kdev) a.k = *a.kdev;
+  if (a.k <= 0) return;
   extern __shared__ double sm[];
   const bool rs = blockIdx.x == 0;
   const DevSide& D = rs ? M.row : M.col;
@@ -500,7 +528,7 @@ __global__ void __launch_bounds__(NT) k_upd_rcache_path(MatDev M, UpdArgs a) {
 constexpr size_t SM_WEIGHTS = (size_t)(PR * KC + KC + 8) * 8;
 constexpr size_t SM_EXT_LEAF = SM_WEIGHTS;  // also runs the ancestors' local weight stacks
 constexpr size_t SM_EXT_LEVEL = (size_t)(LD2 * KC + KC + 8) * 8;
-constexpr size_t SM_SVD = (size_t)(64 * KC + KC * KC + 64 * KC + 64 * KC + KC + KC) * 8 + 64;
+constexpr size_t SM_SVD = (size_t)(RM * KC + KC * KC + RM * KC + KC) * 8 + (KC + 8) * 4;
 constexpr size_t SM_COUPLE = (size_t)(2 * KC * KC) * 8;
 constexpr size_t SM_INSTALL = (size_t)(KC * KC) * 8;
 

@@ -18,7 +18,7 @@ EXPORTED_SYMBOLS = [
     "h2_block_tree", "h2_btree_export", "h2_btree_destroy",
     "h2_from_sparse", "h2_lowrank_update", "h2_matvec", "h2_addmul", "h2_lr_factor", "h2_solve",
     "h2_ranks", "h2_storage_report", "h2_export", "h2_check_device_flags",
-    "h2_profile_enable", "h2_profile_read",
+    "h2_profile_enable", "h2_profile_read", "h2_stats",
     "h2_mat_destroy", "h2_last_error",
 ]
 
@@ -52,6 +52,7 @@ _sig = {
     "h2_export": [_p, _p, _p, _p, _p, _p, _p, _p],
     "h2_check_device_flags": [_p, _p],
     "h2_profile_enable": [_i32],
+    "h2_stats": [_p, _p],
     "h2_profile_read": [_p, _p, _p, _p, _p, _p],
     "h2_mat_destroy": [_p],
     "h2_last_error": [],
@@ -237,7 +238,15 @@ def h2_lr_factor(A: Mat, cholesky: bool = True, trunc=None, stream=None):
 
 
 def h2_solve(F: Mat, x, nrhs: int = 1, ldx: int | None = None, stream=None):
+    """x <- F^{-1} x in place (x: torch float64 CUDA, n x nrhs column-major, ORIGINAL order)."""
     _check(_lib.h2_solve(F.h, _ptr(x), int(nrhs), int(ldx or F.n), _stream(stream)))
+    return x
+
+
+def h2_stats(Z: Mat):
+    out = np.zeros(4, dtype=np.int64)
+    _check(_lib.h2_stats(Z.h, _ptr(out)))
+    return dict(updates=int(out[0]), dense_adds=int(out[1]), temporaries=int(out[2]))
 
 
 def h2_ranks(Z: Mat):

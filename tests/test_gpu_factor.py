@@ -1,0 +1,141 @@
+"""GPU parity of the product, the LR/Cholesky factorizations and the solves (through the C ABI)
+against the oracle on the same seeded inputs (north_star bars: ranks bit-exact, operators on 16
+probes <= 10 eps (adaptive) / <= 1e-9 (fixed rank), PCG iterations +-1, Err within 1e-2 rel.)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from inputs import config
+from inputs.rng import stream, RHS, POWER
+from inputs.updates import c0_global_factors, mixed_stream
+from oracle.structure import ClusterTree, BlockTree
+from oracle.h2 import from_sparse as o_from_sparse
+from oracle.update import Updater, Trunc as OTrunc
+from oracle.arith import Arith, Op, pcg, power_error
+from h2util import setup, operator_rel_diff, gpu_apply, all_targets
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+import paper_1402_5056_b200 as P  # noqa: E402
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _ranks_equal(Z, OZ):
+    kr, kc = P.h2_ranks(Z)
+    np.testing.assert_array_equal(kr, OZ.k)
+    np.testing.assert_array_equal(kc, OZ.l)
+
+
+def _gpu_solve(Z, b):
+    x = _t(b.copy())
+    P.h2_solve(Z, x)
+    return x.cpu().numpy()
+
+
+@pytest.mark.parametrize("name,N", [("C0", None), ("C2", 64)])
+def test_cholesky_parity(name, N):
+    eps = 1e-4
+    s = setup(name, N, lower=True)
+    OZ, Z, A = s["OZ"], s["Z"], s["c"]["A"]
+    ar = Arith(OZ, OTrunc(eps))
+    ar.chol()
+    P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps))
+    assert P.h2_check_device_flags(Z) == 0
+    _ranks_equal(Z, OZ)
+    d = operator_rel_diff(Z, OZ, s["ot"].n)
+    print(f"{name} Cholesky: L operator rel diff {d:.2e}, stats {P.h2_stats(Z)} oracle {ar.stats}")
+    assert d <= 10 * eps
+    # solves, PCG iterations and the convergence factor
+    n = s["ot"].n
+    b = stream(RHS).standard_normal(n)
+    xs_g, xs_o = _gpu_solve(Z, b), ar.solve(b)
+    assert np.linalg.norm(xs_g - xs_o) / np.linalg.norm(xs_o) <= 10 * eps
+    _, m_o, _ = pcg(lambda v: A @ v, lambda v: ar.solve(v), b)
+    _, m_g, rel = pcg(lambda v: A @ v, lambda v: _gpu_solve(Z, v), b)
+    assert rel < 1e-8 and abs(m_g - m_o) <= 1
+    x0 = stream(POWER).standard_normal(n)
+    e_o = power_error(lambda v: A @ v, lambda v: ar.solve(v), x0)
+    e_g = power_error(lambda v: A @ v, lambda v: _gpu_solve(Z, v), x0)
+    print(f"{name}: PCG m gpu {m_g} oracle {m_o}; Err gpu {e_g:.4f} oracle {e_o:.4f}")
+    assert abs(e_g - e_o) <= 1e-2 * max(e_o, 1e-12) + 1e-12
+
+
+def test_lr_parity_c0_rank8():
+    """C0 protocol (R15): rank-8 update with alpha = 1/n on every admissible leaf, then LR."""
+    eps = 1e-4
+    s = setup("C0", rank_cap=48, update_cap=48)  # LR ranks reach 38 on this case
+    OZ, Z, ot, ob = s["OZ"], s["Z"], s["ot"], s["ob"]
+    n = ot.n
+    X, Y = c0_global_factors(n)
+    Xt, Yt = X[ot.perm], Y[ot.perm]
+    up = Updater(OZ, OTrunc(eps))
+    keep = []
+    for b in ob.adm:
+        t0, s0 = int(ob.t[b]), int(ob.s[b])
+        xa, ya = Xt[ot.lo[t0]:ot.hi[t0]], Yt[ot.lo[s0]:ot.hi[s0]]
+        up(t0, s0, xa, ya, alpha=1.0 / n)
+        keep.append(P.h2_lowrank_update(Z, t0, s0, _t(xa), _t(ya), alpha=1.0 / n, trunc=P.Trunc(eps)))
+    ar = Arith(OZ, OTrunc(eps))
+    ar.lr()
+    P.h2_lr_factor(Z, cholesky=False, trunc=P.Trunc(eps))
+    assert P.h2_check_device_flags(Z) == 0
+    _ranks_equal(Z, OZ)
+    d = operator_rel_diff(Z, OZ, n)
+    print(f"C0 LR: operator rel diff {d:.2e}")
+    assert d <= 10 * eps
+    b = stream(RHS).standard_normal(n)
+    xg, xo = _gpu_solve(Z, b), ar.solve(b, cholesky=False)
+    assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) <= 10 * eps
+
+
+def test_addmul_parity():
+    eps = 1e-6
+    c = config("C0")
+    t = P.h2_cluster_tree(c["points"], c["leaf"])
+    bt = P.h2_block_tree(t, t, c["eta"])
+    ot = ClusterTree(c["points"], c["leaf"])
+    ob = BlockTree(ot, ot, c["eta"])
+    targets = all_targets(ot, ob)
+    mats, omats = [], []
+    for seed in (1, 2):
+        G = P.h2_from_sparse(bt, c["A"])
+        O = o_from_sparse(ob, c["A"])
+        up = Updater(O, OTrunc(1e-12))
+        keep = []
+        for t0, s0, a, b in mixed_stream(targets, 6, 4, seed=seed):
+            up(t0, s0, a, b)
+            keep.append(P.h2_lowrank_update(G, t0, s0, _t(a), _t(b), trunc=P.Trunc(1e-12)))
+        mats.append(G)
+        omats.append(O)
+    Z = P.h2_from_sparse(bt, c["A"] * 0.5)
+    OZ = o_from_sparse(ob, c["A"] * 0.5)
+    Arith(OZ, OTrunc(eps)).addmul(-0.75, Op(omats[0]), Op(omats[1]), 0, 0, 0)
+    P.h2_addmul(Z, -0.75, mats[0], mats[1], trunc=P.Trunc(eps))
+    assert P.h2_check_device_flags(Z) == 0
+    _ranks_equal(Z, OZ)
+    d = operator_rel_diff(Z, OZ, ot.n)
+    print(f"addmul parity rel diff {d:.2e}, stats {P.h2_stats(Z)}")
+    assert d <= 10 * eps
+    # A*A of the sparse matrix: exact (far field zero, R14)
+    A1 = P.h2_from_sparse(bt, c["A"])
+    Z2 = P.h2_from_sparse(bt, c["A"] * 0.0)
+    P.h2_addmul(Z2, 1.0, A1, A1, trunc=P.Trunc(eps))
+    Ad = c["A"].toarray()
+    Xp = np.random.default_rng(3).standard_normal((ot.n, 3))
+    assert np.abs(gpu_apply(Z2, Xp) - Ad @ (Ad @ Xp)).max() < 1e-11
+
+
+def test_cholesky_breakdown_reported():
+    c = config("C0")
+    t = P.h2_cluster_tree(c["points"], c["leaf"])
+    bt = P.h2_block_tree(t, t, c["eta"])
+    Z = P.h2_from_sparse(bt, -c["A"], lower=True)  # negative definite
+    P.h2_lr_factor(Z, cholesky=True)
+    with pytest.raises(P.H2Error) as e:
+        P.h2_check_device_flags(Z)
+    assert e.value.status == "H2_ERR_BREAKDOWN"
