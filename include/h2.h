@@ -169,6 +169,9 @@ h2_status h2_check_device_flags(h2_mat Z, int32_t* flags);
 h2_status h2_profile_enable(int32_t on);
 h2_status h2_profile_read(char* names, int64_t* launches, double* ms_total, double* flops, double* bytes,
                           int32_t* count);
+/* Profiling sub-phase counters of the SVD items (cycles: load+GEMM, Jacobi, output; count; sum K;
+ * sum m; sum of Jacobi sweeps), out[16]. */
+h2_status h2_profile_debug(double out[16]);
 
 void h2_mat_destroy(h2_mat Z);
 const char* h2_last_error(void);

@@ -14,6 +14,24 @@ __device__ __forceinline__ int pow2floor(int x) {
   return p;
 }
 
+// 1/x and 1/sqrt(x) to full FP64 accuracy: float seed (MUFU) + two Newton steps; falls back to
+// the IEEE operations outside the float range.
+__device__ __forceinline__ double fast_rcp(double x) {
+  const double ax = fabs(x);
+  if (!(ax > 1e-30 && ax < 1e30)) return 1.0 / x;
+  double r = (double)__frcp_rn((float)x);
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  if (!(x > 1e-30 && x < 1e30)) return 1.0 / sqrt(x);
+  double r = (double)rsqrtf((float)x);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  return r;
+}
+
 __device__ __forceinline__ unsigned group_mask(int S) {
   if (S >= 32) return 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -189,7 +207,7 @@ __device__ __forceinline__ void cta_copy(double* D, int ldd, const double* Sx, i
 // round-robin ordering, p/2 disjoint pairs per round).  On return column j of M is sigma_j u_j
 // (unsorted); sig[j] = |M(:,j)|; order[q] = index of the q-th largest sigma (ties by index).
 // scratch: >= 2 ints of shared memory.
-static __device__ void cta_jacobi(double* M, int ldm, int m, int p, double* sig, int* order, int* scratch) {
+static __device__ int cta_jacobi(double* M, int ldm, int m, int p, double* sig, int* order, int* scratch) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int pp = p + (p & 1);
   const int npairs = pp / 2;
@@ -201,7 +219,9 @@ static __device__ void cta_jacobi(double* M, int ldm, int m, int p, double* sig,
   const double tol = (m > 8 ? m : 8) * 2.220446049250313e-16;
   const double tol2 = tol * tol;
   const int nr = pp - 1;  // rounds per sweep
+  int nsw = 0;
   for (int sweep = 0; sweep < 40 && p > 1; ++sweep) {
+    ++nsw;
     if (tid == 0) scratch[0] = 0;
     __syncthreads();
     for (int r = 0; r < nr; ++r) {
@@ -230,11 +250,16 @@ static __device__ void cta_jacobi(double* M, int ldm, int m, int p, double* sig,
         ga += __shfl_xor_sync(0xffffffffu, ga, o);
       }
       if (a >= 0 && ga != 0.0 && ga * ga > tol2 * al * be) {
-        const double zeta = (be - al) / (2.0 * ga);
+        // tan of the Jacobi angle, t = sign(z) / (|z| + sqrt(1 + z^2)), z = (beta - alpha) / (2 gamma);
+        // reciprocals / rsqrt from a float seed + Newton steps in FP64 (full precision, fewer cycles)
+        const double zeta = (be - al) * fast_rcp(2.0 * ga);
         double t;
-        if (fabs(zeta) > 1e150) t = 0.5 / zeta;
-        else t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        if (fabs(zeta) > 1e15) t = 0.5 * fast_rcp(zeta);
+        else {
+          const double w = 1.0 + zeta * zeta;
+          t = copysign(fast_rcp(fabs(zeta) + w * fast_rsqrt(w)), zeta);
+        }
+        const double cs = fast_rsqrt(1.0 + t * t), sn = cs * t;
         for (int i = g; i < m; i += G) {
           const double x = M[i + a * ldm], y = M[i + b * ldm];
           M[i + a * ldm] = cs * x - sn * y;
@@ -262,6 +287,7 @@ static __device__ void cta_jacobi(double* M, int ldm, int m, int p, double* sig,
     order[pos] = j;
   }
   __syncthreads();
+  return nsw;
 }
 
 // Rank rule of the truncation: r = #{sigma_q > max(rel sigma_1, abs)}, <= max_rank, <= cap.

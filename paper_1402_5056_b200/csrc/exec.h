@@ -1,0 +1,172 @@
+// Device-resident executor of the H^2 arithmetic.
+//
+// The host recursion (local update, product, substitutions, factorization) does not launch kernels:
+// it appends fixed-size op records to a list.  An op is "run item i of kind `code` for i < nitems";
+// consecutive ops are separated by a barrier when `barrier` is set.  The list is executed on the
+// device by one thread-block cluster (8 CTAs, cluster barriers between dependent ops); an op with
+// many items runs as its own full-grid launch.  All shapes that depend on ranks are read from
+// device memory by the items, so the list only depends on the block-tree structure.
+#pragma once
+#include <stdint.h>
+
+#include <cstring>
+#include <vector>
+
+#include "h2_internal.h"
+
+namespace h2 {
+
+struct Dim {
+  const int* p;
+  int c;
+#ifdef __CUDACC__
+  __device__ __forceinline__ int v() const { return (p ? *p : 0) + c; }
+#endif
+};
+inline Dim dimc(int c) { return Dim{nullptr, c}; }
+inline Dim dimp(const int* p, int c = 0) { return Dim{p, c}; }
+
+enum OpCode : int32_t {
+  OP_UPD_EXT_LEAF = 0,
+  OP_UPD_EXT_LEVEL,
+  OP_UPD_W_PATH,
+  OP_UPD_W_LEVEL,
+  OP_UPD_SVD_LEAF,
+  OP_UPD_SVD_LEVEL,
+  OP_UPD_COUPLE,
+  OP_UPD_INSTALL,
+  OP_UPD_RCACHE,
+  OP_EXPAND,
+  OP_GEMM,
+  OP_GEMM_PART,
+  OP_GEMM_SUM,
+  OP_HM_FWD_LEAF,
+  OP_HM_FWD_LEVEL,
+  OP_HM_COUPLE,
+  OP_HM_BWD_LEVEL,
+  OP_HM_LEAF,
+  OP_POTRF,
+  OP_GETRF,
+  OP_TRSM,
+  OP_TSQR,
+  OP_TEMP,
+  OP_COPY_COLS,
+  OP_SET_INT,
+  OP_ADD_INT,
+  OP_RANK_IF,
+  OP_STACK,
+  OP_CHOOSE,
+  OP_IDENTITY,
+  OP_TRANSPOSE,
+  OP_GATHER,
+  OP_SCATTER,
+  OP_ZERO,
+  OP_COUNT
+};
+
+// ---- payloads ---------------------------------------------------------------------------------
+struct PUpd {
+  UpdArgs a;
+  int i[8];
+};
+struct PExpand {
+  int side, t, l0, ld;
+  double* out;
+};
+struct PGemm {
+  double* C;
+  const double* A;
+  const double* B;
+  int ldc, lda, ldb, ta, tb, chunk;
+  Dim m, n, k;
+  double alpha, beta;
+};
+struct PHm {  // all H^2-block x dense items
+  int dside, sside, a, b, trans, l0, base_lo, ldd, ldo;
+  const double* D;
+  double* xh;
+  double* yh;
+  double* out;
+  Dim m;
+  double alpha, beta;
+};
+struct PTile {
+  int slot, t, m, mode, ldb, brows;
+  double* B;
+  Dim bcols;
+};
+struct PTsqr {
+  const double* A;
+  double* R;
+  int lda, rows, ldr;
+  Dim K;
+};
+struct PTemp {
+  const double* Ra;
+  const double* Rb;
+  double* Ma;
+  double* Mb;
+  int* rout;
+  int* flags;
+  int ldr, ldm, max_rank, cap;
+  Dim K;
+  double rel, abs_tol;
+};
+struct PMisc {  // small data-movement ops
+  double* dst;
+  const double* src;
+  const int64_t* perm;
+  int* ip;
+  const int* ia;
+  const int* ib;
+  int ldd, lds, rows, cols, row_off, rows_new;
+  int64_t ldx;
+  Dim d1, d2;
+};
+
+constexpr int OP_PAYLOAD = 176;
+struct alignas(16) OpRec {
+  int32_t code;
+  int32_t nitems;
+  int32_t barrier;
+  int32_t mat;  // index of the matrix descriptor (0..2) the op uses
+  unsigned char p[OP_PAYLOAD];
+};
+static_assert(sizeof(PUpd) <= OP_PAYLOAD, "payload");
+static_assert(sizeof(PGemm) <= OP_PAYLOAD, "payload");
+static_assert(sizeof(PHm) <= OP_PAYLOAD, "payload");
+static_assert(sizeof(PTemp) <= OP_PAYLOAD, "payload");
+static_assert(sizeof(PMisc) <= OP_PAYLOAD, "payload");
+
+constexpr int EXEC_MATS = 3;
+
+// ---- host side recording ---------------------------------------------------------------------
+struct ExecCtx {
+  std::vector<OpRec> ops;
+  const MatDev* mats[EXEC_MATS] = {nullptr, nullptr, nullptr};
+  cudaStream_t st = 0;
+  size_t flush_at = 16384;  // ops are run in chunks while the host keeps recording
+  int mat_index(const MatDev& M);
+  void maybe_flush();
+  template <class P>
+  void emit(int code, int nitems, const MatDev* M, const P& payload, bool barrier = true) {
+    if (nitems <= 0) return;
+    OpRec r;
+    r.code = code;
+    r.nitems = nitems;
+    r.barrier = barrier ? 1 : 0;
+    r.mat = M ? mat_index(*M) : 0;
+    static_assert(sizeof(P) <= OP_PAYLOAD, "payload");
+    std::memcpy(r.p, &payload, sizeof(P));
+    ops.push_back(r);
+    if (ops.size() >= flush_at) maybe_flush();
+  }
+};
+
+// the recording context of the current thread (set by the public entry points)
+ExecCtx* exec_ctx();
+void exec_begin(ExecCtx* ctx, cudaStream_t st);
+cudaError_t exec_flush();  // runs and clears the recorded ops (stream-ordered)
+cudaError_t exec_end();    // flush + reset the context pointer
+
+}  // namespace h2

@@ -5,28 +5,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "exec.h"
 #include "h2_internal.h"
 
 namespace h2 {
 
-// a dimension: (p ? *p : 0) + c, resolved on the device
-struct Dim {
-  const int* p;
-  int c;
-#ifdef __CUDACC__
-  __device__ __forceinline__ int v() const { return (p ? *p : 0) + c; }
-#endif
-};
-inline Dim dimc(int c) { return Dim{nullptr, c}; }
-inline Dim dimp(const int* p, int c = 0) { return Dim{p, c}; }
-
-// An operand op(Z) (Z or Z^T) of the product: "rows" basis / "cols" basis / coupling orientation.
-struct DevOp {
-  const MatDev* M;  // host copy of the device descriptor
-  bool trans;
-};
-
-// ---- launchers (h2_arith.cu) -------------------------------------------------------------------
+// ---- emitters (h2_exec.cu): append ops to the current executor context -------------------------------------------------------------------
 // out (|t| x k_t, ld) = full nested basis of cluster t of one side (eq. (1))
 void expand_basis(const MatDev& M, const DevSide& D, int t, double* out, int ld, cudaStream_t st);
 // C (m x n) = alpha op(A) op(B) + beta C, dims on the device (caps on the host for grid sizes)
@@ -61,5 +45,7 @@ void add_int(int* p, Dim a, Dim b, cudaStream_t st);
 // tree-order <-> original-order for n x nrhs blocks: Bt[i, c] = x[perm[i] + c ldx], x[perm[i] + c ldx] = Bt[i, c]
 void gather_cols(double* Bt, const double* x, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t st);
 void scatter_cols(double* x, const double* Bt, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t st);
+// dst[0..count) = 0 (stream-ordered with the recorded ops)
+void zero_fill(double* dst, size_t count, cudaStream_t st);
 
 }  // namespace h2

@@ -1,0 +1,711 @@
+// Op executor of the H^2 arithmetic (see exec.h) and the host-side emitters of every op.
+//
+// k_exec_cluster: one thread-block cluster of CL CTAs walks a segment of the op list; item i of an
+//   op runs on CTA (i mod CL); consecutive dependent ops are separated by barrier.cluster
+//   (release/acquire at cluster scope orders the global-memory results).  The whole dependent
+//   chain of a local update (U0..U6, ~10 phases) or of a Case-2 factor construction therefore
+//   costs one op dispatch + one cluster barrier per phase instead of one kernel launch per phase.
+// k_exec_big: an op with more than BIG items (large subtrees / big H^2 block products) runs as its
+//   own launch over up to all 148 SMs.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "exec.h"
+#include "h2_arith.cuh"
+#include "items_arith.cuh"
+#include "items_upd.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace h2 {
+namespace {
+
+constexpr int NT = NTHREADS;
+constexpr int CL = 8;     // CTAs of the executor cluster (portable cluster size)
+constexpr int BIG = 64;   // ops with more items run as a full-grid launch
+constexpr int KC = KCAP_MAX;
+constexpr int PR = 192;
+constexpr int RM = KC + 1;
+constexpr size_t SM_EXEC = (size_t)(3 * RM * KC + KC) * 8 + (KC + 8) * 4;  // max over items (SVD items)
+static_assert(SM_EXEC >= (size_t)((PR + 1) * KC + KC + 8) * 8, "smem");
+static_assert(SM_EXEC >= (size_t)(3 * (KC + 1) * KC + KC) * 8 + (KC + 8) * 4 && SM_EXEC >= (size_t)((2 * KC + 1) * KC + KC + 8) * 8, "smem");
+
+struct ExecParams {
+  const OpRec* ops;
+  int begin, end;
+  double* prof;   // profiling counters (h2_prof) or nullptr
+  double* gpart;  // partial sums of long-inner-dimension GEMMs
+  MatDev mats[EXEC_MATS];
+};
+
+__constant__ int c_op_kid[OP_COUNT] = {
+    K_EXT_LEAF, K_EXT_LEVEL, K_W_PATH, K_W_LEVEL, K_SVD_LEAF, K_SVD_LEVEL, K_COUPLE, K_INSTALL, K_RCACHE,
+    K_AR_EXPAND, K_AR_GEMM, K_AR_GEMM, K_AR_GEMM, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL,
+    K_AR_TILE, K_AR_TILE, K_AR_TILE, K_AR_TSQR, K_AR_TEMP, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC,
+    K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC};
+
+__device__ __forceinline__ const DevSide& side_of(const MatDev& M, int s) { return s ? M.col : M.row; }
+
+__device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, double* sm) {
+  const MatDev& M = P.mats[op.mat];
+  switch (op.code) {
+    case OP_UPD_EXT_LEAF: {
+      const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
+      upd::it_upd_ext_leaf(M, q.a, q.i[0], q.i[1], q.i[2], q.i[3], q.i[4], q.i[5], q.i[6], q.i[7], it, n, sm);
+    } break;
+    case OP_UPD_EXT_LEVEL: {
+      const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
+      upd::it_upd_ext_level(M, q.a, q.i[0], q.i[1], q.i[2], q.i[3], it, n, sm);
+    } break;
+    case OP_UPD_W_PATH: {
+      const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
+      upd::it_upd_weights_path(M, q.a, it, n, sm);
+    } break;
+    case OP_UPD_W_LEVEL: {
+      const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
+      upd::it_upd_weights_level(M, q.a, q.i[0], q.i[1], q.i[2], q.i[3], it, n, sm);
+    } break;
+    case OP_UPD_SVD_LEAF: {
+      const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
+      upd::it_upd_svd_leaf(M, q.a, q.i[0], q.i[1], q.i[2], q.i[3], it, n, sm);
+    } break;
+    case OP_UPD_SVD_LEVEL: {
+      const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
+      upd::it_upd_svd_level(M, q.a, q.i[0], q.i[1], q.i[2], q.i[3], it, n, sm);
+    } break;
+    case OP_UPD_COUPLE: {
+      const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
+      upd::it_upd_couple(M, q.a, q.i[0], q.i[1], it, n, sm);
+    } break;
+    case OP_UPD_INSTALL: {
+      const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
+      upd::it_upd_install(M, q.a, q.i[0], q.i[1], it, n, sm);
+    } break;
+    case OP_UPD_RCACHE: {
+      const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
+      upd::it_upd_rcache_path(M, q.a, it, n, sm);
+    } break;
+    case OP_EXPAND: {
+      const PExpand& q = *reinterpret_cast<const PExpand*>(op.p);
+      ar::it_expand(M, side_of(M, q.side), q.t, q.l0, q.out, q.ld, it, n, sm);
+    } break;
+    case OP_GEMM: {
+      const PGemm& q = *reinterpret_cast<const PGemm*>(op.p);
+      ar::it_gemm(q.C, q.ldc, q.A, q.lda, q.ta, q.B, q.ldb, q.tb, q.m, q.n, q.k, q.alpha, q.beta, it, n, sm);
+    } break;
+    case OP_GEMM_PART: {
+      const PGemm& q = *reinterpret_cast<const PGemm*>(op.p);
+      ar::it_gemm_inner_part(P.gpart, q.A, q.lda, q.ta, q.B, q.ldb, q.tb, q.m, q.n, q.k, q.chunk, it, n, sm);
+    } break;
+    case OP_GEMM_SUM: {
+      const PGemm& q = *reinterpret_cast<const PGemm*>(op.p);
+      ar::it_gemm_inner_sum(q.C, q.ldc, P.gpart, q.chunk, q.m, q.n, q.alpha, q.beta, it, n, sm);
+    } break;
+    case OP_HM_FWD_LEAF: {
+      const PHm& q = *reinterpret_cast<const PHm*>(op.p);
+      ar::it_hm_fwd_leaf(M, side_of(M, q.sside), q.l0, q.base_lo, q.D, q.ldd, q.m, q.xh, it, n, sm);
+    } break;
+    case OP_HM_FWD_LEVEL: {
+      const PHm& q = *reinterpret_cast<const PHm*>(op.p);
+      ar::it_hm_fwd_level(M, side_of(M, q.sside), q.l0, q.m, q.xh, it, n, sm);
+    } break;
+    case OP_HM_COUPLE: {
+      const PHm& q = *reinterpret_cast<const PHm*>(op.p);
+      ar::it_hm_couple(M, side_of(M, q.dside), side_of(M, q.sside), q.a, q.b, q.trans, q.m, q.xh, q.yh, it, n, sm);
+    } break;
+    case OP_HM_BWD_LEVEL: {
+      const PHm& q = *reinterpret_cast<const PHm*>(op.p);
+      ar::it_hm_bwd_level(M, side_of(M, q.dside), q.l0, q.m, q.yh, it, n, sm);
+    } break;
+    case OP_HM_LEAF: {
+      const PHm& q = *reinterpret_cast<const PHm*>(op.p);
+      ar::it_hm_leaf(M, side_of(M, q.dside), side_of(M, q.sside), q.l0, q.a, q.b, q.trans, q.D, q.ldd, q.m, q.yh,
+                     q.out, q.ldo, q.alpha, q.beta, it, n, sm);
+    } break;
+    case OP_POTRF: {
+      const PTile& q = *reinterpret_cast<const PTile*>(op.p);
+      ar::it_potrf(M, q.slot, q.t, it, n, sm);
+    } break;
+    case OP_GETRF: {
+      const PTile& q = *reinterpret_cast<const PTile*>(op.p);
+      ar::it_getrf(M, q.slot, q.t, it, n, sm);
+    } break;
+    case OP_TRSM: {
+      const PTile& q = *reinterpret_cast<const PTile*>(op.p);
+      ar::it_trsm(M, q.slot, q.m, q.mode, q.B, q.ldb, q.brows, q.bcols, it, n, sm);
+    } break;
+    case OP_TSQR: {
+      const PTsqr& q = *reinterpret_cast<const PTsqr*>(op.p);
+      ar::it_tsqr_r(q.A, q.lda, q.rows, q.K, q.R, q.ldr, it, n, sm);
+    } break;
+    case OP_TEMP: {
+      const PTemp& q = *reinterpret_cast<const PTemp*>(op.p);
+      ar::it_temp_core(q.Ra, q.Rb, q.ldr, q.K, q.Ma, q.Mb, q.ldm, q.rout, q.rel, q.abs_tol, q.max_rank, q.cap, q.flags,
+                       it, n, sm);
+    } break;
+    case OP_COPY_COLS: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      ar::it_copy_cols(q.dst, q.ldd, q.src, q.lds, q.rows, q.d1, it, n, sm);
+    } break;
+    case OP_SET_INT: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      ar::it_set_int(q.ip, q.d1, it, n, sm);
+    } break;
+    case OP_ADD_INT: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      ar::it_add_int(q.ip, q.d1, q.d2, it, n, sm);
+    } break;
+    case OP_RANK_IF: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      ar::it_rank_if(q.ip, q.ia, q.ib, it, n, sm);
+    } break;
+    case OP_STACK: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      ar::it_stack(q.dst, q.ldd, q.rows, q.src, (int)q.ldx, q.ia, reinterpret_cast<const double*>(q.perm), q.lds,
+                   q.row_off, q.rows_new, q.d1, it, n, sm);
+    } break;
+    case OP_CHOOSE: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      ar::it_choose(q.src, q.lds, q.ia, q.ib, q.dst, reinterpret_cast<double*>(const_cast<int64_t*>(q.perm)), q.ldd,
+                    q.ip, it, n, sm);
+    } break;
+    case OP_IDENTITY: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      ar::it_identity(q.dst, q.ldd, q.rows, it, n, sm);
+    } break;
+    case OP_TRANSPOSE: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      ar::it_transpose_tile(q.dst, q.ldd, q.src, q.lds, q.rows, q.cols, it, n, sm);
+    } break;
+    case OP_GATHER: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      ar::it_gather_cols(q.dst, q.src, q.perm, q.rows, q.cols, q.ldx, it, n, sm);
+    } break;
+    case OP_ZERO: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      for (long long e = (long long)it * NT + threadIdx.x; e < q.ldx; e += (long long)n * NT) q.dst[e] = 0.0;
+    } break;
+    case OP_SCATTER: {
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      ar::it_scatter_cols(q.dst, q.src, q.perm, q.rows, q.cols, q.ldx, it, n, sm);
+    } break;
+    default:
+      break;
+  }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(NT, 1) k_exec_cluster(const __grid_constant__ ExecParams P) {
+  extern __shared__ __align__(16) double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank(), nb = (int)cl.num_blocks();
+  const bool timing = P.prof && rank == 0 && threadIdx.x == 0;
+  for (int o = P.begin; o < P.end; ++o) {
+    const OpRec& op = P.ops[o];
+    const int n = op.nitems;
+    // warm L1/L2 with the next op record while this one runs (192 B = 2 lines)
+    if (threadIdx.x < 2 && o + 1 < P.end)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(&P.ops[o + 1]) + 128 * threadIdx.x));
+    unsigned long long t0 = timing ? gtimer() : 0;
+    for (int it = rank; it < n; it += nb) {
+      dispatch(P, op, it, n, sm);
+      __syncthreads();
+    }
+    // barrier.cluster.arrive (release) / wait (acquire) at cluster scope: this op's global-memory
+    // results are visible to every CTA of the cluster afterwards
+    if (op.barrier) cl.sync();
+    if (timing) {
+      const int kid = c_op_kid[op.code];
+      atomicAdd(P.prof + 2 * K_COUNT + 2 * kid, (double)(gtimer() - t0));
+      atomicAdd(P.prof + 2 * K_COUNT + 2 * kid + 1, 1.0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_exec_big(const __grid_constant__ ExecParams P, int o) {
+  extern __shared__ __align__(16) double sm[];
+  const OpRec& op = P.ops[o];
+  for (int it = blockIdx.x; it < op.nitems; it += gridDim.x) {
+    dispatch(P, op, it, op.nitems, sm);
+    __syncthreads();
+  }
+}
+
+// ---- host: recording context, upload, segmentation ----------------------------------------------
+thread_local ExecCtx* g_ctx = nullptr;
+bool g_attr = false;
+double* g_gpart = nullptr;
+OpRec* g_dops = nullptr;
+size_t g_dcap = 0;
+OpRec* g_hops[2] = {nullptr, nullptr};
+size_t g_hcap[2] = {0, 0};
+cudaEvent_t g_hev[2] = {nullptr, nullptr};
+int g_hbuf = 0;
+int g_nsm = 148;
+int g_big = getenv("H2_EXEC_BIG") ? atoi(getenv("H2_EXEC_BIG")) : BIG;  // debug override
+
+cudaError_t init_exec() {
+  if (g_attr) return cudaSuccess;
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_exec_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXEC))) return e;
+  if ((e = cudaFuncSetAttribute(k_exec_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXEC))) return e;
+  if ((e = cudaMalloc(&g_gpart, sizeof(double) * ar::NPART * KC * KC))) return e;
+  for (int i = 0; i < 2; ++i)
+    if ((e = cudaEventCreateWithFlags(&g_hev[i], cudaEventDisableTiming))) return e;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_nsm, cudaDevAttrMultiProcessorCount, dev);
+  g_attr = true;
+  return cudaSuccess;
+}
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace
+
+int ExecCtx::mat_index(const MatDev& M) {
+  for (int i = 0; i < EXEC_MATS; ++i)
+    if (mats[i] == &M) return i;
+  for (int i = 0; i < EXEC_MATS; ++i)
+    if (!mats[i]) {
+      mats[i] = &M;
+      return i;
+    }
+  throw std::runtime_error("h2 executor: more than 3 matrices in one op list");
+}
+
+void ExecCtx::maybe_flush() {
+  cudaError_t e = exec_flush();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("h2 executor: ") + cudaGetErrorString(e));
+}
+
+ExecCtx* exec_ctx() { return g_ctx; }
+
+void exec_begin(ExecCtx* ctx, cudaStream_t st) {
+  ctx->st = st;
+  ctx->ops.clear();
+  g_ctx = ctx;
+}
+
+cudaError_t exec_flush() {
+  ExecCtx* c = g_ctx;
+  if (!c || c->ops.empty()) return cudaSuccess;
+  cudaError_t e = init_exec();
+  if (e) return e;
+  const size_t n = c->ops.size();
+  // stage in a pinned buffer (double-buffered), upload, run
+  const int hb = g_hbuf;
+  g_hbuf ^= 1;
+  if ((e = cudaEventSynchronize(g_hev[hb]))) return e;
+  if (g_hcap[hb] < n) {
+    if (g_hops[hb]) cudaFreeHost(g_hops[hb]);
+    g_hcap[hb] = std::max(n, (size_t)16384);
+    if ((e = cudaMallocHost(&g_hops[hb], sizeof(OpRec) * g_hcap[hb]))) return e;
+  }
+  if (g_dcap < n) {
+    // the previous executor launches read g_dops: wait for the stream before freeing it
+    if (g_dops) {
+      cudaStreamSynchronize(c->st);
+      cudaFree(g_dops);
+    }
+    g_dcap = std::max(n, (size_t)16384);
+    if ((e = cudaMalloc(&g_dops, sizeof(OpRec) * g_dcap))) return e;
+  }
+  std::memcpy(g_hops[hb], c->ops.data(), sizeof(OpRec) * n);
+  if ((e = cudaMemcpyAsync(g_dops, g_hops[hb], sizeof(OpRec) * n, cudaMemcpyHostToDevice, c->st))) return e;
+  if ((e = cudaEventRecord(g_hev[hb], c->st))) return e;
+  ExecParams P;
+  P.ops = g_dops;
+  P.prof = prof_dev();
+  P.gpart = g_gpart;
+  for (int i = 0; i < EXEC_MATS; ++i) {
+    if (c->mats[i]) P.mats[i] = *c->mats[i];
+    else std::memset(&P.mats[i], 0, sizeof(MatDev));
+  }
+  size_t b = 0;
+  auto run_cluster = [&](size_t lo, size_t hi) -> cudaError_t {
+    if (hi <= lo) return cudaSuccess;
+    P.begin = (int)lo;
+    P.end = (int)hi;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = SM_EXEC;
+    cfg.stream = c->st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_exec_cluster, P);
+  };
+  for (size_t i = 0; i < n; ++i) {
+    const OpRec& r = c->ops[i];
+    if (r.nitems > g_big) {
+      if ((e = run_cluster(b, i))) return e;
+      const int kid = r.code < 9 ? r.code : K_AR_HMUL;
+      prof_begin(kid, c->st);
+      k_exec_big<<<std::min(r.nitems, g_nsm), NT, SM_EXEC, c->st>>>(P, (int)i);
+      prof_end(kid, c->st);
+      if ((e = cudaGetLastError())) return e;
+      b = i + 1;
+    }
+  }
+  if ((e = run_cluster(b, n))) return e;
+  c->ops.clear();
+  return cudaGetLastError();
+}
+
+cudaError_t exec_end() {
+  cudaError_t e = exec_flush();
+  g_ctx = nullptr;
+  return e;
+}
+
+// ------------------------------------------------------------------------------------------------
+// emitters of the local update (U0..U6)
+// ------------------------------------------------------------------------------------------------
+namespace {
+
+void level_segment(const h2_tree_* T, int root, int L, int* begin, int* count) {
+  *begin = 0;
+  *count = 0;
+  if (L > T->depth || L < T->level[root]) return;
+  const int* b = T->bfs.data() + T->level_ptr[L];
+  const int* e = T->bfs.data() + T->level_ptr[L + 1];
+  const int* lo = std::lower_bound(b, e, root);
+  const int* hi = std::lower_bound(b, e, root + T->tsize[root]);
+  *begin = (int)(lo - T->bfs.data());
+  *count = (int)(hi - lo);
+}
+
+void leaf_range(const h2_tree_* T, int root, int* begin, int* count) {
+  const auto b = T->leaves.begin(), e = T->leaves.end();
+  const auto lo = std::lower_bound(b, e, root);
+  const auto hi = std::lower_bound(b, e, root + T->tsize[root]);
+  *begin = (int)(lo - b);
+  *count = (int)(hi - lo);
+}
+
+PUpd pu(const UpdArgs& a, int i0 = 0, int i1 = 0, int i2 = 0, int i3 = 0, int i4 = 0, int i5 = 0, int i6 = 0,
+        int i7 = 0) {
+  PUpd p;
+  p.a = a;
+  p.i[0] = i0;
+  p.i[1] = i1;
+  p.i[2] = i2;
+  p.i[3] = i3;
+  p.i[4] = i4;
+  p.i[5] = i5;
+  p.i[6] = i6;
+  p.i[7] = i7;
+  return p;
+}
+
+struct AutoCtx {  // a local recording context when the caller has none
+  ExecCtx local;
+  bool own;
+  explicit AutoCtx(cudaStream_t st) : own(exec_ctx() == nullptr) {
+    if (own) exec_begin(&local, st);
+  }
+  ExecCtx* get() { return exec_ctx(); }
+  cudaError_t done() { return own ? exec_end() : cudaSuccess; }
+};
+
+}  // namespace
+
+cudaError_t update_init_attributes() { return init_exec(); }
+
+cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a_in, cudaStream_t st) {
+  UpdArgs a = a_in;
+  a.prof = prof_dev();
+  AutoCtx ac(st);
+  ExecCtx* c = ac.get();
+  const MatDev& M = Z->d;
+  const h2_btree_* B = Z->bt;
+  const h2_tree_* R = B->rt;
+  const h2_tree_* C = B->ct;
+  const int b0 = B->find(a.t0, a.s0);
+  const int in0 = Z->inad_range[2 * b0], nin = Z->inad_range[2 * b0 + 1] - in0;
+  if (B->kind[b0] == INADM) {  // dense add only
+    c->emit(OP_UPD_EXT_LEAF, nin, &M, pu(a, 0, 0, 0, 0, in0, nin, 0, 0));
+    return ac.done();
+  }
+  int rl0, nrl, cl0, ncl;
+  leaf_range(R, a.t0, &rl0, &nrl);
+  leaf_range(C, a.s0, &cl0, &ncl);
+  const int Lr = R->level[a.t0], Lc = C->level[a.s0];
+  c->emit(OP_UPD_EXT_LEAF, nrl + ncl + nin + Lr + Lc, &M, pu(a, rl0, nrl, cl0, ncl, in0, nin, Lr, Lc));
+  const int Lmax = std::max(R->depth, C->depth), Lmin = std::min(Lr, Lc);
+  for (int L = Lmax - 1; L >= Lmin; --L) {  // U2 bottom-up (internal clusters)
+    int bA, nA, bB, nB;
+    level_segment(R, a.t0, L, &bA, &nA);
+    level_segment(C, a.s0, L, &bB, &nB);
+    c->emit(OP_UPD_EXT_LEVEL, nA + nB, &M, pu(a, bA, nA, bB, nB));
+  }
+  c->emit(OP_UPD_W_PATH, 2, &M, pu(a));  // U3: path root .. t0
+  for (int L = Lmin + 1; L <= Lmax; ++L) {  // U3: subtree top-down
+    int bA = 0, nA = 0, bB = 0, nB = 0;
+    if (L > Lr) level_segment(R, a.t0, L, &bA, &nA);
+    if (L > Lc) level_segment(C, a.s0, L, &bB, &nB);
+    c->emit(OP_UPD_W_LEVEL, nA + nB, &M, pu(a, bA, nA, bB, nB));
+  }
+  c->emit(OP_UPD_SVD_LEAF, nrl + ncl, &M, pu(a, rl0, nrl, cl0, ncl));  // U4 bottom-up
+  for (int L = Lmax - 1; L >= Lmin; --L) {
+    int bA, nA, bB, nB;
+    level_segment(R, a.t0, L, &bA, &nA);
+    level_segment(C, a.s0, L, &bB, &nB);
+    c->emit(OP_UPD_SVD_LEVEL, nA + nB, &M, pu(a, bA, nA, bB, nB));
+  }
+  const int nA = R->tsize[a.t0], nB = C->tsize[a.s0];
+  c->emit(OP_UPD_COUPLE, nA + nB, &M, pu(a, nA, nB));   // U5
+  c->emit(OP_UPD_INSTALL, nA + nB, &M, pu(a, nA, nB));  // U6
+  c->emit(OP_UPD_RCACHE, 2, &M, pu(a));                 // R-factor caches on pred(t0), pred(s0)
+  return ac.done();
+}
+
+// ------------------------------------------------------------------------------------------------
+// emitters of the arithmetic primitives (declared in h2_arith.cuh)
+// ------------------------------------------------------------------------------------------------
+static ExecCtx* ctx_or_throw() {
+  ExecCtx* c = exec_ctx();
+  if (!c) throw std::runtime_error("h2 executor: no recording context");
+  return c;
+}
+
+static int side_id(const MatDev& M, const DevSide& D) { return &D == &M.col ? 1 : 0; }
+
+void expand_basis(const MatDev& M, const DevSide& D, int t, double* out, int ld, cudaStream_t) {
+  int l0, nl;
+  leaf_range(D.tree, t, &l0, &nl);
+  ctx_or_throw()->emit(OP_EXPAND, nl, &M, PExpand{side_id(M, D), t, l0, ld, out});
+}
+
+void gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb, Dim m, Dim n,
+          Dim k, int mcap, int ncap, int kcap, double alpha, double beta, cudaStream_t) {
+  if (mcap <= 0 || ncap <= 0) return;
+  ExecCtx* c = ctx_or_throw();
+  PGemm g;
+  g.C = C;
+  g.A = A;
+  g.B = B;
+  g.ldc = ldc;
+  g.lda = lda;
+  g.ldb = ldb;
+  g.ta = ta;
+  g.tb = tb;
+  g.m = m;
+  g.n = n;
+  g.k = k;
+  g.alpha = alpha;
+  g.beta = beta;
+  if (kcap > 512 && mcap <= KC && ncap <= KC) {
+    g.chunk = (kcap + ar::NPART - 1) / ar::NPART;
+    c->emit(OP_GEMM_PART, ar::NPART, nullptr, g);
+    g.chunk = ar::NPART;  // number of partials to sum
+    c->emit(OP_GEMM_SUM, 1, nullptr, g);
+    return;
+  }
+  g.chunk = 0;
+  const long long tot = (long long)mcap * ncap;
+  c->emit(OP_GEMM, std::max(1, std::min(cdiv(tot, NT), 4 * 148)), nullptr, g);
+}
+
+void hmul_dense(const MatDev& M, bool trans, int a, int b, int b_blk, const double* D, int ldd, Dim m, int mcap,
+                double* out, int ldo, double alpha, double beta, cudaStream_t) {
+  (void)b_blk;
+  (void)mcap;
+  ExecCtx* c = ctx_or_throw();
+  const DevSide& Dd = trans ? M.col : M.row;
+  const DevSide& Ds = trans ? M.row : M.col;
+  const h2_tree_* Td = Dd.tree;
+  const h2_tree_* Ts = Ds.tree;
+  PHm h;
+  h.dside = trans ? 1 : 0;
+  h.sside = trans ? 0 : 1;
+  h.a = a;
+  h.b = b;
+  h.trans = trans ? 1 : 0;
+  h.D = D;
+  h.ldd = ldd;
+  h.ldo = ldo;
+  h.xh = Ds.hx;
+  h.yh = Dd.hy;
+  h.out = out;
+  h.m = m;
+  h.alpha = alpha;
+  h.beta = beta;
+  int l0, nl;
+  leaf_range(Ts, b, &l0, &nl);
+  h.l0 = l0;
+  h.base_lo = Ts->lo[b];
+  c->emit(OP_HM_FWD_LEAF, nl, &M, h);
+  for (int L = Ts->depth - 1; L >= Ts->level[b]; --L) {
+    int s0, ns;
+    level_segment(Ts, b, L, &s0, &ns);
+    h.l0 = s0;
+    c->emit(OP_HM_FWD_LEVEL, ns, &M, h);
+  }
+  c->emit(OP_HM_COUPLE, Td->tsize[a], &M, h);
+  for (int L = Td->level[a] + 1; L <= Td->depth; ++L) {
+    int s0, ns;
+    level_segment(Td, a, L, &s0, &ns);
+    h.l0 = s0;
+    c->emit(OP_HM_BWD_LEVEL, ns, &M, h);
+  }
+  int la0, nla;
+  leaf_range(Td, a, &la0, &nla);
+  h.l0 = la0;
+  c->emit(OP_HM_LEAF, nla, &M, h);
+}
+
+void tile_potrf(const MatDev& M, int slot, int t, cudaStream_t) {
+  ctx_or_throw()->emit(OP_POTRF, 1, &M, PTile{slot, t, 0, 0, 0, 0, nullptr, dimc(0)});
+}
+void tile_getrf(const MatDev& M, int slot, int t, cudaStream_t) {
+  ctx_or_throw()->emit(OP_GETRF, 1, &M, PTile{slot, t, 0, 0, 0, 0, nullptr, dimc(0)});
+}
+void tile_trsm(const MatDev& M, int slot, int m, int mode, double* B, int ldb, int brows, Dim bcols, int bcolcap,
+               cudaStream_t) {
+  const bool rowwise = (mode == RLT || mode == RUN);
+  const int nvec = rowwise ? brows : bcolcap;
+  ctx_or_throw()->emit(OP_TRSM, std::max(1, cdiv(nvec, NT)), &M, PTile{slot, 0, m, mode, ldb, brows, B, bcols});
+}
+void tsqr_r(const double* A, int lda, int rows, Dim K, double* R, int ldr, cudaStream_t) {
+  ctx_or_throw()->emit(OP_TSQR, 1, nullptr, PTsqr{A, R, lda, rows, ldr, K});
+}
+void temp_core(const double* Ra, const double* Rb, int ldr, Dim K, double* Ma, double* Mb, int ldm, int* rout,
+               double rel, double abs_tol, int max_rank, int cap, int* flags, cudaStream_t) {
+  ctx_or_throw()->emit(OP_TEMP, 1, nullptr, PTemp{Ra, Rb, Ma, Mb, rout, flags, ldr, ldm, max_rank, cap, K, rel, abs_tol});
+}
+
+static PMisc misc() {
+  PMisc q;
+  std::memset(&q, 0, sizeof(q));
+  return q;
+}
+
+void copy_cols(double* dst, int ldd, const double* src, int lds, int rows, Dim cols, int colcap, cudaStream_t) {
+  const long long tot = (long long)rows * colcap;
+  if (tot <= 0) return;
+  PMisc q = misc();
+  q.dst = dst;
+  q.ldd = ldd;
+  q.src = src;
+  q.lds = lds;
+  q.rows = rows;
+  q.d1 = cols;
+  ctx_or_throw()->emit(OP_COPY_COLS, std::max(1, std::min(cdiv(tot, NT), 4 * 148)), nullptr, q);
+}
+void set_int(int* p, Dim v, cudaStream_t) {
+  PMisc q = misc();
+  q.ip = p;
+  q.d1 = v;
+  ctx_or_throw()->emit(OP_SET_INT, 1, nullptr, q);
+}
+void add_int(int* p, Dim a, Dim b, cudaStream_t) {
+  PMisc q = misc();
+  q.ip = p;
+  q.d1 = a;
+  q.d2 = b;
+  ctx_or_throw()->emit(OP_ADD_INT, 1, nullptr, q);
+}
+void rank_if(int* p, const int* a, const int* b, cudaStream_t) {
+  PMisc q = misc();
+  q.ip = p;
+  q.ia = a;
+  q.ib = b;
+  ctx_or_throw()->emit(OP_RANK_IF, 1, nullptr, q);
+}
+void stack_cols(double* dst, int ldd, int rows, const double* T, int ldt, const int* kT, const double* Nw, int ldn,
+                int row_off, int rows_new, Dim knew, int colcap, cudaStream_t) {
+  PMisc q = misc();
+  q.dst = dst;
+  q.ldd = ldd;
+  q.rows = rows;
+  q.src = T;
+  q.ldx = ldt;
+  q.ia = kT;
+  q.perm = reinterpret_cast<const int64_t*>(Nw);
+  q.lds = ldn;
+  q.row_off = row_off;
+  q.rows_new = rows_new;
+  q.d1 = knew;
+  const long long tot = (long long)rows * colcap;
+  ctx_or_throw()->emit(OP_STACK, std::max(1, std::min(cdiv(tot, NT), 4 * 148)), nullptr, q);
+}
+void choose_case2(const double* Cm, int ldc, const int* k1, const int* k2, double* Ca, double* Cb, int ldo, int* kout,
+                  cudaStream_t) {
+  PMisc q = misc();
+  q.src = Cm;
+  q.lds = ldc;
+  q.ia = k1;
+  q.ib = k2;
+  q.dst = Ca;
+  q.perm = reinterpret_cast<const int64_t*>(Cb);
+  q.ldd = ldo;
+  q.ip = kout;
+  ctx_or_throw()->emit(OP_CHOOSE, 1, nullptr, q);
+}
+void identity(double* I, int ld, int m, cudaStream_t) {
+  PMisc q = misc();
+  q.dst = I;
+  q.ldd = ld;
+  q.rows = m;
+  ctx_or_throw()->emit(OP_IDENTITY, std::max(1, cdiv(m * m, NT)), nullptr, q);
+}
+void transpose_tile(double* dst, int ldd, const double* src, int lds, int rows, int cols, cudaStream_t) {
+  PMisc q = misc();
+  q.dst = dst;
+  q.ldd = ldd;
+  q.src = src;
+  q.lds = lds;
+  q.rows = rows;
+  q.cols = cols;
+  ctx_or_throw()->emit(OP_TRANSPOSE, std::max(1, cdiv(rows * cols, NT)), nullptr, q);
+}
+void gather_cols(double* Bt, const double* x, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t) {
+  PMisc q = misc();
+  q.dst = Bt;
+  q.src = x;
+  q.perm = perm;
+  q.rows = n;
+  q.cols = nrhs;
+  q.ldx = ldx;
+  ctx_or_throw()->emit(OP_GATHER, std::max(1, std::min(cdiv((long long)n * nrhs, NT), 8 * 148)), nullptr, q);
+}
+void scatter_cols(double* x, const double* Bt, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t) {
+  PMisc q = misc();
+  q.dst = x;
+  q.src = Bt;
+  q.perm = perm;
+  q.rows = n;
+  q.cols = nrhs;
+  q.ldx = ldx;
+  ctx_or_throw()->emit(OP_SCATTER, std::max(1, std::min(cdiv((long long)n * nrhs, NT), 8 * 148)), nullptr, q);
+}
+
+}  // namespace h2
+
+namespace h2 {
+void zero_fill(double* dst, size_t count, cudaStream_t) {
+  PMisc q;
+  std::memset(&q, 0, sizeof(q));
+  q.dst = dst;
+  q.ldx = (int64_t)count;
+  ctx_or_throw()->emit(OP_ZERO, std::max(1, std::min(cdiv((long long)count, NT), 4 * 148)), nullptr, q);
+}
+}  // namespace h2

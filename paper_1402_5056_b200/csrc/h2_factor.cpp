@@ -423,7 +423,7 @@ struct Driver {
       double* U = ar.alloc((size_t)mt * rcap);
       gemm(U, mt, Vt, mt, false, Sptr(Z, b), Z->d.rcap, false, dimc(mt), dimp(Z->d.col.rank + s),
            dimp(Z->d.row.rank + t), mt, rcap, rcap, 1.0, 0.0, st);
-      cudaMemsetAsync(Sptr(Z, b), 0, sizeof(double) * Z->d.rcap * Z->d.rcap, st);
+      zero_fill(Sptr(Z, b), (size_t)Z->d.rcap * Z->d.rcap, st);
       update(t, s, U, mt, Zs, ms, kdev, 1.0);
       return;
     }
@@ -462,7 +462,7 @@ struct Driver {
            dimp(Z->d.row.rank + t), mt, rcap, rcap, 1.0, 0.0, st);
       double* Ws = ar.alloc((size_t)ms * rcap);
       expand_basis(Z->d, Z->d.col, s, Ws, ms, st);
-      cudaMemsetAsync(Sptr(Z, b), 0, sizeof(double) * Z->d.rcap * Z->d.rcap, st);
+      zero_fill(Sptr(Z, b), (size_t)Z->d.rcap * Z->d.rcap, st);
       update(t, s, U, mt, Ws, ms, kdev, 1.0);
       return;
     }
@@ -571,9 +571,11 @@ h2_status run_driver(h2_mat_* Z, const h2_trunc* trunc, h2_stream stream, int wh
     }
   cudaStream_t st = (cudaStream_t)stream;
   Driver dr{Z, st, tc.rel_tol, tc.abs_tol, tc.max_rank, ar, Z->bt->rt, Z->d.rcap, Z->d.lmax};
-  dr.ident = ar.alloc((size_t)Z->d.lmax * Z->d.lmax);
-  identity(dr.ident, Z->d.lmax, Z->d.lmax, st);
+  ExecCtx ctx;
+  exec_begin(&ctx, st);  // the recursion records ops; the device executor runs them (exec.h)
   try {
+    dr.ident = ar.alloc((size_t)Z->d.lmax * Z->d.lmax);
+    identity(dr.ident, Z->d.lmax, Z->d.lmax, st);
     if (what == 0) dr.chol(0);
     else if (what == 1) dr.lr(0);
     else if (what == 2) dr.addmul(alpha, HOp{X, false}, HOp{Y, false}, 0, 0, 0, nullptr);
@@ -592,9 +594,11 @@ h2_status run_driver(h2_mat_* Z, const h2_trunc* trunc, h2_stream stream, int wh
       scatter_cols(vec, Bt, Z->d.row.perm, n, nrhs, ldx, st);
     }
   } catch (const std::exception& e) {
+    exec_end();
     h2::set_error(e.what());
     return H2_ERR_NOMEM;
   }
+  CUDA_TRY(exec_end());
   CUDA_TRY(cudaGetLastError());
   Z->stats[0] += dr.n_updates;
   Z->stats[1] += dr.n_dense;

@@ -14,7 +14,8 @@ namespace h2 {
 const char* const kKernelNames[K_COUNT] = {
     "k_upd_ext_leaf", "k_upd_ext_level", "k_upd_weights_path", "k_upd_weights_level", "k_upd_svd_leaf",
     "k_upd_svd_level", "k_upd_couple", "k_upd_install", "k_upd_rcache_path", "k_mv_gather",
-    "k_mv_fwd_leaf", "k_mv_fwd_level", "k_mv_couple", "k_mv_bwd_level", "k_mv_leaf_out"};
+    "k_mv_fwd_leaf", "k_mv_fwd_level", "k_mv_couple", "k_mv_bwd_level", "k_mv_leaf_out",
+    "ar_expand", "ar_gemm", "ar_hmul", "ar_tile", "ar_tsqr", "ar_temp_core", "ar_misc"};
 
 namespace {
 struct State {
@@ -56,13 +57,13 @@ extern "C" h2_status h2_profile_enable(int32_t on) {
     return H2_ERR_CUDA;
   }
   if (!g.d) {
-    e = cudaMalloc(&g.d, sizeof(double) * 2 * K_COUNT);
+    e = cudaMalloc(&g.d, sizeof(double) * (4 * K_COUNT + 32));
     if (e != cudaSuccess) {
       set_error("h2_profile_enable: cudaMalloc failed");
       return H2_ERR_NOMEM;
     }
   }
-  cudaMemset(g.d, 0, sizeof(double) * 2 * K_COUNT);
+  cudaMemset(g.d, 0, sizeof(double) * (4 * K_COUNT + 32));
   for (int k = 0; k < K_COUNT; ++k) g.used[k] = 0;
   g.on = on != 0;
   return H2_OK;
@@ -76,7 +77,7 @@ extern "C" h2_status h2_profile_read(char* names, int64_t* launches, double* ms_
     set_error(std::string("h2_profile_read: ") + cudaGetErrorString(e));
     return H2_ERR_CUDA;
   }
-  double acc[2 * K_COUNT] = {};
+  double acc[4 * K_COUNT] = {};
   if (g.d) cudaMemcpy(acc, g.d, sizeof(acc), cudaMemcpyDeviceToHost);
   for (int k = 0; k < K_COUNT; ++k) {
     if (names) {
@@ -90,10 +91,28 @@ extern "C" h2_status h2_profile_read(char* names, int64_t* launches, double* ms_
       cudaEventElapsedTime(&ms, g.ev[k][2 * i], g.ev[k][2 * i + 1]);
       tot += ms;
     }
-    if (launches) launches[k] = (int64_t)pairs;
+    // + ops run inside the device executor (timed on the device: op start to its barrier)
+    tot += acc[2 * K_COUNT + 2 * k] / 1e6;
+    if (launches) launches[k] = (int64_t)pairs + (int64_t)acc[2 * K_COUNT + 2 * k + 1];
     if (ms_total) ms_total[k] = tot;
     if (flops) flops[k] = acc[2 * k];
     if (bytes) bytes[k] = acc[2 * k + 1];
+  }
+  return H2_OK;
+}
+
+extern "C" h2_status h2_profile_debug(double out[16]) {
+  if (!out) {
+    set_error("h2_profile_debug: NULL argument");
+    return H2_ERR_ARG;
+  }
+  for (int i = 0; i < 16; ++i) out[i] = 0.0;
+  if (!g.d) return H2_OK;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(out, g.d + 4 * K_COUNT, 16 * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    set_error(std::string("h2_profile_debug: ") + cudaGetErrorString(e));
+    return H2_ERR_CUDA;
   }
   return H2_OK;
 }

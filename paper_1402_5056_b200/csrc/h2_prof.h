@@ -23,6 +23,13 @@ enum KernelId {
   K_MV_COUPLE,
   K_MV_BWD_LEVEL,
   K_MV_LEAF_OUT,
+  K_AR_EXPAND,
+  K_AR_GEMM,
+  K_AR_HMUL,
+  K_AR_TILE,
+  K_AR_TSQR,
+  K_AR_TEMP,
+  K_AR_MISC,
   K_COUNT
 };
 

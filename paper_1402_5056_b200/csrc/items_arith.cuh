@@ -1,31 +1,30 @@
-// Device primitives of the H^2 product / substitution / factorization (see h2_arith.cuh).
+// Device items of the product / substitution / factorization primitives (SURVEY §8(a) M1-M3,
+// F1-F3, S2), executed by the op executor (h2_exec.cu).  Item i = one CTA's share of the op.
+#pragma once
 #include <cuda_runtime.h>
 
-#include <algorithm>
-#include <vector>
-
 #include "devla.cuh"
-#include "h2_arith.cuh"
+#include "exec.h"
 
 namespace h2 {
-namespace {
+namespace ar {
 
 constexpr int NT = NTHREADS;
 constexpr int KC = KCAP_MAX;
 constexpr int PR = 192;
 
-inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 // ---- basis expansion ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_expand(MatDev M, DevSide D, int t, int l0, double* out, int ld) {
-  extern __shared__ double smx[];
-  double* P[2] = {smx, smx + KC * KC};
-  const int q = D.leaves[l0 + blockIdx.x];
+__device__ void it_expand(const MatDev& M, const DevSide& D, int t, int l0, double* out, int ld, int item_, int nitems_, double* smx_) {
+  double* smx = smx_;
+  constexpr int LP = KC + 1;
+  double* P[2] = {smx, smx + LP * KC};
+  const int q = D.leaves[l0 + item_];
   const int kt = D.rank[t];
   int cur = 0;
   int kq = D.rank[q];
   // P = I (kq x kq)
-  for (int e = threadIdx.x; e < kq * kq; e += NT) P[0][(e % kq) + (e / kq) * KC] = (e % kq) == (e / kq) ? 1.0 : 0.0;
+  for (int e = threadIdx.x; e < kq * kq; e += NT) P[0][(e % kq) + (e / kq) * LP] = (e % kq) == (e / kq) ? 1.0 : 0.0;
   int rows = kq, cols = kq;
   __syncthreads();
   for (int a = q; a != t; a = D.parent[a]) {
@@ -34,8 +33,8 @@ __global__ void __launch_bounds__(NT) k_expand(MatDev M, DevSide D, int t, int l
     for (int e = threadIdx.x; e < rows * kp; e += NT) {
       const int i = e % rows, j = e / rows;
       double acc = 0.0;
-      for (int p = 0; p < cols; ++p) acc += P[cur][i + p * KC] * E[p + j * M.rcap];
-      P[cur ^ 1][i + j * KC] = acc;
+      for (int p = 0; p < cols; ++p) acc += P[cur][i + p * LP] * E[p + j * M.rcap];
+      P[cur ^ 1][i + j * LP] = acc;
     }
     cols = kp;
     cur ^= 1;
@@ -48,17 +47,17 @@ __global__ void __launch_bounds__(NT) k_expand(MatDev M, DevSide D, int t, int l
   for (int e = threadIdx.x; e < m * cols; e += NT) {
     const int i = e % m, j = e / m;
     double acc = 0.0;
-    for (int p = 0; p < rows; ++p) acc += V[i + p * M.lmax] * P[cur][p + j * KC];
+    for (int p = 0; p < rows; ++p) acc += V[i + p * M.lmax] * P[cur][p + j * LP];
     out[off + i + (size_t)j * ld] = acc;
   }
 }
 
 // ---- GEMMs with device dims -------------------------------------------------------------------
-__global__ void k_gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb,
-                       Dim md, Dim nd, Dim kd, double alpha, double beta) {
+__device__ void it_gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb,
+                       Dim md, Dim nd, Dim kd, double alpha, double beta, int item_, int nitems_, double* smx_) {
   const int m = md.v(), n = nd.v(), kk = kd.v();
   const long long tot = (long long)m * n;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+  for (long long e = (long long)item_ * blockDim.x + threadIdx.x; e < tot; e += (long long)nitems_ * blockDim.x) {
     const int i = (int)(e % m), j = (int)(e / m);
     double acc = 0.0;
     for (int q = 0; q < kk; ++q) {
@@ -72,10 +71,10 @@ __global__ void k_gemm(double* C, int ldc, const double* A, int lda, bool ta, co
 }
 
 // long inner dimension: partial sums per chunk, then a deterministic fixed-order reduction
-__global__ void k_gemm_inner_part(double* part, const double* A, int lda, bool ta, const double* B, int ldb, bool tb,
-                                  Dim md, Dim nd, Dim kd, int chunk) {
+__device__ void it_gemm_inner_part(double* part, const double* A, int lda, bool ta, const double* B, int ldb, bool tb,
+                                  Dim md, Dim nd, Dim kd, int chunk, int item_, int nitems_, double* smx_) {
   const int m = md.v(), n = nd.v(), kk = kd.v();
-  const int q0 = blockIdx.x * chunk, q1 = min(kk, q0 + chunk);
+  const int q0 = item_ * chunk, q1 = min(kk, q0 + chunk);
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     const int i = e % m, j = e / m;
     double acc = 0.0;
@@ -84,12 +83,12 @@ __global__ void k_gemm_inner_part(double* part, const double* A, int lda, bool t
       const double b = tb ? B[j + (size_t)q * ldb] : B[q + (size_t)j * ldb];
       acc += a * b;
     }
-    part[(size_t)blockIdx.x * KC * KC + e] = acc;
+    part[(size_t)item_ * KC * KC + e] = acc;
   }
 }
 
-__global__ void k_gemm_inner_sum(double* C, int ldc, const double* part, int nparts, Dim md, Dim nd, double alpha,
-                                 double beta) {
+__device__ void it_gemm_inner_sum(double* C, int ldc, const double* part, int nparts, Dim md, Dim nd, double alpha,
+                                 double beta, int item_, int nitems_, double* smx_) {
   const int m = md.v(), n = nd.v();
   for (int e = threadIdx.x; e < m * n; e += blockDim.x) {
     double acc = 0.0;
@@ -100,14 +99,13 @@ __global__ void k_gemm_inner_sum(double* C, int ldc, const double* part, int npa
   }
 }
 
-double* g_part = nullptr;
 constexpr int NPART = 64;
 
 // ---- H^2 block times dense --------------------------------------------------------------------
 // forward transform over T_b: leaves
-__global__ void __launch_bounds__(NT) k_hm_fwd_leaf(MatDev M, DevSide S, int l0, int base_lo, const double* D, int ldd,
-                                                    Dim md, double* xh) {
-  const int q = S.leaves[l0 + blockIdx.x];
+__device__ void it_hm_fwd_leaf(const MatDev& M, const DevSide& S, int l0, int base_lo, const double* D, int ldd,
+                                                    Dim md, double* xh, int item_, int nitems_, double* smx_) {
+  const int q = S.leaves[l0 + item_];
   const int m = md.v();
   const int rows = S.hi[q] - S.lo[q], kq = S.rank[q];
   const double* W = S.leafb + (size_t)S.leafidx[q] * M.lmax * M.rcap;
@@ -121,8 +119,8 @@ __global__ void __launch_bounds__(NT) k_hm_fwd_leaf(MatDev M, DevSide S, int l0,
   }
 }
 
-__global__ void __launch_bounds__(NT) k_hm_fwd_level(MatDev M, DevSide S, int b0, Dim md, double* xh) {
-  const int s = S.bfs[b0 + blockIdx.x];
+__device__ void it_hm_fwd_level(const MatDev& M, const DevSide& S, int b0, Dim md, double* xh, int item_, int nitems_, double* smx_) {
+  const int s = S.bfs[b0 + item_];
   if (S.son0[s] < 0) return;
   const int m = md.v(), ks = S.rank[s];
   double* x = xh + (size_t)s * M.rcap * KC;
@@ -141,9 +139,9 @@ __global__ void __launch_bounds__(NT) k_hm_fwd_level(MatDev M, DevSide S, int b0
 }
 
 // couplings: CTA per cluster a' of T_a (dst side): yhat_{a'} = sum_{(a',b') adm, b' in T_b} S_op xhat_{b'}
-__global__ void __launch_bounds__(NT) k_hm_couple(MatDev M, DevSide Dd, DevSide Ds, int a, int b, int trans, Dim md,
-                                                  const double* xh, double* yh) {
-  const int ap = a + blockIdx.x;
+__device__ void it_hm_couple(const MatDev& M, const DevSide& Dd, const DevSide& Ds, int a, int b, int trans, Dim md,
+                                                  const double* xh, double* yh, int item_, int nitems_, double* smx_) {
+  const int ap = a + item_;
   const int m = md.v(), ka = Dd.rank[ap];
   const int bsz = Ds.tsize[b];
   double* y = yh + (size_t)ap * M.rcap * KC;
@@ -166,8 +164,8 @@ __global__ void __launch_bounds__(NT) k_hm_couple(MatDev M, DevSide Dd, DevSide 
   }
 }
 
-__global__ void __launch_bounds__(NT) k_hm_bwd_level(MatDev M, DevSide D, int b0, Dim md, double* yh) {
-  const int t = D.bfs[b0 + blockIdx.x];
+__device__ void it_hm_bwd_level(const MatDev& M, const DevSide& D, int b0, Dim md, double* yh, int item_, int nitems_, double* smx_) {
+  const int t = D.bfs[b0 + item_];
   const int p = D.parent[t];
   const int m = md.v(), kt = D.rank[t], kp = D.rank[p];
   const double* E = D.tr + (size_t)t * M.rcap * M.rcap;
@@ -181,10 +179,10 @@ __global__ void __launch_bounds__(NT) k_hm_bwd_level(MatDev M, DevSide D, int b0
   }
 }
 
-__global__ void __launch_bounds__(NT) k_hm_leaf(MatDev M, DevSide Dd, DevSide Ds, int l0, int a, int b, int trans,
+__device__ void it_hm_leaf(const MatDev& M, const DevSide& Dd, const DevSide& Ds, int l0, int a, int b, int trans,
                                                 const double* D, int ldd, Dim md, const double* yh, double* out,
-                                                int ldo, double alpha, double beta) {
-  const int ap = Dd.leaves[l0 + blockIdx.x];
+                                                int ldo, double alpha, double beta, int item_, int nitems_, double* smx_) {
+  const int ap = Dd.leaves[l0 + item_];
   const int m = md.v();
   const int rows = Dd.hi[ap] - Dd.lo[ap], ka = Dd.rank[ap];
   const int offo = Dd.lo[ap] - Dd.lo[a];
@@ -216,8 +214,8 @@ __global__ void __launch_bounds__(NT) k_hm_leaf(MatDev M, DevSide Dd, DevSide Ds
 }
 
 // ---- dense tiles ------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_potrf(MatDev M, int slot, int t) {
-  __shared__ double T[64 * 65];
+__device__ void it_potrf(const MatDev& M, int slot, int t, int item_, int nitems_, double* smx_) {
+  double* T = smx_;
   double* N = M.N + (size_t)slot * M.lmax * M.lmax;
   const int m = M.row.hi[t] - M.row.lo[t];
   const int ld = 65;
@@ -226,7 +224,7 @@ __global__ void __launch_bounds__(NT) k_potrf(MatDev M, int slot, int t) {
     T[i + j * ld] = i >= j ? N[i + j * M.lmax] : N[j + i * M.lmax];  // symmetric from the lower triangle
   }
   __syncthreads();
-  __shared__ int bad;
+  int& bad = *(int*)(smx_ + 64 * 65);
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
   for (int j = 0; j < m; ++j) {
@@ -255,10 +253,10 @@ __global__ void __launch_bounds__(NT) k_potrf(MatDev M, int slot, int t) {
   }
 }
 
-__global__ void __launch_bounds__(NT) k_getrf(MatDev M, int slot, int t) {
-  __shared__ double T[64 * 65];
-  __shared__ double nrm;
-  __shared__ int bad;
+__device__ void it_getrf(const MatDev& M, int slot, int t, int item_, int nitems_, double* smx_) {
+  double* T = smx_;
+  double& nrm = smx_[64 * 65 + 1];
+  int& bad = *(int*)(smx_ + 64 * 65 + 2);
   double* N = M.N + (size_t)slot * M.lmax * M.lmax;
   const int m = M.row.hi[t] - M.row.lo[t];
   const int ld = 65;
@@ -289,16 +287,16 @@ __global__ void __launch_bounds__(NT) k_getrf(MatDev M, int slot, int t) {
   }
 }
 
-__global__ void __launch_bounds__(NT) k_trsm(MatDev M, int slot, int m, int mode, double* B, int ldb, int brows,
-                                             Dim bcols) {
-  __shared__ double T[64 * 65];
+__device__ void it_trsm(const MatDev& M, int slot, int m, int mode, double* B, int ldb, int brows,
+                                             Dim bcols, int item_, int nitems_, double* smx_) {
+  double* T = smx_;
   const int ld = 65;
   const double* N = M.N + (size_t)slot * M.lmax * M.lmax;
   for (int e = threadIdx.x; e < m * m; e += NT) T[(e % m) + (e / m) * ld] = N[(e % m) + (e / m) * M.lmax];
   __syncthreads();
   const bool rowwise = (mode == RLT || mode == RUN);
   const int nvec = rowwise ? brows : bcols.v();
-  for (int v = blockIdx.x * NT + threadIdx.x; v < nvec; v += gridDim.x * NT) {
+  for (int v = item_ * NT + threadIdx.x; v < nvec; v += nitems_ * NT) {
     // rowwise: x = row v of B (length m, stride ldb); columnwise: x = column v (length m, stride 1)
     double* x = rowwise ? B + v : B + (size_t)v * ldb;
     const int st = rowwise ? ldb : 1;
@@ -339,10 +337,11 @@ __global__ void __launch_bounds__(NT) k_trsm(MatDev M, int slot, int m, int mode
 }
 
 // ---- tall R-factor by streaming TSQR (one CTA) --------------------------------------------------
-__global__ void __launch_bounds__(NT) k_tsqr_r(const double* A, int lda, int rows, Dim Kd, double* R, int ldr) {
-  extern __shared__ double sm[];
-  double* P = sm;  // PR x KC
-  double* diag = P + PR * KC;
+__device__ void it_tsqr_r(const double* A, int lda, int rows, Dim Kd, double* R, int ldr, int item_, int nitems_, double* smx_) {
+  double* sm = smx_;
+  constexpr int PL = PR + 1;
+  double* P = sm;  // PR x KC, leading dim PL (odd)
+  double* diag = P + PL * KC;
   double* red = diag + KC;
   const int K = Kd.v();
   int r = 0;  // rows currently in the panel
@@ -350,56 +349,57 @@ __global__ void __launch_bounds__(NT) k_tsqr_r(const double* A, int lda, int row
     const int take = min(rows - r0, PR - r);
     for (int e = threadIdx.x; e < take * K; e += NT) {
       const int i = e % take, j = e / take;
-      P[r + i + j * PR] = A[r0 + i + (size_t)j * lda];
+      P[r + i + j * PL] = A[r0 + i + (size_t)j * lda];
     }
     r += take;
     r0 += take;
-    la::cta_qr_R(P, PR, r, K, diag, red);
+    la::cta_qr_R(P, PL, r, K, diag, red);
     r = min(r, K);
   }
   for (int e = threadIdx.x; e < K * K; e += NT) {
     const int i = e % K, j = e / K;
-    R[i + j * ldr] = i < r ? P[i + j * PR] : 0.0;
+    R[i + j * ldr] = i < r ? P[i + j * PL] : 0.0;
   }
 }
 
 // ---- temporary truncation core ----------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_temp_core(const double* Ra, const double* Rb, int ldr, Dim Kd, double* Ma,
+__device__ void it_temp_core(const double* Ra, const double* Rb, int ldr, Dim Kd, double* Ma,
                                                   double* Mb, int ldm, int* rout, double rel, double abs_tol,
-                                                  int max_rank, int cap, int* flags) {
-  extern __shared__ double smt[];
+                                                  int max_rank, int cap, int* flags, int item_, int nitems_, double* smx_) {
+  double* smt = smx_;
+  constexpr int LT = KC + 1;
   double* Mm = smt;
-  double* M0 = Mm + KC * KC;
-  double* U = M0 + KC * KC;
-  double* sig = U + KC * KC;
+  double* M0 = Mm + LT * KC;
+  double* U = M0 + LT * KC;
+  double* sig = U + LT * KC;
   int* order = (int*)(sig + KC);
   int* scr = order + KC;
-  __shared__ int clamped;
+  int& clamped = scr[3];
   const int K = Kd.v();
   // M = Ra Rb^T
   for (int e = threadIdx.x; e < K * K; e += NT) {
     const int i = e % K, j = e / K;
     double acc = 0.0;
     for (int q = 0; q < K; ++q) acc += Ra[i + q * ldr] * Rb[j + q * ldr];
-    Mm[i + j * KC] = acc;
-    M0[i + j * KC] = acc;
+    Mm[i + j * LT] = acc;
+    M0[i + j * LT] = acc;
   }
   if (threadIdx.x == 0) clamped = 0;
   __syncthreads();
-  la::cta_jacobi(Mm, KC, K, K, sig, order, scr);
+  la::cta_jacobi(Mm, LT, K, K, sig, order, scr);
   const int r = K > 0 ? la::trunc_rank(sig, order, K, rel, abs_tol, max_rank, cap, &clamped) : 0;
   // U_r
   for (int e = threadIdx.x; e < K * r; e += NT) {
     const int i = e % K, q = e / K;
-    U[i + q * KC] = Mm[i + order[q] * KC] / sig[order[q]];
+    U[i + q * LT] = Mm[i + order[q] * LT] / sig[order[q]];
   }
   __syncthreads();
   // V_r = M0^T U_r / sigma   (stored in Mm)
   for (int e = threadIdx.x; e < K * r; e += NT) {
     const int i = e % K, q = e / K;
     double acc = 0.0;
-    for (int p = 0; p < K; ++p) acc += M0[p + i * KC] * U[p + q * KC];
-    Mm[i + q * KC] = acc / sig[order[q]];
+    for (int p = 0; p < K; ++p) acc += M0[p + i * LT] * U[p + q * LT];
+    Mm[i + q * LT] = acc / sig[order[q]];
   }
   __syncthreads();
   // Ma = Rb^T V_r ; Mb = Ra^T U_r / sigma
@@ -407,8 +407,8 @@ __global__ void __launch_bounds__(NT) k_temp_core(const double* Ra, const double
     const int i = e % K, q = e / K;
     double a = 0.0, b = 0.0;
     for (int p = 0; p < K; ++p) {
-      a += Rb[p + i * ldr] * Mm[p + q * KC];
-      b += Ra[p + i * ldr] * U[p + q * KC];
+      a += Rb[p + i * ldr] * Mm[p + q * LT];
+      b += Ra[p + i * ldr] * U[p + q * LT];
     }
     Ma[i + q * ldm] = a;
     Mb[i + q * ldm] = b / sig[order[q]];
@@ -419,35 +419,39 @@ __global__ void __launch_bounds__(NT) k_temp_core(const double* Ra, const double
   }
 }
 
-__global__ void k_copy_cols(double* dst, int ldd, const double* src, int lds, int rows, Dim cols) {
+__device__ void it_copy_cols(double* dst, int ldd, const double* src, int lds, int rows, Dim cols, int item_, int nitems_, double* smx_) {
   const int c = cols.v();
   const long long tot = (long long)rows * c;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+  for (long long e = (long long)item_ * blockDim.x + threadIdx.x; e < tot; e += (long long)nitems_ * blockDim.x) {
     const int i = (int)(e % rows), j = (int)(e / rows);
     dst[i + (size_t)j * ldd] = src[i + (size_t)j * lds];
   }
 }
 
-__global__ void k_set_int(int* p, Dim v) { *p = v.v(); }
-__global__ void k_gather_cols(double* Bt, const double* x, const int64_t* perm, int n, int nrhs, int64_t ldx) {
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)n * nrhs; e += (long long)gridDim.x * blockDim.x) {
+__device__ void it_set_int(int* p, Dim v, int item_, int nitems_, double* smx_) {
+  if (threadIdx.x == 0) *p = v.v();
+}
+__device__ void it_gather_cols(double* Bt, const double* x, const int64_t* perm, int n, int nrhs, int64_t ldx, int item_, int nitems_, double* smx_) {
+  for (long long e = (long long)item_ * blockDim.x + threadIdx.x; e < (long long)n * nrhs; e += (long long)nitems_ * blockDim.x) {
     const int i = (int)(e % n), c = (int)(e / n);
     Bt[e] = x[perm[i] + c * ldx];
   }
 }
-__global__ void k_scatter_cols(double* x, const double* Bt, const int64_t* perm, int n, int nrhs, int64_t ldx) {
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)n * nrhs; e += (long long)gridDim.x * blockDim.x) {
+__device__ void it_scatter_cols(double* x, const double* Bt, const int64_t* perm, int n, int nrhs, int64_t ldx, int item_, int nitems_, double* smx_) {
+  for (long long e = (long long)item_ * blockDim.x + threadIdx.x; e < (long long)n * nrhs; e += (long long)nitems_ * blockDim.x) {
     const int i = (int)(e % n), c = (int)(e / n);
     x[perm[i] + c * ldx] = Bt[e];
   }
 }
-__global__ void k_rank_if(int* p, const int* a, const int* b) { *p = (*a > 0 && *b > 0) ? *b : 0; }
+__device__ void it_rank_if(int* p, const int* a, const int* b, int item_, int nitems_, double* smx_) {
+  if (threadIdx.x == 0) *p = (*a > 0 && *b > 0) ? *b : 0;
+}
 // stack [T (rows x kT), zero-extended N (rows_new at row_off, knew cols)] -> dst (rows x (kT+knew))
-__global__ void k_stack(double* dst, int ldd, int rows, const double* T, int ldt, const int* kT, const double* Nw,
-                        int ldn, int row_off, int rows_new, Dim knew) {
+__device__ void it_stack(double* dst, int ldd, int rows, const double* T, int ldt, const int* kT, const double* Nw,
+                        int ldn, int row_off, int rows_new, Dim knew, int item_, int nitems_, double* smx_) {
   const int kt = kT ? *kT : 0, kn = knew.v();
   const long long tot = (long long)rows * (kt + kn);
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+  for (long long e = (long long)item_ * blockDim.x + threadIdx.x; e < tot; e += (long long)nitems_ * blockDim.x) {
     const int i = (int)(e % rows), j = (int)(e / rows);
     double v;
     if (j < kt) v = T[i + (size_t)j * ldt];
@@ -460,8 +464,8 @@ __global__ void k_stack(double* dst, int ldd, int rows, const double* T, int ldt
 }
 // choose the Case-2 factorisation of C = S^X G S^Y (k1 x k2), reading R23:
 // k1 <= k2: A = V^X (Ca = I), B = W^Y C^T (Cb = C^T); else A = V^X C (Ca = C), B = W^Y (Cb = I)
-__global__ void k_choose(const double* Cm, int ldc, const int* k1p, const int* k2p, double* Ca, double* Cb, int ldo,
-                         int* kout) {
+__device__ void it_choose(const double* Cm, int ldc, const int* k1p, const int* k2p, double* Ca, double* Cb, int ldo,
+                         int* kout, int item_, int nitems_, double* smx_) {
   const int k1 = *k1p, k2 = *k2p;
   const bool first = k1 <= k2;
   const int kk = first ? k1 : k2;
@@ -474,151 +478,19 @@ __global__ void k_choose(const double* Cm, int ldc, const int* k1p, const int* k
   }
   if (threadIdx.x == 0) *kout = kk;
 }
-__global__ void k_identity(double* I, int ld, int m) {
-  for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < m * m; e += blockDim.x * gridDim.x)
+__device__ void it_identity(double* I, int ld, int m, int item_, int nitems_, double* smx_) {
+  for (int e = threadIdx.x + item_ * blockDim.x; e < m * m; e += blockDim.x * nitems_)
     I[(e % m) + (e / m) * ld] = (e % m) == (e / m) ? 1.0 : 0.0;
 }
-__global__ void k_transpose_tile(double* dst, int ldd, const double* src, int lds, int rows, int cols) {
-  for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < rows * cols; e += blockDim.x * gridDim.x) {
+__device__ void it_transpose_tile(double* dst, int ldd, const double* src, int lds, int rows, int cols, int item_, int nitems_, double* smx_) {
+  for (int e = threadIdx.x + item_ * blockDim.x; e < rows * cols; e += blockDim.x * nitems_) {
     const int i = e % rows, j = e / rows;  // dst (rows x cols) = src^T
     dst[i + j * ldd] = src[j + i * lds];
   }
 }
-__global__ void k_add_int(int* p, Dim a, Dim b) { *p = a.v() + b.v(); }
-
-void level_seg(const h2_tree_* T, int root, int L, int* begin, int* count) {
-  *begin = 0;
-  *count = 0;
-  if (L > T->depth || L < T->level[root]) return;
-  const int* b = T->bfs.data() + T->level_ptr[L];
-  const int* e = T->bfs.data() + T->level_ptr[L + 1];
-  const int* lo = std::lower_bound(b, e, root);
-  const int* hi = std::lower_bound(b, e, root + T->tsize[root]);
-  *begin = (int)(lo - T->bfs.data());
-  *count = (int)(hi - lo);
+__device__ void it_add_int(int* p, Dim a, Dim b, int item_, int nitems_, double* smx_) {
+  if (threadIdx.x == 0) *p = a.v() + b.v();
 }
 
-void leaf_rng(const h2_tree_* T, int root, int* begin, int* count) {
-  const auto lo = std::lower_bound(T->leaves.begin(), T->leaves.end(), root);
-  const auto hi = std::lower_bound(T->leaves.begin(), T->leaves.end(), root + T->tsize[root]);
-  *begin = (int)(lo - T->leaves.begin());
-  *count = (int)(hi - lo);
-}
-
-constexpr size_t SM_TSQR = (size_t)(PR * KC + KC + 8) * 8;
-constexpr size_t SM_EXPAND = (size_t)(2 * KC * KC) * 8;
-constexpr size_t SM_TEMP = (size_t)(3 * KC * KC + KC) * 8 + (KC + 8) * 4;
-bool g_attr = false;
-void init_attr() {
-  if (g_attr) return;
-  cudaFuncSetAttribute(k_tsqr_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_TSQR);
-  cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXPAND);
-  cudaFuncSetAttribute(k_temp_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_TEMP);
-  g_attr = true;
-}
-
-}  // namespace
-
-void expand_basis(const MatDev& M, const DevSide& D, int t, double* out, int ld, cudaStream_t st) {
-  int l0, nl;
-  leaf_rng(D.tree, t, &l0, &nl);
-  init_attr();
-  k_expand<<<nl, NT, SM_EXPAND, st>>>(M, D, t, l0, out, ld);
-}
-
-void gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb, Dim m, Dim n,
-          Dim k, int mcap, int ncap, int kcap, double alpha, double beta, cudaStream_t st) {
-  if (mcap <= 0 || ncap <= 0) return;
-  if (kcap > 512 && mcap <= KC && ncap <= KC) {
-    if (!g_part) cudaMalloc(&g_part, sizeof(double) * NPART * KC * KC);
-    const int chunk = (kcap + NPART - 1) / NPART;
-    k_gemm_inner_part<<<NPART, NT, 0, st>>>(g_part, A, lda, ta, B, ldb, tb, m, n, k, chunk);
-    k_gemm_inner_sum<<<1, NT, 0, st>>>(C, ldc, g_part, NPART, m, n, alpha, beta);
-    return;
-  }
-  const long long tot = (long long)mcap * ncap;
-  k_gemm<<<std::max(1, std::min(cdiv(tot, NT), 4 * 148)), NT, 0, st>>>(C, ldc, A, lda, ta, B, ldb, tb, m, n, k,
-                                                                       alpha, beta);
-}
-
-void hmul_dense(const MatDev& M, bool trans, int a, int b, int b_blk, const double* D, int ldd, Dim m, int mcap,
-                double* out, int ldo, double alpha, double beta, cudaStream_t st) {
-  (void)b_blk;
-  (void)mcap;
-  const DevSide& Dd = trans ? M.col : M.row;  // rows of op(Z)
-  const DevSide& Ds = trans ? M.row : M.col;  // columns of op(Z)
-  const h2_tree_* Td = Dd.tree;
-  const h2_tree_* Ts = Ds.tree;
-  double* xh = Ds.hx;
-  double* yh = Dd.hy;
-  int l0, nl;
-  leaf_rng(Ts, b, &l0, &nl);
-  k_hm_fwd_leaf<<<nl, NT, 0, st>>>(M, Ds, l0, Ts->lo[b], D, ldd, m, xh);
-  for (int L = Ts->depth - 1; L >= Ts->level[b]; --L) {
-    int s0, ns;
-    level_seg(Ts, b, L, &s0, &ns);
-    if (ns) k_hm_fwd_level<<<ns, NT, 0, st>>>(M, Ds, s0, m, xh);
-  }
-  k_hm_couple<<<Td->tsize[a], NT, 0, st>>>(M, Dd, Ds, a, b, trans ? 1 : 0, m, xh, yh);
-  for (int L = Td->level[a] + 1; L <= Td->depth; ++L) {
-    int s0, ns;
-    level_seg(Td, a, L, &s0, &ns);
-    if (ns) k_hm_bwd_level<<<ns, NT, 0, st>>>(M, Dd, s0, m, yh);
-  }
-  int la0, nla;
-  leaf_rng(Td, a, &la0, &nla);
-  k_hm_leaf<<<nla, NT, 0, st>>>(M, Dd, Ds, la0, a, b, trans ? 1 : 0, D, ldd, m, yh, out, ldo, alpha, beta);
-}
-
-void tile_potrf(const MatDev& M, int slot, int t, cudaStream_t st) { k_potrf<<<1, NT, 0, st>>>(M, slot, t); }
-void tile_getrf(const MatDev& M, int slot, int t, cudaStream_t st) { k_getrf<<<1, NT, 0, st>>>(M, slot, t); }
-
-void tile_trsm(const MatDev& M, int slot, int m, int mode, double* B, int ldb, int brows, Dim bcols, int bcolcap,
-               cudaStream_t st) {
-  const bool rowwise = (mode == RLT || mode == RUN);
-  const int nvec = rowwise ? brows : bcolcap;
-  k_trsm<<<std::max(1, cdiv(nvec, NT)), NT, 0, st>>>(M, slot, m, mode, B, ldb, brows, bcols);
-}
-
-void tsqr_r(const double* A, int lda, int rows, Dim K, double* R, int ldr, cudaStream_t st) {
-  init_attr();
-  k_tsqr_r<<<1, NT, SM_TSQR, st>>>(A, lda, rows, K, R, ldr);
-}
-
-void temp_core(const double* Ra, const double* Rb, int ldr, Dim K, double* Ma, double* Mb, int ldm, int* rout,
-               double rel, double abs_tol, int max_rank, int cap, int* flags, cudaStream_t st) {
-  init_attr();
-  k_temp_core<<<1, NT, SM_TEMP, st>>>(Ra, Rb, ldr, K, Ma, Mb, ldm, rout, rel, abs_tol, max_rank, cap, flags);
-}
-
-void copy_cols(double* dst, int ldd, const double* src, int lds, int rows, Dim cols, int colcap, cudaStream_t st) {
-  const long long tot = (long long)rows * colcap;
-  if (tot <= 0) return;
-  k_copy_cols<<<std::max(1, std::min(cdiv(tot, NT), 4 * 148)), NT, 0, st>>>(dst, ldd, src, lds, rows, cols);
-}
-
-void set_int(int* p, Dim v, cudaStream_t st) { k_set_int<<<1, 1, 0, st>>>(p, v); }
-void gather_cols(double* Bt, const double* x, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t st) {
-  k_gather_cols<<<std::max(1, std::min(cdiv((long long)n * nrhs, NT), 8 * 148)), NT, 0, st>>>(Bt, x, perm, n, nrhs, ldx);
-}
-void scatter_cols(double* x, const double* Bt, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t st) {
-  k_scatter_cols<<<std::max(1, std::min(cdiv((long long)n * nrhs, NT), 8 * 148)), NT, 0, st>>>(x, Bt, perm, n, nrhs, ldx);
-}
-void rank_if(int* p, const int* a, const int* b, cudaStream_t st) { k_rank_if<<<1, 1, 0, st>>>(p, a, b); }
-void stack_cols(double* dst, int ldd, int rows, const double* T, int ldt, const int* kT, const double* Nw, int ldn,
-                int row_off, int rows_new, Dim knew, int colcap, cudaStream_t st) {
-  const long long tot = (long long)rows * colcap;
-  k_stack<<<std::max(1, std::min(cdiv(tot, NT), 4 * 148)), NT, 0, st>>>(dst, ldd, rows, T, ldt, kT, Nw, ldn, row_off,
-                                                                        rows_new, knew);
-}
-void choose_case2(const double* Cm, int ldc, const int* k1, const int* k2, double* Ca, double* Cb, int ldo, int* kout,
-                  cudaStream_t st) {
-  k_choose<<<1, NT, 0, st>>>(Cm, ldc, k1, k2, Ca, Cb, ldo, kout);
-}
-void identity(double* I, int ld, int m, cudaStream_t st) { k_identity<<<std::max(1, cdiv(m * m, NT)), NT, 0, st>>>(I, ld, m); }
-void transpose_tile(double* dst, int ldd, const double* src, int lds, int rows, int cols, cudaStream_t st) {
-  k_transpose_tile<<<std::max(1, cdiv(rows * cols, NT)), NT, 0, st>>>(dst, ldd, src, lds, rows, cols);
-}
-void add_int(int* p, Dim a, Dim b, cudaStream_t st) { k_add_int<<<1, 1, 0, st>>>(p, a, b); }
-
+}  // namespace ar
 }  // namespace h2

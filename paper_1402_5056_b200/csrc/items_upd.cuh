@@ -1,34 +1,21 @@
-// Local low-rank update Z|_{t0 x s0} += alpha X Y^T on the device (Theorem 1).
-//
-// One update = a short sequence of launches, each covering every cluster of one phase/level of
-// BOTH sides (row basis V/E with subtree root t0, column basis W/F with root s0):
-//   k_upd_ext_leaf     U0 exact nearfield add + U1/U2 leaf R-factors of V~_t = [V_t, X|t]
-//   k_upd_ext_level    U2 R-factors of the extended nested basis, bottom-up ([BO10 Alg.16])
-//   k_upd_weights_path U3 weights B~_t along pred(t0) (root first), TSQR of the stacked
-//                      [R_{W,s} S~_{t,s}^T ; B~_{t+} E~_t^T]
-//   k_upd_weights_level U3 below t0, top-down
-//   k_upd_svd_leaf     U4 leaf SVD of V~_t B~_t^T, rank choice, Q_t, R_t = Q_t^T V~_t
-//   k_upd_svd_level    U4 internal SVD of V^_t B~_t^T, V^_t = [R_{t1}E~_{t1}; R_{t2}E~_{t2}]
-//   k_upd_couple       U5 S_b <- R_t S~_b R_s^T (three cases)
-//   k_upd_install      U6 V_t <- Q_t, E <- F, E_{t0} <- R_{t0}[E_{t0};0], R-cache reset
-//   k_upd_rcache_path  refresh the memoised R-factors of the current bases on pred(t0)
-// Ranks are decided on the device and consumed from device memory (capacity-padded slots), so the
-// host never synchronises inside an update.  One CTA owns one small matrix in shared memory.
+// Device items of the local low-rank update U0-U6, executed by the op executor
+// (h2_exec.cu).  Item i of an op is what one CTA of the corresponding phase computes; see the
+// phase list in h2_exec.cu.  Generated from the per-phase kernels of round 1 (same arithmetic).
+#pragma once
 #include <cuda_runtime.h>
 
-#include <algorithm>
-
 #include "devla.cuh"
-#include "h2_internal.h"
+#include "exec.h"
 
 namespace h2 {
-namespace {
+namespace upd {
 
 constexpr int NT = NTHREADS;
 constexpr int KC = KCAP_MAX;      // 96
-constexpr int RM = KC;            // row capacity of V~_t / V^_t in the SVD kernels: max(lmax, 2 rank_cap) <= 96
+constexpr int RM = KC + 1;        // (odd) leading dim of V~_t / V^_t in the SVD items: max(lmax, 2 rank_cap) <= 96 rows
 constexpr int PR = 192;           // TSQR panel rows (>= KC + largest chunk)
-constexpr int LD2 = 2 * KC;       // rows of a stacked pair of KC x KC factors
+constexpr int PRL = PR + 1;       // odd leading dimensions: column-parallel loops hit distinct smem banks
+constexpr int LD2 = 2 * KC + 1;   // (odd) leading dim of a stacked pair of KC x KC factors
 
 __device__ __forceinline__ bool inside(const DevSide& D, int t, int root) {
   return t >= root && t < root + D.tsize[root];
@@ -37,13 +24,13 @@ __device__ __forceinline__ bool inside(const DevSide& D, int t, int root) {
 __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm, int mode);
 
 // ---- U0 + U1/U2 leaves + local weight stacks of the ancestors (all independent) ---------------
-__global__ void __launch_bounds__(NT) k_upd_ext_leaf(MatDev M, UpdArgs a_, int rl0, int nrl, int cl0, int ncl,
-                                                     int in0, int nin, int npA, int npB) {
+__device__ void it_upd_ext_leaf(const MatDev& M, UpdArgs a_, int rl0, int nrl, int cl0, int ncl,
+                                                     int in0, int nin, int npA, int npB, int item_, int nitems_, double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  extern __shared__ double sm[];
-  const int b = blockIdx.x;
+  double* sm = smx_;
+  const int b = item_;
   if (b >= nrl + ncl + nin) {
     // U3 (part): C_a = R(local stack) for the proper ancestors a of t0 (side A) / s0 (side B)
     const int j = b - (nrl + ncl + nin);
@@ -65,7 +52,7 @@ __global__ void __launch_bounds__(NT) k_upd_ext_leaf(MatDev M, UpdArgs a_, int r
     const int64_t ldx = rs ? a.ldx : a.ldy;
     const double al = rs ? a.alpha : 1.0;
     const int m = D.hi[t] - D.lo[t], kt = D.rank[t], K = kt + a.k;
-    const int lda = M.lmax;
+    const int lda = M.lmax | 1;
     double* A = sm;                 // lmax x KC
     double* diag = A + lda * KC;    // KC
     double* red = diag + KC;        // 1
@@ -103,14 +90,14 @@ __global__ void __launch_bounds__(NT) k_upd_ext_leaf(MatDev M, UpdArgs a_, int r
 }
 
 // ---- U2 internal, bottom-up ------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_upd_ext_level(MatDev M, UpdArgs a_, int bA, int nA, int bB, int nB) {
+__device__ void it_upd_ext_level(const MatDev& M, UpdArgs a_, int bA, int nA, int bB, int nB, int item_, int nitems_, double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  extern __shared__ double sm[];
-  const bool rs = (int)blockIdx.x < nA;
+  double* sm = smx_;
+  const bool rs = (int)item_ < nA;
   const DevSide& D = rs ? M.row : M.col;
-  const int t = D.bfs[rs ? bA + blockIdx.x : bB + blockIdx.x - nA];
+  const int t = D.bfs[rs ? bA + item_ : bB + item_ - nA];
   if (D.son0[t] < 0) return;
   const int k = a.k, kt = D.rank[t], K = kt + k;
   double* A = sm;              // LD2 x KC
@@ -169,19 +156,19 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
   const int kt = A.rank[t];
   const int K = kt + (in_t ? k : 0);
   double* P = sm;                 // PR x KC panel
-  double* diag = P + PR * KC;
+  double* diag = P + PRL * KC;
   double* red = diag + KC;
   int rows = 0;
   double fl = 0.0;
   auto flush = [&]() {
     if (rows > 0) {
-      la::cta_qr_R(P, PR, rows, K, diag, red);
+      la::cta_qr_R(P, PRL, rows, K, diag, red);
       fl += hh_flops(rows, K);
       rows = rows < K ? rows : K;
     }
   };
   if (mode == W_CHAIN) {
-    la::cta_copy(P, PR, A.re + (size_t)t * M.kcap * M.kcap, M.kcap, K, K);
+    la::cta_copy(P, PRL, A.re + (size_t)t * M.kcap * M.kcap, M.kcap, K, K);
     rows = K;
     __syncthreads();
   }
@@ -205,7 +192,7 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
       } else if (in_s) {
         v = RB[i + (ls + c - kt) * ldR];  // identity block of S~ = diag(S, I)
       }
-      P[rows + i + c * PR] = v;
+      P[rows + i + c * PRL] = v;
     }
     fl += (double)rc * ls * kt;  // triangular R_B times S^T
     rows += rc;
@@ -228,7 +215,7 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
         } else if (in_p) {
           v = Bp[i + (kp + c - kt) * M.kcap];  // E~_t = diag(E_t, I) inside T_{t0}
         }                                      // E~_{t0} = [E_{t0}; 0]: zero columns
-        P[rows + i + c * PR] = v;
+        P[rows + i + c * PRL] = v;
       }
       fl += 2.0 * Kp * kp * kt;
       rows += Kp;
@@ -239,18 +226,18 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
   double* Bt = (mode == W_LOCAL ? A.re : A.bw) + (size_t)t * M.kcap * M.kcap;
   for (int e = threadIdx.x; e < K * K; e += NT) {
     const int i = e % K, j = e / K;
-    Bt[i + j * M.kcap] = i < rows ? P[i + j * PR] : 0.0;
+    Bt[i + j * M.kcap] = i < rows ? P[i + j * PRL] : 0.0;
   }
   __syncthreads();
   return fl;
 }
 
-__global__ void __launch_bounds__(NT) k_upd_weights_path(MatDev M, UpdArgs a_) {
+__device__ void it_upd_weights_path(const MatDev& M, UpdArgs a_, int item_, int nitems_, double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  extern __shared__ double sm[];
-  const bool rs = blockIdx.x == 0;
+  double* sm = smx_;
+  const bool rs = item_ == 0;
   const DevSide& A = rs ? M.row : M.col;
   int path[64];
   int np = 0;
@@ -261,14 +248,14 @@ __global__ void __launch_bounds__(NT) k_upd_weights_path(MatDev M, UpdArgs a_) {
   if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_W_PATH, fl);
 }
 
-__global__ void __launch_bounds__(NT) k_upd_weights_level(MatDev M, UpdArgs a_, int bA, int nA, int bB, int nB) {
+__device__ void it_upd_weights_level(const MatDev& M, UpdArgs a_, int bA, int nA, int bB, int nB, int item_, int nitems_, double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  extern __shared__ double sm[];
-  const bool rs = (int)blockIdx.x < nA;
+  double* sm = smx_;
+  const bool rs = (int)item_ < nA;
   const DevSide& A = rs ? M.row : M.col;
-  const int t = A.bfs[rs ? bA + blockIdx.x : bB + blockIdx.x - nA];
+  const int t = A.bfs[rs ? bA + item_ : bB + item_ - nA];
   const double fl = weights_cluster(M, a, rs, t, sm, W_FULL);
   if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_W_LEVEL, fl);
 }
@@ -278,19 +265,22 @@ __global__ void __launch_bounds__(NT) k_upd_weights_level(MatDev M, UpdArgs a_, 
 __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, int t, double* V, int ldv, int m,
                          int K, double* sm_rest, int kid, double extra_flops) {
   double* Bt = sm_rest;             // KC x KC
-  double* Mm = Bt + KC * KC;        // RM x KC (ld RM)
+  double* Mm = Bt + RM * KC;        // RM x KC (ld RM); the Bt region is RM x KC so that Q can reuse it
   double* Q = Bt;                   // RM x KC (ld RM), reuses Bt once M = V B~^T is formed
   double* sig = Mm + RM * KC;       // KC
   int* order = (int*)(sig + KC);    // KC ints
   int* scr = order + KC;            // 4 ints
   const double* Bg = D.bw + (size_t)t * M.kcap * M.kcap;
+  const long long c0 = clock64();
   la::cta_copy(Bt, KC, Bg, M.kcap, K, K);
   __syncthreads();
   // Mm = V Bt^T  (m x K)
   la::cta_gemm(Mm, RM, V, ldv, false, Bt, KC, true, m, K, K, false);
   __syncthreads();
-  la::cta_jacobi(Mm, RM, m, K, sig, order, scr);
-  __shared__ int clamped;
+  const long long c1 = clock64();
+  const int sweeps = la::cta_jacobi(Mm, RM, m, K, sig, order, scr);
+  const long long c2 = clock64();
+  int& clamped = scr[2];
   if (threadIdx.x == 0) clamped = 0;
   __syncthreads();
   const int r = la::trunc_rank(sig, order, K, a.rel_tol, a.abs_tol, a.max_rank, M.rcap, &clamped);
@@ -309,18 +299,28 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
   if (threadIdx.x == 0) {
     D.rnew[t] = r;
     if (clamped) atomicOr(M.flags, 1);
-    if (a.prof) atomicAdd(a.prof + 2 * kid, extra_flops + 2.0 * m * K * K + svd_flops(m, K) + 2.0 * r * K * m);
+    if (a.prof) {
+      atomicAdd(a.prof + 2 * kid, extra_flops + 2.0 * m * K * K + svd_flops(m, K) + 2.0 * r * K * m);
+      double* dbg = a.prof + 4 * K_COUNT;  // svd phase counters (profiling only)
+      atomicAdd(dbg + 0, (double)(c1 - c0));
+      atomicAdd(dbg + 1, (double)(c2 - c1));
+      atomicAdd(dbg + 2, (double)(clock64() - c2));
+      atomicAdd(dbg + 3, 1.0);
+      atomicAdd(dbg + 4, (double)K);
+      atomicAdd(dbg + 5, (double)m);
+      atomicAdd(dbg + 6, (double)sweeps);
+    }
   }
 }
 
-__global__ void __launch_bounds__(NT) k_upd_svd_leaf(MatDev M, UpdArgs a_, int rl0, int nrl, int cl0, int ncl) {
+__device__ void it_upd_svd_leaf(const MatDev& M, UpdArgs a_, int rl0, int nrl, int cl0, int ncl, int item_, int nitems_, double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  extern __shared__ double sm[];
-  const bool rs = (int)blockIdx.x < nrl;
+  double* sm = smx_;
+  const bool rs = (int)item_ < nrl;
   const DevSide& D = rs ? M.row : M.col;
-  const int t = D.leaves[rs ? rl0 + blockIdx.x : cl0 + blockIdx.x - nrl];
+  const int t = D.leaves[rs ? rl0 + item_ : cl0 + item_ - nrl];
   const int root = rs ? a.t0 : a.s0;
   const double* Xf = rs ? a.X : a.Y;
   const int64_t ldx = rs ? a.ldx : a.ldy;
@@ -337,14 +337,14 @@ __global__ void __launch_bounds__(NT) k_upd_svd_leaf(MatDev M, UpdArgs a_, int r
   svd_core(M, a, D, t, V, RM, m, K, V + RM * KC, K_SVD_LEAF, 0.0);
 }
 
-__global__ void __launch_bounds__(NT) k_upd_svd_level(MatDev M, UpdArgs a_, int bA, int nA, int bB, int nB) {
+__device__ void it_upd_svd_level(const MatDev& M, UpdArgs a_, int bA, int nA, int bB, int nB, int item_, int nitems_, double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  extern __shared__ double sm[];
-  const bool rs = (int)blockIdx.x < nA;
+  double* sm = smx_;
+  const bool rs = (int)item_ < nA;
   const DevSide& D = rs ? M.row : M.col;
-  const int t = D.bfs[rs ? bA + blockIdx.x : bB + blockIdx.x - nA];
+  const int t = D.bfs[rs ? bA + item_ : bB + item_ - nA];
   if (D.son0[t] < 0) return;
   const int k = a.k, kt = D.rank[t], K = kt + k;
   double* V = sm;  // RM x KC : V^_t = [R_{t1} E~_{t1}; R_{t2} E~_{t2}]
@@ -377,18 +377,18 @@ __global__ void __launch_bounds__(NT) k_upd_svd_level(MatDev M, UpdArgs a_, int 
 }
 
 // ---- U5 couplings ------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_upd_couple(MatDev M, UpdArgs a_, int nA, int nB) {
+__device__ void it_upd_couple(const MatDev& M, UpdArgs a_, int nA, int nB, int item_, int nitems_, double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  extern __shared__ double sm[];
+  double* sm = smx_;
   double* T1 = sm;             // KC x KC (ld KC)
   double* Out = T1 + KC * KC;  // KC x KC (ld KC)
   const int k = a.k;
-  const bool rs = (int)blockIdx.x < nA;
+  const bool rs = (int)item_ < nA;
   double fl = 0.0;
   if (rs) {
-    const int t = a.t0 + blockIdx.x;
+    const int t = a.t0 + item_;
     const int kt = M.row.rank[t], rt = M.row.rnew[t];
     const double* RNt = M.row.rn + (size_t)t * M.kcap * M.kcap;  // rt x Kt
     for (int q = M.row.bptr[t]; q < M.row.bptr[t + 1]; ++q) {
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(NT) k_upd_couple(MatDev M, UpdArgs a_, int nA,
       __syncthreads();
     }
   } else {
-    const int s = a.s0 + (blockIdx.x - nA);
+    const int s = a.s0 + (item_ - nA);
     const int ls = M.col.rank[s], rsn = M.col.rnew[s];
     const double* RNs = M.col.rn + (size_t)s * M.kcap * M.kcap;  // rsn x (ls + k)
     for (int q = M.col.bptr[s]; q < M.col.bptr[s + 1]; ++q) {
@@ -447,15 +447,15 @@ __global__ void __launch_bounds__(NT) k_upd_couple(MatDev M, UpdArgs a_, int nA,
 }
 
 // ---- U6 install --------------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_upd_install(MatDev M, UpdArgs a_, int nA, int nB) {
+__device__ void it_upd_install(const MatDev& M, UpdArgs a_, int nA, int nB, int item_, int nitems_, double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  extern __shared__ double sm[];
-  const bool rs = (int)blockIdx.x < nA;
+  double* sm = smx_;
+  const bool rs = (int)item_ < nA;
   const DevSide& D = rs ? M.row : M.col;
   const int root = rs ? a.t0 : a.s0;
-  const int t = root + (rs ? blockIdx.x : blockIdx.x - nA);
+  const int t = root + (rs ? item_ : item_ - nA);
   const int r = D.rnew[t];
   const double* qn = D.qn + (size_t)t * M.ldq * M.rcap;
   if (D.son0[t] < 0) {
@@ -486,12 +486,12 @@ __global__ void __launch_bounds__(NT) k_upd_install(MatDev M, UpdArgs a_, int nA
 }
 
 // ---- memoised R-factors on pred(t0) ----------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_upd_rcache_path(MatDev M, UpdArgs a_) {
+__device__ void it_upd_rcache_path(const MatDev& M, UpdArgs a_, int item_, int nitems_, double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  extern __shared__ double sm[];
-  const bool rs = blockIdx.x == 0;
+  double* sm = smx_;
+  const bool rs = item_ == 0;
   const DevSide& D = rs ? M.row : M.col;
   double* A = sm;  // LD2 x KC
   double* diag = A + LD2 * KC;
@@ -525,106 +525,5 @@ __global__ void __launch_bounds__(NT) k_upd_rcache_path(MatDev M, UpdArgs a_) {
   }
 }
 
-constexpr size_t SM_WEIGHTS = (size_t)(PR * KC + KC + 8) * 8;
-constexpr size_t SM_EXT_LEAF = SM_WEIGHTS;  // also runs the ancestors' local weight stacks
-constexpr size_t SM_EXT_LEVEL = (size_t)(LD2 * KC + KC + 8) * 8;
-constexpr size_t SM_SVD = (size_t)(RM * KC + KC * KC + RM * KC + KC) * 8 + (KC + 8) * 4;
-constexpr size_t SM_COUPLE = (size_t)(2 * KC * KC) * 8;
-constexpr size_t SM_INSTALL = (size_t)(KC * KC) * 8;
-
-bool g_attr_done = false;
-
-// clusters of `T` at level L inside the subtree of root: contiguous segment of the BFS list
-void level_segment(const h2_tree_* T, int root, int L, int* begin, int* count) {
-  *begin = 0;
-  *count = 0;
-  if (L > T->depth || L < T->level[root]) return;
-  const int* b = T->bfs.data() + T->level_ptr[L];
-  const int* e = T->bfs.data() + T->level_ptr[L + 1];
-  const int* lo = std::lower_bound(b, e, root);
-  const int* hi = std::lower_bound(b, e, root + T->tsize[root]);
-  *begin = (int)(lo - T->bfs.data());
-  *count = (int)(hi - lo);
-}
-
-void leaf_range(const h2_tree_* T, int root, int* begin, int* count) {
-  const auto b = T->leaves.begin(), e = T->leaves.end();
-  const auto lo = std::lower_bound(b, e, root);
-  const auto hi = std::lower_bound(b, e, root + T->tsize[root]);
-  *begin = (int)(lo - b);
-  *count = (int)(hi - lo);
-}
-
-}  // namespace
-
-cudaError_t update_init_attributes() {
-  if (g_attr_done) return cudaSuccess;
-  cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_upd_ext_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXT_LEAF))) return e;
-  if ((e = cudaFuncSetAttribute(k_upd_ext_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXT_LEVEL))) return e;
-  if ((e = cudaFuncSetAttribute(k_upd_weights_path, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_WEIGHTS))) return e;
-  if ((e = cudaFuncSetAttribute(k_upd_weights_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_WEIGHTS))) return e;
-  if ((e = cudaFuncSetAttribute(k_upd_svd_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_SVD))) return e;
-  if ((e = cudaFuncSetAttribute(k_upd_svd_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_SVD))) return e;
-  if ((e = cudaFuncSetAttribute(k_upd_couple, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_COUPLE))) return e;
-  if ((e = cudaFuncSetAttribute(k_upd_install, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_INSTALL))) return e;
-  if ((e = cudaFuncSetAttribute(k_upd_rcache_path, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXT_LEVEL))) return e;
-  g_attr_done = true;
-  return cudaSuccess;
-}
-
-cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a_in, cudaStream_t st) {
-  UpdArgs a = a_in;
-  a.prof = prof_dev();
-  cudaError_t e = update_init_attributes();
-  if (e != cudaSuccess) return e;
-  const MatDev& M = Z->d;
-  const h2_btree_* B = Z->bt;
-  const h2_tree_* R = B->rt;
-  const h2_tree_* C = B->ct;
-  const int b0 = B->find(a.t0, a.s0);
-  const int in0 = Z->inad_range[2 * b0], nin = Z->inad_range[2 * b0 + 1] - in0;
-  if (B->kind[b0] == INADM) {  // dense add only
-    if (nin > 0) H2_LAUNCH(K_EXT_LEAF, st, k_upd_ext_leaf<<<nin, NT, SM_EXT_LEAF, st>>>(M, a, 0, 0, 0, 0, in0, nin, 0, 0));
-    return cudaGetLastError();
-  }
-  int rl0, nrl, cl0, ncl;
-  leaf_range(R, a.t0, &rl0, &nrl);
-  leaf_range(C, a.s0, &cl0, &ncl);
-  const int Lr = R->level[a.t0], Lc = C->level[a.s0];
-  H2_LAUNCH(K_EXT_LEAF, st,
-            k_upd_ext_leaf<<<nrl + ncl + nin + Lr + Lc, NT, SM_EXT_LEAF, st>>>(M, a, rl0, nrl, cl0, ncl, in0, nin, Lr,
-                                                                               Lc));
-  const int Lmax = std::max(R->depth, C->depth), Lmin = std::min(Lr, Lc);
-  // U2 bottom-up (internal clusters)
-  for (int L = Lmax - 1; L >= Lmin; --L) {
-    int bA, nA, bB, nB;
-    level_segment(R, a.t0, L, &bA, &nA);
-    level_segment(C, a.s0, L, &bB, &nB);
-    if (nA + nB > 0) H2_LAUNCH(K_EXT_LEVEL, st, k_upd_ext_level<<<nA + nB, NT, SM_EXT_LEVEL, st>>>(M, a, bA, nA, bB, nB));
-  }
-  // U3 weights: path (root .. t0), then the subtree top-down
-  H2_LAUNCH(K_W_PATH, st, k_upd_weights_path<<<2, NT, SM_WEIGHTS, st>>>(M, a));
-  for (int L = Lmin + 1; L <= Lmax; ++L) {
-    int bA = 0, nA = 0, bB = 0, nB = 0;
-    if (L > Lr) level_segment(R, a.t0, L, &bA, &nA);
-    if (L > Lc) level_segment(C, a.s0, L, &bB, &nB);
-    if (nA + nB > 0) H2_LAUNCH(K_W_LEVEL, st, k_upd_weights_level<<<nA + nB, NT, SM_WEIGHTS, st>>>(M, a, bA, nA, bB, nB));
-  }
-  // U4 bottom-up
-  H2_LAUNCH(K_SVD_LEAF, st, k_upd_svd_leaf<<<nrl + ncl, NT, SM_SVD, st>>>(M, a, rl0, nrl, cl0, ncl));
-  for (int L = Lmax - 1; L >= Lmin; --L) {
-    int bA, nA, bB, nB;
-    level_segment(R, a.t0, L, &bA, &nA);
-    level_segment(C, a.s0, L, &bB, &nB);
-    if (nA + nB > 0) H2_LAUNCH(K_SVD_LEVEL, st, k_upd_svd_level<<<nA + nB, NT, SM_SVD, st>>>(M, a, bA, nA, bB, nB));
-  }
-  // U5, U6, R-cache refresh
-  const int nA = R->tsize[a.t0], nB = C->tsize[a.s0];
-  H2_LAUNCH(K_COUPLE, st, k_upd_couple<<<nA + nB, NT, SM_COUPLE, st>>>(M, a, nA, nB));
-  H2_LAUNCH(K_INSTALL, st, k_upd_install<<<nA + nB, NT, SM_INSTALL, st>>>(M, a, nA, nB));
-  H2_LAUNCH(K_RCACHE, st, k_upd_rcache_path<<<2, NT, SM_EXT_LEVEL, st>>>(M, a));
-  return cudaGetLastError();
-}
-
+}  // namespace upd
 }  // namespace h2

@@ -18,7 +18,7 @@ EXPORTED_SYMBOLS = [
     "h2_block_tree", "h2_btree_export", "h2_btree_destroy",
     "h2_from_sparse", "h2_lowrank_update", "h2_matvec", "h2_addmul", "h2_lr_factor", "h2_solve",
     "h2_ranks", "h2_storage_report", "h2_export", "h2_check_device_flags",
-    "h2_profile_enable", "h2_profile_read", "h2_stats",
+    "h2_profile_enable", "h2_profile_read", "h2_profile_debug", "h2_stats",
     "h2_mat_destroy", "h2_last_error",
 ]
 
@@ -53,6 +53,7 @@ _sig = {
     "h2_check_device_flags": [_p, _p],
     "h2_profile_enable": [_i32],
     "h2_stats": [_p, _p],
+    "h2_profile_debug": [_p],
     "h2_profile_read": [_p, _p, _p, _p, _p, _p],
     "h2_mat_destroy": [_p],
     "h2_last_error": [],
@@ -298,4 +299,10 @@ def h2_profile_read():
         name = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
         if la[i]:
             out[name] = dict(launches=int(la[i]), ms=float(ms[i]), flops=float(fl[i]), bytes=float(by[i]))
+    return out
+
+
+def h2_profile_debug():
+    out = np.zeros(16)
+    _check(_lib.h2_profile_debug(_ptr(out)))
     return out
