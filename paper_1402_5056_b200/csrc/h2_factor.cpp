@@ -88,6 +88,7 @@ struct Temp {
   double* A;
   double* B;
   int* k;
+  bool nz;  // some contribution of possibly non-zero rank was added (host-side, symbolic)
 };
 
 struct Driver {
@@ -102,6 +103,15 @@ struct Driver {
   long long n_updates = 0, n_dense = 0, n_temps = 0;
 
   int size(int t) const { return T->hi[t] - T->lo[t]; }
+  // Symbolic rank tracking (host): a cluster basis can only have a non-zero rank after an update
+  // touched its subtree; a Case-2 factor / substitution whose rank is structurally zero is skipped,
+  // exactly where the oracle skips a zero-column factor (the device would run a no-op).
+  static bool nzr(const HOp& X, int t) { return X.trans ? X.Z->nzc[t] != 0 : X.Z->nzr[t] != 0; }
+  static bool nzc(const HOp& X, int s) { return X.trans ? X.Z->nzr[s] != 0 : X.Z->nzc[s] != 0; }
+  void mark_update(int t, int r) {
+    for (int q = t; q < t + T->tsize[t]; ++q) Z->nzr[q] = 1;
+    for (int q = r; q < r + T->tsize[r]; ++q) Z->nzc[q] = 1;
+  }
   bool leaf(int t) const { return T->son0[t] < 0; }
   std::vector<int> sons_plus(int t) const {
     if (leaf(t)) return {t};
@@ -128,6 +138,7 @@ struct Driver {
     a.prof = nullptr;
     cudaError_t e = launch_update(Z, a, st);
     if (e != cudaSuccess) throw std::runtime_error(std::string("h2 update launch: ") + cudaGetErrorString(e));
+    if (Z->bt->kind[Z->bt->find(t, r)] != INADM) mark_update(t, r);
     ++n_updates;
   }
 
@@ -165,6 +176,7 @@ struct Driver {
            double alpha) {
     if (kcap == 0) return;
     if (tgt) {
+      tgt->nz = true;
       temp_add(*tgt, t, r, A, lda, B, ldb, kdev, kcap, alpha);
       return;
     }
@@ -189,6 +201,7 @@ struct Driver {
     *kdev = ar.ialloc();
     if (kx == ADM && ky == ADM) {
       if (X.Z->blk2adm[bx] < 0 || Y.Z->blk2adm[by] < 0) return 0;
+      if (!nzr(X, t) || !nzc(Y, r)) return 0;  // min(k^X_t, k^Y_r) = 0
       const DevSide& Xr = X.rows();
       const DevSide& Xc = X.cols();
       const DevSide& Yr = Y.rows();
@@ -230,6 +243,7 @@ struct Driver {
     }
     if (kx == ADM) {
       if (X.Z->blk2adm[bx] < 0) return 0;
+      if (!nzr(X, t)) return 0;  // k = k^X_t = 0
       const DevSide& Xr = X.rows();
       const DevSide& Xc = X.cols();
       *A = ar.alloc((size_t)mt * rcap);
@@ -250,6 +264,7 @@ struct Driver {
     }
     if (ky == ADM) {
       if (Y.Z->blk2adm[by] < 0) return 0;
+      if (!nzc(Y, r)) return 0;  // k = k^Y_r = 0
       const DevSide& Yr = Y.rows();
       const DevSide& Yc = Y.cols();
       double* Vys = ar.alloc((size_t)ms * rcap);
@@ -313,7 +328,7 @@ struct Driver {
           for (int t2 : T2)
             for (int r2 : R2) {
               Temp tm{t2, r2, size(t2), size(r2), ar.alloc((size_t)size(t2) * rcap), ar.alloc((size_t)size(r2) * rcap),
-                      ar.ialloc()};
+                      ar.ialloc(), false};
               set_int(tm.k, dimc(0), st);
               temps.push_back(tm);
             }
@@ -325,6 +340,7 @@ struct Driver {
           for (size_t i = 0; i < T2.size(); ++i)
             for (size_t j = 0; j < R2.size(); ++j) {
               const Temp& tm = temps[i * R2.size() + j];
+              if (!tm.nz) continue;  // nothing of possibly non-zero rank was added
               Mark mk2(ar);
               double* A = ar.alloc((size_t)size(t) * rcap);
               double* B = ar.alloc((size_t)size(r) * rcap);
@@ -410,6 +426,7 @@ struct Driver {
     }
     if (k == ADM) {
       if (Z->blk2adm[b] < 0) return;
+      if (!Z->nzr[t] || !Z->nzc[s]) return;  // k_t l_s = 0 structurally (oracle: S.size == 0)
       Mark mk(ar);
       const int mt = size(t), ms = size(s);
       int* kdev = ar.ialloc();
@@ -450,6 +467,7 @@ struct Driver {
     }
     if (k == ADM) {
       if (Z->blk2adm[b] < 0) return;
+      if (!Z->nzr[t] || !Z->nzc[s]) return;  // k_t l_s = 0 structurally
       Mark mk(ar);
       const int mt = size(t), ms = size(s);
       int* kdev = ar.ialloc();

@@ -469,6 +469,8 @@ extern "C" h2_status h2_from_sparse(h2_btree bt, int64_t n, const int64_t* rowpt
   TRY_ALLOC(dalloc(Z, &M.xt, n));
   TRY_ALLOC(dalloc(Z, &M.yt, n));
 #undef TRY_ALLOC
+  Z->nzr.assign(R->nclusters, 0);  // every rank is 0 after h2_from_sparse
+  Z->nzc.assign(C->nclusters, 0);
   if ((st = setup_side(Z, M.row, R, true)) != H2_OK) { free_mat(Z); return st; }
   if ((st = setup_side(Z, M.col, C, false)) != H2_OK) { free_mat(Z); return st; }
   e = cudaStreamSynchronize((cudaStream_t)stream);
@@ -525,6 +527,10 @@ extern "C" h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t
   a.kdev = nullptr;
   a.prof = nullptr;
   CUDA_TRY(launch_update(Z, a, (cudaStream_t)stream));
+  if (B->kind[b0] != INADM) {  // the update may give the bases of T_{t0} / T_{s0} a non-zero rank
+    for (int q = t0; q < t0 + B->rt->tsize[t0]; ++q) Z->nzr[q] = 1;
+    for (int q = s0; q < s0 + B->ct->tsize[s0]; ++q) Z->nzc[q] = 1;
+  }
   return H2_OK;
 }
 

@@ -124,6 +124,7 @@ struct h2_mat_ {
   int* iws = nullptr;
   size_t iws_cap = 0;
   int factored = 0;              // 0 no, 1 Cholesky, 2 LR
+  std::vector<char> nzr, nzc;    // host: cluster rank possibly non-zero (row / column basis)
   long long stats[4] = {0, 0, 0, 0};  // local updates, dense adds, temporaries issued by the driver
 };
 
