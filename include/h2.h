@@ -136,8 +136,20 @@ h2_status h2_lr_factor(h2_mat A, h2_factor_kind kind, const h2_trunc* trunc, h2_
  * column-major with leading dimension ldx >= n, ORIGINAL order; 1 <= nrhs <= 64. */
 h2_status h2_solve(h2_mat F, double* x, int32_t nrhs, int64_t ldx, h2_stream stream);
 
+/* Preconditioned CG (reading R12): solves A x = b with the factored F as the
+ * preconditioner ((L L^T)^{-1} or (L R)^{-1} via h2_solve), x0 = 0, stops when ||r||/||b|| < tol
+ * or after maxit iterations.  b, x: device vectors of length n in ORIGINAL order.  *iters receives
+ * the number of A-applications, *relres (may be NULL) the final relative residual.  Synchronizes
+ * the stream once per iteration (residual norm). */
+h2_status h2_pcg(h2_mat A, h2_mat F, const double* b, double* x, double tol, int32_t maxit, int32_t* iters,
+                 double* relres, h2_stream stream);
+
+/* Number of kernels this library has launched since it was loaded (bench / test hook). */
+h2_status h2_launch_count(int64_t* out);
+
 /* Counters of the work the product/factorization driver issued on this matrix:
- * out[0] local low-rank updates, out[1] dense nearfield adds, out[2] temporaries, out[3] 0. */
+ * out[0] local low-rank update calls, out[1] dense nearfield adds, out[2] temporaries, out[3] local
+ * updates that had a non-zero rank on the device (the oracle's update count; synchronizes). */
 h2_status h2_stats(h2_mat Z, int64_t out[4]);
 
 /* ---- inspection (synchronous: these synchronize the given stream) -------------------------- */

@@ -26,6 +26,8 @@ from .h2 import (  # noqa: F401
     h2_profile_enable,
     h2_profile_read,
     h2_stats,
+    h2_pcg,
+    h2_launch_count,
     library_path,
     EXPORTED_SYMBOLS,
 )

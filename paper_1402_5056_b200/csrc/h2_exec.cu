@@ -254,6 +254,7 @@ cudaEvent_t g_hev[2] = {nullptr, nullptr};
 int g_hbuf = 0;
 int g_nsm = 148;
 int g_big = getenv("H2_EXEC_BIG") ? atoi(getenv("H2_EXEC_BIG")) : BIG;  // debug override
+int g_cl = getenv("H2_EXEC_CL") ? atoi(getenv("H2_EXEC_CL")) : CL;   // executor cluster size
 
 cudaError_t init_exec() {
   if (g_attr) return cudaSuccess;
@@ -339,17 +340,18 @@ cudaError_t exec_flush() {
     P.begin = (int)lo;
     P.end = (int)hi;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CL);
+    cfg.gridDim = dim3(g_cl);
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = SM_EXEC;
     cfg.stream = c->st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.x = g_cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    count_launch(1);
     return cudaLaunchKernelEx(&cfg, k_exec_cluster, P);
   };
   for (size_t i = 0; i < n; ++i) {
@@ -358,6 +360,7 @@ cudaError_t exec_flush() {
       if ((e = run_cluster(b, i))) return e;
       const int kid = r.code < 9 ? r.code : K_AR_HMUL;
       prof_begin(kid, c->st);
+      count_launch(1);
       k_exec_big<<<std::min(r.nitems, g_nsm), NT, SM_EXEC, c->st>>>(P, (int)i);
       prof_end(kid, c->st);
       if ((e = cudaGetLastError())) return e;

@@ -552,7 +552,7 @@ extern "C" h2_status h2_check_device_flags(h2_mat Z, int32_t* flags) {
   CUDA_TRY(cudaDeviceSynchronize());
   int32_t f[3];
   CUDA_TRY(cudaMemcpy(f, Z->d.flags, sizeof(f), cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemset(Z->d.flags, 0, 3 * sizeof(int32_t)));
+  CUDA_TRY(cudaMemset(Z->d.flags, 0, 3 * sizeof(int32_t)));  // flags[3] (update counter) is kept
   flags[0] = f[0] | (f[1] ? 2 : 0);
   if (f[1]) {
     char msg[160];
@@ -565,7 +565,11 @@ extern "C" h2_status h2_check_device_flags(h2_mat Z, int32_t* flags) {
 
 extern "C" h2_status h2_stats(h2_mat Z, int64_t out[4]) {
   if (!Z || !out) H2_FAIL(H2_ERR_ARG, "h2_stats: NULL argument");
-  for (int i = 0; i < 4; ++i) out[i] = Z->stats[i];
+  for (int i = 0; i < 3; ++i) out[i] = Z->stats[i];
+  int32_t nz = 0;
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(&nz, Z->d.flags + 3, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  out[3] = nz;
   return H2_OK;
 }
 

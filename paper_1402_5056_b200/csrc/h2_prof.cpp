@@ -29,6 +29,9 @@ State g;
 
 double* prof_dev() { return g.on ? g.d : nullptr; }
 
+static long long g_launches = 0;
+void count_launch(int n) { g_launches += n; }
+
 static cudaEvent_t next_event(int kid) {
   if (g.used[kid] == g.ev[kid].size()) {
     cudaEvent_t e;
@@ -114,5 +117,14 @@ extern "C" h2_status h2_profile_debug(double out[16]) {
     set_error(std::string("h2_profile_debug: ") + cudaGetErrorString(e));
     return H2_ERR_CUDA;
   }
+  return H2_OK;
+}
+
+extern "C" h2_status h2_launch_count(int64_t* out) {
+  if (!out) {
+    set_error("h2_launch_count: NULL argument");
+    return H2_ERR_ARG;
+  }
+  *out = (int64_t)g_launches;
   return H2_OK;
 }

@@ -39,6 +39,7 @@ extern const char* const kKernelNames[K_COUNT];
 double* prof_dev();
 void prof_begin(int kid, cudaStream_t st);
 void prof_end(int kid, cudaStream_t st);
+void count_launch(int n);  // library kernel-launch counter (h2_launch_count)
 
 // Householder QR of an m x n matrix: 2 m n^2 - 2/3 n^3 (m >= n), SURVEY §8(d)
 __host__ __device__ inline double hh_flops(int m, int n) {
@@ -57,6 +58,7 @@ __host__ __device__ inline double svd_flops(int m, int n) {
 
 #define H2_LAUNCH(KID, ST, ...)        \
   do {                                 \
+    ::h2::count_launch(1);             \
     ::h2::prof_begin((KID), (ST));     \
     __VA_ARGS__;                       \
     ::h2::prof_end((KID), (ST));       \

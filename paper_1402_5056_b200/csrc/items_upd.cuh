@@ -43,6 +43,7 @@ __device__ void it_upd_ext_leaf(const MatDev& M, UpdArgs a_, int rl0, int nrl, i
     if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_W_PATH, fl);
     return;
   }
+  if (b == 0 && threadIdx.x == 0 && nrl + ncl > 0) atomicAdd(M.flags + 3, 1);  // non-zero-rank update count
   if (b < nrl + ncl) {
     const bool rs = b < nrl;
     const DevSide& D = rs ? M.row : M.col;

@@ -18,7 +18,7 @@ EXPORTED_SYMBOLS = [
     "h2_block_tree", "h2_btree_export", "h2_btree_destroy",
     "h2_from_sparse", "h2_lowrank_update", "h2_matvec", "h2_addmul", "h2_lr_factor", "h2_solve",
     "h2_ranks", "h2_storage_report", "h2_export", "h2_check_device_flags",
-    "h2_profile_enable", "h2_profile_read", "h2_profile_debug", "h2_stats",
+    "h2_profile_enable", "h2_profile_read", "h2_profile_debug", "h2_stats", "h2_pcg", "h2_launch_count",
     "h2_mat_destroy", "h2_last_error",
 ]
 
@@ -54,6 +54,8 @@ _sig = {
     "h2_profile_enable": [_i32],
     "h2_stats": [_p, _p],
     "h2_profile_debug": [_p],
+    "h2_pcg": [_p, _p, _p, _p, _f64, _i32, _p, _p, _p],
+    "h2_launch_count": [_p],
     "h2_profile_read": [_p, _p, _p, _p, _p, _p],
     "h2_mat_destroy": [_p],
     "h2_last_error": [],
@@ -247,7 +249,7 @@ def h2_solve(F: Mat, x, nrhs: int = 1, ldx: int | None = None, stream=None):
 def h2_stats(Z: Mat):
     out = np.zeros(4, dtype=np.int64)
     _check(_lib.h2_stats(Z.h, _ptr(out)))
-    return dict(updates=int(out[0]), dense_adds=int(out[1]), temporaries=int(out[2]))
+    return dict(updates=int(out[0]), dense_adds=int(out[1]), temporaries=int(out[2]), updates_nonzero=int(out[3]))
 
 
 def h2_ranks(Z: Mat):
@@ -306,3 +308,20 @@ def h2_profile_debug():
     out = np.zeros(16)
     _check(_lib.h2_profile_debug(_ptr(out)))
     return out
+
+
+def h2_pcg(A: Mat, F: Mat, b, x=None, tol: float = 1e-8, maxit: int = 500, stream=None):
+    """Preconditioned CG on the device: returns (x, iterations, relative residual)."""
+    if x is None:
+        import torch
+        x = torch.empty_like(b)
+    it = _i32()
+    rr = _f64()
+    _check(_lib.h2_pcg(A.h, F.h, _ptr(b), _ptr(x), float(tol), int(maxit), C.byref(it), C.byref(rr), _stream(stream)))
+    return x, it.value, rr.value
+
+
+def h2_launch_count() -> int:
+    v = _i64()
+    _check(_lib.h2_launch_count(C.byref(v)))
+    return v.value
