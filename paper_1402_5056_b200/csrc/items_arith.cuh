@@ -381,10 +381,22 @@ __device__ void it_temp_core(const double* Ra, const double* Rb, int ldr, Dim Kd
     const int i = e % K, j = e / K;
     double acc = 0.0;
     for (int q = 0; q < K; ++q) acc += Ra[i + q * ldr] * Rb[j + q * ldr];
-    Mm[i + j * LT] = acc;
+    U[j + i * LT] = acc;   // M^T
     M0[i + j * LT] = acc;
   }
   if (threadIdx.x == 0) clamped = 0;
+  __syncthreads();
+  // SVD of W = R_A^T with M^T = Q_A R_A (same singular values / left vectors, triangular start
+  // for the Jacobi sweeps); small K: Jacobi on M directly
+  if (K > 8) {
+    la::cta_qr_R(U, LT, K, K, sig, (double*)order);
+    for (int e = threadIdx.x; e < K * K; e += NT) {
+      const int i = e % K, j = e / K;
+      Mm[i + j * LT] = U[j + i * LT];
+    }
+  } else {
+    for (int e = threadIdx.x; e < K * K; e += NT) Mm[(e % K) + (e / K) * LT] = M0[(e % K) + (e / K) * LT];
+  }
   __syncthreads();
   la::cta_jacobi(Mm, LT, K, K, sig, order, scr);
   const int r = K > 0 ? la::trunc_rank(sig, order, K, rel, abs_tol, max_rank, cap, &clamped) : 0;

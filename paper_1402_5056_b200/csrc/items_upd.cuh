@@ -265,31 +265,52 @@ __device__ void it_upd_weights_level(const MatDev& M, UpdArgs a_, int bA, int nA
 // Given V (m x K, ldv) in shared memory and B~_t, compute M = V B~^T, its SVD, the rank, Q and R_t.
 __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, int t, double* V, int ldv, int m,
                          int K, double* sm_rest, int kid, double extra_flops) {
-  double* Bt = sm_rest;             // KC x KC
-  double* Mm = Bt + RM * KC;        // RM x KC (ld RM); the Bt region is RM x KC so that Q can reuse it
-  double* Q = Bt;                   // RM x KC (ld RM), reuses Bt once M = V B~^T is formed
+  // U4: left singular vectors / values of M = V B~^T (m x K).  For K > 8 the SVD is taken of
+  // W = R_A^T (m x p, p = min(m, K)) where M^T = Q_A R_A (Householder): M = W Q_A^T with Q_A
+  // orthonormal, so W has the singular values and left singular vectors of M, fewer columns and
+  // a triangular (preconditioned) start for the one-sided Jacobi.
+  double* Bt = sm_rest;             // KC x KC (ld RM); later W = R_A^T (m x p, ld RM)
+  double* Mm = Bt + RM * KC;        // M^T (K x m, ld RM); later Q (m x r, ld RM)
   double* sig = Mm + RM * KC;       // KC
   int* order = (int*)(sig + KC);    // KC ints
   int* scr = order + KC;            // 4 ints
   const double* Bg = D.bw + (size_t)t * M.kcap * M.kcap;
   const long long c0 = clock64();
-  la::cta_copy(Bt, KC, Bg, M.kcap, K, K);
+  la::cta_copy(Bt, RM, Bg, M.kcap, K, K);
   __syncthreads();
-  // Mm = V Bt^T  (m x K)
-  la::cta_gemm(Mm, RM, V, ldv, false, Bt, KC, true, m, K, K, false);
+  // M^T = B~ V^T  (K x m)
+  la::cta_gemm(Mm, RM, Bt, RM, false, V, ldv, true, K, m, K, false);
+  __syncthreads();
+  int p;
+  double* W = Bt;
+  if (K > 8) {
+    la::cta_qr_R(Mm, RM, K, m, sig, (double*)order);  // R_A in the first min(K, m) rows (sig/order: scratch)
+    p = K < m ? K : m;
+    for (int e = threadIdx.x; e < m * p; e += NT) {
+      const int i = e % m, j = e / m;
+      W[i + j * RM] = Mm[j + i * RM];  // W = R_A^T
+    }
+  } else {
+    p = K;
+    for (int e = threadIdx.x; e < m * K; e += NT) {
+      const int i = e % m, j = e / m;
+      W[i + j * RM] = Mm[j + i * RM];  // W = M
+    }
+  }
   __syncthreads();
   const long long c1 = clock64();
-  const int sweeps = la::cta_jacobi(Mm, RM, m, K, sig, order, scr);
+  const int sweeps = la::cta_jacobi(W, RM, m, p, sig, order, scr);
   const long long c2 = clock64();
   int& clamped = scr[2];
   if (threadIdx.x == 0) clamped = 0;
   __syncthreads();
-  const int r = la::trunc_rank(sig, order, K, a.rel_tol, a.abs_tol, a.max_rank, M.rcap, &clamped);
-  // Q(:, q) = Mm(:, order[q]) / sigma
+  const int r = la::trunc_rank(sig, order, p, a.rel_tol, a.abs_tol, a.max_rank, M.rcap, &clamped);
+  double* Q = Mm;
+  // Q(:, q) = W(:, order[q]) / sigma
   for (int e = threadIdx.x; e < m * r; e += NT) {
     const int i = e % m, q = e / m;
     const int j = order[q];
-    Q[i + q * RM] = Mm[i + j * RM] / sig[j];
+    Q[i + q * RM] = W[i + j * RM] / sig[j];
   }
   __syncthreads();
   double* qn = D.qn + (size_t)t * M.ldq * M.rcap;
