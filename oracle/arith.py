@@ -189,6 +189,11 @@ class Arith:
                 return np.zeros((self.rt.size(t), 0)), np.zeros((Wy.shape[0], 0))
             A = X.mul_dense(t, s, Y.row_basis(s) @ Sy)
             return A, Wy
+        # reading own-6: a contribution whose dense factor tile is exactly zero adds nothing and is
+        # skipped (the tiles of the factor that never receive fill stay exactly zero)
+        if (kx == INADM and X.dense(t, s) is not None and not X.dense(t, s).any()) or \
+           (ky == INADM and Y.dense(s, r) is not None and not Y.dense(s, r).any()):
+            return np.zeros((self.rt.size(t), 0)), np.zeros((self.rt.size(r), 0))
         if kx == INADM:
             Nx = X.dense(t, s)
             if Nx is None:

@@ -61,6 +61,8 @@ enum OpCode : int32_t {
   OP_GATHER,
   OP_SCATTER,
   OP_ZERO,
+  OP_DD,
+  OP_NZTILE,
   OP_COUNT
 };
 
@@ -108,6 +110,7 @@ struct PTemp {
   double* Mb;
   int* rout;
   int* flags;
+  const int* knew;  // rank of the contribution being added (0: the temporary is left exactly as is)
   int ldr, ldm, max_rank, cap;
   Dim K;
   double rel, abs_tol;
@@ -122,6 +125,14 @@ struct PMisc {  // small data-movement ops
   int ldd, lds, rows, cols, row_off, rows_new;
   int64_t ldx;
   Dim d1, d2;
+};
+
+struct PDD {  // dense x dense Case-2 factors
+  int mx, my, slotx, sloty, transx, transy, mt, ms, mr, lda, ldb;
+  double* A;
+  double* B;
+  int* kout;
+  double rel;
 };
 
 constexpr int OP_PAYLOAD = 176;

@@ -30,7 +30,9 @@ void tile_trsm(const MatDev& M, int slot, int m, int mode, double* B, int ldb, i
 void tsqr_r(const double* A, int lda, int rows, Dim K, double* R, int ldr, cudaStream_t st);
 // temporary truncation core: from Ra, Rb (K x K) -> Ma = Rb^T V_r, Mb = Ra^T U_r S_r^-1 (K x r), r -> *rout
 void temp_core(const double* Ra, const double* Rb, int ldr, Dim K, double* Ma, double* Mb, int ldm, int* rout,
-               double rel, double abs_tol, int max_rank, int cap, int* flags, cudaStream_t st);
+               double rel, double abs_tol, int max_rank, int cap, int* flags, const int* knew, cudaStream_t st);
+// *kdev = 0 if the nearfield tile `slot` is exactly zero (reading own-6)
+void zero_rank_if_zero_tile(const MatDev& M, int slot, int count, int* kdev, cudaStream_t st);
 // copy a (rows x cols) block with device column count into dst (zero-extended rows are the caller's)
 void copy_cols(double* dst, int ldd, const double* src, int lds, int rows, Dim cols, int colcap, cudaStream_t st);
 void set_int(int* p, Dim v, cudaStream_t st);
@@ -47,5 +49,8 @@ void gather_cols(double* Bt, const double* x, const int64_t* perm, int n, int nr
 void scatter_cols(double* x, const double* Bt, const int64_t* perm, int n, int nrhs, int64_t ldx, cudaStream_t st);
 // dst[0..count) = 0 (stream-ordered with the recorded ops)
 void zero_fill(double* dst, size_t count, cudaStream_t st);
+// dense x dense Case-2 factors: A (mt x r), B (mr x r), r -> *kout (see items_arith.cuh it_dd_compress)
+void dd_compress(const MatDev& MX, int slotx, bool transx, const MatDev& MY, int sloty, bool transy, int mt, int ms,
+                 int mr, double* A, int lda, double* B, int ldb, int* kout, double rel, cudaStream_t st);
 
 }  // namespace h2

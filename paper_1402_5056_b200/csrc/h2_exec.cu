@@ -48,7 +48,7 @@ __constant__ int c_op_kid[OP_COUNT] = {
     K_EXT_LEAF, K_EXT_LEVEL, K_W_PATH, K_W_LEVEL, K_SVD_LEAF, K_SVD_LEVEL, K_COUPLE, K_INSTALL, K_RCACHE,
     K_AR_EXPAND, K_AR_GEMM, K_AR_GEMM, K_AR_GEMM, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL,
     K_AR_TILE, K_AR_TILE, K_AR_TILE, K_AR_TSQR, K_AR_TEMP, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC,
-    K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC};
+    K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_TEMP, K_AR_MISC};
 
 __device__ __forceinline__ const DevSide& side_of(const MatDev& M, int s) { return s ? M.col : M.row; }
 
@@ -147,7 +147,7 @@ __device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, do
     case OP_TEMP: {
       const PTemp& q = *reinterpret_cast<const PTemp*>(op.p);
       ar::it_temp_core(q.Ra, q.Rb, q.ldr, q.K, q.Ma, q.Mb, q.ldm, q.rout, q.rel, q.abs_tol, q.max_rank, q.cap, q.flags,
-                       it, n, sm);
+                       q.knew, it, n, sm);
     } break;
     case OP_COPY_COLS: {
       const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
@@ -186,6 +186,19 @@ __device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, do
     case OP_GATHER: {
       const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
       ar::it_gather_cols(q.dst, q.src, q.perm, q.rows, q.cols, q.ldx, it, n, sm);
+    } break;
+    case OP_DD: {
+      const PDD& q = *reinterpret_cast<const PDD*>(op.p);
+      ar::it_dd_compress(P.mats[q.mx], P.mats[q.my], q.slotx, q.transx, q.sloty, q.transy, q.mt, q.ms, q.mr, q.A,
+                         q.lda, q.B, q.ldb, q.kout, q.rel, it, n, sm);
+    } break;
+    case OP_NZTILE: {  // *ip = 0 if the nearfield tile is exactly zero (reading own-6)
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      const double* T = q.src;
+      int any = 0;
+      for (int e = threadIdx.x; e < q.rows; e += NT) any |= (T[e] != 0.0);
+      any = __syncthreads_or(any);
+      if (!any && threadIdx.x == 0) *q.ip = 0;
     } break;
     case OP_ZERO: {
       const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
@@ -591,8 +604,9 @@ void tsqr_r(const double* A, int lda, int rows, Dim K, double* R, int ldr, cudaS
   ctx_or_throw()->emit(OP_TSQR, 1, nullptr, PTsqr{A, R, lda, rows, ldr, K});
 }
 void temp_core(const double* Ra, const double* Rb, int ldr, Dim K, double* Ma, double* Mb, int ldm, int* rout,
-               double rel, double abs_tol, int max_rank, int cap, int* flags, cudaStream_t) {
-  ctx_or_throw()->emit(OP_TEMP, 1, nullptr, PTemp{Ra, Rb, Ma, Mb, rout, flags, ldr, ldm, max_rank, cap, K, rel, abs_tol});
+               double rel, double abs_tol, int max_rank, int cap, int* flags, const int* knew, cudaStream_t) {
+  ctx_or_throw()->emit(OP_TEMP, 1, nullptr,
+                       PTemp{Ra, Rb, Ma, Mb, rout, flags, knew, ldr, ldm, max_rank, cap, K, rel, abs_tol});
 }
 
 static PMisc misc() {
@@ -710,5 +724,41 @@ void zero_fill(double* dst, size_t count, cudaStream_t) {
   q.dst = dst;
   q.ldx = (int64_t)count;
   ctx_or_throw()->emit(OP_ZERO, std::max(1, std::min(cdiv((long long)count, NT), 4 * 148)), nullptr, q);
+}
+}  // namespace h2
+
+namespace h2 {
+void dd_compress(const MatDev& MX, int slotx, bool transx, const MatDev& MY, int sloty, bool transy, int mt, int ms,
+                 int mr, double* A, int lda, double* B, int ldb, int* kout, double rel, cudaStream_t) {
+  ExecCtx* c = ctx_or_throw();
+  PDD q;
+  q.mx = c->mat_index(MX);
+  q.my = c->mat_index(MY);
+  q.slotx = slotx;
+  q.sloty = sloty;
+  q.transx = transx ? 1 : 0;
+  q.transy = transy ? 1 : 0;
+  q.mt = mt;
+  q.ms = ms;
+  q.mr = mr;
+  q.A = A;
+  q.lda = lda;
+  q.B = B;
+  q.ldb = ldb;
+  q.kout = kout;
+  q.rel = rel;
+  c->emit(OP_DD, 1, nullptr, q);
+}
+}  // namespace h2
+
+namespace h2 {
+void zero_rank_if_zero_tile(const MatDev& M, int slot, int count, int* kdev, cudaStream_t) {
+  (void)count;
+  PMisc q;
+  std::memset(&q, 0, sizeof(q));
+  q.src = M.N + (size_t)slot * M.lmax * M.lmax;
+  q.rows = M.lmax * M.lmax;  // padding of the tile slots is zero
+  q.ip = kdev;
+  ctx_or_throw()->emit(OP_NZTILE, 1, nullptr, q);
 }
 }  // namespace h2

@@ -166,7 +166,7 @@ struct Driver {
     tsqr_r(B2, Tm.mb, Tm.mb, dimp(K), Rb, KC, st);
     double* Ma = ar.alloc(KC * KC);
     double* Mb = ar.alloc(KC * KC);
-    temp_core(Ra, Rb, KC, dimp(K), Ma, Mb, KC, Tm.k, rel, abs_tol, max_rank, rcap, Z->d.flags, st);
+    temp_core(Ra, Rb, KC, dimp(K), Ma, Mb, KC, Tm.k, rel, abs_tol, max_rank, rcap, Z->d.flags, kdev, st);
     gemm(Tm.A, Tm.ma, A2, Tm.ma, false, Ma, KC, false, dimc(Tm.ma), dimp(Tm.k), dimp(K), Tm.ma, rcap, K2, 1.0, 0.0, st);
     gemm(Tm.B, Tm.mb, B2, Tm.mb, false, Mb, KC, false, dimc(Tm.mb), dimp(Tm.k), dimp(K), Tm.mb, rcap, K2, 1.0, 0.0, st);
   }
@@ -258,6 +258,8 @@ struct Driver {
       const HOp Yt = Y.t();
       hmul_dense(Y.Z->d, Yt.trans, r, s, 0, Dm, ms, dimp(Xr.rank + t), rcap, *B, mr, 1.0, 0.0, st);
       set_int(*kdev, dimp(Xr.rank + t), st);
+      if (ky == INADM && Y.Z->blk2inad[by] >= 0)
+        zero_rank_if_zero_tile(Y.Z->d, Y.Z->blk2inad[by], ms * mr, *kdev, st);  // reading own-6
       *lda = mt;
       *ldb = mr;
       return rcap;
@@ -278,6 +280,8 @@ struct Driver {
       *B = ar.alloc((size_t)mr * rcap);
       expand_basis(Y.Z->d, Yc, r, *B, mr, st);
       set_int(*kdev, dimp(Yc.rank + r), st);
+      if (kx == INADM && X.Z->blk2inad[bx] >= 0)
+        zero_rank_if_zero_tile(X.Z->d, X.Z->blk2inad[bx], mt * ms, *kdev, st);  // reading own-6
       *lda = mt;
       *ldb = mr;
       return rcap;
@@ -291,6 +295,8 @@ struct Driver {
       const HOp Yt = Y.t();
       hmul_dense(Y.Z->d, Yt.trans, r, s, 0, ident, lmax, dimc(ms), ms, *B, mr, 1.0, 0.0, st);
       set_int(*kdev, dimc(ms), st);
+      zero_rank_if_zero_tile(X.Z->d, X.Z->blk2inad[bx], mt * ms, *kdev, st);  // reading own-6
+      if (ky == INADM && Y.Z->blk2inad[by] >= 0) zero_rank_if_zero_tile(Y.Z->d, Y.Z->blk2inad[by], ms * mr, *kdev, st);
       *lda = mt;
       *ldb = mr;
       return ms;
@@ -304,6 +310,7 @@ struct Driver {
     hmul_dense(X.Z->d, X.trans, t, s, 0, Ny, ms, dimc(mr), mr, *A, mt, 1.0, 0.0, st);
     *B = ident;
     set_int(*kdev, dimc(mr), st);
+    zero_rank_if_zero_tile(Y.Z->d, Y.Z->blk2inad[by], ms * mr, *kdev, st);  // reading own-6
     *lda = mt;
     *ldb = lmax;
     return mr;

@@ -365,7 +365,18 @@ __device__ void it_tsqr_r(const double* A, int lda, int rows, Dim Kd, double* R,
 // ---- temporary truncation core ----------------------------------------------------------------
 __device__ void it_temp_core(const double* Ra, const double* Rb, int ldr, Dim Kd, double* Ma,
                                                   double* Mb, int ldm, int* rout, double rel, double abs_tol,
-                                                  int max_rank, int cap, int* flags, int item_, int nitems_, double* smx_) {
+                                                  int max_rank, int cap, int* flags, const int* knew, int item_,
+                                                  int nitems_, double* smx_) {
+  if (knew && *knew == 0) {  // nothing added: the temporary stays exactly as it is (Ma = Mb = I)
+    const int K = Kd.v();
+    for (int e = threadIdx.x; e < K * K; e += NT) {
+      const int i = e % K, j = e / K;
+      Ma[i + j * ldm] = i == j ? 1.0 : 0.0;
+      Mb[i + j * ldm] = i == j ? 1.0 : 0.0;
+    }
+    if (threadIdx.x == 0) *rout = K;
+    return;
+  }
   double* smt = smx_;
   constexpr int LT = KC + 1;
   double* Mm = smt;
@@ -504,5 +515,64 @@ __device__ void it_add_int(int* p, Dim a, Dim b, int item_, int nitems_, double*
   if (threadIdx.x == 0) *p = a.v() + b.v();
 }
 
+}  // namespace ar
+}  // namespace h2
+
+namespace h2 {
+namespace ar {
+// Case 2 with both factors dense leaf blocks (reading own-6): P = op(X)|_{t x s} op(Y)|_{s x r}
+// (mt x mr) and its minimal-rank factorisation A = U_r S_r, B = P^T U_r S_r^-1 = V_r with
+// r = #{sigma_i > rel sigma_1} (rel = 1e-12; an exactly zero product gives r = 0: no update).
+// SVD as in U4: one-sided Jacobi on W = R_A^T, P^T = Q_A R_A.
+__device__ void it_dd_compress(const MatDev& MX, const MatDev& MY, int slotx, int transx, int sloty, int transy,
+                               int mt, int ms, int mr, double* A, int lda, double* B, int ldb, int* kout, double rel,
+                               int item_, int nitems_, double* smx_) {
+  constexpr int L = KC + 1;
+  double* P = smx_;        // mt x mr
+  double* W = P + L * KC;  // R_A^T (mt x p)
+  double* T = W + L * KC;  // P^T (mr x mt), QR in place
+  double* sig = T + L * KC;
+  int* order = (int*)(sig + KC);
+  int* scr = order + KC;
+  const double* NX = MX.N + (size_t)slotx * MX.lmax * MX.lmax;
+  const double* NY = MY.N + (size_t)sloty * MY.lmax * MY.lmax;
+  const int lx = MX.lmax, ly = MY.lmax;
+  for (int e = threadIdx.x; e < mt * mr; e += NT) {
+    const int i = e % mt, j = e / mt;
+    double acc = 0.0;
+    for (int q = 0; q < ms; ++q) {
+      const double x = transx ? NX[q + i * lx] : NX[i + q * lx];
+      const double y = transy ? NY[j + q * ly] : NY[q + j * ly];
+      acc += x * y;
+    }
+    P[i + j * L] = acc;
+    T[j + i * L] = acc;
+  }
+  __syncthreads();
+  la::cta_qr_R(T, L, mr, mt, sig, (double*)order);
+  const int p = mr < mt ? mr : mt;
+  for (int e = threadIdx.x; e < mt * p; e += NT) {
+    const int i = e % mt, j = e / mt;
+    W[i + j * L] = T[j + i * L];
+  }
+  __syncthreads();
+  la::cta_jacobi(W, L, mt, p, sig, order, scr);
+  int& clamped = scr[3];
+  if (threadIdx.x == 0) clamped = 0;
+  __syncthreads();
+  const int r = la::trunc_rank(sig, order, p, rel, 0.0, 0, KC, &clamped);
+  for (int e = threadIdx.x; e < mt * r; e += NT) {
+    const int i = e % mt, q = e / mt;
+    A[i + (size_t)q * lda] = W[i + order[q] * L];  // u_q sigma_q
+  }
+  for (int e = threadIdx.x; e < mr * r; e += NT) {
+    const int j = e % mr, q = e / mr;
+    const int o = order[q];
+    double acc = 0.0;
+    for (int i = 0; i < mt; ++i) acc += P[i + j * L] * W[i + o * L];
+    B[j + (size_t)q * ldb] = acc / (sig[o] * sig[o]);  // P^T u_q / sigma_q
+  }
+  if (threadIdx.x == 0) *kout = r;
+}
 }  // namespace ar
 }  // namespace h2
