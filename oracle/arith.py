@@ -163,7 +163,7 @@ class Arith:
         self.up(t, r, A, B)
         self.stats["updates"] += 1
 
-    def _factors(self, X: Op, Y: Op, t, s, r):
+    def _factors(self, X: Op, Y: Op, t, s, r, dense_target=False):
         """Low-rank factors A, B with X|_{t x s} Y|_{s x r} = A B^T (Case 2; R23)."""
         kx, ky = X.kind(t, s), Y.kind(s, r)
         if kx == ADM and ky == ADM:
@@ -194,6 +194,15 @@ class Arith:
         if (kx == INADM and X.dense(t, s) is not None and not X.dense(t, s).any()) or \
            (ky == INADM and Y.dense(s, r) is not None and not Y.dense(s, r).any()):
             return np.zeros((self.rt.size(t), 0)), np.zeros((self.rt.size(r), 0))
+        if kx == INADM and ky == INADM and not dense_target:
+            # reading own-7: both factors dense leaf blocks, low-rank target (P:505-509 leaves the factorization
+            # open): interpolative decomposition of P = X_ts Y_sr by column-pivoted QR,
+            # P Pi = Q R, r = #{|R_kk| > 1e-12 |R_00|}, A = P[:, J] (the r pivot columns),
+            # B^T = [I, R_11^{-1} R_12] Pi^T, so that A B^T = P up to |R_rr| <= 1e-12 |R_00|.
+            Nx, Ny = X.dense(t, s), Y.dense(s, r)
+            if Nx is None or Ny is None:
+                return np.zeros((self.rt.size(t), 0)), np.zeros((self.rt.size(r), 0))
+            return self._interp_decomp(Nx @ Ny)
         if kx == INADM:
             Nx = X.dense(t, s)
             if Nx is None:
@@ -206,6 +215,24 @@ class Arith:
             return np.zeros((self.rt.size(t), 0)), np.zeros((self.rt.size(r), 0))
         A = X.mul_dense(t, s, Ny)
         return A, np.eye(self.rt.size(r))
+
+    @staticmethod
+    def _interp_decomp(P, rel=1e-12):
+        """Interpolative decomposition P ~ A B^T with A = r columns of P (LAPACK dgeqp3 pivots)."""
+        from scipy.linalg import qr
+        mt, mr = P.shape
+        _, R, piv = qr(P, mode="economic", pivoting=True)
+        d = np.abs(np.diag(R))
+        if d.size == 0 or d[0] == 0.0:
+            return np.zeros((mt, 0)), np.zeros((mr, 0))
+        small = np.nonzero(d <= rel * d[0])[0]
+        r = int(small[0]) if small.size else d.size  # the pivoted QR stops at the first small |R_kk|
+        A = P[:, piv[:r]]
+        T = solve_triangular(R[:r, :r], R[:r, r:])
+        B = np.zeros((mr, r))
+        B[piv[:r], :] = np.eye(r)
+        B[piv[r:], :] = T.T
+        return A, B
 
     def _target_stored(self, t, r):
         b = self.Z.bt.index.get((t, r))
@@ -254,7 +281,8 @@ class Arith:
                     for r2 in rt.sons_plus(r):
                         self.addmul(alpha, X, Y, t2, s2, r2, target)
             return
-        A, B = self._factors(X, Y, t, s, r)
+        dense_target = target is None and self.Z.bt.kind[self.Z.bt.index[(t, r)]] == INADM
+        A, B = self._factors(X, Y, t, s, r, dense_target)
         if A.shape[1]:
             self._add(target, t, r, alpha * A, B)
 

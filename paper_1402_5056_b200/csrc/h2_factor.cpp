@@ -194,7 +194,7 @@ struct Driver {
   // ---- Case 2 factors (reading R23) -----------------------------------------------
   // returns kcap (0: nothing to add); A: size(t) x k, B: size(r) x k; *kdev set on the device
   int factors(const HOp& X, const HOp& Y, int t, int s, int r, double** A, int* lda, double** B, int* ldb,
-              int** kdev) {
+              int** kdev, bool dense_target) {
     const int kx = X.kind(t, s), ky = Y.kind(s, r);
     const int bx = X.bid(t, s), by = Y.bid(s, r);
     const int mt = size(t), ms = size(s), mr = size(r);
@@ -286,6 +286,18 @@ struct Driver {
       *ldb = mr;
       return rcap;
     }
+    if (kx == INADM && ky == INADM && !dense_target) {
+      // reading own-7: interpolative decomposition of the dense product (a zero tile gives r = 0)
+      if (X.Z->blk2inad[bx] < 0 || Y.Z->blk2inad[by] < 0) return 0;
+      const int kc = std::min(mt, mr);
+      *A = ar.alloc((size_t)mt * kc);
+      *B = ar.alloc((size_t)mr * kc);
+      dd_compress(X.Z->d, X.Z->blk2inad[bx], X.trans, Y.Z->d, Y.Z->blk2inad[by], Y.trans, mt, ms, mr, *A, mt, *B,
+                  mr, *kdev, 1e-12, st);
+      *lda = mt;
+      *ldb = mr;
+      return kc;
+    }
     if (kx == INADM) {
       if (X.Z->blk2inad[bx] < 0) return 0;
       *A = ar.alloc((size_t)mt * ms);
@@ -374,7 +386,8 @@ struct Driver {
     double *A, *B;
     int lda, ldb;
     int* kdev;
-    const int kcap = factors(X, Y, t, s, r, &A, &lda, &B, &ldb, &kdev);
+    const bool dense_target = !tgt && Z->bt->kind[Z->bt->find(t, r)] == INADM;
+    const int kcap = factors(X, Y, t, s, r, &A, &lda, &B, &ldb, &kdev, dense_target);
     if (kcap) add(tgt, t, r, A, lda, B, ldb, kdev, kcap, alpha);
   }
 

@@ -520,25 +520,30 @@ __device__ void it_add_int(int* p, Dim a, Dim b, int item_, int nitems_, double*
 
 namespace h2 {
 namespace ar {
-// Case 2 with both factors dense leaf blocks (reading own-6): P = op(X)|_{t x s} op(Y)|_{s x r}
-// (mt x mr) and its minimal-rank factorisation A = U_r S_r, B = P^T U_r S_r^-1 = V_r with
-// r = #{sigma_i > rel sigma_1} (rel = 1e-12; an exactly zero product gives r = 0: no update).
-// SVD as in U4: one-sided Jacobi on W = R_A^T, P^T = Q_A R_A.
+// Case 2 with both factors dense leaf blocks and a low-rank target (reading own-7):
+// P = op(X)|_{t x s} op(Y)|_{s x r} (mt x mr), interpolative decomposition by column-pivoted
+// Householder QR  P Pi = Q R  (pivot = remaining column of largest norm, first index on ties),
+// stopped at the first step j with |R_jj| <= rel |R_00| -> r = j (P = 0 -> r = 0);
+// A = P[:, piv[0..r)] (the r pivot columns, exact copies), B^T = [I_r, R_11^{-1} R_12] Pi^T.
+// One CTA; groups of S lanes own one column each (as la::cta_qr_R); the remaining-row norms of
+// every column are recomputed exactly after each reflection by the owning group.
 __device__ void it_dd_compress(const MatDev& MX, const MatDev& MY, int slotx, int transx, int sloty, int transy,
                                int mt, int ms, int mr, double* A, int lda, double* B, int ldb, int* kout, double rel,
                                int item_, int nitems_, double* smx_) {
   constexpr int L = KC + 1;
-  double* P = smx_;        // mt x mr
-  double* W = P + L * KC;  // R_A^T (mt x p)
-  double* T = W + L * KC;  // P^T (mr x mt), QR in place
-  double* sig = T + L * KC;
-  int* order = (int*)(sig + KC);
-  int* scr = order + KC;
+  double* P = smx_;        // mt x mr, QR in place
+  double* P0 = P + L * KC; // copy of P (original column order)
+  double* cn = P0 + L * KC;  // squared norms of the remaining rows, per (current) column
+  double* diag = cn + KC;    // R_jj
+  double* red = diag + KC;   // [0] = |R_00|, [1] = |a_j|^2
+  int* piv = (int*)(red + 8);
+  int* ctl = piv + KC;       // [0] = pivot column (-1: stop)
   const double* NX = MX.N + (size_t)slotx * MX.lmax * MX.lmax;
   const double* NY = MY.N + (size_t)sloty * MY.lmax * MY.lmax;
   const int lx = MX.lmax, ly = MY.lmax;
-  for (int e = threadIdx.x; e < mt * mr; e += NT) {
-    const int i = e % mt, j = e / mt;
+  const int tid = threadIdx.x, m = mt, n = mr;
+  for (int e = tid; e < m * n; e += NT) {
+    const int i = e % m, j = e / m;
     double acc = 0.0;
     for (int q = 0; q < ms; ++q) {
       const double x = transx ? NX[q + i * lx] : NX[i + q * lx];
@@ -546,33 +551,109 @@ __device__ void it_dd_compress(const MatDev& MX, const MatDev& MY, int slotx, in
       acc += x * y;
     }
     P[i + j * L] = acc;
-    T[j + i * L] = acc;
+    P0[i + j * L] = acc;
+  }
+  for (int j = tid; j < n; j += NT) piv[j] = j;
+  int npow = 1;
+  while (npow < n) npow *= 2;
+  int S = NT / npow;
+  if (S > 32) S = 32;
+  if (S < 1) S = 1;
+  const int c = tid / S, sl = tid % S;
+  const unsigned gm = la::group_mask(S);
+  __syncthreads();
+  {
+    double part = 0.0;
+    if (c < n)
+      for (int i = sl; i < m; i += S) part += P[i + c * L] * P[i + c * L];
+    for (int o = S / 2; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (c < n && sl == 0) cn[c] = part;
   }
   __syncthreads();
-  la::cta_qr_R(T, L, mr, mt, sig, (double*)order);
-  const int p = mr < mt ? mr : mt;
-  for (int e = threadIdx.x; e < mt * p; e += NT) {
-    const int i = e % mt, j = e / mt;
-    W[i + j * L] = T[j + i * L];
+  const int jmax = m < n ? m : n;
+  int r = jmax;
+  for (int j = 0; j < jmax; ++j) {
+    if (tid == 0) {
+      int p = j;
+      double best = cn[j];
+      for (int q = j + 1; q < n; ++q)
+        if (cn[q] > best) {
+          best = cn[q];
+          p = q;
+        }
+      const double nrm = sqrt(best);
+      if (j == 0) red[0] = nrm;
+      if (nrm <= rel * red[0]) {
+        ctl[0] = -1;
+      } else {
+        ctl[0] = p;
+        const int tp = piv[j];
+        piv[j] = piv[p];
+        piv[p] = tp;
+        cn[p] = cn[j];
+        cn[j] = best;
+      }
+    }
+    __syncthreads();
+    const int p = ctl[0];
+    if (p < 0) {
+      r = j;
+      break;
+    }
+    if (p != j) {
+      for (int i = tid; i < m; i += NT) {
+        const double tmp = P[i + j * L];
+        P[i + j * L] = P[i + p * L];
+        P[i + p * L] = tmp;
+      }
+      __syncthreads();
+    }
+    double part = 0.0;
+    if (c >= j && c < n)
+      for (int i = j + sl; i < m; i += S) part += P[i + j * L] * P[i + c * L];
+    for (int o = S / 2; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (c == j && sl == 0) red[1] = part;
+    __syncthreads();
+    const double nrm2 = red[1];
+    const double ajj = P[j + j * L];
+    const double nrm = sqrt(nrm2);
+    const double alpha = ajj > 0.0 ? -nrm : nrm;
+    const double half_vtv = nrm2 - alpha * ajj;
+    if (c > j && c < n) {
+      const double ajc = P[j + c * L];
+      __syncwarp(gm);
+      const double f = (part - alpha * ajc) / half_vtv;
+      for (int i = j + sl; i < m; i += S) {
+        const double vi = (i == j) ? (ajj - alpha) : P[i + j * L];
+        P[i + c * L] -= f * vi;
+      }
+      __syncwarp(gm);
+      double q2 = 0.0;
+      for (int i = j + 1 + sl; i < m; i += S) q2 += P[i + c * L] * P[i + c * L];
+      for (int o = S / 2; o; o >>= 1) q2 += __shfl_xor_sync(gm, q2, o);
+      if (sl == 0) cn[c] = q2;
+    }
+    if (tid == 0) diag[j] = alpha;
+    __syncthreads();
+  }
+  // T = R_11^{-1} R_12 in place of R_12 (one thread per right-hand side column)
+  for (int cc = r + tid; cc < n; cc += NT) {
+    for (int i = r - 1; i >= 0; --i) {
+      double x = P[i + cc * L];
+      for (int k = i + 1; k < r; ++k) x -= P[i + k * L] * P[k + cc * L];
+      P[i + cc * L] = x / diag[i];
+    }
   }
   __syncthreads();
-  la::cta_jacobi(W, L, mt, p, sig, order, scr);
-  int& clamped = scr[3];
-  if (threadIdx.x == 0) clamped = 0;
-  __syncthreads();
-  const int r = la::trunc_rank(sig, order, p, rel, 0.0, 0, KC, &clamped);
-  for (int e = threadIdx.x; e < mt * r; e += NT) {
-    const int i = e % mt, q = e / mt;
-    A[i + (size_t)q * lda] = W[i + order[q] * L];  // u_q sigma_q
+  for (int e = tid; e < m * r; e += NT) {
+    const int i = e % m, q = e / m;
+    A[i + (size_t)q * lda] = P0[i + piv[q] * L];
   }
-  for (int e = threadIdx.x; e < mr * r; e += NT) {
-    const int j = e % mr, q = e / mr;
-    const int o = order[q];
-    double acc = 0.0;
-    for (int i = 0; i < mt; ++i) acc += P[i + j * L] * W[i + o * L];
-    B[j + (size_t)q * ldb] = acc / (sig[o] * sig[o]);  // P^T u_q / sigma_q
+  for (int e = tid; e < n * r; e += NT) {
+    const int cc = e % n, q = e / n;  // row piv[cc] of B
+    B[piv[cc] + (size_t)q * ldb] = cc < r ? (cc == q ? 1.0 : 0.0) : P[q + cc * L];
   }
-  if (threadIdx.x == 0) *kout = r;
+  if (tid == 0) *kout = r;
 }
 }  // namespace ar
 }  // namespace h2

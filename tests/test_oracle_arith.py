@@ -147,3 +147,19 @@ def test_pcg_and_power_special_cases():
     D = np.diag([1.0, 2.0])  # A = diag(1,2), M = I -> ||I - A|| = 1
     assert abs(power_error(lambda v: D @ v, lambda v: v, np.array([0.3, 1.0])) - 1.0) < 1e-3
     assert power_error(lambda v: A @ v, lambda v: np.linalg.solve(A, v), b) < 1e-8
+
+
+def test_interpolative_decomposition_reading_own7():
+    """own-7: A = r pivot columns of P, A B^T = P to the truncation level; exact rank recovered."""
+    rng = np.random.default_rng(12)
+    for rank in (0, 1, 5, 12):
+        P = rng.standard_normal((32, rank)) @ rng.standard_normal((rank, 30))
+        A, B = Arith._interp_decomp(P)
+        assert A.shape[1] == rank and B.shape == (30, rank)
+        if rank:
+            assert np.abs(A @ B.T - P).max() <= 1e-11 * np.abs(P).max()
+            cols = [j for j in range(30) if any(np.array_equal(P[:, j], A[:, q]) for q in range(rank))]
+            assert len(cols) >= rank  # A consists of columns of P
+    P = np.diag([3.0, 1e-13, 0.0, 2.0])
+    A, B = Arith._interp_decomp(P)
+    assert A.shape[1] == 2 and np.abs(A @ B.T - np.diag([3.0, 0, 0, 2.0])).max() == 0.0
