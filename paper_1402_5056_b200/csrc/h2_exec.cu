@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -321,7 +322,11 @@ cudaError_t exec_flush() {
   // stage in a pinned buffer (double-buffered), upload, run
   const int hb = g_hbuf;
   g_hbuf ^= 1;
-  if ((e = cudaEventSynchronize(g_hev[hb]))) return e;
+  {
+    const auto w0 = std::chrono::steady_clock::now();
+    if ((e = cudaEventSynchronize(g_hev[hb]))) return e;
+    g_host_wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+  }
   if (g_hcap[hb] < n) {
     if (g_hops[hb]) cudaFreeHost(g_hops[hb]);
     g_hcap[hb] = std::max(n, (size_t)16384);

@@ -30,6 +30,7 @@ State g;
 double* prof_dev() { return g.on ? g.d : nullptr; }
 
 static long long g_launches = 0;
+double g_host_wait_s = 0.0;
 void count_launch(int n) { g_launches += n; }
 
 static cudaEvent_t next_event(int kid) {
@@ -113,6 +114,7 @@ extern "C" h2_status h2_profile_debug(double out[16]) {
   if (!g.d) return H2_OK;
   cudaError_t e = cudaDeviceSynchronize();
   if (e == cudaSuccess) e = cudaMemcpy(out, g.d + 4 * K_COUNT, 16 * sizeof(double), cudaMemcpyDeviceToHost);
+  out[15] = g_host_wait_s;  // host seconds spent waiting for a free op buffer (executor back-pressure)
   if (e != cudaSuccess) {
     set_error(std::string("h2_profile_debug: ") + cudaGetErrorString(e));
     return H2_ERR_CUDA;

@@ -39,6 +39,7 @@ extern const char* const kKernelNames[K_COUNT];
 double* prof_dev();
 void prof_begin(int kid, cudaStream_t st);
 void prof_end(int kid, cudaStream_t st);
+extern double g_host_wait_s;  // accumulated host wait in exec_flush (h2_profile_debug out[15])
 void count_launch(int n);  // library kernel-launch counter (h2_launch_count)
 
 // Householder QR of an m x n matrix: 2 m n^2 - 2/3 n^3 (m >= n), SURVEY §8(d)

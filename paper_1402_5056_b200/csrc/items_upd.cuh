@@ -265,10 +265,12 @@ __device__ void it_upd_weights_level(const MatDev& M, UpdArgs a_, int bA, int nA
 // Given V (m x K, ldv) in shared memory and B~_t, compute M = V B~^T, its SVD, the rank, Q and R_t.
 __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, int t, double* V, int ldv, int m,
                          int K, double* sm_rest, int kid, double extra_flops) {
-  // U4: left singular vectors / values of M = V B~^T (m x K).  For K > 8 the SVD is taken of
-  // W = R_A^T (m x p, p = min(m, K)) where M^T = Q_A R_A (Householder): M = W Q_A^T with Q_A
-  // orthonormal, so W has the singular values and left singular vectors of M, fewer columns and
-  // a triangular (preconditioned) start for the one-sided Jacobi.
+  // U4: left singular vectors / values of M = V B~^T (m x K).  m, K <= 32: one-sided Jacobi on M
+  // in registers of one warp.  K <= 16: the same on the K x K factor R_M (M = Q_M R_M) with the
+  // rotations accumulated, U Sigma = M J (see below).  Otherwise: the
+  // SVD is taken of W = R_A^T (m x p, p = min(m, K)) where M^T = Q_A R_A (Householder):
+  // M = W Q_A^T with Q_A orthonormal, so W has the singular values and left singular vectors of
+  // M, fewer columns and a triangular (preconditioned) start for the one-sided Jacobi.
   double* Bt = sm_rest;             // KC x KC (ld RM); later W = R_A^T (m x p, ld RM)
   double* Mm = Bt + RM * KC;        // M^T (K x m, ld RM); later Q (m x r, ld RM)
   double* sig = Mm + RM * KC;       // KC
@@ -278,28 +280,51 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
   const long long c0 = clock64();
   la::cta_copy(Bt, RM, Bg, M.kcap, K, K);
   __syncthreads();
-  // M^T = B~ V^T  (K x m)
-  la::cta_gemm(Mm, RM, Bt, RM, false, V, ldv, true, K, m, K, false);
-  __syncthreads();
-  int p;
+  long long c1;
+  int p, sweeps;
   double* W = Bt;
-  if (K > 8) {
+  if (K <= 32 && (m <= 16 || (m <= 32 && K > 8))) {
+    // M = V B~^T (m x K) in Mm; one-sided Jacobi on M in registers of one warp (lane j owns
+    // column j), W = M J = [sigma_j u_j] into Bt (free after the product)
+    la::cta_gemm(Mm, RM, V, ldv, false, Bt, RM, true, m, K, K, false);
+    __syncthreads();
+    c1 = clock64();
+    if (m <= 16) sweeps = la::warp_jacobi<16, false>(Mm, RM, m, K, W, RM, sig, order, scr);
+    else sweeps = la::warp_jacobi<32, false>(Mm, RM, m, K, W, RM, sig, order, scr);
+    p = K;
+  } else if (K <= 16) {
+    // M = V B~^T (m x K) in Mm; R_M of M = Q_M R_M (Householder) in Bt[:, 0:32); one-sided Jacobi
+    // on R_M in registers with the rotations J accumulated (Bt[:, 32:64)): R_M J = U_R Sigma,
+    // so M J = Q_M U_R Sigma and column j of W = M J (Bt[:, 64:96)) is sigma_j u_j.
+    la::cta_gemm(Mm, RM, V, ldv, false, Bt, RM, true, m, K, K, false);
+    __syncthreads();
+    double* Rw = Bt;
+    double* J = Bt + 32 * RM;
+    W = Bt + 64 * RM;
+    la::cta_copy(Rw, RM, Mm, RM, m, K);
+    __syncthreads();
+    la::cta_qr_R(Rw, RM, m, K, sig, (double*)order);
+    const int pr = m < K ? m : K;
+    c1 = clock64();
+    if (K <= 8) sweeps = la::warp_jacobi<8, true>(Rw, RM, pr, K, J, RM, sig, order, scr);
+    else sweeps = la::warp_jacobi<16, true>(Rw, RM, pr, K, J, RM, sig, order, scr);
+    la::cta_gemm(W, RM, Mm, RM, false, J, RM, false, m, K, K, false);
+    p = K;
+    __syncthreads();
+  } else {
+    // M^T = B~ V^T  (K x m)
+    la::cta_gemm(Mm, RM, Bt, RM, false, V, ldv, true, K, m, K, false);
+    __syncthreads();
     la::cta_qr_R(Mm, RM, K, m, sig, (double*)order);  // R_A in the first min(K, m) rows (sig/order: scratch)
     p = K < m ? K : m;
     for (int e = threadIdx.x; e < m * p; e += NT) {
       const int i = e % m, j = e / m;
       W[i + j * RM] = Mm[j + i * RM];  // W = R_A^T
     }
-  } else {
-    p = K;
-    for (int e = threadIdx.x; e < m * K; e += NT) {
-      const int i = e % m, j = e / m;
-      W[i + j * RM] = Mm[j + i * RM];  // W = M
-    }
+    __syncthreads();
+    c1 = clock64();
+    sweeps = la::cta_jacobi(W, RM, m, p, sig, order, scr);
   }
-  __syncthreads();
-  const long long c1 = clock64();
-  const int sweeps = la::cta_jacobi(W, RM, m, p, sig, order, scr);
   const long long c2 = clock64();
   int& clamped = scr[2];
   if (threadIdx.x == 0) clamped = 0;
