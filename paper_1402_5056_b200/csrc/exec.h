@@ -162,6 +162,9 @@ struct ExecCtx {
   template <class P>
   void emit(int code, int nitems, const MatDev* M, const P& payload, bool barrier = true) {
     if (nitems <= 0) return;
+    // two consecutive single-item ops both run on CTA 0 of the cluster, in order: the block
+    // barrier after each item orders them, the cluster barrier between them is not needed
+    if (nitems == 1 && !ops.empty() && ops.back().nitems == 1) ops.back().barrier = 0;
     OpRec r;
     r.code = code;
     r.nitems = nitems;
