@@ -312,6 +312,8 @@ static h2_status setup_side(h2_mat_* Z, DevSide& D, const h2_tree_* T, bool row_
   CUDA_TRY(dalloc(Z, &D.rc, (size_t)T->nclusters * r2));
   CUDA_TRY(cudaMemset(D.rc, 0, sizeof(double) * (size_t)T->nclusters * r2));
   CUDA_TRY(dalloc(Z, &D.xh, (size_t)T->nclusters * M.rcap));
+  CUDA_TRY(dalloc(Z, &D.mvsync, (size_t)2 * T->nclusters + 4));
+  CUDA_TRY(cudaMemset(D.mvsync, 0, sizeof(int32_t) * ((size_t)2 * T->nclusters + 4)));
   return H2_OK;
 }
 

@@ -1,12 +1,22 @@
 // H^2 matrix-vector product y = alpha op(Z) x + beta y ([BO10 Thm 3.42]).
 //
 //   forward transform   xhat_s = W_s^T x|s (leaves),  xhat_s = sum_{s'} F_{s'}^T xhat_{s'}   bottom-up
-//   couplings           yhat_t = sum_{s in row(t)} S_(t,s) xhat_s                              one warp / cluster
+//   couplings           yhat_t = sum_{s in row(t)} S_(t,s) xhat_s
 //   backward transform  yhat_{t'} += E_{t'} yhat_t  top-down; leaves y|t = V_t yhat_t
-//   nearfield           y|t += sum_{b=(t,s) inadmissible} N_b x|s                            fused in the leaf pass
+//   nearfield           y|t += sum_{b=(t,s) inadmissible} N_b x|s
 //
-// Bytes are dominated by the nearfield tiles: the leaf pass is written for HBM
-// bandwidth (coalesced column reads of the column-major tiles, several loads in flight per lane).
+// ONE launch, no grid-wide barrier: every warp takes a ticket (atomic counter, so tickets are
+// handed out in order and a warp only ever waits on lower tickets, which are resident).
+//   tickets [0, #leaves)            forward transform of a source leaf, then climb: the second
+//                                   of two siblings to finish (arrival counter) computes the
+//                                   father, up to the root, whose completion publishes "xhat done"
+//   tickets [#leaves, +#clusters)   destination clusters in level (BFS) order: a leaf first streams
+//                                   its nearfield tiles (independent of the transforms), then
+//                                   waits for "xhat done" (couplings) and for its father's yhat
+//                                   ready flag (backward transform), and writes y|t in original order.
+// Ready flags hold the call's epoch (no reset); arrival counters and the ticket counter are reset
+// by their last user.  Bytes are dominated by the nearfield tiles: lanes own rows,
+// every tile column is one coalesced 256 B load, 8 columns in flight per lane, streaming loads.
 #include <cuda_runtime.h>
 
 #include "h2_internal.h"
@@ -14,182 +24,236 @@
 namespace h2 {
 namespace {
 
-__global__ void k_gather(const double* __restrict__ x, const int64_t* __restrict__ perm, double* __restrict__ xt,
-                         int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) xt[i] = x[perm[i]];
+struct MvArgs {
+  // source side (the basis applied to x)
+  const int32_t *s_leaves, *s_lo, *s_hi, *s_leafidx, *s_rank, *s_parent, *s_son0, *s_son1;
+  const int64_t* s_perm;
+  const double *s_leafb, *s_tr;
+  double* s_xh;
+  int32_t* s_arrive;
+  int s_nleaves;
+  // destination side (the basis producing y)
+  const int32_t *d_bfs, *d_lo, *d_hi, *d_leafidx, *d_rank, *d_parent, *d_son0, *d_bptr, *d_bidx;
+  const int64_t* d_perm;
+  const double *d_leafb, *d_tr;
+  double* d_xh;
+  int32_t* d_ready;
+  int d_nclusters;
+  // blocks
+  const int32_t* partner;  // admissible slot -> source cluster
+  const double* S;
+  const int32_t *nptr, *nidx, *npartner;
+  const double* N;
+  int lmax, rcap, transpose, epoch;
+  int32_t* ctl;  // [0] ticket counter, [1] "xhat done" (epoch)
+  const double* x;
+  double* y;
+  double alpha, beta;
+};
+
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ int ld_acquire(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int32_t* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// all lanes: wait until *flag == epoch, then every lane has acquired it
+__device__ __forceinline__ void wait_epoch(const int32_t* flag, int epoch, int lane) {
+  if (lane == 0)
+    while (ld_acquire(flag) != epoch) __nanosleep(32);
+  __syncwarp();
+  (void)ld_acquire(flag);
 }
 
-// One warp per leaf cluster of the source basis: xhat_s = W_s^T x|s.
-__global__ void k_fwd_leaf(const int32_t* __restrict__ leaves, int nleaves, const int32_t* __restrict__ lo,
-                           const int32_t* __restrict__ hi, const int32_t* __restrict__ leafidx,
-                           const int32_t* __restrict__ rank, const double* __restrict__ leafb, int lmax, int rcap,
-                           const double* __restrict__ xt, double* __restrict__ xh) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= nleaves) return;
-  const int s = leaves[w];
-  const int m = hi[s] - lo[s];
-  const int k = rank[s];
-  const double* Wb = leafb + (size_t)leafidx[s] * lmax * rcap;
-  const double x0 = lane < m ? xt[lo[s] + lane] : 0.0;
-  const double x1 = lane + 32 < m ? xt[lo[s] + lane + 32] : 0.0;
-  double mine = 0.0;
-  for (int j = 0; j < k; ++j) {
-    double p = 0.0;
-    if (lane < m) p = Wb[lane + (size_t)j * lmax] * x0;
-    if (lane + 32 < m) p += Wb[lane + 32 + (size_t)j * lmax] * x1;
+// ---- forward transform of one source leaf, then the climb ---------------------------------------
+__device__ void mv_up(const MvArgs& a, int s, int lane) {
+  const int rcap = a.rcap, lmax = a.lmax;
+  {
+    const int lo = a.s_lo[s], m = a.s_hi[s] - lo, k = a.s_rank[s];
+    if (k > 0) {
+      const double x0 = lane < m ? a.x[a.s_perm[lo + lane]] : 0.0;
+      const double x1 = lane + 32 < m ? a.x[a.s_perm[lo + lane + 32]] : 0.0;
+      const double* W = a.s_leafb + (size_t)a.s_leafidx[s] * lmax * rcap;
+      double mine0 = 0.0, mine1 = 0.0;
+      for (int j = 0; j < k; ++j) {
+        double p = 0.0;
+        if (lane < m) p = W[lane + (size_t)j * lmax] * x0;
+        if (lane + 32 < m) p += W[lane + 32 + (size_t)j * lmax] * x1;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-    if (lane == (j & 31)) mine = p;
-    if ((j & 31) == 31 || j == k - 1) {
-      const int base = j & ~31;
-      if (base + lane <= j) xh[(size_t)s * rcap + base + lane] = mine;
+        for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(FULL, p, o);
+        if (lane == (j & 31)) {
+          if (j < 32) mine0 = p;
+          else mine1 = p;
+        }
+      }
+      if (lane < k) a.s_xh[(size_t)s * rcap + lane] = mine0;
+      if (lane + 32 < k) a.s_xh[(size_t)s * rcap + lane + 32] = mine1;
     }
   }
-}
-
-// Internal clusters of one level: xhat_s = F_{s1}^T xhat_{s1} + F_{s2}^T xhat_{s2}; thread per entry.
-__global__ void k_fwd_level(const int32_t* __restrict__ list, int count, const int32_t* __restrict__ son0,
-                            const int32_t* __restrict__ son1, const int32_t* __restrict__ rank,
-                            const double* __restrict__ tr, int rcap, double* __restrict__ xh) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int c = idx / rcap, j = idx % rcap;
-  if (c >= count) return;
-  const int s = list[c];
-  if (son0[s] < 0) return;
-  if (j >= rank[s]) return;
-  double acc = 0.0;
-  for (int q = 0; q < 2; ++q) {
-    const int sq = q ? son1[s] : son0[s];
-    const int kq = rank[sq];
-    const double* F = tr + (size_t)sq * rcap * rcap;
-    for (int i = 0; i < kq; ++i) acc += F[i + (size_t)j * rcap] * xh[(size_t)sq * rcap + i];
+  for (;;) {
+    const int p = a.s_parent[s];
+    __threadfence();
+    __syncwarp();
+    if (p < 0) {
+      if (lane == 0) st_release(a.ctl + 1, a.epoch);
+      return;
+    }
+    int old = 0;
+    if (lane == 0) old = atomicAdd(a.s_arrive + p, 1);
+    old = __shfl_sync(FULL, old, 0);
+    if (old == 0) return;  // first of the two sons: the sibling finishes the father
+    if (lane == 0) a.s_arrive[p] = 0;
+    __threadfence();
+    const int kp = a.s_rank[p];
+    for (int j = lane; j < kp; j += 32) {
+      double acc = 0.0;
+      for (int q = 0; q < 2; ++q) {
+        const int c = q ? a.s_son1[p] : a.s_son0[p];
+        const int kc = a.s_rank[c];
+        const double* F = a.s_tr + (size_t)c * rcap * rcap;
+        const double* xc = a.s_xh + (size_t)c * rcap;
+        for (int i = 0; i < kc; ++i) acc += F[i + (size_t)j * rcap] * __ldcg(xc + i);
+      }
+      a.s_xh[(size_t)p * rcap + j] = acc;
+    }
+    s = p;
   }
-  xh[(size_t)s * rcap + j] = acc;
 }
 
-// Couplings: one warp per destination cluster.  Non-transposed: yhat_t = sum S_b xhat_s over row(t).
-// Transposed: yhat_s = sum S_b^T xhat_t over col(s).
-__global__ void k_couple(int ndst, const int32_t* __restrict__ bptr, const int32_t* __restrict__ bidx,
-                         const int32_t* __restrict__ partner, const int32_t* __restrict__ rank_dst,
-                         const int32_t* __restrict__ rank_src, const double* __restrict__ S, int rcap, int transpose,
-                         const double* __restrict__ xh_src, double* __restrict__ yh_dst) {
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= ndst) return;
-  const int kt = rank_dst[t];
-  for (int i0 = 0; i0 < kt; i0 += 32) {
-    const int i = i0 + lane;
-    double acc = 0.0;
-    for (int q = bptr[t]; q < bptr[t + 1]; ++q) {
-      const int a = bidx[q];
-      const int s = partner[a];
-      const int ks = rank_src[s];
-      const double* Sa = S + (size_t)a * rcap * rcap;
-      const double* xs = xh_src + (size_t)s * rcap;
-      if (i < kt) {
-        if (!transpose)
-          for (int j = 0; j < ks; ++j) acc += Sa[i + (size_t)j * rcap] * xs[j];
-        else
-          for (int j = 0; j < ks; ++j) acc += Sa[j + (size_t)i * rcap] * xs[j];
+// ---- nearfield rows of a destination leaf: (a0, a1) += sum_b N_b x|s ----------------------------
+__device__ __forceinline__ void mv_near(const MvArgs& a, int t, int m, int lane, double& a0, double& a1) {
+  const int lmax = a.lmax;
+  for (int q = a.nptr[t]; q < a.nptr[t + 1]; ++q) {
+    const int slot = a.nidx[q];
+    const int s = a.npartner[slot];
+    const int los = a.s_lo[s], ms = a.s_hi[s] - los;
+    const double xs0 = lane < ms ? a.x[a.s_perm[los + lane]] : 0.0;
+    const double xs1 = lane + 32 < ms ? a.x[a.s_perm[los + lane + 32]] : 0.0;
+    const double* Na = a.N + (size_t)slot * lmax * lmax;
+    if (!a.transpose) {
+      const int j1 = ms < 32 ? ms : 32;
+#pragma unroll 8
+      for (int j = 0; j < j1; ++j) {
+        const double xj = __shfl_sync(FULL, xs0, j);
+        if (lane < m) a0 += __ldcs(Na + lane + (size_t)j * lmax) * xj;
+        if (lane + 32 < m) a1 += __ldcs(Na + lane + 32 + (size_t)j * lmax) * xj;
+      }
+#pragma unroll 8
+      for (int j = 32; j < ms; ++j) {
+        const double xj = __shfl_sync(FULL, xs1, j - 32);
+        if (lane < m) a0 += __ldcs(Na + lane + (size_t)j * lmax) * xj;
+        if (lane + 32 < m) a1 += __ldcs(Na + lane + 32 + (size_t)j * lmax) * xj;
+      }
+    } else {  // y|t += N_b^T x|s: row `lane` of N_b^T is column `lane` of N_b
+      const int i1 = ms < 32 ? ms : 32;
+#pragma unroll 8
+      for (int i = 0; i < i1; ++i) {
+        const double xi = __shfl_sync(FULL, xs0, i);
+        if (lane < m) a0 += __ldg(Na + i + (size_t)lane * lmax) * xi;
+        if (lane + 32 < m) a1 += __ldg(Na + i + (size_t)(lane + 32) * lmax) * xi;
+      }
+#pragma unroll 8
+      for (int i = 32; i < ms; ++i) {
+        const double xi = __shfl_sync(FULL, xs1, i - 32);
+        if (lane < m) a0 += __ldg(Na + i + (size_t)lane * lmax) * xi;
+        if (lane + 32 < m) a1 += __ldg(Na + i + (size_t)(lane + 32) * lmax) * xi;
       }
     }
-    if (i < kt) yh_dst[(size_t)t * rcap + i] = acc;
   }
 }
 
-// Backward transform for one level (L >= 1): yhat_t += E_t yhat_parent; thread per entry.
-__global__ void k_bwd_level(const int32_t* __restrict__ list, int count, const int32_t* __restrict__ parent,
-                            const int32_t* __restrict__ rank, const double* __restrict__ tr, int rcap,
-                            double* __restrict__ yh) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int c = idx / rcap, i = idx % rcap;
-  if (c >= count) return;
-  const int t = list[c];
-  const int p = parent[t];
-  const int kt = rank[t], kp = rank[p];
-  if (i >= kt) return;
-  const double* E = tr + (size_t)t * rcap * rcap;
-  double acc = yh[(size_t)t * rcap + i];
-  for (int j = 0; j < kp; ++j) acc += E[i + (size_t)j * rcap] * yh[(size_t)p * rcap + j];
-  yh[(size_t)t * rcap + i] = acc;
-}
-
-// Leaf pass, one warp per destination leaf: y|t = V_t yhat_t + sum_b N_b x|s, then scatter to the
-// original order with alpha/beta.  Tiles are column-major (lane = row): every column load is coalesced.
-__global__ void __launch_bounds__(256) k_leaf_out(
-    const int32_t* __restrict__ leaves, int nleaves, const int32_t* __restrict__ lo_d,
-    const int32_t* __restrict__ hi_d, const int32_t* __restrict__ leafidx_d, const int32_t* __restrict__ rank_d,
-    const double* __restrict__ leafb_d, const int32_t* __restrict__ nptr, const int32_t* __restrict__ nidx,
-    const int32_t* __restrict__ npartner, const int32_t* __restrict__ lo_s, const int32_t* __restrict__ hi_s,
-    const double* __restrict__ N, int lmax, int rcap, int transpose, const double* __restrict__ yh,
-    const double* __restrict__ xt, const int64_t* __restrict__ perm_d, double alpha, double beta,
-    double* __restrict__ y, double* __restrict__ prof) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= nleaves) return;
-  const int t = leaves[w];
-  const int m = hi_d[t] - lo_d[t];
-  const int kt = rank_d[t];
-  const double* Vb = leafb_d + (size_t)leafidx_d[t] * lmax * rcap;
-  const double* yht = yh + (size_t)t * rcap;
+// ---- couplings + backward transform of one destination cluster (+ leaf output) ------------------
+__device__ void mv_down(const MvArgs& a, int t, int lane) {
+  const int rcap = a.rcap, lmax = a.lmax;
+  const bool leaf = a.d_son0[t] < 0;
   double a0 = 0.0, a1 = 0.0;
+  int lo = 0, m = 0;
+  if (leaf) {
+    lo = a.d_lo[t];
+    m = a.d_hi[t] - lo;
+    mv_near(a, t, m, lane, a0, a1);
+  }
+  const int kt = a.d_rank[t];
+  double y0 = 0.0, y1 = 0.0;  // yhat_t rows lane, lane + 32
+  const int p = a.d_parent[t];
+  const int kp = p >= 0 ? a.d_rank[p] : 0;
+  const int qb = a.d_bptr[t], qe = a.d_bptr[t + 1];
+  if (kt > 0 && qe > qb) {
+    wait_epoch(a.ctl + 1, a.epoch, lane);
+    for (int q = qb; q < qe; ++q) {
+      const int slot = a.d_bidx[q];
+      const int s = a.partner[slot];
+      const int ks = a.s_rank[s];
+      const double* Sa = a.S + (size_t)slot * rcap * rcap;
+      const double* xs = a.s_xh + (size_t)s * rcap;
+      if (!a.transpose) {
+#pragma unroll 4
+        for (int j = 0; j < ks; ++j) {
+          const double xj = __ldcg(xs + j);
+          if (lane < kt) y0 += Sa[lane + (size_t)j * rcap] * xj;
+          if (lane + 32 < kt) y1 += Sa[lane + 32 + (size_t)j * rcap] * xj;
+        }
+      } else {
+#pragma unroll 4
+        for (int j = 0; j < ks; ++j) {
+          const double xj = __ldcg(xs + j);
+          if (lane < kt) y0 += Sa[j + (size_t)lane * rcap] * xj;
+          if (lane + 32 < kt) y1 += Sa[j + (size_t)(lane + 32) * rcap] * xj;
+        }
+      }
+    }
+  }
+  if (kt > 0 && kp > 0) {
+    wait_epoch(a.d_ready + p, a.epoch, lane);
+    const double* E = a.d_tr + (size_t)t * rcap * rcap;
+    const double* yp = a.d_xh + (size_t)p * rcap;
+#pragma unroll 4
+    for (int j = 0; j < kp; ++j) {
+      const double yj = __ldcg(yp + j);
+      if (lane < kt) y0 += E[lane + (size_t)j * rcap] * yj;
+      if (lane + 32 < kt) y1 += E[lane + 32 + (size_t)j * rcap] * yj;
+    }
+  }
+  if (!leaf) {
+    if (lane < kt) a.d_xh[(size_t)t * rcap + lane] = y0;
+    if (lane + 32 < kt) a.d_xh[(size_t)t * rcap + lane + 32] = y1;
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(a.d_ready + t, a.epoch);
+    return;
+  }
+  const double* V = a.d_leafb + (size_t)a.d_leafidx[t] * lmax * rcap;
   for (int j = 0; j < kt; ++j) {
-    const double c = yht[j];
-    if (lane < m) a0 += Vb[lane + (size_t)j * lmax] * c;
-    if (lane + 32 < m) a1 += Vb[lane + 32 + (size_t)j * lmax] * c;
-  }
-  for (int q = nptr[t]; q < nptr[t + 1]; ++q) {
-    const int a = nidx[q];
-    const int s = npartner[a];
-    const int ms = hi_s[s] - lo_s[s];
-    const double* Na = N + (size_t)a * lmax * lmax;
-    const double* xs = xt + lo_s[s];
-    if (!transpose) {
-      int j = 0;
-      for (; j + 4 <= ms; j += 4) {
-        const double x0 = xs[j], x1 = xs[j + 1], x2 = xs[j + 2], x3 = xs[j + 3];
-        if (lane < m) {
-          const double* col = Na + lane + (size_t)j * lmax;
-          a0 += col[0] * x0 + col[lmax] * x1 + col[2 * lmax] * x2 + col[3 * lmax] * x3;
-        }
-        if (lane + 32 < m) {
-          const double* col = Na + lane + 32 + (size_t)j * lmax;
-          a1 += col[0] * x0 + col[lmax] * x1 + col[2 * lmax] * x2 + col[3 * lmax] * x3;
-        }
-      }
-      for (; j < ms; ++j) {
-        const double xj = xs[j];
-        if (lane < m) a0 += Na[lane + (size_t)j * lmax] * xj;
-        if (lane + 32 < m) a1 += Na[lane + 32 + (size_t)j * lmax] * xj;
-      }
-    } else {  // y|t += N_a^T x|s : row `lane` of N_a^T is column `lane` of N_a
-      for (int i = 0; i < ms; ++i) {
-        const double xi = xs[i];
-        if (lane < m) a0 += Na[i + (size_t)lane * lmax] * xi;
-        if (lane + 32 < m) a1 += Na[i + (size_t)(lane + 32) * lmax] * xi;
-      }
-    }
-  }
-  if (prof && lane == 0) {
-    // algorithmic bytes: leaf basis m x k_t, every nearfield tile, x|t (read once), y|t written (+read)
-    double bytes = 8.0 * ((double)m * kt + m * (beta == 0.0 ? 1 : 2) + m);
-    for (int q = nptr[t]; q < nptr[t + 1]; ++q) {
-      const int s = npartner[nidx[q]];
-      bytes += 8.0 * m * (hi_s[s] - lo_s[s]);
-    }
-    atomicAdd(prof + 2 * K_MV_LEAF_OUT + 1, bytes);
-    atomicAdd(prof + 2 * K_MV_LEAF_OUT, 2.0 * bytes / 8.0);
+    const double yj = __shfl_sync(FULL, j < 32 ? y0 : y1, j & 31);
+    if (lane < m) a0 += V[lane + (size_t)j * lmax] * yj;
+    if (lane + 32 < m) a1 += V[lane + 32 + (size_t)j * lmax] * yj;
   }
   if (lane < m) {
-    const int64_t o = perm_d[lo_d[t] + lane];
-    y[o] = beta == 0.0 ? alpha * a0 : alpha * a0 + beta * y[o];
+    const int64_t o = a.d_perm[lo + lane];
+    a.y[o] = a.beta == 0.0 ? a.alpha * a0 : a.alpha * a0 + a.beta * a.y[o];
   }
   if (lane + 32 < m) {
-    const int64_t o = perm_d[lo_d[t] + lane + 32];
-    y[o] = beta == 0.0 ? alpha * a1 : alpha * a1 + beta * y[o];
+    const int64_t o = a.d_perm[lo + lane + 32];
+    a.y[o] = a.beta == 0.0 ? a.alpha * a1 : a.alpha * a1 + a.beta * a.y[o];
   }
+}
+
+__global__ void __launch_bounds__(256) k_matvec(const __grid_constant__ MvArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int total = a.s_nleaves + a.d_nclusters;
+  if ((int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) >= total) return;  // exactly `total` tickets
+  int ticket = 0;
+  if (lane == 0) {
+    ticket = atomicAdd(a.ctl, 1);
+    if (ticket == total - 1) atomicExch(a.ctl, 0);  // every other ticket is already taken
+  }
+  ticket = __shfl_sync(FULL, ticket, 0);
+  if (ticket < a.s_nleaves) mv_up(a, a.s_leaves[ticket], lane);
+  else mv_down(a, a.d_bfs[ticket - a.s_nleaves], lane);
 }
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
@@ -201,44 +265,54 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   const MatDev& M = Z->d;
   const DevSide& src = transpose ? M.row : M.col;  // basis applied to x
   const DevSide& dst = transpose ? M.col : M.row;  // basis producing y
-  const h2_tree_* Ts = src.tree;
-  const h2_tree_* Td = dst.tree;
-  const int64_t n = Ts->n;
-  double* prof = prof_dev();
-  H2_LAUNCH(K_MV_GATHER, st, k_gather<<<cdiv(n, 256), 256, 0, st>>>(x, src.perm, M.xt, n));
-  // forward transform: leaves (all levels), then internal clusters deepest level first
-  H2_LAUNCH(K_MV_FWD_LEAF, st,
-            k_fwd_leaf<<<cdiv((long long)src.nleaves * 32, 256), 256, 0, st>>>(
-                src.leaves, src.nleaves, src.lo, src.hi, src.leafidx, src.rank, src.leafb, M.lmax, M.rcap, M.xt,
-                src.xh));
-  for (int L = Ts->depth - 1; L >= 0; --L) {
-    const int b = Ts->level_ptr[L], e = Ts->level_ptr[L + 1];
-    if (e > b)
-      H2_LAUNCH(K_MV_FWD_LEVEL, st,
-                k_fwd_level<<<cdiv((long long)(e - b) * M.rcap, 256), 256, 0, st>>>(
-                    src.bfs + b, e - b, src.son0, src.son1, src.rank, src.tr, M.rcap, src.xh));
-  }
-  // couplings
-  H2_LAUNCH(K_MV_COUPLE, st,
-            k_couple<<<cdiv((long long)Td->nclusters * 32, 256), 256, 0, st>>>(
-                Td->nclusters, dst.bptr, dst.bidx, transpose ? M.adm_t : M.adm_s, dst.rank, src.rank, M.S, M.rcap,
-                transpose, src.xh, dst.xh));
-  // backward transform
-  for (int L = 1; L <= Td->depth; ++L) {
-    const int b = Td->level_ptr[L], e = Td->level_ptr[L + 1];
-    if (e > b)
-      H2_LAUNCH(K_MV_BWD_LEVEL, st,
-                k_bwd_level<<<cdiv((long long)(e - b) * M.rcap, 256), 256, 0, st>>>(
-                    dst.bfs + b, e - b, dst.parent, dst.rank, dst.tr, M.rcap, dst.xh));
-  }
-  // leaves + nearfield + scatter
-  const int32_t* np = transpose ? M.ntptr : M.nptr;
-  const int32_t* ni = transpose ? M.ntidx : M.nidx;
-  const int32_t* npart = transpose ? M.in_t : M.in_s;
-  H2_LAUNCH(K_MV_LEAF_OUT, st,
-            k_leaf_out<<<cdiv((long long)dst.nleaves * 32, 256), 256, 0, st>>>(
-                dst.leaves, dst.nleaves, dst.lo, dst.hi, dst.leafidx, dst.rank, dst.leafb, np, ni, npart, src.lo,
-                src.hi, M.N, M.lmax, M.rcap, transpose, dst.xh, M.xt, dst.perm, alpha, beta, y, prof));
+  if (++Z->mv_epoch <= 0) Z->mv_epoch = 1;
+  MvArgs a;
+  a.s_leaves = src.leaves;
+  a.s_lo = src.lo;
+  a.s_hi = src.hi;
+  a.s_leafidx = src.leafidx;
+  a.s_rank = src.rank;
+  a.s_parent = src.parent;
+  a.s_son0 = src.son0;
+  a.s_son1 = src.son1;
+  a.s_perm = src.perm;
+  a.s_leafb = src.leafb;
+  a.s_tr = src.tr;
+  a.s_xh = src.xh;
+  a.s_arrive = src.mvsync;
+  a.s_nleaves = src.nleaves;
+  a.d_bfs = dst.bfs;
+  a.d_lo = dst.lo;
+  a.d_hi = dst.hi;
+  a.d_leafidx = dst.leafidx;
+  a.d_rank = dst.rank;
+  a.d_parent = dst.parent;
+  a.d_son0 = dst.son0;
+  a.d_bptr = dst.bptr;
+  a.d_bidx = dst.bidx;
+  a.d_perm = dst.perm;
+  a.d_leafb = dst.leafb;
+  a.d_tr = dst.tr;
+  a.d_xh = dst.xh;
+  a.d_ready = dst.mvsync + dst.nclusters;
+  a.d_nclusters = dst.nclusters;
+  a.partner = transpose ? M.adm_t : M.adm_s;
+  a.S = M.S;
+  a.nptr = transpose ? M.ntptr : M.nptr;
+  a.nidx = transpose ? M.ntidx : M.nidx;
+  a.npartner = transpose ? M.in_t : M.in_s;
+  a.N = M.N;
+  a.lmax = M.lmax;
+  a.rcap = M.rcap;
+  a.transpose = transpose;
+  a.epoch = Z->mv_epoch;
+  a.ctl = dst.mvsync + 2 * dst.nclusters;
+  a.x = x;
+  a.y = y;
+  a.alpha = alpha;
+  a.beta = beta;
+  const long long total = (long long)src.nleaves + dst.nclusters;
+  H2_LAUNCH(K_MV, st, k_matvec<<<cdiv(total, 8), 256, 0, st>>>(a));
   return cudaGetLastError();
 }
 

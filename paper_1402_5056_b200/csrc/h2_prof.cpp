@@ -13,8 +13,7 @@ namespace h2 {
 
 const char* const kKernelNames[K_COUNT] = {
     "k_upd_ext_leaf", "k_upd_ext_level", "k_upd_weights_path", "k_upd_weights_level", "k_upd_svd_leaf",
-    "k_upd_svd_level", "k_upd_couple", "k_upd_install", "k_upd_rcache_path", "k_mv_gather",
-    "k_mv_fwd_leaf", "k_mv_fwd_level", "k_mv_couple", "k_mv_bwd_level", "k_mv_leaf_out",
+    "k_upd_svd_level", "k_upd_couple", "k_upd_install", "k_upd_rcache_path", "k_matvec",
     "ar_expand", "ar_gemm", "ar_hmul", "ar_tile", "ar_tsqr", "ar_temp_core", "ar_misc"};
 
 namespace {

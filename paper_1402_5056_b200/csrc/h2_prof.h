@@ -17,12 +17,7 @@ enum KernelId {
   K_COUPLE,
   K_INSTALL,
   K_RCACHE,
-  K_MV_GATHER,
-  K_MV_FWD_LEAF,
-  K_MV_FWD_LEVEL,
-  K_MV_COUPLE,
-  K_MV_BWD_LEVEL,
-  K_MV_LEAF_OUT,
+  K_MV,
   K_AR_EXPAND,
   K_AR_GEMM,
   K_AR_HMUL,
