@@ -184,6 +184,9 @@ h2_status h2_profile_read(char* names, int64_t* launches, double* ms_total, doub
 /* Profiling sub-phase counters of the SVD items (cycles: load+GEMM, Jacobi, output; count; sum K;
  * sum m; sum of Jacobi sweeps), out[16]. */
 h2_status h2_profile_debug(double out[16]);
+/* Profiling: device-executor time (ns) and count per op code (exec.h OpCode order), cap entries;
+ * *nops = number of op-code slots (64). */
+h2_status h2_profile_ops(double* ns, double* count, int32_t cap, int32_t* nops);
 
 void h2_mat_destroy(h2_mat Z);
 const char* h2_last_error(void);

@@ -241,8 +241,11 @@ __global__ void __launch_bounds__(NT, 1) k_exec_cluster(const __grid_constant__ 
     if (op.barrier) cl.sync();
     if (timing) {
       const int kid = c_op_kid[op.code];
-      atomicAdd(P.prof + 2 * K_COUNT + 2 * kid, (double)(gtimer() - t0));
+      const double dt = (double)(gtimer() - t0);
+      atomicAdd(P.prof + 2 * K_COUNT + 2 * kid, dt);
       atomicAdd(P.prof + 2 * K_COUNT + 2 * kid + 1, 1.0);
+      atomicAdd(P.prof + 4 * K_COUNT + 32 + 2 * op.code, dt);  // per op code (h2_profile_ops)
+      atomicAdd(P.prof + 4 * K_COUNT + 32 + 2 * op.code + 1, 1.0);
     }
   }
 }

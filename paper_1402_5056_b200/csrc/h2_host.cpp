@@ -285,6 +285,13 @@ static h2_status setup_side(h2_mat_* Z, DevSide& D, const h2_tree_* T, bool row_
   CUDA_TRY(dupload(Z, &D.leaves, T->leaves));
   CUDA_TRY(dupload(Z, &D.level, T->level));
   CUDA_TRY(dupload(Z, &D.perm, T->perm));
+  {  // ancestors of every leaf by level (matvec backward transform walks them root -> leaf)
+    D.ancw = T->depth + 1;
+    std::vector<int32_t> anc((size_t)D.nleaves * D.ancw, -1);
+    for (int li = 0; li < D.nleaves; ++li)
+      for (int c = T->leaves[li]; c >= 0; c = T->parent[c]) anc[(size_t)li * D.ancw + T->level[c]] = c;
+    CUDA_TRY(dupload(Z, &D.anc, anc));
+  }
   // admissible stored blocks per cluster (adm slots in DFS order)
   std::vector<int32_t> ptr(T->nclusters + 1, 0), idx;
   for (size_t a = 0; a < Z->adm_blk.size(); ++a) {
@@ -312,8 +319,8 @@ static h2_status setup_side(h2_mat_* Z, DevSide& D, const h2_tree_* T, bool row_
   CUDA_TRY(dalloc(Z, &D.rc, (size_t)T->nclusters * r2));
   CUDA_TRY(cudaMemset(D.rc, 0, sizeof(double) * (size_t)T->nclusters * r2));
   CUDA_TRY(dalloc(Z, &D.xh, (size_t)T->nclusters * M.rcap));
-  CUDA_TRY(dalloc(Z, &D.mvsync, (size_t)2 * T->nclusters + 4));
-  CUDA_TRY(cudaMemset(D.mvsync, 0, sizeof(int32_t) * ((size_t)2 * T->nclusters + 4)));
+  CUDA_TRY(dalloc(Z, &D.mvsync, (size_t)T->nclusters));
+  CUDA_TRY(cudaMemset(D.mvsync, 0, sizeof(int32_t) * (size_t)T->nclusters));
   return H2_OK;
 }
 

@@ -75,7 +75,9 @@ struct DevSide {
   int32_t* rnew = nullptr;  // new ranks
   // matvec workspace
   double* xh = nullptr;     // nclusters * rcap coefficients
-  int32_t* mvsync = nullptr;  // fused matvec: nclusters arrival counters, nclusters ready flags, 4 control
+  int32_t* mvsync = nullptr;  // matvec: nclusters arrival counters (forward-transform climb)
+  int32_t* anc = nullptr;     // matvec: per leaf ordinal its ancestors by level (ancw ints, -1 padded)
+  int ancw = 0;
   double* hx = nullptr;     // H^2-block x dense workspace: nclusters * rcap * 64 (forward coefficients)
   double* hy = nullptr;     // nclusters * rcap * 64 (coupling/backward coefficients)
 };
@@ -127,7 +129,6 @@ struct h2_mat_ {
   int factored = 0;              // 0 no, 1 Cholesky, 2 LR
   std::vector<char> nzr, nzc;    // host: cluster rank possibly non-zero (row / column basis)
   long long stats[4] = {0, 0, 0, 0};  // local updates, dense adds, temporaries issued by the driver
-  mutable int mv_epoch = 0;            // fused matvec call counter (ready-flag epochs)
 };
 
 namespace h2 {

@@ -5,18 +5,18 @@
 //   backward transform  yhat_{t'} += E_{t'} yhat_t  top-down; leaves y|t = V_t yhat_t
 //   nearfield           y|t += sum_{b=(t,s) inadmissible} N_b x|s
 //
-// ONE launch, no grid-wide barrier: every warp takes a ticket (atomic counter, so tickets are
-// handed out in order and a warp only ever waits on lower tickets, which are resident).
-//   tickets [0, #leaves)            forward transform of a source leaf, then climb: the second
-//                                   of two siblings to finish (arrival counter) computes the
-//                                   father, up to the root, whose completion publishes "xhat done"
-//   tickets [#leaves, +#clusters)   destination clusters in level (BFS) order: a leaf first streams
-//                                   its nearfield tiles (independent of the transforms), then
-//                                   waits for "xhat done" (couplings) and for its father's yhat
-//                                   ready flag (backward transform), and writes y|t in original order.
-// Ready flags hold the call's epoch (no reset); arrival counters and the ticket counter are reset
-// by their last user.  Bytes are dominated by the nearfield tiles: lanes own rows,
-// every tile column is one coalesced 256 B load, 8 columns in flight per lane, streaming loads.
+// Three launches, no grid-wide barrier, no spin-waits:
+//   k_matvec_up    warps [0, #dst leaves): nearfield of a destination leaf, y|t = alpha sum_b N_b x|s
+//                  + beta y|t (streams the tiles, the bulk of the bytes); warps [.., +#src leaves):
+//                  forward transform of a source leaf, then climb: the second of two siblings to
+//                  finish (arrival counter) computes the father, up to the root.  No waits.
+//   k_matvec_couple  warp per destination cluster: yc_t = sum_b S_b xhat_s.
+//   k_matvec_walk    warp per destination leaf: yhat along its ancestor path, root first
+//                    (yhat_c = yc_c + E_c yhat_father), then y|t += alpha V_t yhat_t; the path
+//                    prefix shared by a block's 8 leaves is walked once (shared memory).  No
+//                    level-by-level chain of launches or flags.
+// The arrival counters are reset by their last user.  Bytes are dominated by the nearfield tiles
+// (SURVEY §8(d)): lanes own rows, a 32-column panel is 32 coalesced 256 B streaming loads in flight.
 #include <cuda_runtime.h>
 
 #include "h2_internal.h"
@@ -33,41 +33,25 @@ struct MvArgs {
   int32_t* s_arrive;
   int s_nleaves;
   // destination side (the basis producing y)
-  const int32_t *d_bfs, *d_lo, *d_hi, *d_leafidx, *d_rank, *d_parent, *d_son0, *d_bptr, *d_bidx;
+  const int32_t *d_bfs, *d_leaves, *d_lo, *d_hi, *d_leafidx, *d_rank, *d_parent, *d_son0, *d_bptr, *d_bidx;
   const int64_t* d_perm;
   const double *d_leafb, *d_tr;
   double* d_xh;
-  int32_t* d_ready;
-  int d_nclusters;
+  const int32_t* d_anc;
+  int d_ancw;
+  int d_nclusters, d_nleaves;
   // blocks
   const int32_t* partner;  // admissible slot -> source cluster
   const double* S;
   const int32_t *nptr, *nidx, *npartner;
   const double* N;
-  int lmax, rcap, transpose, epoch;
-  int32_t* ctl;  // [0] ticket counter, [1] "xhat done" (epoch)
+  int lmax, rcap, transpose;
   const double* x;
   double* y;
   double alpha, beta;
 };
 
 constexpr unsigned FULL = 0xffffffffu;
-
-__device__ __forceinline__ int ld_acquire(const int32_t* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int32_t* p, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-// all lanes: wait until *flag == epoch, then every lane has acquired it
-__device__ __forceinline__ void wait_epoch(const int32_t* flag, int epoch, int lane) {
-  if (lane == 0)
-    while (ld_acquire(flag) != epoch) __nanosleep(32);
-  __syncwarp();
-  (void)ld_acquire(flag);
-}
 
 // ---- forward transform of one source leaf, then the climb ---------------------------------------
 __device__ void mv_up(const MvArgs& a, int s, int lane) {
@@ -99,7 +83,6 @@ __device__ void mv_up(const MvArgs& a, int s, int lane) {
     __threadfence();
     __syncwarp();
     if (p < 0) {
-      if (lane == 0) st_release(a.ctl + 1, a.epoch);
       return;
     }
     int old = 0;
@@ -135,18 +118,29 @@ __device__ __forceinline__ void mv_near(const MvArgs& a, int t, int m, int lane,
     const double xs1 = lane + 32 < ms ? a.x[a.s_perm[los + lane + 32]] : 0.0;
     const double* Na = a.N + (size_t)slot * lmax * lmax;
     if (!a.transpose) {
-      const int j1 = ms < 32 ? ms : 32;
+      for (int j0 = 0; j0 < ms; j0 += 32) {
+        const int jn = ms - j0 < 32 ? ms - j0 : 32;
+        const double xsrc = j0 ? xs1 : xs0;
+        const double* Nj = Na + (size_t)j0 * lmax;
+        if (jn == 32) {  // whole 32-column panel in flight: 32 coalesced 256 B loads per row set
+          for (int r0 = 0; r0 < m; r0 += 32) {
+            double v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = r0 + lane < m ? __ldcs(Nj + r0 + lane + (size_t)j * lmax) : 0.0;
+            double acc = 0.0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc += v[j] * __shfl_sync(FULL, xsrc, j);
+            if (r0) a1 += acc;
+            else a0 += acc;
+          }
+        } else {
 #pragma unroll 8
-      for (int j = 0; j < j1; ++j) {
-        const double xj = __shfl_sync(FULL, xs0, j);
-        if (lane < m) a0 += __ldcs(Na + lane + (size_t)j * lmax) * xj;
-        if (lane + 32 < m) a1 += __ldcs(Na + lane + 32 + (size_t)j * lmax) * xj;
-      }
-#pragma unroll 8
-      for (int j = 32; j < ms; ++j) {
-        const double xj = __shfl_sync(FULL, xs1, j - 32);
-        if (lane < m) a0 += __ldcs(Na + lane + (size_t)j * lmax) * xj;
-        if (lane + 32 < m) a1 += __ldcs(Na + lane + 32 + (size_t)j * lmax) * xj;
+          for (int j = 0; j < jn; ++j) {
+            const double xj = __shfl_sync(FULL, xsrc, j);
+            if (lane < m) a0 += __ldcs(Nj + lane + (size_t)j * lmax) * xj;
+            if (lane + 32 < m) a1 += __ldcs(Nj + lane + 32 + (size_t)j * lmax) * xj;
+          }
+        }
       }
     } else {  // y|t += N_b^T x|s: row `lane` of N_b^T is column `lane` of N_b
       const int i1 = ms < 32 ? ms : 32;
@@ -166,72 +160,11 @@ __device__ __forceinline__ void mv_near(const MvArgs& a, int t, int m, int lane,
   }
 }
 
-// ---- couplings + backward transform of one destination cluster (+ leaf output) ------------------
-__device__ void mv_down(const MvArgs& a, int t, int lane) {
-  const int rcap = a.rcap, lmax = a.lmax;
-  const bool leaf = a.d_son0[t] < 0;
+// ---- nearfield of one destination leaf: y|t = alpha sum_b N_b x|s + beta y|t ----------------------
+__device__ void mv_leaf_near(const MvArgs& a, int t, int lane) {
+  const int lo = a.d_lo[t], m = a.d_hi[t] - lo;
   double a0 = 0.0, a1 = 0.0;
-  int lo = 0, m = 0;
-  if (leaf) {
-    lo = a.d_lo[t];
-    m = a.d_hi[t] - lo;
-    mv_near(a, t, m, lane, a0, a1);
-  }
-  const int kt = a.d_rank[t];
-  double y0 = 0.0, y1 = 0.0;  // yhat_t rows lane, lane + 32
-  const int p = a.d_parent[t];
-  const int kp = p >= 0 ? a.d_rank[p] : 0;
-  const int qb = a.d_bptr[t], qe = a.d_bptr[t + 1];
-  if (kt > 0 && qe > qb) {
-    wait_epoch(a.ctl + 1, a.epoch, lane);
-    for (int q = qb; q < qe; ++q) {
-      const int slot = a.d_bidx[q];
-      const int s = a.partner[slot];
-      const int ks = a.s_rank[s];
-      const double* Sa = a.S + (size_t)slot * rcap * rcap;
-      const double* xs = a.s_xh + (size_t)s * rcap;
-      if (!a.transpose) {
-#pragma unroll 4
-        for (int j = 0; j < ks; ++j) {
-          const double xj = __ldcg(xs + j);
-          if (lane < kt) y0 += Sa[lane + (size_t)j * rcap] * xj;
-          if (lane + 32 < kt) y1 += Sa[lane + 32 + (size_t)j * rcap] * xj;
-        }
-      } else {
-#pragma unroll 4
-        for (int j = 0; j < ks; ++j) {
-          const double xj = __ldcg(xs + j);
-          if (lane < kt) y0 += Sa[j + (size_t)lane * rcap] * xj;
-          if (lane + 32 < kt) y1 += Sa[j + (size_t)(lane + 32) * rcap] * xj;
-        }
-      }
-    }
-  }
-  if (kt > 0 && kp > 0) {
-    wait_epoch(a.d_ready + p, a.epoch, lane);
-    const double* E = a.d_tr + (size_t)t * rcap * rcap;
-    const double* yp = a.d_xh + (size_t)p * rcap;
-#pragma unroll 4
-    for (int j = 0; j < kp; ++j) {
-      const double yj = __ldcg(yp + j);
-      if (lane < kt) y0 += E[lane + (size_t)j * rcap] * yj;
-      if (lane + 32 < kt) y1 += E[lane + 32 + (size_t)j * rcap] * yj;
-    }
-  }
-  if (!leaf) {
-    if (lane < kt) a.d_xh[(size_t)t * rcap + lane] = y0;
-    if (lane + 32 < kt) a.d_xh[(size_t)t * rcap + lane + 32] = y1;
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(a.d_ready + t, a.epoch);
-    return;
-  }
-  const double* V = a.d_leafb + (size_t)a.d_leafidx[t] * lmax * rcap;
-  for (int j = 0; j < kt; ++j) {
-    const double yj = __shfl_sync(FULL, j < 32 ? y0 : y1, j & 31);
-    if (lane < m) a0 += V[lane + (size_t)j * lmax] * yj;
-    if (lane + 32 < m) a1 += V[lane + 32 + (size_t)j * lmax] * yj;
-  }
+  mv_near(a, t, m, lane, a0, a1);
   if (lane < m) {
     const int64_t o = a.d_perm[lo + lane];
     a.y[o] = a.beta == 0.0 ? a.alpha * a0 : a.alpha * a0 + a.beta * a.y[o];
@@ -242,18 +175,156 @@ __device__ void mv_down(const MvArgs& a, int t, int lane) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_matvec(const __grid_constant__ MvArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int total = a.s_nleaves + a.d_nclusters;
-  if ((int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) >= total) return;  // exactly `total` tickets
-  int ticket = 0;
-  if (lane == 0) {
-    ticket = atomicAdd(a.ctl, 1);
-    if (ticket == total - 1) atomicExch(a.ctl, 0);  // every other ticket is already taken
+// ---- couplings of one destination cluster: yc_t = sum_{b in row(t)} S_b xhat_s --------------------
+// Lane groups of R >= k_t lanes (R in {8, 16, 32}; lane = row) take the blocks round-robin, so
+// 32 / R block products are in flight at once; the block list is prefetched one block per lane.
+__device__ void mv_couple(const MvArgs& a, int t, int lane) {
+  const int rcap = a.rcap;
+  const int kt = a.d_rank[t];
+  if (kt == 0) return;
+  const int R = kt <= 8 ? 8 : kt <= 16 ? 16 : 32;
+  const int ng = 32 / R, g = lane / R, r = lane % R;
+  double y0 = 0.0, y1 = 0.0;  // rows r, r + 32 (R = 32 only)
+  const int qb = a.d_bptr[t], qe = a.d_bptr[t + 1];
+  for (int q0 = qb; q0 < qe; q0 += 32) {
+    const int nq = qe - q0 < 32 ? qe - q0 : 32;
+    int slot_l = 0, s_l = 0, ks_l = 0;
+    if (lane < nq) {
+      slot_l = a.d_bidx[q0 + lane];
+      s_l = a.partner[slot_l];
+      ks_l = a.s_rank[s_l];
+    }
+    for (int qq = 0; qq < nq; qq += ng) {
+      const int mine = qq + g;  // this group's block
+      const int slot = __shfl_sync(FULL, slot_l, mine & 31);
+      const int s = __shfl_sync(FULL, s_l, mine & 31);
+      const int ksv = __shfl_sync(FULL, ks_l, mine & 31);
+      const int ks = mine < nq ? ksv : 0;
+      const double* Sa = a.S + (size_t)slot * rcap * rcap;
+      const double* xs = a.s_xh + (size_t)s * rcap;
+      if (!a.transpose) {
+#pragma unroll 8
+        for (int j = 0; j < ks; ++j) {
+          const double xj = xs[j];
+          if (r < kt) y0 += Sa[r + (size_t)j * rcap] * xj;
+          if (r + 32 < kt) y1 += Sa[r + 32 + (size_t)j * rcap] * xj;
+        }
+      } else {
+#pragma unroll 8
+        for (int j = 0; j < ks; ++j) {
+          const double xj = xs[j];
+          if (r < kt) y0 += Sa[j + (size_t)r * rcap] * xj;
+          if (r + 32 < kt) y1 += Sa[j + (size_t)(r + 32) * rcap] * xj;
+        }
+      }
+    }
   }
-  ticket = __shfl_sync(FULL, ticket, 0);
-  if (ticket < a.s_nleaves) mv_up(a, a.s_leaves[ticket], lane);
-  else mv_down(a, a.d_bfs[ticket - a.s_nleaves], lane);
+  for (int o = R; o < 32; o <<= 1) {
+    y0 += __shfl_xor_sync(FULL, y0, o);
+    y1 += __shfl_xor_sync(FULL, y1, o);
+  }
+  if (g == 0) {
+    if (r < kt) a.d_xh[(size_t)t * rcap + r] = y0;
+    if (r + 32 < kt) a.d_xh[(size_t)t * rcap + r + 32] = y1;
+  }
+}
+
+// ---- backward transform along the path root -> leaf t, then y|t += alpha V_t yhat_t ---------------
+// yhat_c = yc_c + E_c yhat_{father(c)} level by level along the leaf's ancestor row (lane L holds the
+// cluster of level L).  The 8 leaves of a block are consecutive in DFS order, so their paths share
+// a prefix (the common ancestors of the first and the last leaf): warp 0 walks it once and leaves
+// yhat of the deepest common ancestor in shared memory, then every warp walks its own remainder.
+// No cross-block synchronisation.
+__device__ __forceinline__ void walk_levels(const MvArgs& a, int c0, int c1, int k0, int k1, int Lb, int Le,
+                                            int lane, double& y0, double& y1, int& kprev) {
+  const int rcap = a.rcap;
+  for (int L = Lb; L < Le; ++L) {
+    const int c = __shfl_sync(FULL, L < 32 ? c0 : c1, L & 31);
+    const int kc = __shfl_sync(FULL, L < 32 ? k0 : k1, L & 31);
+    const double* yc = a.d_xh + (size_t)c * rcap;
+    double n0 = lane < kc ? yc[lane] : 0.0;
+    double n1 = lane + 32 < kc ? yc[lane + 32] : 0.0;
+    if (kprev > 0 && kc > 0) {
+      const double* E = a.d_tr + (size_t)c * rcap * rcap;
+#pragma unroll 4
+      for (int j = 0; j < kprev; ++j) {
+        const double yj = __shfl_sync(FULL, j < 32 ? y0 : y1, j & 31);
+        if (lane < kc) n0 += E[lane + (size_t)j * rcap] * yj;
+        if (lane + 32 < kc) n1 += E[lane + 32 + (size_t)j * rcap] * yj;
+      }
+    }
+    y0 = n0;
+    y1 = n1;
+    kprev = kc;
+  }
+}
+
+__device__ void mv_walk(const MvArgs& a, int lane) {
+  __shared__ double ysh[64];
+  __shared__ int sh[2];  // common prefix length, rank at its end
+  const int rcap = a.rcap, lmax = a.lmax, aw = a.d_ancw;
+  const int warp = threadIdx.x >> 5;
+  const int lf = blockIdx.x * 8, ll = min(lf + 8, a.d_nleaves) - 1;  // first / last leaf ordinal
+  if (warp == 0) {
+    const int32_t* pf = a.d_anc + (size_t)lf * aw;
+    const int32_t* pl = a.d_anc + (size_t)ll * aw;
+    const int f0 = lane < aw ? pf[lane] : -2, f1 = lane + 32 < aw ? pf[lane + 32] : -2;
+    const int l0 = lane < aw ? pl[lane] : -3, l1 = lane + 32 < aw ? pl[lane + 32] : -3;
+    const unsigned d0 = __ballot_sync(FULL, f0 != l0 || f0 < 0), d1 = __ballot_sync(FULL, f1 != l1 || f1 < 0);
+    const int Lc = d0 ? __ffs(d0) - 1 : (d1 ? 32 + __ffs(d1) - 1 : 64);  // first differing level
+    const int k0 = f0 >= 0 ? a.d_rank[f0] : 0, k1 = f1 >= 0 ? a.d_rank[f1] : 0;
+    double y0 = 0.0, y1 = 0.0;
+    int kprev = 0;
+    walk_levels(a, f0, f1, k0, k1, 0, Lc, lane, y0, y1, kprev);
+    if (lane < kprev) ysh[lane] = y0;
+    if (lane + 32 < kprev) ysh[lane + 32] = y1;
+    if (lane == 0) {
+      sh[0] = Lc;
+      sh[1] = kprev;
+    }
+  }
+  __syncthreads();
+  const int li = lf + warp;
+  if (li >= a.d_nleaves) return;
+  const int Lc = sh[0];
+  int kprev = sh[1];
+  double y0 = lane < kprev ? ysh[lane] : 0.0, y1 = lane + 32 < kprev ? ysh[lane + 32] : 0.0;
+  const int32_t* path = a.d_anc + (size_t)li * aw;
+  const int c0 = lane < aw ? path[lane] : -1;
+  const int c1 = lane + 32 < aw ? path[lane + 32] : -1;
+  const int nl = __popc(__ballot_sync(FULL, c0 >= 0)) + __popc(__ballot_sync(FULL, c1 >= 0));  // path length
+  const int k0 = c0 >= 0 ? a.d_rank[c0] : 0, k1 = c1 >= 0 ? a.d_rank[c1] : 0;
+  walk_levels(a, c0, c1, k0, k1, Lc, nl, lane, y0, y1, kprev);
+  const int t = __shfl_sync(FULL, (nl - 1) < 32 ? c0 : c1, (nl - 1) & 31);
+  const int kt = kprev;
+  if (kt == 0) return;
+  const int lo = a.d_lo[t], m = a.d_hi[t] - lo;
+  const double* V = a.d_leafb + (size_t)a.d_leafidx[t] * lmax * rcap;
+  double a0 = 0.0, a1 = 0.0;
+  for (int j = 0; j < kt; ++j) {
+    const double yj = __shfl_sync(FULL, j < 32 ? y0 : y1, j & 31);
+    if (lane < m) a0 += V[lane + (size_t)j * lmax] * yj;
+    if (lane + 32 < m) a1 += V[lane + 32 + (size_t)j * lmax] * yj;
+  }
+  if (lane < m) a.y[a.d_perm[lo + lane]] += a.alpha * a0;
+  if (lane + 32 < m) a.y[a.d_perm[lo + lane + 32]] += a.alpha * a1;
+}
+
+__global__ void __launch_bounds__(256) k_matvec_up(const __grid_constant__ MvArgs a) {
+  // no waits in this kernel: static assignment, nearfield leaves first
+  const int lane = threadIdx.x & 31;
+  const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  if (w < a.d_nleaves) mv_leaf_near(a, a.d_leaves[w], lane);
+  else if (w < a.d_nleaves + a.s_nleaves) mv_up(a, a.s_leaves[w - a.d_nleaves], lane);
+}
+
+__global__ void __launch_bounds__(256) k_matvec_couple(const __grid_constant__ MvArgs a) {
+  const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  if (w < a.d_nclusters) mv_couple(a, w, threadIdx.x & 31);
+}
+
+__global__ void __launch_bounds__(256) k_matvec_walk(const __grid_constant__ MvArgs a) {
+  mv_walk(a, threadIdx.x & 31);
 }
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
@@ -265,7 +336,6 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   const MatDev& M = Z->d;
   const DevSide& src = transpose ? M.row : M.col;  // basis applied to x
   const DevSide& dst = transpose ? M.col : M.row;  // basis producing y
-  if (++Z->mv_epoch <= 0) Z->mv_epoch = 1;
   MvArgs a;
   a.s_leaves = src.leaves;
   a.s_lo = src.lo;
@@ -282,6 +352,8 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   a.s_arrive = src.mvsync;
   a.s_nleaves = src.nleaves;
   a.d_bfs = dst.bfs;
+  a.d_leaves = dst.leaves;
+  a.d_nleaves = dst.nleaves;
   a.d_lo = dst.lo;
   a.d_hi = dst.hi;
   a.d_leafidx = dst.leafidx;
@@ -294,7 +366,8 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   a.d_leafb = dst.leafb;
   a.d_tr = dst.tr;
   a.d_xh = dst.xh;
-  a.d_ready = dst.mvsync + dst.nclusters;
+  a.d_anc = dst.anc;
+  a.d_ancw = dst.ancw;
   a.d_nclusters = dst.nclusters;
   a.partner = transpose ? M.adm_t : M.adm_s;
   a.S = M.S;
@@ -305,14 +378,13 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   a.lmax = M.lmax;
   a.rcap = M.rcap;
   a.transpose = transpose;
-  a.epoch = Z->mv_epoch;
-  a.ctl = dst.mvsync + 2 * dst.nclusters;
   a.x = x;
   a.y = y;
   a.alpha = alpha;
   a.beta = beta;
-  const long long total = (long long)src.nleaves + dst.nclusters;
-  H2_LAUNCH(K_MV, st, k_matvec<<<cdiv(total, 8), 256, 0, st>>>(a));
+  H2_LAUNCH(K_MV, st, k_matvec_up<<<cdiv((long long)src.nleaves + dst.nleaves, 8), 256, 0, st>>>(a));
+  H2_LAUNCH(K_MV, st, k_matvec_couple<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
+  H2_LAUNCH(K_MV, st, k_matvec_walk<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
   return cudaGetLastError();
 }
 

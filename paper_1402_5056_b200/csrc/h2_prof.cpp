@@ -60,13 +60,13 @@ extern "C" h2_status h2_profile_enable(int32_t on) {
     return H2_ERR_CUDA;
   }
   if (!g.d) {
-    e = cudaMalloc(&g.d, sizeof(double) * (4 * K_COUNT + 32));
+    e = cudaMalloc(&g.d, sizeof(double) * (4 * K_COUNT + 32 + 2 * 64));
     if (e != cudaSuccess) {
       set_error("h2_profile_enable: cudaMalloc failed");
       return H2_ERR_NOMEM;
     }
   }
-  cudaMemset(g.d, 0, sizeof(double) * (4 * K_COUNT + 32));
+  cudaMemset(g.d, 0, sizeof(double) * (4 * K_COUNT + 32 + 2 * 64));
   for (int k = 0; k < K_COUNT; ++k) g.used[k] = 0;
   g.on = on != 0;
   return H2_OK;
@@ -117,6 +117,28 @@ extern "C" h2_status h2_profile_debug(double out[16]) {
   if (e != cudaSuccess) {
     set_error(std::string("h2_profile_debug: ") + cudaGetErrorString(e));
     return H2_ERR_CUDA;
+  }
+  return H2_OK;
+}
+
+extern "C" h2_status h2_profile_ops(double* ns, double* count, int32_t cap, int32_t* nops) {
+  if (!ns || !count || cap < 0) {
+    set_error("h2_profile_ops: NULL argument");
+    return H2_ERR_ARG;
+  }
+  if (nops) *nops = 64;
+  double acc[2 * 64] = {};
+  if (g.d) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(acc, g.d + 4 * K_COUNT + 32, sizeof(acc), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) {
+      set_error(std::string("h2_profile_ops: ") + cudaGetErrorString(e));
+      return H2_ERR_CUDA;
+    }
+  }
+  for (int i = 0; i < cap && i < 64; ++i) {
+    ns[i] = acc[2 * i];
+    count[i] = acc[2 * i + 1];
   }
   return H2_OK;
 }

@@ -287,12 +287,78 @@ __device__ void it_getrf(const MatDev& M, int slot, int t, int item_, int nitems
   }
 }
 
+// Triangular solve with a leaf tile (m <= 32), one warp per 4 right-hand sides: lane i holds row
+// i of the 4 vectors and the 32 tile entries it needs (loaded once from the tile), every step is
+// one scaling, one shuffle broadcast and one FMA per vector (no shared memory, no block barrier).
+__device__ __forceinline__ void trsm_warp32(int mode, int m, const double* N, int lmax, double* B, int ldb,
+                                            int nvec, int v0, int vstride) {
+  const int lane = threadIdx.x & 31;
+  const bool rowwise = (mode == RLT || mode == RUN);
+  const bool fwd = !(mode == LLT || mode == LUN);
+  const bool unit = mode == LLU;
+  // lane i needs A[i][j] of the operator applied: L (LLN/LLU/RLT), L^T (LLT), U^T (RUN/LUT), U (LUN)
+  const bool byrow = (mode == RLT || mode == LLN || mode == LLU || mode == LUN);
+  double r[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    r[j] = (lane < m && j < m) ? (byrow ? N[lane + (size_t)j * lmax] : N[j + (size_t)lane * lmax]) : 0.0;
+  const double invd = lane < m ? 1.0 / N[lane + (size_t)lane * lmax] : 0.0;
+  constexpr int VPW = 4;
+  for (int vb = v0; vb < nvec; vb += vstride) {
+    double x[VPW];
+#pragma unroll
+    for (int q = 0; q < VPW; ++q) {
+      const int v = vb + q;
+      x[q] = (v < nvec && lane < m) ? (rowwise ? B[v + (size_t)lane * ldb] : B[(size_t)v * ldb + lane]) : 0.0;
+    }
+    if (fwd) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < m) {
+#pragma unroll
+          for (int q = 0; q < VPW; ++q) {
+            const double z = __shfl_sync(0xffffffffu, unit ? x[q] : x[q] * invd, j);
+            x[q] = lane == j ? z : (lane > j ? x[q] - r[j] * z : x[q]);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 31; j >= 0; --j) {
+        if (j < m) {
+#pragma unroll
+          for (int q = 0; q < VPW; ++q) {
+            const double z = __shfl_sync(0xffffffffu, x[q] * invd, j);
+            x[q] = lane == j ? z : (lane < j ? x[q] - r[j] * z : x[q]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < VPW; ++q) {
+      const int v = vb + q;
+      if (v < nvec && lane < m) {
+        if (rowwise) B[v + (size_t)lane * ldb] = x[q];
+        else B[(size_t)v * ldb + lane] = x[q];
+      }
+    }
+  }
+}
+
 __device__ void it_trsm(const MatDev& M, int slot, int m, int mode, double* B, int ldb, int brows,
                                              Dim bcols, int item_, int nitems_, double* smx_) {
+  const double* N = M.N + (size_t)slot * M.lmax * M.lmax;
+  if (m <= 32) {
+    const int nv = (mode == RLT || mode == RUN) ? brows : bcols.v();
+    const int w = threadIdx.x >> 5;
+    trsm_warp32(mode, m, N, M.lmax, B, ldb, nv, item_ * (NT / 8) + w * 4, nitems_ * (NT / 8));
+    return;
+  }
   double* T = smx_;
   const int ld = 65;
-  const double* N = M.N + (size_t)slot * M.lmax * M.lmax;
+  double* invd = T + 64 * ld;
   for (int e = threadIdx.x; e < m * m; e += NT) T[(e % m) + (e / m) * ld] = N[(e % m) + (e / m) * M.lmax];
+  for (int j = threadIdx.x; j < m; j += NT) invd[j] = 1.0 / N[j + (size_t)j * M.lmax];
   __syncthreads();
   const bool rowwise = (mode == RLT || mode == RUN);
   const int nvec = rowwise ? brows : bcols.v();
@@ -307,14 +373,14 @@ __device__ void it_trsm(const MatDev& M, int slot, int m, int mode, double* B, i
         for (int j = 0; j < m; ++j) {
           double acc = x[j * st];
           for (int i = 0; i < j; ++i) acc -= T[j + i * ld] * x[i * st];
-          x[j * st] = mode == LLU ? acc : acc / T[j + j * ld];
+          x[j * st] = mode == LLU ? acc : acc * invd[j];
         }
         break;
       case LLT:  // L^T x = b  backward
         for (int j = m - 1; j >= 0; --j) {
           double acc = x[j * st];
           for (int i = j + 1; i < m; ++i) acc -= T[i + j * ld] * x[i * st];
-          x[j * st] = acc / T[j + j * ld];
+          x[j * st] = acc * invd[j];
         }
         break;
       case RUN:  // x U = b  <=>  U^T x^T = b^T  forward
@@ -322,14 +388,14 @@ __device__ void it_trsm(const MatDev& M, int slot, int m, int mode, double* B, i
         for (int j = 0; j < m; ++j) {
           double acc = x[j * st];
           for (int i = 0; i < j; ++i) acc -= T[i + j * ld] * x[i * st];
-          x[j * st] = acc / T[j + j * ld];
+          x[j * st] = acc * invd[j];
         }
         break;
       case LUN:  // U x = b  backward
         for (int j = m - 1; j >= 0; --j) {
           double acc = x[j * st];
           for (int i = j + 1; i < m; ++i) acc -= T[j + i * ld] * x[i * st];
-          x[j * st] = acc / T[j + j * ld];
+          x[j * st] = acc * invd[j];
         }
         break;
     }

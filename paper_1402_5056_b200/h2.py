@@ -18,7 +18,7 @@ EXPORTED_SYMBOLS = [
     "h2_block_tree", "h2_btree_export", "h2_btree_destroy",
     "h2_from_sparse", "h2_lowrank_update", "h2_matvec", "h2_addmul", "h2_lr_factor", "h2_solve",
     "h2_ranks", "h2_storage_report", "h2_export", "h2_check_device_flags",
-    "h2_profile_enable", "h2_profile_read", "h2_profile_debug", "h2_stats", "h2_pcg", "h2_launch_count",
+    "h2_profile_enable", "h2_profile_read", "h2_profile_debug", "h2_profile_ops", "h2_stats", "h2_pcg", "h2_launch_count",
     "h2_mat_destroy", "h2_last_error",
 ]
 
@@ -54,6 +54,7 @@ _sig = {
     "h2_profile_enable": [_i32],
     "h2_stats": [_p, _p],
     "h2_profile_debug": [_p],
+    "h2_profile_ops": [_p, _p, _i32, _p],
     "h2_pcg": [_p, _p, _p, _p, _f64, _i32, _p, _p, _p],
     "h2_launch_count": [_p],
     "h2_profile_read": [_p, _p, _p, _p, _p, _p],
@@ -308,6 +309,22 @@ def h2_profile_debug():
     out = np.zeros(16)
     _check(_lib.h2_profile_debug(_ptr(out)))
     return out
+
+
+OP_NAMES = ["upd_ext_leaf", "upd_ext_level", "upd_w_path", "upd_w_level", "upd_svd_leaf", "upd_svd_level",
+            "upd_couple", "upd_install", "upd_rcache", "expand", "gemm", "gemm_part", "gemm_sum", "hm_fwd_leaf",
+            "hm_fwd_level", "hm_couple", "hm_bwd_level", "hm_leaf", "potrf", "getrf", "trsm", "tsqr", "temp",
+            "copy_cols", "set_int", "add_int", "rank_if", "stack", "choose", "identity", "transpose", "gather",
+            "scatter", "zero", "dd", "nztile"]
+
+
+def h2_profile_ops():
+    """Per executor op code: {name: (count, ms)} (profiling must be enabled)."""
+    ns = np.zeros(64)
+    cnt = np.zeros(64)
+    _check(_lib.h2_profile_ops(_ptr(ns), _ptr(cnt), 64, None))
+    return {OP_NAMES[i] if i < len(OP_NAMES) else str(i): (int(cnt[i]), round(ns[i] / 1e6, 1))
+            for i in range(64) if cnt[i] > 0}
 
 
 def h2_pcg(A: Mat, F: Mat, b, x=None, tol: float = 1e-8, maxit: int = 500, stream=None):

@@ -33,6 +33,7 @@ if prof:
     out["kernels"] = {k: (v["launches"], round(v["ms"], 1)) for k, v in P.h2_profile_read().items()}
     d = P.h2.h2_profile_debug()
     out["host_wait_s"] = round(d[15], 3)
+    out["ops"] = P.h2.h2_profile_ops()
     if d[3]:
         out["svd_phases_cycles_per_call"] = [round(d[0] / d[3]), round(d[1] / d[3]), round(d[2] / d[3])]
         out["svd_avg_K_m_sweeps"] = [d[4] / d[3], d[5] / d[3], d[6] / d[3]]
