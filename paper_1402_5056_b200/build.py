@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libh2b200.so")
-SOURCES = ["h2_host.cpp", "h2_prof.cpp", "h2_factor.cpp", "h2_matvec.cu", "h2_exec.cu", "h2_pcg.cu"]
+SOURCES = ["h2_host.cpp", "h2_prof.cpp", "h2_factor.cpp", "h2_matvec.cu", "h2_exec.cu", "h2_pcg.cu", "h2_solve.cu"]
 HEADERS = ["h2_internal.h", "h2_prof.h", "h2_arith.cuh", "exec.h", "items_upd.cuh", "items_arith.cuh", "devla.cuh", os.path.join("..", "..", "include", "h2.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

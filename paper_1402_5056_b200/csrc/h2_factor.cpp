@@ -706,5 +706,10 @@ extern "C" h2_status h2_solve(h2_mat F, double* x, int32_t nrhs, int64_t ldx, h2
     h2::set_error("h2_solve: need 1 <= nrhs <= 64 and ldx >= n");
     return H2_ERR_SHAPE;
   }
-  return run_driver(F, nullptr, stream, F->factored == 1 ? 3 : 4, nullptr, nullptr, 0.0, x, nrhs, ldx);
+  cudaError_t e = h2::solve_factored(F, x, nrhs, ldx, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    h2::set_error(std::string("h2_solve: ") + cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? H2_ERR_NOMEM : H2_ERR_CUDA;
+  }
+  return H2_OK;
 }

@@ -113,6 +113,16 @@ struct MatDev {
 
 }  // namespace h2
 
+// Schedule of one sequential block substitution sweep (h2_solve.cu), device arrays, built once.
+struct SolveSched {
+  int built = 0, nl = 0;
+  int32_t *order = nullptr, *diag = nullptr;            // leaf cluster / diagonal tile slot per position
+  int32_t *near_ptr = nullptr, *near_slot = nullptr, *near_src = nullptr;  // off-diagonal tiles per position
+  int32_t *enter_ptr = nullptr, *enter = nullptr;       // destination clusters entered (top-down)
+  int32_t *done_ptr = nullptr, *done = nullptr;         // source clusters completed (bottom-up)
+  int32_t *push_ptr = nullptr, *push_slot = nullptr, *push_dst = nullptr;  // per source cluster
+};
+
 struct h2_mat_ {
   h2_btree_* bt = nullptr;
   bool lower = false;
@@ -129,6 +139,7 @@ struct h2_mat_ {
   int factored = 0;              // 0 no, 1 Cholesky, 2 LR
   std::vector<char> nzr, nzc;    // host: cluster rank possibly non-zero (row / column basis)
   long long stats[4] = {0, 0, 0, 0};  // local updates, dense adds, temporaries issued by the driver
+  SolveSched sched[3];                 // h2_solve sweeps: L (ascending), U (descending), L^T (descending)
 };
 
 namespace h2 {
@@ -137,6 +148,8 @@ void set_error(const std::string& msg);
 // launchers (h2_matvec.cu)
 cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const double* x, double beta,
                           double* y, cudaStream_t st);
+// sequential block substitution (h2_solve.cu): x (original order, n x nrhs, ld ldx) <- F^{-1} x
+cudaError_t solve_factored(h2_mat_* F, double* x, int nrhs, int64_t ldx, cudaStream_t st);
 // launchers (h2_update.cu)
 cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a, cudaStream_t st);
 cudaError_t update_init_attributes();

@@ -13,7 +13,7 @@ namespace h2 {
 
 const char* const kKernelNames[K_COUNT] = {
     "k_upd_ext_leaf", "k_upd_ext_level", "k_upd_weights_path", "k_upd_weights_level", "k_upd_svd_leaf",
-    "k_upd_svd_level", "k_upd_couple", "k_upd_install", "k_upd_rcache_path", "k_matvec",
+    "k_upd_svd_level", "k_upd_couple", "k_upd_install", "k_upd_rcache_path", "k_matvec", "k_solve_sweep",
     "ar_expand", "ar_gemm", "ar_hmul", "ar_tile", "ar_tsqr", "ar_temp_core", "ar_misc"};
 
 namespace {

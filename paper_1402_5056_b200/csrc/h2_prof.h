@@ -18,6 +18,7 @@ enum KernelId {
   K_INSTALL,
   K_RCACHE,
   K_MV,
+  K_SOLVE,
   K_AR_EXPAND,
   K_AR_GEMM,
   K_AR_HMUL,

@@ -55,6 +55,14 @@ def test_cholesky_parity(name, N):
     b = stream(RHS).standard_normal(n)
     xs_g, xs_o = _gpu_solve(Z, b), ar.solve(b)
     assert np.linalg.norm(xs_g - xs_o) / np.linalg.norm(xs_o) <= 10 * eps
+    # the substitution sweeps invert the device factor itself: L (L^T x) = b to rounding, for a
+    # block of 11 right-hand sides (two sweeps of 8 + 3 columns)
+    Bm = stream(RHS).standard_normal((11, n))
+    Xm = _t(Bm.copy())  # (11, n) row-major = n x 11 column-major, ld n
+    P.h2_solve(Z, Xm, nrhs=11)
+    for j in range(11):
+        w = P.h2_matvec(Z, P.h2_matvec(Z, Xm[j].contiguous(), transpose=True))
+        assert torch.linalg.norm(w - _t(Bm[j])) / np.linalg.norm(Bm[j]) <= 1e-11
     _, m_o, _ = pcg(lambda v: A @ v, lambda v: ar.solve(v), b)
     _, m_g, rel = pcg(lambda v: A @ v, lambda v: _gpu_solve(Z, v), b)
     assert rel < 1e-8 and abs(m_g - m_o) <= 1
