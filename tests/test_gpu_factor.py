@@ -37,7 +37,7 @@ def _gpu_solve(Z, b):
     return x.cpu().numpy()
 
 
-@pytest.mark.parametrize("name,N", [("C0", None), ("C2", 64)])
+@pytest.mark.parametrize("name,N", [("C0", None), ("C2", 64), ("C3", 12)])
 def test_cholesky_parity(name, N):
     eps = 1e-4
     s = setup(name, N, lower=True)
