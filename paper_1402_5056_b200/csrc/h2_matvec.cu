@@ -118,25 +118,25 @@ __device__ __forceinline__ void mv_near(const MvArgs& a, int t, int m, int lane,
     const double xs1 = lane + 32 < ms ? a.x[a.s_perm[los + lane + 32]] : 0.0;
     const double* Na = a.N + (size_t)slot * lmax * lmax;
     if (!a.transpose) {
-      for (int j0 = 0; j0 < ms; j0 += 32) {
-        const int jn = ms - j0 < 32 ? ms - j0 : 32;
-        const double xsrc = j0 ? xs1 : xs0;
+      for (int j0 = 0; j0 < ms; j0 += 16) {
+        const int jn = ms - j0 < 16 ? ms - j0 : 16;
+        const double xsrc = j0 >= 32 ? xs1 : xs0;
+        const int jl = j0 & 31;
         const double* Nj = Na + (size_t)j0 * lmax;
-        if (jn == 32) {  // whole 32-column panel in flight: 32 coalesced 256 B loads per row set
+        if (jn == 16) {  // 16-column panel in flight: 16 coalesced 256 B loads per row set
           for (int r0 = 0; r0 < m; r0 += 32) {
-            double v[32];
+            double v[16];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = r0 + lane < m ? __ldcs(Nj + r0 + lane + (size_t)j * lmax) : 0.0;
+            for (int j = 0; j < 16; ++j) v[j] = r0 + lane < m ? __ldcs(Nj + r0 + lane + (size_t)j * lmax) : 0.0;
             double acc = 0.0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) acc += v[j] * __shfl_sync(FULL, xsrc, j);
+            for (int j = 0; j < 16; ++j) acc += v[j] * __shfl_sync(FULL, xsrc, jl + j);
             if (r0) a1 += acc;
             else a0 += acc;
           }
         } else {
-#pragma unroll 8
           for (int j = 0; j < jn; ++j) {
-            const double xj = __shfl_sync(FULL, xsrc, j);
+            const double xj = __shfl_sync(FULL, xsrc, jl + j);
             if (lane < m) a0 += __ldcs(Nj + lane + (size_t)j * lmax) * xj;
             if (lane + 32 < m) a1 += __ldcs(Nj + lane + 32 + (size_t)j * lmax) * xj;
           }
@@ -310,7 +310,7 @@ __device__ void mv_walk(const MvArgs& a, int lane) {
   if (lane + 32 < m) a.y[a.d_perm[lo + lane + 32]] += a.alpha * a1;
 }
 
-__global__ void __launch_bounds__(256) k_matvec_up(const __grid_constant__ MvArgs a) {
+__global__ void __launch_bounds__(256, 4) k_matvec_up(const __grid_constant__ MvArgs a) {
   // no waits in this kernel: static assignment, nearfield leaves first
   const int lane = threadIdx.x & 31;
   const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
