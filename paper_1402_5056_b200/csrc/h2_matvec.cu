@@ -5,11 +5,12 @@
 //   backward transform  yhat_{t'} += E_{t'} yhat_t  top-down; leaves y|t = V_t yhat_t
 //   nearfield           y|t += sum_{b=(t,s) inadmissible} N_b x|s
 //
-// Three launches, no grid-wide barrier, no spin-waits:
-//   k_matvec_up    warps [0, #dst leaves): nearfield of a destination leaf, y|t = alpha sum_b N_b x|s
-//                  + beta y|t (streams the tiles, the bulk of the bytes); warps [.., +#src leaves):
-//                  forward transform of a source leaf, then climb: the second of two siblings to
-//                  finish (arrival counter) computes the father, up to the root.  No waits.
+// Four launches on two streams (nearfield || forward transform + couplings, then the walk), no
+// grid-wide barrier, no spin-waits; a matrix whose bases all have rank 0 launches the nearfield only:
+//   k_matvec_near  warp per destination leaf: y|t = alpha sum_b N_b x|s + beta y|t (streams the
+//                  tiles, the bulk of the bytes) -- on a second stream, concurrently with:
+//   k_matvec_fwd   warp per source leaf: forward transform, then climb: the second of two siblings
+//                  to finish (arrival counter) computes the father, up to the root.  No waits.
 //   k_matvec_couple  warp per destination cluster: yc_t = sum_b S_b xhat_s.
 //   k_matvec_walk    warp per destination leaf: yhat along its ancestor path, root first
 //                    (yhat_c = yc_c + E_c yhat_father), then y|t += alpha V_t yhat_t; the path
@@ -18,6 +19,8 @@
 // The arrival counters are reset by their last user.  Bytes are dominated by the nearfield tiles
 // (SURVEY §8(d)): lanes own rows, a 32-column panel is 32 coalesced 256 B streaming loads in flight.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "h2_internal.h"
 
@@ -310,12 +313,14 @@ __device__ void mv_walk(const MvArgs& a, int lane) {
   if (lane + 32 < m) a.y[a.d_perm[lo + lane + 32]] += a.alpha * a1;
 }
 
-__global__ void __launch_bounds__(256, 4) k_matvec_up(const __grid_constant__ MvArgs a) {
-  // no waits in this kernel: static assignment, nearfield leaves first
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(256, 4) k_matvec_near(const __grid_constant__ MvArgs a) {
   const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
-  if (w < a.d_nleaves) mv_leaf_near(a, a.d_leaves[w], lane);
-  else if (w < a.d_nleaves + a.s_nleaves) mv_up(a, a.s_leaves[w - a.d_nleaves], lane);
+  if (w < a.d_nleaves) mv_leaf_near(a, a.d_leaves[w], threadIdx.x & 31);
+}
+
+__global__ void __launch_bounds__(256) k_matvec_fwd(const __grid_constant__ MvArgs a) {
+  const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  if (w < a.s_nleaves) mv_up(a, a.s_leaves[w], threadIdx.x & 31);
 }
 
 __global__ void __launch_bounds__(256) k_matvec_couple(const __grid_constant__ MvArgs a) {
@@ -382,8 +387,30 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   a.y = y;
   a.alpha = alpha;
   a.beta = beta;
-  H2_LAUNCH(K_MV, st, k_matvec_up<<<cdiv((long long)src.nleaves + dst.nleaves, 8), 256, 0, st>>>(a));
+  // the far field contributes only if some row and some column basis may have a non-zero rank
+  const bool far = std::find(Z->nzr.begin(), Z->nzr.end(), 1) != Z->nzr.end() &&
+                   std::find(Z->nzc.begin(), Z->nzc.end(), 1) != Z->nzc.end();
+  if (!far) {
+    H2_LAUNCH(K_MV, st, k_matvec_near<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
+    return cudaGetLastError();
+  }
+  // the nearfield stream (the bulk of the bytes) runs on a second stream, concurrently with the
+  // forward transform and the couplings; the backward walk adds V_t yhat_t after both
+  static cudaStream_t s2 = nullptr;
+  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaError_t e;
+  if (!s2) {
+    if ((e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking))) return e;
+    if ((e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming))) return e;
+    if ((e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming))) return e;
+  }
+  if ((e = cudaEventRecord(ev_fork, st))) return e;
+  if ((e = cudaStreamWaitEvent(s2, ev_fork, 0))) return e;
+  H2_LAUNCH(K_MV, s2, k_matvec_near<<<cdiv(dst.nleaves, 8), 256, 0, s2>>>(a));
+  if ((e = cudaEventRecord(ev_join, s2))) return e;
+  H2_LAUNCH(K_MV, st, k_matvec_fwd<<<cdiv(src.nleaves, 8), 256, 0, st>>>(a));
   H2_LAUNCH(K_MV, st, k_matvec_couple<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
+  if ((e = cudaStreamWaitEvent(st, ev_join, 0))) return e;
   H2_LAUNCH(K_MV, st, k_matvec_walk<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
   return cudaGetLastError();
 }
