@@ -190,18 +190,25 @@ def run_gpu(args, rank, world):
         rels.append(rel)
         if j == args.steps - 1:
             sto = P.h2_storage_report(Z)
-            # matvec of the factor L (HBM-bound: ~1.4 KB/DOF, larger than L2)
+            # matvecs (HBM-bound, both larger than L2): the factor L (~1.4 KB/DOF) and the sparse
+            # input A in H^2 form (rank-0 bases; the matvec PCG applies every iteration)
             xv = torch.randn(n, dtype=torch.float64, device=dev)
             yv = torch.empty_like(xv)
-            for _ in range(3):
-                P.h2_matvec(Z, xv, yv)
-            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            m0.record(cs)
-            for _ in range(20):
-                P.h2_matvec(Z, xv, yv)
-            m1.record(cs)
-            torch.cuda.synchronize()
-            mv_ms = m0.elapsed_time(m1) / 20
+
+            def time_mv(M):
+                for _ in range(3):
+                    P.h2_matvec(M, xv, yv)
+                m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                m0.record(cs)
+                for _ in range(20):
+                    P.h2_matvec(M, xv, yv)
+                m1.record(cs)
+                torch.cuda.synchronize()
+                return m0.elapsed_time(m1) / 20
+
+            mv_ms = time_mv(Z)
+            mvA_ms = time_mv(Aop)
+            mvA_bytes = 8.0 * float(P.h2_storage_report(Aop).sum()) + 16.0 * n
         del Z
     step_ms = fact_ms + pcg_ms
     if dist is not None:
@@ -210,7 +217,7 @@ def run_gpu(args, rank, world):
     mv_bytes = 8.0 * float(sto.sum()) + 16.0 * n
     return dict(n=n, structure_s=structure_s, fact_ms=fact_ms, pcg_ms=pcg_ms, step_ms=step_ms, nz=nz_total,
                 stats=stats, iters=iters, rels=rels, launches=launches, prof=prof, e2e=e2e, clocks=clocks,
-                sto=sto.tolist(), mv_ms=mv_ms, mv_bytes=mv_bytes)
+                sto=sto.tolist(), mv_ms=mv_ms, mv_bytes=mv_bytes, mvA_ms=mvA_ms, mvA_bytes=mvA_bytes)
 
 
 def oracle_sample(N, seed=0):
@@ -322,6 +329,10 @@ def main():
         "roofline": roof,
         "matvec": {"GBps": mv_gbs, "ms": res["mv_ms"], "bytes": res["mv_bytes"], "peak": hbm, "frac": mv_gbs / hbm,
                    "bound": "hbm", "of": "factor L"},
+        "matvec_A": {"GBps": res["mvA_bytes"] / (res["mvA_ms"] / 1e3) / 1e9, "ms": res["mvA_ms"],
+                     "bytes": res["mvA_bytes"], "peak": hbm,
+                     "frac": res["mvA_bytes"] / (res["mvA_ms"] / 1e3) / 1e9 / hbm, "bound": "hbm",
+                     "of": "input A (H2 form, the PCG operator)"},
         "cpu_baseline": {"value": cpu["updates"] / cpu["fact_s"], "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"oracle H2 Cholesky of the C2-shaped jump problem at {args.cpu_N}x{args.cpu_N} "
                                    f"nodes (n={cpu['n']}): {cpu['updates']} updates in {cpu['fact_s']:.1f} s, "
