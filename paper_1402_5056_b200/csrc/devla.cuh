@@ -131,29 +131,40 @@ static __device__ void cta_qr_R(double* A, int lda, int m, int n, double* diag, 
   __syncthreads();
   for (int j = 0; j < jmax; ++j) {
     double part = 0.0;
+    // every active group also forms |a_j|^2 itself (same lanes, same order as column j's own
+    // group, hence bit-identical), so no broadcast through shared memory and one barrier per column
+    double nj = 0.0;
     if (c >= j && c < n)
-      for (int i = j + sl; i < m; i += S) part += A[i + j * lda] * A[i + c * lda];
-    for (int o = S / 2; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (c == j && sl == 0) red[0] = part;
-    __syncthreads();
-    const double nrm2 = red[0];
-    const double ajj = A[j + j * lda];
-    if (nrm2 > 0.0) {
-      const double nrm = sqrt(nrm2);
-      const double alpha = ajj > 0.0 ? -nrm : nrm;
-      const double half_vtv = nrm2 - alpha * ajj;
-      if (c > j && c < n) {
-        const double ajc = A[j + c * lda];
-        __syncwarp(gm);
-        const double f = (part - alpha * ajc) / half_vtv;
-        for (int i = j + sl; i < m; i += S) {
-          const double vi = (i == j) ? (ajj - alpha) : A[i + j * lda];
-          A[i + c * lda] -= f * vi;
-        }
+      for (int i = j + sl; i < m; i += S) {
+        const double aij = A[i + j * lda];
+        part += aij * A[i + c * lda];
+        nj += aij * aij;
       }
-      if (tid == 0) diag[j] = alpha;
-    } else if (tid == 0) {
-      diag[j] = 0.0;
+    for (int o = S / 2; o; o >>= 1) {
+      part += __shfl_xor_sync(0xffffffffu, part, o);
+      nj += __shfl_xor_sync(0xffffffffu, nj, o);
+    }
+    if (c >= j && c < n) {
+      const double nrm2 = nj;
+      const double ajj = A[j + j * lda];
+      if (nrm2 > 0.0) {
+        const double nrm = sqrt(nrm2);
+        const double alpha = ajj > 0.0 ? -nrm : nrm;
+        const double half_vtv = nrm2 - alpha * ajj;
+        if (c > j) {
+          const double ajc = A[j + c * lda];
+          __syncwarp(gm);
+          const double f = (part - alpha * ajc) / half_vtv;
+          for (int i = j + sl; i < m; i += S) {
+            const double vi = (i == j) ? (ajj - alpha) : A[i + j * lda];
+            A[i + c * lda] -= f * vi;
+          }
+        } else if (sl == 0) {
+          diag[j] = alpha;
+        }
+      } else if (c == j && sl == 0) {
+        diag[j] = 0.0;
+      }
     }
     __syncthreads();
   }
