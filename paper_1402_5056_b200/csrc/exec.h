@@ -63,6 +63,7 @@ enum OpCode : int32_t {
   OP_ZERO,
   OP_DD,
   OP_NZTILE,
+  OP_SKIPZ,  // all CTAs: if *ip == 0 skip the next `count` ops (a zero-rank local update)
   OP_COUNT
 };
 
@@ -159,12 +160,16 @@ struct ExecCtx {
   size_t flush_at = 16384;  // ops are run in chunks while the host keeps recording
   int mat_index(const MatDev& M);
   void maybe_flush();
+  int hold = 0;             // > 0 while a skip region is open (no flush inside it)
   template <class P>
   void emit(int code, int nitems, const MatDev* M, const P& payload, bool barrier = true) {
     if (nitems <= 0) return;
     // two consecutive single-item ops both run on CTA 0 of the cluster, in order: the block
     // barrier after each item orders them, the cluster barrier between them is not needed
-    if (nitems == 1 && !ops.empty() && ops.back().nitems == 1) ops.back().barrier = 0;
+    // (a skip op reads its flag on every CTA: the barrier before it stays)
+    if (nitems == 1 && code != OP_SKIPZ && !ops.empty() && ops.back().nitems == 1 &&
+        ops.back().code != OP_SKIPZ)
+      ops.back().barrier = 0;
     OpRec r;
     r.code = code;
     r.nitems = nitems;
@@ -173,8 +178,12 @@ struct ExecCtx {
     static_assert(sizeof(P) <= OP_PAYLOAD, "payload");
     std::memcpy(r.p, &payload, sizeof(P));
     ops.push_back(r);
-    if (ops.size() >= flush_at) maybe_flush();
+    if (ops.size() >= flush_at && hold == 0) maybe_flush();
   }
+  // skip region: the ops recorded between begin_skip and end_skip are skipped on the device when
+  // *k == 0 (they must all run inside the cluster executor: end_skip cancels the skip otherwise)
+  size_t begin_skip(const int* k);
+  void end_skip(size_t at, int big_items);
 };
 
 // the recording context of the current thread (set by the public entry points)

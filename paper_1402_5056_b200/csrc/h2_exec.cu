@@ -49,7 +49,8 @@ __constant__ int c_op_kid[OP_COUNT] = {
     K_EXT_LEAF, K_EXT_LEVEL, K_W_PATH, K_W_LEVEL, K_SVD_LEAF, K_SVD_LEVEL, K_COUPLE, K_INSTALL, K_RCACHE,
     K_AR_EXPAND, K_AR_GEMM, K_AR_GEMM, K_AR_GEMM, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL,
     K_AR_TILE, K_AR_TILE, K_AR_TILE, K_AR_TSQR, K_AR_TEMP, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC,
-    K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_TEMP, K_AR_MISC};
+    K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_TEMP, K_AR_MISC,
+    K_AR_MISC};
 
 __device__ __forceinline__ const DevSide& side_of(const MatDev& M, int s) { return s ? M.col : M.row; }
 
@@ -228,6 +229,11 @@ __global__ void __launch_bounds__(NT, 1) k_exec_cluster(const __grid_constant__ 
   for (int o = P.begin; o < P.end; ++o) {
     const OpRec& op = P.ops[o];
     const int n = op.nitems;
+    if (op.code == OP_SKIPZ) {  // every CTA reads the same (final) flag: uniform skip
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      if (*(volatile const int*)q.ip == 0) o += q.cols;
+      continue;
+    }
     // warm L1/L2 with the next op record while this one runs (192 B = 2 lines)
     if (threadIdx.x < 2 && o + 1 < P.end)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(&P.ops[o + 1]) + 128 * threadIdx.x));
@@ -309,6 +315,27 @@ void ExecCtx::maybe_flush() {
 }
 
 ExecCtx* exec_ctx() { return g_ctx; }
+
+size_t ExecCtx::begin_skip(const int* k) {
+  PMisc q{};
+  q.ip = const_cast<int*>(k);
+  q.cols = 0;
+  emit(OP_SKIPZ, 1, nullptr, q);
+  ++hold;
+  return ops.size() - 1;
+}
+
+void ExecCtx::end_skip(size_t at, int big_items) {
+  --hold;
+  int cnt = (int)(ops.size() - at - 1);
+  for (size_t i = at + 1; i < ops.size(); ++i)
+    if (ops[i].nitems > big_items) cnt = 0;  // a full-grid op cannot be skipped from inside the cluster
+  PMisc q;
+  std::memcpy(&q, ops[at].p, sizeof(PMisc));
+  q.cols = cnt;
+  std::memcpy(ops[at].p, &q, sizeof(PMisc));
+  if (ops.size() >= flush_at && hold == 0) maybe_flush();
+}
 
 void exec_begin(ExecCtx* ctx, cudaStream_t st) {
   ctx->st = st;
@@ -468,6 +495,10 @@ cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a_in, cudaStream_t st
     c->emit(OP_UPD_EXT_LEAF, nin, &M, pu(a, 0, 0, 0, 0, in0, nin, 0, 0));
     return ac.done();
   }
+  // a device-determined rank (internal callers) may be zero at run time: skip the whole update
+  static const bool no_skip = getenv("H2_NO_SKIP") != nullptr;  // A/B switch (tools)
+  const bool skip = a.kdev && !no_skip;
+  const size_t skip_at = skip ? c->begin_skip(a.kdev) : 0;
   int rl0, nrl, cl0, ncl;
   leaf_range(R, a.t0, &rl0, &nrl);
   leaf_range(C, a.s0, &cl0, &ncl);
@@ -498,6 +529,7 @@ cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a_in, cudaStream_t st
   c->emit(OP_UPD_COUPLE, nA + nB, &M, pu(a, nA, nB));   // U5
   c->emit(OP_UPD_INSTALL, nA + nB, &M, pu(a, nA, nB));  // U6
   c->emit(OP_UPD_RCACHE, 2, &M, pu(a));                 // R-factor caches on pred(t0), pred(s0)
+  if (skip) c->end_skip(skip_at, g_big);
   return ac.done();
 }
 
