@@ -190,6 +190,7 @@ struct ExecCtx {
 ExecCtx* exec_ctx();
 void exec_begin(ExecCtx* ctx, cudaStream_t st);
 cudaError_t exec_flush();  // runs and clears the recorded ops (stream-ordered)
+int exec_big_items();      // ops with more items run as their own full-grid launch
 cudaError_t exec_end();    // flush + reset the context pointer
 
 }  // namespace h2

@@ -28,7 +28,7 @@ namespace h2 {
 namespace {
 
 constexpr int NT = NTHREADS;
-constexpr int CL = 8;     // CTAs of the executor cluster (portable cluster size)
+constexpr int CL = 16;    // CTAs of the executor cluster (non-portable size 16; falls back to 8)
 constexpr int BIG = 64;   // ops with more items run as a full-grid launch
 constexpr int KC = KCAP_MAX;
 constexpr int PR = 192;
@@ -283,6 +283,25 @@ cudaError_t init_exec() {
   if (g_attr) return cudaSuccess;
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(k_exec_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXEC))) return e;
+  if (g_cl > 8) {
+    // a non-portable cluster size: use it only if the device can place such a cluster
+    int ncl = 0;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    cfg.gridDim = dim3(g_cl);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = SM_EXEC;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = g_cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaFuncSetAttribute(k_exec_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+        cudaOccupancyMaxActiveClusters(&ncl, k_exec_cluster, &cfg) != cudaSuccess || ncl < 1)
+      g_cl = 8;
+    cudaGetLastError();
+  }
   if ((e = cudaFuncSetAttribute(k_exec_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SM_EXEC))) return e;
   if ((e = cudaMalloc(&g_gpart, sizeof(double) * ar::NPART * KC * KC))) return e;
   for (int i = 0; i < 2; ++i)
@@ -315,6 +334,7 @@ void ExecCtx::maybe_flush() {
 }
 
 ExecCtx* exec_ctx() { return g_ctx; }
+int exec_big_items() { return g_big; }
 
 size_t ExecCtx::begin_skip(const int* k) {
   PMisc q{};

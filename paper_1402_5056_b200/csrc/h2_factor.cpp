@@ -177,7 +177,11 @@ struct Driver {
     if (kcap == 0) return;
     if (tgt) {
       tgt->nz = true;
+      // a zero device rank leaves the temporary unchanged (own-3): skip the whole truncated addition
+      ExecCtx* c = exec_ctx();
+      const size_t at = c->begin_skip(kdev);
       temp_add(*tgt, t, r, A, lda, B, ldb, kdev, kcap, alpha);
+      c->end_skip(at, exec_big_items());
       return;
     }
     const int b = Z->bt->find(t, r);
