@@ -283,7 +283,7 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
   long long c1;
   int p, sweeps;
   double* W = Bt;
-  if (K <= 32 && (m <= 16 || (m <= 32 && K > 8))) {
+  if (K <= 32 && (m <= 16 || (m <= 32 && K > 16))) {
     // M = V B~^T (m x K) in Mm; one-sided Jacobi on M in registers of one warp (lane j owns
     // column j), W = M J = [sigma_j u_j] into Bt (free after the product)
     la::cta_gemm(Mm, RM, V, ldv, false, Bt, RM, true, m, K, K, false);
@@ -293,23 +293,34 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
     else sweeps = la::warp_jacobi<32, false>(Mm, RM, m, K, W, RM, sig, order, scr);
     p = K;
   } else if (K <= 16) {
-    // M = V B~^T (m x K) in Mm; R_M of M = Q_M R_M (Householder) in Bt[:, 0:32); one-sided Jacobi
-    // on R_M in registers with the rotations J accumulated (Bt[:, 32:64)): R_M J = U_R Sigma,
-    // so M J = Q_M U_R Sigma and column j of W = M J (Bt[:, 64:96)) is sigma_j u_j.
+    // M = V B~^T (m x K) in Mm; R of M = Q R (Householder, in Bt[:, 0:32)); one-sided Jacobi on
+    // the columns of R^T (K x p, p = min(m, K)) in registers of one warp: R^T J = Y with columns
+    // y_j = sigma_j v_j (v_j: right singular vectors of R and M), so M y_j / sigma_j = sigma_j u_j
+    // is column j of W (Bt[:, 64:96)).  No rotations to accumulate, columns of length K.
     la::cta_gemm(Mm, RM, V, ldv, false, Bt, RM, true, m, K, K, false);
     __syncthreads();
     double* Rw = Bt;
-    double* J = Bt + 32 * RM;
+    double* Y = Bt + 32 * RM;
     W = Bt + 64 * RM;
     la::cta_copy(Rw, RM, Mm, RM, m, K);
     __syncthreads();
     la::cta_qr_R(Rw, RM, m, K, sig, (double*)order);
     const int pr = m < K ? m : K;
+    for (int e = threadIdx.x; e < K * pr; e += NT) {  // R^T (K x pr) into W's slot as the input
+      const int i = e % K, j = e / K;
+      W[i + j * RM] = j <= i ? Rw[j + i * RM] : 0.0;
+    }
+    __syncthreads();
     c1 = clock64();
-    if (K <= 8) sweeps = la::warp_jacobi<8, true>(Rw, RM, pr, K, J, RM, sig, order, scr);
-    else sweeps = la::warp_jacobi<16, true>(Rw, RM, pr, K, J, RM, sig, order, scr);
-    la::cta_gemm(W, RM, Mm, RM, false, J, RM, false, m, K, K, false);
-    p = K;
+    if (K <= 8) sweeps = la::warp_jacobi<8, false>(W, RM, K, pr, Y, RM, sig, order, scr);
+    else sweeps = la::warp_jacobi<16, false>(W, RM, K, pr, Y, RM, sig, order, scr);
+    for (int e = threadIdx.x; e < m * pr; e += NT) {
+      const int i = e % m, j = e / m;
+      double acc = 0.0;
+      for (int q = 0; q < K; ++q) acc += Mm[i + q * RM] * Y[q + j * RM];
+      W[i + j * RM] = sig[j] > 0.0 ? acc / sig[j] : 0.0;
+    }
+    p = pr;
     __syncthreads();
   } else {
     // M^T = B~ V^T  (K x m)

@@ -19,8 +19,16 @@ __global__ void kb(const double* Ain, int m, int K, long long* cyc, double* sig_
   for (int e = threadIdx.x; e < m * K; e += blockDim.x) A[(e % m) + (e / m) * LD] = Ain[e];
   __syncthreads();
   long long c0 = clock64();
-  if (mode == 0) {
+  if (mode == 0 || mode == 3) {
     la::cta_qr_R(A, LD, m, K, sig, (double*)order);
+  }
+  if (mode == 3) {  // W = R^T (K x K) in J
+    const int pr = m < K ? m : K;
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+      const int i = e % K, j = e / K;
+      J[i + j * LD] = (j < pr && j <= i) ? A[j + i * LD] : 0.0;
+    }
+    __syncthreads();
   }
   long long c1 = clock64();
   int sw = 0;
@@ -28,6 +36,9 @@ __global__ void kb(const double* Ain, int m, int K, long long* cyc, double* sig_
   if (mode == 0) {
     if (K <= 8) sw = la::warp_jacobi<8, true>(A, LD, pr, K, J, LD, sig, order, scr);
     else sw = la::warp_jacobi<16, true>(A, LD, pr, K, J, LD, sig, order, scr);
+  } else if (mode == 3) {
+    if (K <= 8) sw = la::warp_jacobi<8, false>(J, LD, K, K, A, LD, sig, order, scr);
+    else sw = la::warp_jacobi<16, false>(J, LD, K, K, A, LD, sig, order, scr);
   } else if (mode == 2) {
     if (m <= 16) sw = la::warp_jacobi<16, false>(A, LD, m, K, J, LD, sig, order, scr);
     else sw = la::warp_jacobi<32, false>(A, LD, m, K, J, LD, sig, order, scr);
@@ -56,14 +67,14 @@ int main(int argc, char** argv) {
   cudaMemcpy(d, h, sizeof(double) * m * K, cudaMemcpyHostToDevice);
   const int smem = (2 * LD * 96 + 96) * 8 + 200 * 4;
   cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 4; ++mode) {
     for (int rep = 0; rep < 3; ++rep) kb<<<1, 256, smem>>>(d, m, K, c, s, mode);
     long long hc[4];
     double hs[96];
     cudaMemcpy(hc, c, sizeof(hc), cudaMemcpyDeviceToHost);
     cudaMemcpy(hs, s, sizeof(double) * K, cudaMemcpyDeviceToHost);
     printf("%s m=%d K=%d qr=%lld jacobi=%lld sweeps=%lld sig0=%.15g sigK=%.15g err=%s\n",
-           mode == 2 ? "warp_direct" : mode ? "cta_jacobi " : "qr+warp_jac", m, K, hc[0], hc[1], hc[2], hs[0], hs[K - 1],
+           mode == 3 ? "qr+jac(R^T)" : mode == 2 ? "warp_direct" : mode ? "cta_jacobi " : "qr+warp_jac", m, K, hc[0], hc[1], hc[2], hs[0], hs[K - 1],
            cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
