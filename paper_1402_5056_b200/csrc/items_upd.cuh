@@ -265,12 +265,12 @@ __device__ void it_upd_weights_level(const MatDev& M, UpdArgs a_, int bA, int nA
 // Given V (m x K, ldv) in shared memory and B~_t, compute M = V B~^T, its SVD, the rank, Q and R_t.
 __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, int t, double* V, int ldv, int m,
                          int K, double* sm_rest, int kid, double extra_flops) {
-  // U4: left singular vectors / values of M = V B~^T (m x K).  m, K <= 32: one-sided Jacobi on M
-  // in registers of one warp.  K <= 16: the same on the K x K factor R_M (M = Q_M R_M) with the
-  // rotations accumulated, U Sigma = M J (see below).  Otherwise: the
-  // SVD is taken of W = R_A^T (m x p, p = min(m, K)) where M^T = Q_A R_A (Householder):
-  // M = W Q_A^T with Q_A orthonormal, so W has the singular values and left singular vectors of
-  // M, fewer columns and a triangular (preconditioned) start for the one-sided Jacobi.
+  // U4: left singular vectors / values of M = V B~^T (m x K).  m <= 16, K <= 32: one-sided
+  // Jacobi on M in registers of one warp.  K <= 32: Householder R of M, then the same on the
+  // columns of R^T (length K), U Sigma = M Y Sigma^-1 (see below).  Otherwise: the SVD is taken
+  // of W = R_A^T (m x p, p = min(m, K)) where M^T = Q_A R_A (Householder): M = W Q_A^T with Q_A
+  // orthonormal, so W has the singular values and left singular vectors of M, fewer columns and
+  // a triangular (preconditioned) start for the one-sided Jacobi (CTA version).
   double* Bt = sm_rest;             // KC x KC (ld RM); later W = R_A^T (m x p, ld RM)
   double* Mm = Bt + RM * KC;        // M^T (K x m, ld RM); later Q (m x r, ld RM)
   double* sig = Mm + RM * KC;       // KC
@@ -283,7 +283,7 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
   long long c1;
   int p, sweeps;
   double* W = Bt;
-  if (K <= 32 && (m <= 16 || (m <= 32 && K > 16))) {
+  if (K <= 32 && m <= 16) {
     // M = V B~^T (m x K) in Mm; one-sided Jacobi on M in registers of one warp (lane j owns
     // column j), W = M J = [sigma_j u_j] into Bt (free after the product)
     la::cta_gemm(Mm, RM, V, ldv, false, Bt, RM, true, m, K, K, false);
@@ -292,7 +292,7 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
     if (m <= 16) sweeps = la::warp_jacobi<16, false>(Mm, RM, m, K, W, RM, sig, order, scr);
     else sweeps = la::warp_jacobi<32, false>(Mm, RM, m, K, W, RM, sig, order, scr);
     p = K;
-  } else if (K <= 16) {
+  } else if (K <= 32) {
     // M = V B~^T (m x K) in Mm; R of M = Q R (Householder, in Bt[:, 0:32)); one-sided Jacobi on
     // the columns of R^T (K x p, p = min(m, K)) in registers of one warp: R^T J = Y with columns
     // y_j = sigma_j v_j (v_j: right singular vectors of R and M), so M y_j / sigma_j = sigma_j u_j
@@ -313,7 +313,8 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
     __syncthreads();
     c1 = clock64();
     if (K <= 8) sweeps = la::warp_jacobi<8, false>(W, RM, K, pr, Y, RM, sig, order, scr);
-    else sweeps = la::warp_jacobi<16, false>(W, RM, K, pr, Y, RM, sig, order, scr);
+    else if (K <= 16) sweeps = la::warp_jacobi<16, false>(W, RM, K, pr, Y, RM, sig, order, scr);
+    else sweeps = la::warp_jacobi<32, false>(W, RM, K, pr, Y, RM, sig, order, scr);
     for (int e = threadIdx.x; e < m * pr; e += NT) {
       const int i = e % m, j = e / m;
       double acc = 0.0;
