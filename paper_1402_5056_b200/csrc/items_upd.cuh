@@ -265,9 +265,9 @@ __device__ void it_upd_weights_level(const MatDev& M, UpdArgs a_, int bA, int nA
 // Given V (m x K, ldv) in shared memory and B~_t, compute M = V B~^T, its SVD, the rank, Q and R_t.
 __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, int t, double* V, int ldv, int m,
                          int K, double* sm_rest, int kid, double extra_flops) {
-  // U4: left singular vectors / values of M = V B~^T (m x K).  m <= 16, K <= 32: one-sided
-  // Jacobi on M in registers of one warp.  K <= 32: Householder R of M, then the same on the
-  // columns of R^T (length K), U Sigma = M Y Sigma^-1 (see below).  Otherwise: the SVD is taken
+  // U4: left singular vectors / values of M = V B~^T (m x K).  K <= m <= 16: one-sided Jacobi
+  // on M in registers of one warp.  K <= 32: Householder R of M, then the same on the
+  // min(m, K) columns of R^T (length K), U Sigma = M Y Sigma^-1 (see below).  Otherwise: the SVD is taken
   // of W = R_A^T (m x p, p = min(m, K)) where M^T = Q_A R_A (Householder): M = W Q_A^T with Q_A
   // orthonormal, so W has the singular values and left singular vectors of M, fewer columns and
   // a triangular (preconditioned) start for the one-sided Jacobi (CTA version).
@@ -283,7 +283,7 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
   long long c1;
   int p, sweeps;
   double* W = Bt;
-  if (K <= 32 && m <= 16) {
+  if (K <= m && m <= 16) {  // K columns of length m <= 16 (no QR)
     // M = V B~^T (m x K) in Mm; one-sided Jacobi on M in registers of one warp (lane j owns
     // column j), W = M J = [sigma_j u_j] into Bt (free after the product)
     la::cta_gemm(Mm, RM, V, ldv, false, Bt, RM, true, m, K, K, false);
