@@ -153,11 +153,12 @@ static_assert(sizeof(PMisc) <= OP_PAYLOAD, "payload");
 constexpr int EXEC_MATS = 3;
 
 // ---- host side recording ---------------------------------------------------------------------
+size_t default_flush_at();  // 16384 ops; H2_EXEC_FLUSH overrides (tests: frequent chunk boundaries)
 struct ExecCtx {
   std::vector<OpRec> ops;
   const MatDev* mats[EXEC_MATS] = {nullptr, nullptr, nullptr};
   cudaStream_t st = 0;
-  size_t flush_at = 16384;  // ops are run in chunks while the host keeps recording
+  size_t flush_at = default_flush_at();  // ops are run in chunks while the host keeps recording
   int mat_index(const MatDev& M);
   void maybe_flush();
   int hold = 0;             // > 0 while a skip region is open (no flush inside it)

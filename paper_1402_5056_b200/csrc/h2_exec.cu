@@ -333,6 +333,11 @@ void ExecCtx::maybe_flush() {
   if (e != cudaSuccess) throw std::runtime_error(std::string("h2 executor: ") + cudaGetErrorString(e));
 }
 
+size_t default_flush_at() {
+  static const size_t v = getenv("H2_EXEC_FLUSH") ? std::max(1, atoi(getenv("H2_EXEC_FLUSH"))) : 16384;
+  return v;
+}
+
 ExecCtx* exec_ctx() { return g_ctx; }
 int exec_big_items() { return g_big; }
 
@@ -340,8 +345,8 @@ size_t ExecCtx::begin_skip(const int* k) {
   PMisc q{};
   q.ip = const_cast<int*>(k);
   q.cols = 0;
+  ++hold;  // before emit: a flush triggered by this very op would clear the list it indexes
   emit(OP_SKIPZ, 1, nullptr, q);
-  ++hold;
   return ops.size() - 1;
 }
 
@@ -366,6 +371,11 @@ void exec_begin(ExecCtx* ctx, cudaStream_t st) {
 cudaError_t exec_flush() {
   ExecCtx* c = g_ctx;
   if (!c || c->ops.empty()) return cudaSuccess;
+  static const bool dry = getenv("H2_EXEC_DRYRUN") != nullptr;  // tools: time the host recording alone
+  if (dry) {
+    c->ops.clear();
+    return cudaSuccess;
+  }
   cudaError_t e = init_exec();
   if (e) return e;
   const size_t n = c->ops.size();

@@ -10,7 +10,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(_HERE, "libh2b200.so")
+_LIBPATH = os.path.join(_HERE, os.environ.get("H2_LIB_NAME", "libh2b200.so"))  # override: sanitizer builds (tools)
 
 # every symbol include/h2.h declares (checked by tests/test_abi.py)
 EXPORTED_SYMBOLS = [

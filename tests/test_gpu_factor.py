@@ -147,3 +147,43 @@ def test_cholesky_breakdown_reported():
     with pytest.raises(P.H2Error) as e:
         P.h2_check_device_flags(Z)
     assert e.value.status == "H2_ERR_BREAKDOWN"
+
+
+_FLUSH_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1402_5056_b200 as P
+from inputs import config
+c = config("C2", N=48)
+t = P.h2_cluster_tree(c["points"], c["leaf"])
+bt = P.h2_block_tree(t, t, c["eta"])
+Z = P.h2_from_sparse(bt, c["A"], lower=True, rank_cap=32, update_cap=32)
+P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(1e-4))
+kr, kc = P.h2_ranks(Z)
+x = torch.from_numpy(np.random.default_rng(5).standard_normal(c["n"])).cuda()
+y = P.h2_matvec(Z, x).cpu().numpy()
+np.savez(sys.argv[2], kr=kr, kc=kc, y=y, st=np.array(list(P.h2_stats(Z).values())))
+"""
+
+
+@pytest.mark.parametrize("flush", [None, 1, 7, 61])
+def test_factor_invariant_to_op_chunking(tmp_path, flush):
+    """The recorded op list is run in chunks while the host keeps recording (exec.h); a chunk
+    boundary anywhere (inside a skip region of a zero-rank update included) must not change the
+    result: bit-identical ranks, counts and operator to the default chunking."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for f in (None, flush):
+        env = dict(os.environ)
+        env.pop("H2_EXEC_FLUSH", None)
+        if f is not None:
+            env["H2_EXEC_FLUSH"] = str(f)
+        p = tmp_path / f"r_{f}.npz"
+        subprocess.run([sys.executable, "-c", _FLUSH_SCRIPT, root, str(p)], env=env, check=True, timeout=600)
+        out[f] = np.load(p)
+    a, b = out[None], out[flush]
+    for k in ("kr", "kc", "st", "y"):
+        np.testing.assert_array_equal(a[k], b[k])
