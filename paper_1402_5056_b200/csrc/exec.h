@@ -63,6 +63,7 @@ enum OpCode : int32_t {
   OP_ZERO,
   OP_DD,
   OP_NZTILE,
+  OP_C2CORE,  // Case 2, both factors admissible: [G =] W^T V, C = S^X G S^Y, choose (one CTA)
   OP_SKIPZ,  // all CTAs: if *ip == 0 skip the next `count` ops (a zero-rank local update)
   OP_COUNT
 };
@@ -136,11 +137,24 @@ struct PDD {  // dense x dense Case-2 factors
   double rel;
 };
 
+struct PC2 {  // fused Case-2 core (items_arith.cuh it_c2core)
+  const double* W;   // W^X_s (ms x kxs, ld ms) or nullptr: G given
+  const double* V;   // V^Y_s (ms x kys, ld ms)
+  const double* G;   // G (ld KC) when W == nullptr
+  const double* Sx;
+  const double* Sy;
+  double* Ca;
+  double* Cb;
+  const int* kd[4];  // kxt, kxs, kys, kyr
+  int* kout;
+  int ms, ldsx, ldsy, tx, ty, ldo;
+};
+
 constexpr int OP_PAYLOAD = 176;
 struct alignas(16) OpRec {
   int32_t code;
   int32_t nitems;
-  int32_t barrier;
+  int32_t barrier;  // bit 0: cluster barrier after this op; bit 1: never elide it; bits 8-15: CTA of item 0
   int32_t mat;  // index of the matrix descriptor (0..2) the op uses
   unsigned char p[OP_PAYLOAD];
 };
@@ -149,6 +163,7 @@ static_assert(sizeof(PGemm) <= OP_PAYLOAD, "payload");
 static_assert(sizeof(PHm) <= OP_PAYLOAD, "payload");
 static_assert(sizeof(PTemp) <= OP_PAYLOAD, "payload");
 static_assert(sizeof(PMisc) <= OP_PAYLOAD, "payload");
+static_assert(sizeof(PC2) <= OP_PAYLOAD, "payload");
 
 constexpr int EXEC_MATS = 3;
 
@@ -162,24 +177,45 @@ struct ExecCtx {
   int mat_index(const MatDev& M);
   void maybe_flush();
   int hold = 0;             // > 0 while a skip region is open (no flush inside it)
+  int group = 0;             // > 0 inside an independence group (group_begin / group_end)
+  int group_off = 0;         // CTA of the next grouped op's item 0
   template <class P>
   void emit(int code, int nitems, const MatDev* M, const P& payload, bool barrier = true) {
     if (nitems <= 0) return;
-    // two consecutive single-item ops both run on CTA 0 of the cluster, in order: the block
-    // barrier after each item orders them, the cluster barrier between them is not needed
-    // (a skip op reads its flag on every CTA: the barrier before it stays)
-    if (nitems == 1 && code != OP_SKIPZ && !ops.empty() && ops.back().nitems == 1 &&
-        ops.back().code != OP_SKIPZ)
-      ops.back().barrier = 0;
     OpRec r;
     r.code = code;
     r.nitems = nitems;
-    r.barrier = barrier ? 1 : 0;
+    if (group > 0) {
+      // independent ops of a group: no barrier between them, items spread over the cluster's CTAs
+      // (item i of this op runs on CTA (group_off + i) mod CL); group_end places one barrier
+      r.barrier = (group_off & 0xff) << 8;
+      group_off += nitems;
+    } else {
+      // two consecutive single-item ops both run on CTA 0 of the cluster, in order: the block
+      // barrier after each item orders them, the cluster barrier between them is not needed
+      // (a skip op reads its flag on every CTA: the barrier before it stays; a group's closing
+      // barrier orders ops on other CTAs and stays too)
+      if (nitems == 1 && code != OP_SKIPZ && !ops.empty() && ops.back().nitems == 1 &&
+          ops.back().code != OP_SKIPZ && (ops.back().barrier & ~1) == 0)
+        ops.back().barrier = 0;
+      r.barrier = barrier ? 1 : 0;
+    }
     r.mat = M ? mat_index(*M) : 0;
     static_assert(sizeof(P) <= OP_PAYLOAD, "payload");
     std::memcpy(r.p, &payload, sizeof(P));
     ops.push_back(r);
     if (ops.size() >= flush_at && hold == 0) maybe_flush();
+  }
+  // independence group: the ops recorded between group_begin and group_end neither read what
+  // another op of the group writes nor write what another reads or writes (the caller's promise);
+  // they run without cluster barriers between them, on different CTAs where possible.
+  // A chunk flush inside a group is a kernel boundary (a stronger ordering): still correct.
+  void group_begin() {
+    ++group;
+    group_off = 0;
+  }
+  void group_end() {
+    if (--group == 0 && !ops.empty()) ops.back().barrier |= 3;
   }
   // skip region: the ops recorded between begin_skip and end_skip are skipped on the device when
   // *k == 0 (they must all run inside the cluster executor: end_skip cancels the skip otherwise)

@@ -41,6 +41,12 @@ void stack_cols(double* dst, int ldd, int rows, const double* T, int ldt, const 
                 int row_off, int rows_new, Dim knew, int colcap, cudaStream_t st);
 void choose_case2(const double* Cm, int ldc, const int* k1, const int* k2, double* Ca, double* Cb, int ldo, int* kout,
                   cudaStream_t st);
+// Case 2, both factors admissible: C = S^X_or (W^T V) S^Y_or and the factored side (choose_case2),
+// one op; W, V (ms x k, ld ms; ms <= case2_core_max_ms()) or G (ld KCAP_MAX) when W == nullptr
+void case2_core(const double* W, const double* V, int ms, const double* G, const double* Sx, int ldsx, bool tx,
+                const double* Sy, int ldsy, bool ty, const int* kxt, const int* kxs, const int* kys, const int* kyr,
+                double* Ca, double* Cb, int ldo, int* kout, cudaStream_t st);
+int case2_core_max_ms();
 void identity(double* I, int ld, int m, cudaStream_t st);
 void transpose_tile(double* dst, int ldd, const double* src, int lds, int rows, int cols, cudaStream_t st);
 void add_int(int* p, Dim a, Dim b, cudaStream_t st);

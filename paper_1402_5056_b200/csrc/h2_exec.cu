@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <chrono>
 #include <cstring>
@@ -35,6 +36,7 @@ constexpr int PR = 192;
 constexpr int RM = KC + 1;
 constexpr size_t SM_EXEC = (size_t)(3 * RM * KC + KC) * 8 + (KC + 8) * 4;  // max over items (SVD items)
 static_assert(SM_EXEC >= (size_t)((PR + 1) * KC + KC + 8) * 8, "smem");
+static_assert(SM_EXEC >= (size_t)(3 * (RCAP_MAX + 1) + 2 * ar::C2_MS) * RCAP_MAX * 8, "smem (it_c2core)");
 static_assert(SM_EXEC >= (size_t)(3 * (KC + 1) * KC + KC) * 8 + (KC + 8) * 4 && SM_EXEC >= (size_t)((2 * KC + 1) * KC + KC + 8) * 8, "smem");
 
 struct ExecParams {
@@ -50,7 +52,7 @@ __constant__ int c_op_kid[OP_COUNT] = {
     K_AR_EXPAND, K_AR_GEMM, K_AR_GEMM, K_AR_GEMM, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL,
     K_AR_TILE, K_AR_TILE, K_AR_TILE, K_AR_TSQR, K_AR_TEMP, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC,
     K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_TEMP, K_AR_MISC,
-    K_AR_MISC};
+    K_AR_GEMM, K_AR_MISC};
 
 __device__ __forceinline__ const DevSide& side_of(const MatDev& M, int s) { return s ? M.col : M.row; }
 
@@ -194,6 +196,9 @@ __device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, do
       ar::it_dd_compress(P.mats[q.mx], P.mats[q.my], q.slotx, q.transx, q.sloty, q.transy, q.mt, q.ms, q.mr, q.A,
                          q.lda, q.B, q.ldb, q.kout, q.rel, it, n, sm);
     } break;
+    case OP_C2CORE: {
+      ar::it_c2core(*reinterpret_cast<const PC2*>(op.p), sm);
+    } break;
     case OP_NZTILE: {  // *ip = 0 if the nearfield tile is exactly zero (reading own-6)
       const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
       const double* T = q.src;
@@ -238,13 +243,14 @@ __global__ void __launch_bounds__(NT, 1) k_exec_cluster(const __grid_constant__ 
     if (threadIdx.x < 2 && o + 1 < P.end)
       asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(&P.ops[o + 1]) + 128 * threadIdx.x));
     unsigned long long t0 = timing ? gtimer() : 0;
-    for (int it = rank; it < n; it += nb) {
+    const int off = (op.barrier >> 8) & 0xff;  // item i runs on CTA (off + i) mod nb
+    for (int it = ((rank - off) % nb + nb) % nb; it < n; it += nb) {
       dispatch(P, op, it, n, sm);
       __syncthreads();
     }
     // barrier.cluster.arrive (release) / wait (acquire) at cluster scope: this op's global-memory
     // results are visible to every CTA of the cluster afterwards
-    if (op.barrier) cl.sync();
+    if (op.barrier & 1) cl.sync();
     if (timing) {
       const int kid = c_op_kid[op.code];
       const double dt = (double)(gtimer() - t0);
@@ -373,6 +379,14 @@ cudaError_t exec_flush() {
   if (!c || c->ops.empty()) return cudaSuccess;
   static const bool dry = getenv("H2_EXEC_DRYRUN") != nullptr;  // tools: time the host recording alone
   if (dry) {
+    static FILE* tf = getenv("H2_EXEC_TRACE") ? fopen(getenv("H2_EXEC_TRACE"), "wb") : nullptr;
+    if (tf) {  // (code, nitems, barrier) per op: the op mix of a recording (tools)
+      for (const OpRec& r : c->ops) {
+        const int32_t rec[3] = {r.code, r.nitems, r.barrier};
+        fwrite(rec, sizeof(rec), 1, tf);
+      }
+      fflush(tf);
+    }
     c->ops.clear();
     return cudaSuccess;
   }
@@ -747,6 +761,31 @@ void choose_case2(const double* Cm, int ldc, const int* k1, const int* k2, doubl
   q.ip = kout;
   ctx_or_throw()->emit(OP_CHOOSE, 1, nullptr, q);
 }
+void case2_core(const double* W, const double* V, int ms, const double* G, const double* Sx, int ldsx, bool tx,
+                const double* Sy, int ldsy, bool ty, const int* kxt, const int* kxs, const int* kys, const int* kyr,
+                double* Ca, double* Cb, int ldo, int* kout, cudaStream_t) {
+  PC2 q;
+  q.W = W;
+  q.V = V;
+  q.G = G;
+  q.Sx = Sx;
+  q.Sy = Sy;
+  q.Ca = Ca;
+  q.Cb = Cb;
+  q.kd[0] = kxt;
+  q.kd[1] = kxs;
+  q.kd[2] = kys;
+  q.kd[3] = kyr;
+  q.kout = kout;
+  q.ms = ms;
+  q.ldsx = ldsx;
+  q.ldsy = ldsy;
+  q.tx = tx ? 1 : 0;
+  q.ty = ty ? 1 : 0;
+  q.ldo = ldo;
+  ctx_or_throw()->emit(OP_C2CORE, 1, nullptr, q);
+}
+int case2_core_max_ms() { return ar::C2_MS; }
 void identity(double* I, int ld, int m, cudaStream_t) {
   PMisc q = misc();
   q.dst = I;

@@ -67,6 +67,14 @@ struct Mark {
   }
 };
 
+// independence group of recorded ops (ExecCtx::group_begin): the caller guarantees that the ops
+// recorded inside neither read nor write what another op of the group writes
+struct Group {
+  ExecCtx* c;
+  Group() : c(exec_ctx()) { c->group_begin(); }
+  ~Group() { c->group_end(); }
+};
+
 // an operand op(Z) of the product
 struct HOp {
   h2_mat_* Z;
@@ -149,7 +157,6 @@ struct Driver {
     double* A2 = ar.alloc((size_t)Tm.ma * K2);
     double* B2 = ar.alloc((size_t)Tm.mb * K2);
     int* K = ar.ialloc();
-    add_int(K, dimp(Tm.k), dimp(kdev), st);
     // alpha is folded into A: stack [T.A, alpha A]
     double* Aa = const_cast<double*>(A);
     if (alpha != 1.0) {
@@ -158,17 +165,29 @@ struct Driver {
            kcap, alpha, 0.0, st);  // A * (alpha I)
       lda = size(a);
     }
-    stack_cols(A2, Tm.ma, Tm.ma, Tm.A, Tm.ma, Tm.k, Aa, lda, T->lo[a] - T->lo[Tm.ra], size(a), dimp(kdev), K2, st);
-    stack_cols(B2, Tm.mb, Tm.mb, Tm.B, Tm.mb, Tm.k, B, ldb, T->lo[b] - T->lo[Tm.rb], size(b), dimp(kdev), K2, st);
+    {
+      Group g;  // K = k_T + k_new and the two stacks read the old k_T only
+      add_int(K, dimp(Tm.k), dimp(kdev), st);
+      stack_cols(A2, Tm.ma, Tm.ma, Tm.A, Tm.ma, Tm.k, Aa, lda, T->lo[a] - T->lo[Tm.ra], size(a), dimp(kdev), K2, st);
+      stack_cols(B2, Tm.mb, Tm.mb, Tm.B, Tm.mb, Tm.k, B, ldb, T->lo[b] - T->lo[Tm.rb], size(b), dimp(kdev), K2, st);
+    }
     double* Ra = ar.alloc(KC * KC);
     double* Rb = ar.alloc(KC * KC);
-    tsqr_r(A2, Tm.ma, Tm.ma, dimp(K), Ra, KC, st);
-    tsqr_r(B2, Tm.mb, Tm.mb, dimp(K), Rb, KC, st);
+    {
+      Group g;
+      tsqr_r(A2, Tm.ma, Tm.ma, dimp(K), Ra, KC, st);
+      tsqr_r(B2, Tm.mb, Tm.mb, dimp(K), Rb, KC, st);
+    }
     double* Ma = ar.alloc(KC * KC);
     double* Mb = ar.alloc(KC * KC);
     temp_core(Ra, Rb, KC, dimp(K), Ma, Mb, KC, Tm.k, rel, abs_tol, max_rank, rcap, Z->d.flags, kdev, st);
-    gemm(Tm.A, Tm.ma, A2, Tm.ma, false, Ma, KC, false, dimc(Tm.ma), dimp(Tm.k), dimp(K), Tm.ma, rcap, K2, 1.0, 0.0, st);
-    gemm(Tm.B, Tm.mb, B2, Tm.mb, false, Mb, KC, false, dimc(Tm.mb), dimp(Tm.k), dimp(K), Tm.mb, rcap, K2, 1.0, 0.0, st);
+    {
+      Group g;
+      gemm(Tm.A, Tm.ma, A2, Tm.ma, false, Ma, KC, false, dimc(Tm.ma), dimp(Tm.k), dimp(K), Tm.ma, rcap, K2, 1.0, 0.0,
+           st);
+      gemm(Tm.B, Tm.mb, B2, Tm.mb, false, Mb, KC, false, dimc(Tm.mb), dimp(Tm.k), dimp(K), Tm.mb, rcap, K2, 1.0, 0.0,
+           st);
+    }
   }
 
   // add alpha A B^T at rows t, cols r of the target (temporary or the H^2 block (t, r) of Z)
@@ -214,33 +233,37 @@ struct Driver {
       double* Wy = ar.alloc((size_t)mr * rcap);
       double* Wxs = ar.alloc((size_t)ms * rcap);
       double* Vys = ar.alloc((size_t)ms * rcap);
-      expand_basis(X.Z->d, Xr, t, Vx, mt, st);
-      expand_basis(Y.Z->d, Yc, r, Wy, mr, st);
-      expand_basis(X.Z->d, Xc, s, Wxs, ms, st);
-      expand_basis(Y.Z->d, Yr, s, Vys, ms, st);
-      double* G = ar.alloc(KC * KC);
-      double* T1 = ar.alloc(KC * KC);
-      double* Cm = ar.alloc(KC * KC);
-      // G = W^X_s^T V^Y_s
-      gemm(G, KC, Wxs, ms, true, Vys, ms, false, dimp(Xc.rank + s), dimp(Yr.rank + s), dimc(ms), rcap, rcap, ms, 1.0,
-           0.0, st);
-      // T1 = S^X G  (S^X oriented k^X_t x k^X_s)
+      {
+        Group g;  // four independent basis expansions
+        expand_basis(X.Z->d, Xr, t, Vx, mt, st);
+        expand_basis(Y.Z->d, Yc, r, Wy, mr, st);
+        expand_basis(X.Z->d, Xc, s, Wxs, ms, st);
+        expand_basis(Y.Z->d, Yr, s, Vys, ms, st);
+      }
       const double* Sx = Sptr(X.Z, bx);
       const double* Sy = Sptr(Y.Z, by);
-      const int rc = X.Z->d.rcap;
-      gemm(T1, KC, Sx, rc, X.trans, G, KC, false, dimp(Xr.rank + t), dimp(Yr.rank + s), dimp(Xc.rank + s), rcap, rcap,
-           rcap, 1.0, 0.0, st);
-      gemm(Cm, KC, T1, KC, false, Sy, Y.Z->d.rcap, Y.trans, dimp(Xr.rank + t), dimp(Yc.rank + r), dimp(Yr.rank + s),
-           rcap, rcap, rcap, 1.0, 0.0, st);
       double* Ca = ar.alloc(KC * KC);
       double* Cb = ar.alloc(KC * KC);
-      choose_case2(Cm, KC, Xr.rank + t, Yc.rank + r, Ca, Cb, KC, *kdev, st);
+      // C = S^X (W^X_s^T V^Y_s) S^Y (S^X oriented k^X_t x k^X_s) and the factored side, one op
+      if (ms <= case2_core_max_ms()) {
+        case2_core(Wxs, Vys, ms, nullptr, Sx, X.Z->d.rcap, X.trans, Sy, Y.Z->d.rcap, Y.trans, Xr.rank + t,
+                   Xc.rank + s, Yr.rank + s, Yc.rank + r, Ca, Cb, KC, *kdev, st);
+      } else {
+        double* G = ar.alloc(KC * KC);  // G = W^X_s^T V^Y_s (long inner dimension: its own op)
+        gemm(G, KC, Wxs, ms, true, Vys, ms, false, dimp(Xc.rank + s), dimp(Yr.rank + s), dimc(ms), rcap, rcap, ms,
+             1.0, 0.0, st);
+        case2_core(nullptr, nullptr, ms, G, Sx, X.Z->d.rcap, X.trans, Sy, Y.Z->d.rcap, Y.trans, Xr.rank + t,
+                   Xc.rank + s, Yr.rank + s, Yc.rank + r, Ca, Cb, KC, *kdev, st);
+      }
       *A = ar.alloc((size_t)mt * rcap);
       *B = ar.alloc((size_t)mr * rcap);
-      gemm(*A, mt, Vx, mt, false, Ca, KC, false, dimc(mt), dimp(*kdev), dimp(Xr.rank + t), mt, rcap, rcap, 1.0, 0.0,
-           st);
-      gemm(*B, mr, Wy, mr, false, Cb, KC, false, dimc(mr), dimp(*kdev), dimp(Yc.rank + r), mr, rcap, rcap, 1.0, 0.0,
-           st);
+      {
+        Group g;
+        gemm(*A, mt, Vx, mt, false, Ca, KC, false, dimc(mt), dimp(*kdev), dimp(Xr.rank + t), mt, rcap, rcap, 1.0, 0.0,
+             st);
+        gemm(*B, mr, Wy, mr, false, Cb, KC, false, dimc(mr), dimp(*kdev), dimp(Yc.rank + r), mr, rcap, rcap, 1.0, 0.0,
+             st);
+      }
       *lda = mt;
       *ldb = mr;
       return rcap;
@@ -251,9 +274,12 @@ struct Driver {
       const DevSide& Xr = X.rows();
       const DevSide& Xc = X.cols();
       *A = ar.alloc((size_t)mt * rcap);
-      expand_basis(X.Z->d, Xr, t, *A, mt, st);
       double* Wxs = ar.alloc((size_t)ms * rcap);
-      expand_basis(X.Z->d, Xc, s, Wxs, ms, st);
+      {
+        Group g;
+        expand_basis(X.Z->d, Xr, t, *A, mt, st);
+        expand_basis(X.Z->d, Xc, s, Wxs, ms, st);
+      }
       double* Dm = ar.alloc((size_t)ms * rcap);
       // D = W^X_s S^X_or^T  (ms x k^X_t)
       gemm(Dm, ms, Wxs, ms, false, Sptr(X.Z, bx), X.Z->d.rcap, !X.trans, dimc(ms), dimp(Xr.rank + t),
@@ -274,15 +300,18 @@ struct Driver {
       const DevSide& Yr = Y.rows();
       const DevSide& Yc = Y.cols();
       double* Vys = ar.alloc((size_t)ms * rcap);
-      expand_basis(Y.Z->d, Yr, s, Vys, ms, st);
+      *B = ar.alloc((size_t)mr * rcap);
+      {
+        Group g;
+        expand_basis(Y.Z->d, Yr, s, Vys, ms, st);
+        expand_basis(Y.Z->d, Yc, r, *B, mr, st);
+      }
       double* Dm = ar.alloc((size_t)ms * rcap);
       // D = V^Y_s S^Y_or (ms x k^Y_r)
       gemm(Dm, ms, Vys, ms, false, Sptr(Y.Z, by), Y.Z->d.rcap, Y.trans, dimc(ms), dimp(Yc.rank + r),
            dimp(Yr.rank + s), ms, rcap, rcap, 1.0, 0.0, st);
       *A = ar.alloc((size_t)mt * rcap);
       hmul_dense(X.Z->d, X.trans, t, s, 0, Dm, ms, dimp(Yc.rank + r), rcap, *A, mt, 1.0, 0.0, st);
-      *B = ar.alloc((size_t)mr * rcap);
-      expand_basis(Y.Z->d, Yc, r, *B, mr, st);
       set_int(*kdev, dimp(Yc.rank + r), st);
       if (kx == INADM && X.Z->blk2inad[bx] >= 0)
         zero_rank_if_zero_tile(X.Z->d, X.Z->blk2inad[bx], mt * ms, *kdev, st);  // reading own-6
@@ -367,10 +396,13 @@ struct Driver {
               Mark mk2(ar);
               double* A = ar.alloc((size_t)size(t) * rcap);
               double* B = ar.alloc((size_t)size(r) * rcap);
-              stack_cols(A, size(t), size(t), nullptr, 0, nullptr, tm.A, tm.ma, T->lo[tm.ra] - T->lo[t], tm.ma,
-                         dimp(tm.k), rcap, st);
-              stack_cols(B, size(r), size(r), nullptr, 0, nullptr, tm.B, tm.mb, T->lo[tm.rb] - T->lo[r], tm.mb,
-                         dimp(tm.k), rcap, st);
+              {
+                Group g;
+                stack_cols(A, size(t), size(t), nullptr, 0, nullptr, tm.A, tm.ma, T->lo[tm.ra] - T->lo[t], tm.ma,
+                           dimp(tm.k), rcap, st);
+                stack_cols(B, size(r), size(r), nullptr, 0, nullptr, tm.B, tm.mb, T->lo[tm.rb] - T->lo[r], tm.mb,
+                           dimp(tm.k), rcap, st);
+              }
               add(nullptr, t, r, A, size(t), B, size(r), tm.k, rcap, 1.0);
             }
           return;
@@ -454,13 +486,16 @@ struct Driver {
       Mark mk(ar);
       const int mt = size(t), ms = size(s);
       int* kdev = ar.ialloc();
-      rank_if(kdev, Z->d.row.rank + t, Z->d.col.rank + s, st);  // rank 0 block -> nothing (oracle: S.size == 0)
       double* Zs = ar.alloc((size_t)ms * rcap);
-      expand_basis(Z->d, Z->d.col, s, Zs, ms, st);
+      double* Vt = ar.alloc((size_t)mt * rcap);
+      {
+        Group g;  // the solves below touch Zs only
+        rank_if(kdev, Z->d.row.rank + t, Z->d.col.rank + s, st);  // rank 0 block -> nothing (oracle: S.size == 0)
+        expand_basis(Z->d, Z->d.col, s, Zs, ms, st);
+        expand_basis(Z->d, Z->d.row, t, Vt, mt, st);
+      }
       if (chol) lsolve(s, Zs, ms, dimp(Z->d.col.rank + s), rcap, false);
       else utsolve(s, Zs, ms, dimp(Z->d.col.rank + s), rcap);
-      double* Vt = ar.alloc((size_t)mt * rcap);
-      expand_basis(Z->d, Z->d.row, t, Vt, mt, st);
       double* U = ar.alloc((size_t)mt * rcap);
       gemm(U, mt, Vt, mt, false, Sptr(Z, b), Z->d.rcap, false, dimc(mt), dimp(Z->d.col.rank + s),
            dimp(Z->d.row.rank + t), mt, rcap, rcap, 1.0, 0.0, st);
@@ -495,15 +530,18 @@ struct Driver {
       Mark mk(ar);
       const int mt = size(t), ms = size(s);
       int* kdev = ar.ialloc();
-      rank_if(kdev, Z->d.row.rank + t, Z->d.col.rank + s, st);
       double* Vt = ar.alloc((size_t)mt * rcap);
-      expand_basis(Z->d, Z->d.row, t, Vt, mt, st);
+      double* Ws = ar.alloc((size_t)ms * rcap);
+      {
+        Group g;  // the solve below touches Vt only
+        rank_if(kdev, Z->d.row.rank + t, Z->d.col.rank + s, st);
+        expand_basis(Z->d, Z->d.row, t, Vt, mt, st);
+        expand_basis(Z->d, Z->d.col, s, Ws, ms, st);
+      }
       lsolve(t, Vt, mt, dimp(Z->d.row.rank + t), rcap, true);
       double* U = ar.alloc((size_t)mt * rcap);
       gemm(U, mt, Vt, mt, false, Sptr(Z, b), Z->d.rcap, false, dimc(mt), dimp(Z->d.col.rank + s),
            dimp(Z->d.row.rank + t), mt, rcap, rcap, 1.0, 0.0, st);
-      double* Ws = ar.alloc((size_t)ms * rcap);
-      expand_basis(Z->d, Z->d.col, s, Ws, ms, st);
       zero_fill(Sptr(Z, b), (size_t)Z->d.rcap * Z->d.rcap, st);
       update(t, s, U, mt, Ws, ms, kdev, 1.0);
       return;

@@ -567,6 +567,63 @@ __device__ void it_choose(const double* Cm, int ldc, const int* k1p, const int* 
   }
   if (threadIdx.x == 0) *kout = kk;
 }
+// Case 2 with both factors admissible (reading R23), fused into one CTA (was up to
+// three GEMM ops and a choose op, each behind a cluster barrier): G = W^X_s^T V^Y_s (when the
+// bases are passed; ms <= C2_MS, staged in shared memory), T1 = S^X_or G, C = T1 S^Y_or, then the
+// factored side as it_choose.  Every sum runs over the inner index in increasing order, exactly
+// as it_gemm, so the result is bit-identical to the unfused sequence.
+constexpr int C2_MS = 64;
+__device__ void it_c2core(const PC2& q, double* sm) {
+  constexpr int RC = RCAP_MAX, LD = RC + 1;  // every rank here is a stored rank (<= rank_cap)
+  const int kxt = *q.kd[0], kxs = *q.kd[1], kys = *q.kd[2], kyr = *q.kd[3];
+  double* Gs = sm;              // kxs x kys (ld LD)
+  double* T1 = Gs + LD * RC;    // kxt x kys
+  double* Cm = T1 + LD * RC;    // kxt x kyr
+  double* Ws = Cm + LD * RC;    // ms x kxs (ld C2_MS)
+  double* Vs = Ws + C2_MS * RC; // ms x kys
+  const double* G = q.G;
+  int ldg = KC;
+  if (q.W) {
+    const int ms = q.ms;
+    for (int e = threadIdx.x; e < ms * kxs; e += NT) Ws[(e % ms) + (e / ms) * C2_MS] = q.W[(e % ms) + (size_t)(e / ms) * ms];
+    for (int e = threadIdx.x; e < ms * kys; e += NT) Vs[(e % ms) + (e / ms) * C2_MS] = q.V[(e % ms) + (size_t)(e / ms) * ms];
+    __syncthreads();
+    for (int e = threadIdx.x; e < kxs * kys; e += NT) {
+      const int i = e % kxs, j = e / kxs;
+      double acc = 0.0;
+      for (int r = 0; r < ms; ++r) acc += Ws[r + i * C2_MS] * Vs[r + j * C2_MS];
+      Gs[i + j * LD] = acc;
+    }
+    __syncthreads();
+    G = Gs;
+    ldg = LD;
+  }
+  for (int e = threadIdx.x; e < kxt * kys; e += NT) {
+    const int i = e % kxt, j = e / kxt;
+    double acc = 0.0;
+    for (int r = 0; r < kxs; ++r) acc += (q.tx ? q.Sx[r + (size_t)i * q.ldsx] : q.Sx[i + (size_t)r * q.ldsx]) * G[r + j * ldg];
+    T1[i + j * LD] = acc;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kxt * kyr; e += NT) {
+    const int i = e % kxt, j = e / kxt;
+    double acc = 0.0;
+    for (int r = 0; r < kys; ++r) acc += T1[i + r * LD] * (q.ty ? q.Sy[j + (size_t)r * q.ldsy] : q.Sy[r + (size_t)j * q.ldsy]);
+    Cm[i + j * LD] = acc;
+  }
+  __syncthreads();
+  const bool first = kxt <= kyr;
+  const int kk = first ? kxt : kyr;
+  for (int e = threadIdx.x; e < RC * RC; e += NT) {
+    const int i = e % RC, j = e / RC;
+    if (j < kk) {
+      if (i < kxt) q.Ca[i + j * q.ldo] = first ? (i == j ? 1.0 : 0.0) : Cm[i + j * LD];
+      if (i < kyr) q.Cb[i + j * q.ldo] = first ? Cm[j + i * LD] : (i == j ? 1.0 : 0.0);
+    }
+  }
+  if (threadIdx.x == 0) *q.kout = kk;
+}
+
 __device__ void it_identity(double* I, int ld, int m, int item_, int nitems_, double* smx_) {
   for (int e = threadIdx.x + item_ * blockDim.x; e < m * m; e += blockDim.x * nitems_)
     I[(e % m) + (e / m) * ld] = (e % m) == (e / m) ? 1.0 : 0.0;
