@@ -35,7 +35,10 @@ constexpr int KC = KCAP_MAX;
 constexpr int PR = 192;
 constexpr int RM = KC + 1;
 constexpr size_t SM_EXEC = (size_t)(3 * RM * KC + KC) * 8 + (KC + 8) * 4;  // max over items (SVD items)
-static_assert(SM_EXEC >= (size_t)((PR + 1) * KC + KC + 8) * 8, "smem");
+static_assert(SM_EXEC >= (size_t)((PR + 1) * KC + KC + 8) * 8 + (5 * 128 + PR) * 4, "smem (weights_cluster panel + block descriptors)");
+static_assert(SM_EXEC >= (size_t)((RCAP_MAX + 1) * RCAP_MAX + (PR + 1) * KC + KC + 8) * 8 + (5 * 128 + PR) * 4, "smem (weights path: B~ + weights_cluster)");
+static_assert(SM_EXEC >= (size_t)24000 * 8 + 9 * 128 * 4 + 16, "smem (couplings)");
+static_assert(SM_EXEC >= (size_t)(7 * (RCAP_MAX + 1) * RCAP_MAX + (2 * RCAP_MAX + 1) * RCAP_MAX + KC) * 8 + 5 * 64 * 4, "smem (rcache path)");
 static_assert(SM_EXEC >= (size_t)(3 * (RCAP_MAX + 1) + 2 * ar::C2_MS) * RCAP_MAX * 8, "smem (it_c2core)");
 static_assert(SM_EXEC >= (size_t)(3 * (KC + 1) * KC + KC) * 8 + (KC + 8) * 4 && SM_EXEC >= (size_t)((2 * KC + 1) * KC + KC + 8) * 8, "smem");
 
@@ -69,7 +72,7 @@ __device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, do
     } break;
     case OP_UPD_W_PATH: {
       const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
-      upd::it_upd_weights_path(M, q.a, it, n, sm);
+      upd::it_upd_weights_path(M, q.a, q.i[0], q.i[1], q.i[2], q.i[3], it, sm);
     } break;
     case OP_UPD_W_LEVEL: {
       const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
@@ -93,7 +96,7 @@ __device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, do
     } break;
     case OP_UPD_RCACHE: {
       const PUpd& q = *reinterpret_cast<const PUpd*>(op.p);
-      upd::it_upd_rcache_path(M, q.a, it, n, sm);
+      upd::it_upd_rcache_path(M, q.a, q.i[0], q.i[1], q.i[2], q.i[3], it, sm);
     } break;
     case OP_EXPAND: {
       const PExpand& q = *reinterpret_cast<const PExpand*>(op.p);
@@ -555,7 +558,7 @@ cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a_in, cudaStream_t st
     level_segment(C, a.s0, L, &bB, &nB);
     c->emit(OP_UPD_EXT_LEVEL, nA + nB, &M, pu(a, bA, nA, bB, nB));
   }
-  c->emit(OP_UPD_W_PATH, 2, &M, pu(a));  // U3: path root .. t0
+  c->emit(OP_UPD_W_PATH, 2, &M, pu(a, rl0, cl0, Lr, Lc));  // U3: path root .. t0
   for (int L = Lmin + 1; L <= Lmax; ++L) {  // U3: subtree top-down
     int bA = 0, nA = 0, bB = 0, nB = 0;
     if (L > Lr) level_segment(R, a.t0, L, &bA, &nA);
@@ -572,7 +575,7 @@ cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a_in, cudaStream_t st
   const int nA = R->tsize[a.t0], nB = C->tsize[a.s0];
   c->emit(OP_UPD_COUPLE, nA + nB, &M, pu(a, nA, nB));   // U5
   c->emit(OP_UPD_INSTALL, nA + nB, &M, pu(a, nA, nB));  // U6
-  c->emit(OP_UPD_RCACHE, 2, &M, pu(a));                 // R-factor caches on pred(t0), pred(s0)
+  c->emit(OP_UPD_RCACHE, 2, &M, pu(a, rl0, cl0, Lr, Lc));  // R-factor caches on pred(t0), pred(s0)
   if (skip) c->end_skip(skip_at, g_big);
   return ac.done();
 }

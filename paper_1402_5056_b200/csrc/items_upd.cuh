@@ -21,7 +21,8 @@ __device__ __forceinline__ bool inside(const DevSide& D, int t, int root) {
   return t >= root && t < root + D.tsize[root];
 }
 
-__device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm, int mode);
+__device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm, int mode,
+                                  const double* bp_sm = nullptr, int ldbp = 0);
 
 // ---- U0 + U1/U2 leaves + local weight stacks of the ancestors (all independent) ---------------
 __device__ void it_upd_ext_leaf(const MatDev& M, UpdArgs a_, int rl0, int nrl, int cl0, int ncl,
@@ -148,17 +149,31 @@ __device__ void it_upd_ext_level(const MatDev& M, UpdArgs a_, int bA, int nA, in
 // mode W_CHAIN: B~_t = R([C_t; B~_{t+} E_t^T])   -> bw[t]  (C_t from re[t])
 enum { W_FULL = 0, W_LOCAL = 1, W_CHAIN = 2 };
 
-__device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm, int mode) {
+__device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm, int mode,
+                                  const double* bp_sm, int ldbp) {
   const DevSide& A = rs ? M.row : M.col;
   const DevSide& B = rs ? M.col : M.row;
   const int a0 = rs ? a.t0 : a.s0, b0 = rs ? a.s0 : a.t0;
   const int k = a.k;
-  const bool in_t = inside(A, t, a0);
+  // independent structure loads first (one memory round trip instead of one per block)
   const int kt = A.rank[t];
+  const int p = A.parent[t];
+  const int asz = A.tsize[a0], bsz = B.tsize[b0];
+  const int qb = mode == W_CHAIN ? 0 : A.bptr[t], qe = mode == W_CHAIN ? 0 : A.bptr[t + 1];
+  const int kp = (p >= 0 && mode != W_LOCAL) ? A.rank[p] : 0;
+  const bool in_t = t >= a0 && t < a0 + asz;
   const int K = kt + (in_t ? k : 0);
   double* P = sm;                 // PR x KC panel
   double* diag = P + PRL * KC;
   double* red = diag + KC;
+  // block descriptors of one batch of the block row (shared memory, after the panel)
+  constexpr int NBD = 128;
+  int* d_slot = reinterpret_cast<int*>(red + 8);
+  int* d_s = d_slot + NBD;
+  int* d_ls = d_s + NBD;
+  int* d_rc = d_ls + NBD;
+  int* d_off = d_rc + NBD;
+  int* rowblk = d_off + NBD;      // PR: panel row -> descriptor
   int rows = 0;
   double fl = 0.0;
   auto flush = [&]() {
@@ -173,48 +188,79 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
     rows = K;
     __syncthreads();
   }
-  for (int q = A.bptr[t]; mode != W_CHAIN && q < A.bptr[t + 1]; ++q) {
-    const int slot = A.bidx[q];
-    const int s = rs ? M.adm_s[slot] : M.adm_t[slot];
-    const double* Sa = M.S + (size_t)slot * M.rcap * M.rcap;
-    const bool in_s = inside(B, s, b0);
-    const int ls = B.rank[s];
-    const int rc = in_s ? ls + k : ls;
-    if (rc == 0) continue;
-    if (rows + rc > PR) flush();
-    const double* RB = in_s ? B.re + (size_t)s * M.kcap * M.kcap : B.rc + (size_t)s * M.rcap * M.rcap;
-    const int ldR = in_s ? M.kcap : M.rcap;
-    for (int e = threadIdx.x; e < rc * K; e += NT) {
-      const int i = e % rc, c = e / rc;
-      double v = 0.0;
-      if (c < kt) {
-        // (R_B S~^T)(i,c) = sum_j R_B(i,j) S_or(c,j),   S_or = S (row side) or S^T (column side)
-        for (int j = i; j < ls; ++j) v += RB[i + j * ldR] * (rs ? Sa[c + j * M.rcap] : Sa[j + c * M.rcap]);
-      } else if (in_s) {
-        v = RB[i + (ls + c - kt) * ldR];  // identity block of S~ = diag(S, I)
-      }
-      P[rows + i + c * PRL] = v;
+  // local stack: R_{W,s} S~_b^T for the blocks b = (t, s) of row(t), in block order, flushed
+  // (QR -> its R-factor) before a block that does not fit the panel -- the same flush points and
+  // sums as one block at a time, but every block of a segment is filled in one parallel pass
+  for (int base = qb; base < qe; base += NBD) {
+    const int cnt = qe - base < NBD ? qe - base : NBD;
+    for (int j = threadIdx.x; j < cnt; j += NT) {
+      const int slot = A.bidx[base + j];
+      const int s = rs ? M.adm_s[slot] : M.adm_t[slot];
+      const bool in_s = s >= b0 && s < b0 + bsz;
+      const int ls = B.rank[s];
+      d_slot[j] = slot;
+      d_s[j] = s;
+      d_ls[j] = ls;
+      d_rc[j] = in_s ? ls + k : ls;  // k > 0: in_s <=> rc > ls
     }
-    fl += (double)rc * ls * kt;  // triangular R_B times S^T
-    rows += rc;
     __syncthreads();
+    int j = 0;
+    while (j < cnt) {
+      // the segment [j, je): blocks that fit after `rows` (identical walk on every thread)
+      int je = j, r = rows;
+      while (je < cnt && (d_rc[je] == 0 || r + d_rc[je] <= PR)) {
+        if (threadIdx.x == 0) {
+          d_off[je] = r;
+          fl += (double)d_rc[je] * d_ls[je] * kt;  // triangular R_B times S^T
+        }
+        r += d_rc[je];
+        ++je;
+      }
+      __syncthreads();  // d_off
+      for (int b = j + (int)threadIdx.x; b < je; b += NT)
+        for (int i = 0; i < d_rc[b]; ++i) rowblk[d_off[b] + i] = b;
+      __syncthreads();
+      const int nr = r - rows;
+      for (int e = threadIdx.x; e < nr * K; e += NT) {
+        const int rr = rows + e % nr, c = e / nr;
+        const int b = rowblk[rr];
+        const int i = rr - d_off[b];
+        const int ls = d_ls[b], s = d_s[b];
+        const bool in_s = d_rc[b] > ls;
+        const double* Sa = M.S + (size_t)d_slot[b] * M.rcap * M.rcap;
+        const double* RB = in_s ? B.re + (size_t)s * M.kcap * M.kcap : B.rc + (size_t)s * M.rcap * M.rcap;
+        const int ldR = in_s ? M.kcap : M.rcap;
+        double v = 0.0;
+        if (c < kt) {
+          // (R_B S~^T)(i,c) = sum_j R_B(i,j) S_or(c,j),   S_or = S (row side) or S^T (column side)
+          for (int jj = i; jj < ls; ++jj) v += RB[i + jj * ldR] * (rs ? Sa[c + jj * M.rcap] : Sa[jj + c * M.rcap]);
+        } else if (in_s) {
+          v = RB[i + (ls + c - kt) * ldR];  // identity block of S~ = diag(S, I)
+        }
+        P[rr + c * PRL] = v;
+      }
+      __syncthreads();
+      rows = r;
+      j = je;
+      if (j < cnt) flush();  // block j does not fit: compress first
+    }
   }
-  const int p = A.parent[t];
-  if (p >= 0 && mode != W_LOCAL) {
-    const bool in_p = inside(A, p, a0);
-    const int kp = A.rank[p];
+  if (kp >= 0 && p >= 0 && mode != W_LOCAL) {
+    const bool in_p = p >= a0 && p < a0 + asz;
     const int Kp = kp + (in_p ? k : 0);
     if (Kp > 0) {
       if (rows + Kp > PR) flush();
-      const double* Bp = A.bw + (size_t)p * M.kcap * M.kcap;
+      // B~_{t+}: from global, or from shared memory when the caller chained it there
+      const double* Bp = bp_sm ? bp_sm : A.bw + (size_t)p * M.kcap * M.kcap;
+      const int ldb = bp_sm ? ldbp : M.kcap;
       const double* E = A.tr + (size_t)t * M.rcap * M.rcap;  // kt x kp
       for (int e = threadIdx.x; e < Kp * K; e += NT) {
         const int i = e % Kp, c = e / Kp;
         double v = 0.0;
         if (c < kt) {
-          for (int j = 0; j < kp; ++j) v += Bp[i + j * M.kcap] * E[c + j * M.rcap];
+          for (int j = 0; j < kp; ++j) v += Bp[i + j * ldb] * E[c + j * M.rcap];
         } else if (in_p) {
-          v = Bp[i + (kp + c - kt) * M.kcap];  // E~_t = diag(E_t, I) inside T_{t0}
+          v = Bp[i + (kp + c - kt) * ldb];  // E~_t = diag(E_t, I) inside T_{t0}
         }                                      // E~_{t0} = [E_{t0}; 0]: zero columns
         P[rows + i + c * PRL] = v;
       }
@@ -233,19 +279,95 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
   return fl;
 }
 
-__device__ void it_upd_weights_path(const MatDev& M, UpdArgs a_, int item_, int nitems_, double* smx_) {
+// cp.async (8-byte) global -> shared copies: the operands of the next chain level load while the
+// current level computes
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// U3 along pred(t0): B~_t = R([C_t; B~_{t+} E_t^T]) from the root down to the father of
+// t0 (C_t = R-factor of t's local stack, computed in parallel by the ext_leaf op into re[t]), then
+// t0 itself with its full stack (W_FULL).  The path comes from the leaf-ancestor table (one load
+// round), the ranks are loaded at once, B~ stays in shared memory from level to level, and C_t,
+// E_t of the next level are fetched with cp.async while the current level factorizes.  Same sums
+// and the same QR as weights_cluster(W_CHAIN) level by level.
+__device__ void it_upd_weights_path(const MatDev& M, UpdArgs a_, int l0r, int l0c, int Lr, int Lc, int item_,
+                                    double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  double* sm = smx_;
   const bool rs = item_ == 0;
   const DevSide& A = rs ? M.row : M.col;
-  int path[64];
-  int np = 0;
-  for (int t = rs ? a.t0 : a.s0; t >= 0 && np < 64; t = A.parent[t]) path[np++] = t;
+  const int L = rs ? Lr : Lc;                  // level of t0: path = anc[0..L]
+  const int32_t* anc = A.anc + (size_t)(rs ? l0r : l0c) * A.ancw;
+  constexpr int RC = RCAP_MAX, LB = RC + 1, LP = 2 * RC + 1;
+  double* Bsh = smx_;                          // B~ of the previous level (LB x RC)
+  double* Pn = Bsh + LB * RC;                  // chain panel ((2 RC) x RC, ld LP)
+  double* Cb[2] = {Pn + LP * RC, Pn + LP * RC + LB * RC};           // C_t double buffer
+  double* Eb[2] = {Cb[1] + LB * RC, Cb[1] + 2 * LB * RC};           // E_t double buffer
+  double* diag = Eb[1] + LB * RC;
+  int* pc = reinterpret_cast<int*>(diag + KC);  // path clusters (64)
+  int* pk = pc + 64;                            // their ranks
+  for (int l = threadIdx.x; l <= L; l += NT) pc[l] = anc[l];
+  __syncthreads();
+  for (int l = threadIdx.x; l <= L; l += NT) pk[l] = A.rank[pc[l]];
+  __syncthreads();
+  auto fetch = [&](int l, int buf) {  // C_t (K x K, ld kcap) and E_t (k_t x k_p, ld rcap) of level l
+    const int t = pc[l], kt = pk[l], kp = l > 0 ? pk[l - 1] : 0;
+    const double* C = A.re + (size_t)t * M.kcap * M.kcap;
+    const double* E = A.tr + (size_t)t * M.rcap * M.rcap;
+    for (int e = threadIdx.x; e < kt * kt; e += NT) cp_async8(Cb[buf] + (e % kt) + (e / kt) * LB, C + (e % kt) + (e / kt) * M.kcap);
+    for (int e = threadIdx.x; e < kt * kp; e += NT) cp_async8(Eb[buf] + (e % kt) + (e / kt) * LB, E + (e % kt) + (e / kt) * M.rcap);
+    cp_async_commit();
+  };
   double fl = 0.0;
-  // proper ancestors: chain on their local stacks (computed in parallel by k_upd_ext_leaf); t0: full
-  for (int q = np - 1; q >= 0; --q) fl += weights_cluster(M, a, rs, path[q], sm, q == 0 ? W_FULL : W_CHAIN);
+  int kb = 0;  // rank (rows = cols) of B~ in Bsh
+  if (L > 0) fetch(0, 0);
+  for (int l = 0; l < L; ++l) {
+    const int buf = l & 1;
+    if (l + 1 < L) {
+      fetch(l + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int kt = pk[l], kp = l > 0 ? pk[l - 1] : 0;
+    // panel [C_t; B~_{t+} E_t^T]  (K = k_t: a proper ancestor is not extended)
+    for (int e = threadIdx.x; e < kt * kt; e += NT) Pn[(e % kt) + (e / kt) * LP] = Cb[buf][(e % kt) + (e / kt) * LB];
+    int rows = kt;
+    const int Kp = l > 0 ? kb : 0;
+    if (Kp > 0) {
+      for (int e = threadIdx.x; e < Kp * kt; e += NT) {
+        const int i = e % Kp, c = e / Kp;
+        double v = 0.0;
+        for (int j = 0; j < kp; ++j) v += Bsh[i + j * LB] * Eb[buf][c + j * LB];
+        Pn[rows + i + c * LP] = v;
+      }
+      fl += 2.0 * Kp * kp * kt;
+      rows += Kp;
+    }
+    __syncthreads();
+    if (rows > 0 && kt > 0) {
+      la::cta_qr_R(Pn, LP, rows, kt, diag, diag);
+      fl += hh_flops(rows, kt);
+    }
+    const int mk = rows < kt ? rows : kt;
+    // B~_t (kt x kt, zero rows below min(rows, kt)) -> Bsh
+    for (int e = threadIdx.x; e < kt * kt; e += NT) {
+      const int i = e % kt, j = e / kt;
+      Bsh[i + j * LB] = i < mk ? Pn[i + j * LP] : 0.0;
+    }
+    kb = kt;
+    __syncthreads();
+  }
+  // t0: full local stack + B~_{t0+} E~_{t0}^T (B~ of the father from shared memory)
+  double* rest = smx_ + LB * RC;  // weights_cluster's panel after Bsh
+  fl += weights_cluster(M, a, rs, pc[L], rest, W_FULL, L > 0 ? Bsh : nullptr, LB);
   if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_W_PATH, fl);
 }
 
@@ -436,70 +558,146 @@ __device__ void it_upd_svd_level(const MatDev& M, UpdArgs a_, int bA, int nA, in
 }
 
 // ---- U5 couplings ------------------------------------------------------------------------------
+__device__ __forceinline__ int seg_find(const int* cum, int nb, int e) {  // last b with cum[b] <= e
+  int lo = 0, hi = nb - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (cum[mid] <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// U5: every admissible block of row(t), t in T_{t0}, gets S <- R_t S~ R_s^T (s in
+// T_{s0}) or R_t [S; 0]; every block of col(s), s in T_{s0}, with its row outside T_{t0} gets
+// [S, 0] R_s^T.  The blocks of one cluster are independent: their descriptors are loaded at once and
+// all blocks of a segment (as many as fit the shared-memory budget) are multiplied in the same
+// parallel passes -- the same sums, in the same order, as one block at a time.
 __device__ void it_upd_couple(const MatDev& M, UpdArgs a_, int nA, int nB, int item_, int nitems_, double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  double* sm = smx_;
-  double* T1 = sm;             // KC x KC (ld KC)
-  double* Out = T1 + KC * KC;  // KC x KC (ld KC)
   const int k = a.k;
   const bool rs = (int)item_ < nA;
+  constexpr int NBD = 128;
+  constexpr int BUDGET = 24000;  // doubles of per-block scratch per segment
+  double* buf = smx_;
+  int* d_slot = reinterpret_cast<int*>(smx_ + BUDGET);
+  int* d_p = d_slot + NBD;    // partner cluster
+  int* d_kp = d_p + NBD;      // partner's old rank (l_s, or k_t on the column side)
+  int* d_rn = d_kp + NBD;     // partner's new rank (in_s only), -1: partner outside (no column change)
+  int* d_t1 = d_rn + NBD;     // scratch offset of T1 (in_s) / -1
+  int* d_out = d_t1 + NBD;    // scratch offset of Out
+  int* cumA = d_out + NBD;    // cumulative T1 entries
+  int* cumB = cumA + NBD;     // cumulative Out entries
+  int* sc = cumB + NBD;       // [0]: segment end, [1]: T1 total, [2]: Out total
   double fl = 0.0;
-  if (rs) {
-    const int t = a.t0 + item_;
-    const int kt = M.row.rank[t], rt = M.row.rnew[t];
-    const double* RNt = M.row.rn + (size_t)t * M.kcap * M.kcap;  // rt x Kt
-    for (int q = M.row.bptr[t]; q < M.row.bptr[t + 1]; ++q) {
-      const int slot = M.row.bidx[q];
-      const int s = M.adm_s[slot];
-      double* Sa = M.S + (size_t)slot * M.rcap * M.rcap;  // kt x ls
-      const int ls = M.col.rank[s];
-      if (inside(M.col, s, a.s0)) {
-        const int Ls = ls + k, rsn = M.col.rnew[s];
-        const double* RNs = M.col.rn + (size_t)s * M.kcap * M.kcap;  // rsn x Ls
-        // T1 = R_t diag(S, I)  (rt x Ls)
-        for (int e = threadIdx.x; e < rt * Ls; e += NT) {
-          const int i = e % rt, j = e / rt;
-          double v;
-          if (j < ls) {
-            v = 0.0;
-            for (int p = 0; p < kt; ++p) v += RNt[i + p * M.kcap] * Sa[p + j * M.rcap];
-          } else {
-            v = RNt[i + (kt + j - ls) * M.kcap];
+  const DevSide& Dm = rs ? M.row : M.col;
+  const int c = rs ? a.t0 + item_ : a.s0 + (item_ - nA);  // this item's cluster
+  const int kc = Dm.rank[c], rcn = Dm.rnew[c];
+  const double* RNc = Dm.rn + (size_t)c * M.kcap * M.kcap;  // rcn x (kc + k)
+  const int qb = Dm.bptr[c], qe = Dm.bptr[c + 1];
+  const int osz = rs ? M.col.tsize[a.s0] : M.row.tsize[a.t0];
+  for (int base = qb; base < qe; base += NBD) {
+    const int cnt = qe - base < NBD ? qe - base : NBD;
+    for (int j = threadIdx.x; j < cnt; j += NT) {
+      const int slot = Dm.bidx[base + j];
+      const int p = rs ? M.adm_s[slot] : M.adm_t[slot];
+      const bool in_o = rs ? (p >= a.s0 && p < a.s0 + osz) : (p >= a.t0 && p < a.t0 + osz);
+      d_slot[j] = slot;
+      d_p[j] = p;
+      d_kp[j] = rs ? M.col.rank[p] : M.row.rank[p];
+      d_rn[j] = rs ? (in_o ? M.col.rnew[p] : -1) : (in_o ? -2 : -1);  // column side: -2 = handled by the row CTA
+    }
+    __syncthreads();
+    int j = 0;
+    while (j < cnt) {
+      if (threadIdx.x == 0) {  // pack a segment of blocks into the scratch budget
+        int used = 0, je = j, na = 0, nbo = 0;
+        for (; je < cnt; ++je) {
+          const int kp = d_kp[je], rn = d_rn[je];
+          int t1 = 0, ou = 0;
+          if (rs) {
+            if (rn >= 0) {
+              t1 = rcn * (kp + k);
+              ou = rcn * rn;
+            } else {
+              ou = rcn * kp;
+            }
+          } else if (rn == -1) {
+            ou = kp * rcn;
           }
-          T1[i + j * KC] = v;
+          if (used + t1 + ou > BUDGET && je > j) break;
+          cumA[je - j] = na;
+          cumB[je - j] = nbo;
+          d_t1[je] = t1 ? used : -1;
+          d_out[je] = used + t1;
+          used += t1 + ou;
+          na += t1;
+          nbo += ou;
         }
-        __syncthreads();
-        la::cta_gemm(Out, KC, T1, KC, false, RNs, M.kcap, true, rt, rsn, Ls, false);
-        __syncthreads();
-        la::cta_copy(Sa, M.rcap, Out, KC, rt, rsn);
-        fl += 2.0 * rt * kt * ls + 2.0 * rt * Ls * rsn;
-      } else {
-        // S <- R_t [S; 0] = R_t(:, :kt) S
-        la::cta_gemm(Out, KC, RNt, M.kcap, false, Sa, M.rcap, false, rt, ls, kt, false);
-        __syncthreads();
-        la::cta_copy(Sa, M.rcap, Out, KC, rt, ls);
-        fl += 2.0 * rt * kt * ls;
+        sc[0] = je;
+        sc[1] = na;
+        sc[2] = nbo;
       }
       __syncthreads();
-    }
-  } else {
-    const int s = a.s0 + (item_ - nA);
-    const int ls = M.col.rank[s], rsn = M.col.rnew[s];
-    const double* RNs = M.col.rn + (size_t)s * M.kcap * M.kcap;  // rsn x (ls + k)
-    for (int q = M.col.bptr[s]; q < M.col.bptr[s + 1]; ++q) {
-      const int slot = M.col.bidx[q];
-      const int t = M.adm_t[slot];
-      if (inside(M.row, t, a.t0)) continue;  // handled by the row-side CTA
-      double* Sa = M.S + (size_t)slot * M.rcap * M.rcap;
-      const int kt = M.row.rank[t];
-      // S <- [S, 0] R_s^T = S R_s(:, :ls)^T
-      la::cta_gemm(Out, KC, Sa, M.rcap, false, RNs, M.kcap, true, kt, rsn, ls, false);
+      const int je = sc[0], na = sc[1], nbo = sc[2], nb = je - j;
+      // pass A (row side, partner inside T_{s0}): T1 = R_t diag(S, I)  (rt x (l_s + k), ld rt)
+      for (int e = threadIdx.x; e < na; e += NT) {
+        const int b = j + seg_find(cumA, nb, e);
+        const int x = e - cumA[b - j];
+        const int ls = d_kp[b], i = x % rcn, jj = x / rcn;
+        const double* Sa = M.S + (size_t)d_slot[b] * M.rcap * M.rcap;
+        double v;
+        if (jj < ls) {
+          v = 0.0;
+          for (int p = 0; p < kc; ++p) v += RNc[i + p * M.kcap] * Sa[p + jj * M.rcap];
+        } else {
+          v = RNc[i + (kc + jj - ls) * M.kcap];
+        }
+        buf[d_t1[b] + x] = v;
+      }
       __syncthreads();
-      la::cta_copy(Sa, M.rcap, Out, KC, kt, rsn);
-      fl += 2.0 * kt * ls * rsn;
+      // pass B: the new couplings into the scratch
+      for (int e = threadIdx.x; e < nbo; e += NT) {
+        const int b = j + seg_find(cumB, nb, e);
+        const int x = e - cumB[b - j];
+        const double* Sa = M.S + (size_t)d_slot[b] * M.rcap * M.rcap;
+        const int kp = d_kp[b], rn = d_rn[b];
+        double acc = 0.0;
+        if (rs && rn >= 0) {  // T1 R_s^T  (rt x rsn), inner l_s + k
+          const double* RNs = M.col.rn + (size_t)d_p[b] * M.kcap * M.kcap;
+          const double* T1 = buf + d_t1[b];
+          const int i = x % rcn, jj = x / rcn, Ls = kp + k;
+          for (int q = 0; q < Ls; ++q) acc += T1[i + q * rcn] * RNs[jj + q * M.kcap];
+        } else if (rs) {  // R_t(:, :kt) S  (rt x ls), inner kt
+          const int i = x % rcn, jj = x / rcn;
+          for (int q = 0; q < kc; ++q) acc += RNc[i + q * M.kcap] * Sa[q + jj * M.rcap];
+        } else {  // S R_s(:, :ls)^T  (kt x rsn), inner ls
+          const int i = x % kp, jj = x / kp;
+          for (int q = 0; q < kc; ++q) acc += Sa[i + q * M.rcap] * RNc[jj + q * M.kcap];
+        }
+        buf[d_out[b] + x] = acc;
+      }
       __syncthreads();
+      // pass C: write back (every read of the old couplings is done)
+      for (int e = threadIdx.x; e < nbo; e += NT) {
+        const int b = j + seg_find(cumB, nb, e);
+        const int x = e - cumB[b - j];
+        double* Sa = M.S + (size_t)d_slot[b] * M.rcap * M.rcap;
+        const int rows = rs ? rcn : d_kp[b];
+        Sa[(x % rows) + (x / rows) * M.rcap] = buf[d_out[b] + x];
+      }
+      if (threadIdx.x == 0 && a.prof) {
+        for (int b = j; b < je; ++b) {
+          const int kp = d_kp[b], rn = d_rn[b];
+          if (rs && rn >= 0) fl += 2.0 * rcn * kc * kp + 2.0 * rcn * (kp + k) * rn;
+          else if (rs) fl += 2.0 * rcn * kc * kp;
+          else if (rn == -1) fl += 2.0 * kp * kc * rcn;
+        }
+      }
+      __syncthreads();
+      j = je;
     }
   }
   if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_COUPLE, fl);
@@ -545,40 +743,105 @@ __device__ void it_upd_install(const MatDev& M, UpdArgs a_, int nA, int nB, int 
 }
 
 // ---- memoised R-factors on pred(t0) ----------------------------------------------------------
-__device__ void it_upd_rcache_path(const MatDev& M, UpdArgs a_, int item_, int nitems_, double* smx_) {
+// rc[t] = R([rc[t1] E_t1; rc[t2] E_t2]) from the father of t0 up to the root (Alg. 16 recursion on the
+// changed path, reading R7).  The on-path son's R stays in shared memory from level to level; the
+// sibling's R and both transfer matrices of the next level arrive by cp.async while the current
+// level factorizes; the path, ranks and sons are loaded in three rounds up front.
+__device__ void it_upd_rcache_path(const MatDev& M, UpdArgs a_, int l0r, int l0c, int Lr, int Lc, int item_,
+                                   double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  double* sm = smx_;
   const bool rs = item_ == 0;
   const DevSide& D = rs ? M.row : M.col;
-  double* A = sm;  // LD2 x KC
-  double* diag = A + LD2 * KC;
-  double* red = diag + KC;
-  for (int t = D.parent[rs ? a.t0 : a.s0]; t >= 0; t = D.parent[t]) {
-    const int kt = D.rank[t];
+  const int L = rs ? Lr : Lc;
+  if (L == 0) return;
+  const int32_t* anc = D.anc + (size_t)(rs ? l0r : l0c) * D.ancw;
+  constexpr int RC = RCAP_MAX, LB = RC + 1, LP = 2 * RC + 1;
+  double* Ron = smx_;                                  // R of the on-path son (LB x RC)
+  double* Pn = Ron + LB * RC;                          // panel (2 RC x RC, ld LP)
+  double* Rb[2] = {Pn + LP * RC, Pn + LP * RC + LB * RC};  // sibling R (double buffer)
+  double* E0[2] = {Rb[1] + LB * RC, Rb[1] + 2 * LB * RC};  // E of son0
+  double* E1[2] = {E0[1] + LB * RC, E0[1] + 2 * LB * RC};  // E of son1
+  double* diag = E1[1] + LB * RC;
+  int* pc = reinterpret_cast<int*>(diag + KC);  // path clusters
+  int* pk = pc + 64;                            // their ranks
+  int* ps = pk + 64;                            // sibling of the on-path son at level l
+  int* psk = ps + 64;                           // its rank
+  int* pon0 = psk + 64;                         // 1 if the on-path son is son0
+  for (int l = threadIdx.x; l <= L; l += NT) pc[l] = anc[l];
+  __syncthreads();
+  for (int l = threadIdx.x; l <= L; l += NT) {
+    pk[l] = D.rank[pc[l]];
+    if (l < L) {
+      const int s0 = D.son0[pc[l]], s1 = D.son1[pc[l]];
+      const bool on0 = s0 == pc[l + 1];
+      ps[l] = on0 ? s1 : s0;
+      pon0[l] = on0 ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < L; l += NT) psk[l] = D.rank[ps[l]];
+  __syncthreads();
+  auto fetch = [&](int l, int buf) {  // level l: sibling R, E of both sons (k_son x k_t, ld rcap)
+    const int t = pc[l], kt = pk[l];
+    const int son_on = pc[l + 1], kon = pk[l + 1], sib = ps[l], ksib = psk[l];
+    const int c0 = pon0[l] ? son_on : sib, c1 = pon0[l] ? sib : son_on;
+    const int k0 = pon0[l] ? kon : ksib, k1 = pon0[l] ? ksib : kon;
+    const double* R = D.rc + (size_t)sib * M.rcap * M.rcap;
+    const double* Ea = D.tr + (size_t)c0 * M.rcap * M.rcap;
+    const double* Eb = D.tr + (size_t)c1 * M.rcap * M.rcap;
+    (void)t;
+    for (int e = threadIdx.x; e < ksib * ksib; e += NT)
+      cp_async8(Rb[buf] + (e % ksib) + (e / ksib) * LB, R + (e % ksib) + (e / ksib) * M.rcap);
+    for (int e = threadIdx.x; e < k0 * kt; e += NT)
+      cp_async8(E0[buf] + (e % k0) + (e / k0) * LB, Ea + (e % k0) + (e / k0) * M.rcap);
+    for (int e = threadIdx.x; e < k1 * kt; e += NT)
+      cp_async8(E1[buf] + (e % k1) + (e / k1) * LB, Eb + (e % k1) + (e / k1) * M.rcap);
+    cp_async_commit();
+  };
+  // R of t0 (installed by the previous op) into Ron
+  {
+    const int kon = pk[L];
+    const double* R = D.rc + (size_t)pc[L] * M.rcap * M.rcap;
+    for (int e = threadIdx.x; e < kon * kon; e += NT) Ron[(e % kon) + (e / kon) * LB] = R[(e % kon) + (e / kon) * M.rcap];
+  }
+  fetch(L - 1, 0);
+  for (int l = L - 1, it = 0; l >= 0; --l, ++it) {
+    const int buf = it & 1;
+    if (l > 0) {
+      fetch(l - 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int kt = pk[l], kon = pk[l + 1], ksib = psk[l];
+    const bool on0 = pon0[l] != 0;
     int row0 = 0;
     for (int q = 0; q < 2; ++q) {
-      const int c = q ? D.son1[t] : D.son0[t];
-      const int kc = D.rank[c];
-      const double* RC = D.rc + (size_t)c * M.rcap * M.rcap;
-      const double* E = D.tr + (size_t)c * M.rcap * M.rcap;
+      const bool on = (q == 0) == on0;
+      const int kc = on ? kon : ksib;
+      const double* RC = on ? Ron : Rb[buf];
+      const double* E = q ? E1[buf] : E0[buf];
       for (int e = threadIdx.x; e < kc * kt; e += NT) {
         const int i = e % kc, j = e / kc;
         double v = 0.0;
-        for (int p = i; p < kc; ++p) v += RC[i + p * M.rcap] * E[p + j * M.rcap];
-        A[row0 + i + j * LD2] = v;
+        for (int p = i; p < kc; ++p) v += RC[i + p * LB] * E[p + j * LB];
+        Pn[row0 + i + j * LP] = v;
       }
       row0 += kc;
     }
     __syncthreads();
-    if (kt > 0) la::cta_qr_R(A, LD2, row0, kt, diag, red);
+    if (kt > 0) la::cta_qr_R(Pn, LP, row0, kt, diag, diag);
     if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_RCACHE, hh_flops(row0, kt) + (double)row0 * row0 * kt);
-    double* RC = D.rc + (size_t)t * M.rcap * M.rcap;
+    double* RCg = D.rc + (size_t)pc[l] * M.rcap * M.rcap;
     const int mk = row0 < kt ? row0 : kt;
     for (int e = threadIdx.x; e < kt * kt; e += NT) {
       const int i = e % kt, j = e / kt;
-      RC[i + j * M.rcap] = i < mk ? A[i + j * LD2] : 0.0;
+      const double v = i < mk ? Pn[i + j * LP] : 0.0;
+      RCg[i + j * M.rcap] = v;
+      Ron[i + j * LB] = v;
     }
     __syncthreads();
   }

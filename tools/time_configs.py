@@ -1,0 +1,141 @@
+"""Timings of the BASELINE configs beyond the bench's C2 line; one JSON line each.
+
+  python tools/time_configs.py c1 [count]        C1: `count` (10,000) seeded random rank-k_u updates
+                                                 at fixed rank 16, k_u in {4, 8, 16, 32}; updates/s
+                                                 = count / device time of the dependent stream
+                                                 (inputs resident in HBM), median of 3 fresh runs
+  python tools/time_configs.py c3 [N]            C3: 3D Kuhn P1 Laplacian N^3 (64^3), leaf 64:
+                                                 H^2 Cholesky at eps 1e-4 + PCG to 1e-8
+  python tools/time_configs.py c4 [N] [eps...]   C4: 2D jump problem N^2 (1024^2): Z = A A (h2_addmul
+                                                 into a fresh rank-0 Z), then H^2 Cholesky of Z
+
+Every call goes through the C ABI (paper_1402_5056_b200); times are CUDA events on the stream.
+"""
+import json
+import sys
+import time
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+sys.path.insert(0, ".")
+import paper_1402_5056_b200 as P  # noqa: E402
+from inputs import config  # noqa: E402
+from inputs.rng import stream, RHS  # noqa: E402
+from inputs.updates import c1_stream  # noqa: E402
+
+dev = torch.device("cuda", 0)
+ADM = 1  # h2_btree_export kind of an admissible leaf (include/h2.h)
+
+
+def ev():
+    return torch.cuda.Event(enable_timing=True)
+
+
+def structure(c):
+    t = P.h2_cluster_tree(c["points"], c["leaf"])
+    bt = P.h2_block_tree(t, t, c["eta"])
+    return t, bt
+
+
+def adm_targets(t, bt):
+    """Admissible leaves (t0, s0, |t0|, |s0|) in block-tree DFS order, from the ABI exports."""
+    adm = np.nonzero(bt.kind == ADM)[0]
+    return [(int(bt.t[i]), int(bt.s[i]), t.size(bt.t[i]), t.size(bt.s[i])) for i in adm]
+
+
+def run_c1(count):
+    c = config("C1")
+    t, bt = structure(c)
+    targets = adm_targets(t, bt)
+    out = {"config": "C1", "n": c["n"], "count": count, "trunc": "fixed rank 16 (rel 1e-12, max_rank 16)"}
+    for ku in (4, 8, 16, 32):
+        ups = c1_stream(targets, count, ku, seed=0)
+        # all factors resident in HBM before the clock starts (one buffer, column-major slices)
+        Xs = [torch.from_numpy(np.asfortranarray(X)).to(dev) for _, _, X, _ in ups]
+        Ys = [torch.from_numpy(np.asfortranarray(Y)).to(dev) for _, _, _, Y in ups]
+        runs = []
+        for rep in range(3):
+            Z = P.h2_from_sparse(bt, c["A"], lower=False, rank_cap=16, update_cap=32)
+            torch.cuda.synchronize()
+            e0, e1 = ev(), ev()
+            w0 = time.perf_counter()
+            e0.record()
+            for (t0, s0, _, _), X, Y in zip(ups, Xs, Ys):
+                P.h2_lowrank_update(Z, t0, s0, X, Y, trunc=P.Trunc(1e-12, 0.0, 16))
+            e1.record()
+            torch.cuda.synchronize()
+            runs.append((e0.elapsed_time(e1) / 1e3, time.perf_counter() - w0))
+            kr, kc = P.h2_ranks(Z)
+            flags = P.h2_check_device_flags(Z)
+            del Z
+        dev_s = sorted(r[0] for r in runs)[1]
+        out[f"k{ku}"] = {"updates_per_s": count / dev_s, "device_s": dev_s, "wall_s": sorted(r[1] for r in runs)[1],
+                         "max_rank": [int(kr.max()), int(kc.max())], "flags": flags}
+    print(json.dumps(out), flush=True)
+
+
+def factor_and_pcg(c, bt, Z, Aop, eps, label, extra):
+    e0, e1, e2 = ev(), ev(), ev()
+    torch.cuda.synchronize()
+    e0.record()
+    P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps))
+    e1.record()
+    b = torch.from_numpy(stream(RHS).standard_normal(c["n"])).to(dev)
+    x = torch.zeros_like(b)
+    _, m, rel = P.h2_pcg(Aop, Z, b, x, tol=1e-8)
+    e2.record()
+    torch.cuda.synchronize()
+    kr, kc = P.h2_ranks(Z)
+    out = {"config": label, "n": c["n"], "eps": eps, "setup_s": e0.elapsed_time(e1) / 1e3,
+           "pcg_iterations": m, "pcg_relres": rel, "pcg_s": e1.elapsed_time(e2) / 1e3, "stats": P.h2_stats(Z),
+           "max_rank": [int(kr.max()), int(kc.max())], "flags": P.h2_check_device_flags(Z),
+           "storage_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / c["n"] / 1e3)}
+    out.update(extra)
+    print(json.dumps(out), flush=True)
+
+
+def run_c3(N):
+    c = config("C3", N=N)
+    w0 = time.perf_counter()
+    t, bt = structure(c)
+    st = time.perf_counter() - w0
+    Aop = P.h2_from_sparse(bt, c["A"], lower=False, rank_cap=32, update_cap=32)
+    Z = P.h2_from_sparse(bt, c["A"], lower=True, rank_cap=32, update_cap=32)
+    factor_and_pcg(c, bt, Z, Aop, 1e-4, f"C3 {N}^3", {"structure_s": st})
+
+
+def run_c4(N, epss):
+    c = config("C4", N=N)
+    w0 = time.perf_counter()
+    t, bt = structure(c)
+    st = time.perf_counter() - w0
+    A = P.h2_from_sparse(bt, c["A"], lower=False, rank_cap=32, update_cap=32)
+    A2 = (c["A"] @ c["A"]).tocsr()
+    A2op = P.h2_from_sparse(bt, A2, lower=False, rank_cap=32, update_cap=32)  # PCG operator A^2 (nearfield form)
+    zero = sp.csr_matrix(c["A"].shape)
+    for eps in epss:
+        Z = P.h2_from_sparse(bt, zero, lower=True, rank_cap=32, update_cap=32)
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record()
+        P.h2_addmul(Z, 1.0, A, A, trunc=P.Trunc(eps))
+        e1.record()
+        torch.cuda.synchronize()
+        prod_s = e0.elapsed_time(e1) / 1e3
+        factor_and_pcg(c, bt, Z, A2op, eps, f"C4 {N}^2 A*A", {"structure_s": st, "product_s": prod_s,
+                                                              "product_stats": P.h2_stats(Z)})
+        del Z
+
+
+if __name__ == "__main__":
+    what = sys.argv[1]
+    if what == "c1":
+        run_c1(int(sys.argv[2]) if len(sys.argv) > 2 else 10000)
+    elif what == "c3":
+        run_c3(int(sys.argv[2]) if len(sys.argv) > 2 else 64)
+    elif what == "c4":
+        N = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+        epss = [float(e) for e in sys.argv[3:]] or [1e-2, 1e-4, 1e-6]
+        run_c4(N, epss)
