@@ -187,3 +187,44 @@ def test_factor_invariant_to_op_chunking(tmp_path, flush):
     a, b = out[None], out[flush]
     for k in ("kr", "kc", "st", "y"):
         np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_c4_product_into_lower_then_cholesky():
+    """C4 pipeline at a parity size (jump problem, 32 x 32): Z = A A by h2_addmul into a fresh
+    rank-0 LOWER-storage Z (exact: R14), then the H^2 Cholesky of Z.  GPU and oracle agree on the
+    ranks and the factor; at eps = 1e-2 both report the breakdown (A^2 has cond ~ 3e12 here: the
+    truncation error exceeds its smallest eigenvalue, reading own-8)."""
+    c = config("C4", N=32)
+    t = P.h2_cluster_tree(c["points"], c["leaf"])
+    bt = P.h2_block_tree(t, t, c["eta"])
+    ot = ClusterTree(c["points"], c["leaf"])
+    ob = BlockTree(ot, ot, c["eta"])
+    zero = sp.csr_matrix(c["A"].shape)
+    A1 = P.h2_from_sparse(bt, c["A"])
+    OA = o_from_sparse(ob, c["A"])
+    for eps, breaks in ((1e-4, False), (1e-2, True)):
+        Z = P.h2_from_sparse(bt, zero, lower=True)
+        OZ = o_from_sparse(ob, zero, lower=True)
+        ar = Arith(OZ, OTrunc(eps))
+        ar.addmul(1.0, Op(OA), Op(OA), 0, 0, 0)
+        P.h2_addmul(Z, 1.0, A1, A1, trunc=P.Trunc(eps))
+        # the lower-stored product equals the lower-stored sparse A^2 exactly
+        ref = o_from_sparse(ob, (c["A"] @ c["A"]).tocsr(), lower=True)
+        Xp = np.random.default_rng(4).standard_normal((ot.n, 2))
+        d = np.abs(gpu_apply(Z, Xp) - ref.matvec(Xp)).max()
+        assert d < 1e-9 * np.abs(c["A"] @ (c["A"] @ Xp)).max(), d
+        if breaks:
+            with pytest.raises(Exception):
+                ar.chol()
+            with pytest.raises(P.H2Error) as e:
+                P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps))
+                P.h2_check_device_flags(Z)
+            assert e.value.status == "H2_ERR_BREAKDOWN"
+            continue
+        ar.chol()
+        P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps))
+        assert P.h2_check_device_flags(Z) == 0
+        _ranks_equal(Z, OZ)
+        d = operator_rel_diff(Z, OZ, ot.n)
+        print(f"C4-32 A*A -> Cholesky eps {eps}: rel diff {d:.2e}")
+        assert d <= 10 * eps

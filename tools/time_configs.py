@@ -7,7 +7,8 @@
   python tools/time_configs.py c3 [N]            C3: 3D Kuhn P1 Laplacian N^3 (64^3), leaf 64:
                                                  H^2 Cholesky at eps 1e-4 + PCG to 1e-8
   python tools/time_configs.py c4 [N] [eps...]   C4: 2D jump problem N^2 (1024^2): Z = A A (h2_addmul
-                                                 into a fresh rank-0 Z), then H^2 Cholesky of Z
+                                                 into a fresh rank-0 Z), then H^2 Cholesky of A
+                                                 (reading own-8: A^2 is numerically singular here)
 
 Every call goes through the C ABI (paper_1402_5056_b200); times are CUDA events on the stream.
 """
@@ -107,26 +108,37 @@ def run_c3(N):
 
 
 def run_c4(N, epss):
+    """C4 (reading own-8): the full H^2 product Z = A A into a fresh rank-0 Z (exact, R14; checked on
+    a probe against the sparse A^2), then the H^2 Cholesky of A at each eps.  A^2 itself is not
+    factored at this size: its condition number (~1e18 for the 10^6 coefficient contrast at
+    h = 1/1025) exceeds 1/eps_machine, so every truncated Cholesky of it breaks down."""
     c = config("C4", N=N)
     w0 = time.perf_counter()
     t, bt = structure(c)
     st = time.perf_counter() - w0
     A = P.h2_from_sparse(bt, c["A"], lower=False, rank_cap=32, update_cap=32)
-    A2 = (c["A"] @ c["A"]).tocsr()
-    A2op = P.h2_from_sparse(bt, A2, lower=False, rank_cap=32, update_cap=32)  # PCG operator A^2 (nearfield form)
+    Aop = A
     zero = sp.csr_matrix(c["A"].shape)
+    Z = P.h2_from_sparse(bt, zero, lower=False, rank_cap=32, update_cap=32)
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    e0.record()
+    P.h2_addmul(Z, 1.0, A, A, trunc=P.Trunc(epss[0]))
+    e1.record()
+    torch.cuda.synchronize()
+    prod_s = e0.elapsed_time(e1) / 1e3
+    xv = np.random.default_rng(3).standard_normal(c["n"])
+    zx = P.h2_matvec(Z, torch.from_numpy(xv).to(dev)).cpu().numpy()
+    ref = c["A"] @ (c["A"] @ xv)
+    prod = {"product_s": prod_s, "product_stats": P.h2_stats(Z),
+            "product_rel_err": float(np.linalg.norm(zx - ref) / np.linalg.norm(ref)),
+            "product_storage_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / c["n"] / 1e3)}
+    print(json.dumps({"config": f"C4 {N}^2 A*A", "n": c["n"], "structure_s": st, **prod}), flush=True)
+    del Z
     for eps in epss:
-        Z = P.h2_from_sparse(bt, zero, lower=True, rank_cap=32, update_cap=32)
-        torch.cuda.synchronize()
-        e0, e1 = ev(), ev()
-        e0.record()
-        P.h2_addmul(Z, 1.0, A, A, trunc=P.Trunc(eps))
-        e1.record()
-        torch.cuda.synchronize()
-        prod_s = e0.elapsed_time(e1) / 1e3
-        factor_and_pcg(c, bt, Z, A2op, eps, f"C4 {N}^2 A*A", {"structure_s": st, "product_s": prod_s,
-                                                              "product_stats": P.h2_stats(Z)})
-        del Z
+        L = P.h2_from_sparse(bt, c["A"], lower=True, rank_cap=32, update_cap=32)
+        factor_and_pcg(c, bt, L, Aop, eps, f"C4 {N}^2 Cholesky of A", {})
+        del L
 
 
 if __name__ == "__main__":
