@@ -177,6 +177,7 @@ struct ExecCtx {
   int mat_index(const MatDev& M);
   void maybe_flush();
   int hold = 0;             // > 0 while a skip region is open (no flush inside it)
+  int skip_tag = 0;         // origin tag recorded with the next skip op (profiling statistics)
   int group = 0;             // > 0 inside an independence group (group_begin / group_end)
   int group_off = 0;         // CTA of the next grouped op's item 0
   template <class P>

@@ -239,7 +239,12 @@ __global__ void __launch_bounds__(NT, 1) k_exec_cluster(const __grid_constant__ 
     const int n = op.nitems;
     if (op.code == OP_SKIPZ) {  // every CTA reads the same (final) flag: uniform skip
       const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
-      if (*(volatile const int*)q.ip == 0) o += q.cols;
+      const bool zero = *(volatile const int*)q.ip == 0;
+      if (zero) o += q.cols;
+      if (timing) {  // skip statistics per origin tag (h2_profile_ops slots 48 + tag: skipped, seen)
+        atomicAdd(P.prof + 4 * K_COUNT + 32 + 2 * (48 + q.rows), zero ? 1.0 : 0.0);
+        atomicAdd(P.prof + 4 * K_COUNT + 32 + 2 * (48 + q.rows) + 1, 1.0);
+      }
       continue;
     }
     // warm L1/L2 with the next op record while this one runs (192 B = 2 lines)
@@ -354,6 +359,7 @@ size_t ExecCtx::begin_skip(const int* k) {
   PMisc q{};
   q.ip = const_cast<int*>(k);
   q.cols = 0;
+  q.rows = skip_tag & 15;  // origin of the region (profiling statistics only)
   ++hold;  // before emit: a flush triggered by this very op would clear the list it indexes
   emit(OP_SKIPZ, 1, nullptr, q);
   return ops.size() - 1;

@@ -109,6 +109,16 @@ struct Driver {
   int rcap, lmax;
   double* ident;  // lmax x lmax identity
   long long n_updates = 0, n_dense = 0, n_temps = 0;
+  static constexpr size_t NO_SKIP = ~size_t(0);
+  size_t pre_skip = NO_SKIP;  // skip region opened by factors() (closed by addmul after the addition)
+
+  // reading own-6 ahead of the work: the contribution's rank and the zero-tile checks are recorded
+  // first, then a skip region covers the factor construction and the addition, so a contribution
+  // that turns out exactly zero on the device costs no hmul / expansion at all (the addition was
+  // skipped before as well: same result)
+  void open_pre_skip(int* kdev) { pre_skip = exec_ctx()->begin_skip(kdev); }
+  // profiling tag of the skip regions recorded next (h2_profile_ops slots 48 + tag)
+  void tag(int v) { exec_ctx()->skip_tag = v; }
 
   int size(int t) const { return T->hi[t] - T->lo[t]; }
   // Symbolic rank tracking (host): a cluster basis can only have a non-zero rank after an update
@@ -198,7 +208,10 @@ struct Driver {
       tgt->nz = true;
       // a zero device rank leaves the temporary unchanged (own-3): skip the whole truncated addition
       ExecCtx* c = exec_ctx();
+      const int old_tag = c->skip_tag;
+      c->skip_tag = 2;
       const size_t at = c->begin_skip(kdev);
+      c->skip_tag = old_tag;
       temp_add(*tgt, t, r, A, lda, B, ldb, kdev, kcap, alpha);
       c->end_skip(at, exec_big_items());
       return;
@@ -225,6 +238,12 @@ struct Driver {
     if (kx == ADM && ky == ADM) {
       if (X.Z->blk2adm[bx] < 0 || Y.Z->blk2adm[by] < 0) return 0;
       if (!nzr(X, t) || !nzc(Y, r)) return 0;  // min(k^X_t, k^Y_r) = 0
+      const DevSide& Xr0 = X.rows();
+      const DevSide& Yc0 = Y.cols();
+      rank_if(*kdev, Xr0.rank + t, Yc0.rank + r, st);  // 0 iff min(k^X_t, k^Y_r) = 0 (c2core sets the rank)
+      tag(3);
+      open_pre_skip(*kdev);
+      tag(9);
       const DevSide& Xr = X.rows();
       const DevSide& Xc = X.cols();
       const DevSide& Yr = Y.rows();
@@ -273,6 +292,12 @@ struct Driver {
       if (!nzr(X, t)) return 0;  // k = k^X_t = 0
       const DevSide& Xr = X.rows();
       const DevSide& Xc = X.cols();
+      set_int(*kdev, dimp(Xr.rank + t), st);
+      if (ky == INADM && Y.Z->blk2inad[by] >= 0)
+        zero_rank_if_zero_tile(Y.Z->d, Y.Z->blk2inad[by], ms * mr, *kdev, st);  // reading own-6
+      tag(4);
+      open_pre_skip(*kdev);
+      tag(10);
       *A = ar.alloc((size_t)mt * rcap);
       double* Wxs = ar.alloc((size_t)ms * rcap);
       {
@@ -287,9 +312,6 @@ struct Driver {
       *B = ar.alloc((size_t)mr * rcap);
       const HOp Yt = Y.t();
       hmul_dense(Y.Z->d, Yt.trans, r, s, 0, Dm, ms, dimp(Xr.rank + t), rcap, *B, mr, 1.0, 0.0, st);
-      set_int(*kdev, dimp(Xr.rank + t), st);
-      if (ky == INADM && Y.Z->blk2inad[by] >= 0)
-        zero_rank_if_zero_tile(Y.Z->d, Y.Z->blk2inad[by], ms * mr, *kdev, st);  // reading own-6
       *lda = mt;
       *ldb = mr;
       return rcap;
@@ -299,6 +321,12 @@ struct Driver {
       if (!nzc(Y, r)) return 0;  // k = k^Y_r = 0
       const DevSide& Yr = Y.rows();
       const DevSide& Yc = Y.cols();
+      set_int(*kdev, dimp(Yc.rank + r), st);
+      if (kx == INADM && X.Z->blk2inad[bx] >= 0)
+        zero_rank_if_zero_tile(X.Z->d, X.Z->blk2inad[bx], mt * ms, *kdev, st);  // reading own-6
+      tag(5);
+      open_pre_skip(*kdev);
+      tag(11);
       double* Vys = ar.alloc((size_t)ms * rcap);
       *B = ar.alloc((size_t)mr * rcap);
       {
@@ -312,9 +340,6 @@ struct Driver {
            dimp(Yr.rank + s), ms, rcap, rcap, 1.0, 0.0, st);
       *A = ar.alloc((size_t)mt * rcap);
       hmul_dense(X.Z->d, X.trans, t, s, 0, Dm, ms, dimp(Yc.rank + r), rcap, *A, mt, 1.0, 0.0, st);
-      set_int(*kdev, dimp(Yc.rank + r), st);
-      if (kx == INADM && X.Z->blk2inad[bx] >= 0)
-        zero_rank_if_zero_tile(X.Z->d, X.Z->blk2inad[bx], mt * ms, *kdev, st);  // reading own-6
       *lda = mt;
       *ldb = mr;
       return rcap;
@@ -322,6 +347,7 @@ struct Driver {
     if (kx == INADM && ky == INADM && !dense_target) {
       // reading own-7: interpolative decomposition of the dense product (a zero tile gives r = 0)
       if (X.Z->blk2inad[bx] < 0 || Y.Z->blk2inad[by] < 0) return 0;
+      tag(12);
       const int kc = std::min(mt, mr);
       *A = ar.alloc((size_t)mt * kc);
       *B = ar.alloc((size_t)mr * kc);
@@ -333,29 +359,35 @@ struct Driver {
     }
     if (kx == INADM) {
       if (X.Z->blk2inad[bx] < 0) return 0;
+      set_int(*kdev, dimc(ms), st);
+      zero_rank_if_zero_tile(X.Z->d, X.Z->blk2inad[bx], mt * ms, *kdev, st);  // reading own-6
+      if (ky == INADM && Y.Z->blk2inad[by] >= 0) zero_rank_if_zero_tile(Y.Z->d, Y.Z->blk2inad[by], ms * mr, *kdev, st);
+      tag(7);
+      open_pre_skip(*kdev);
+      tag(13);
       *A = ar.alloc((size_t)mt * ms);
       if (X.trans) transpose_tile(*A, mt, Nptr(X.Z, bx), lmax, mt, ms, st);
       else copy_cols(*A, mt, Nptr(X.Z, bx), lmax, mt, dimc(ms), ms, st);
       *B = ar.alloc((size_t)mr * ms);
       const HOp Yt = Y.t();
       hmul_dense(Y.Z->d, Yt.trans, r, s, 0, ident, lmax, dimc(ms), ms, *B, mr, 1.0, 0.0, st);
-      set_int(*kdev, dimc(ms), st);
-      zero_rank_if_zero_tile(X.Z->d, X.Z->blk2inad[bx], mt * ms, *kdev, st);  // reading own-6
-      if (ky == INADM && Y.Z->blk2inad[by] >= 0) zero_rank_if_zero_tile(Y.Z->d, Y.Z->blk2inad[by], ms * mr, *kdev, st);
       *lda = mt;
       *ldb = mr;
       return ms;
     }
     // ky == INADM
     if (Y.Z->blk2inad[by] < 0) return 0;
+    set_int(*kdev, dimc(mr), st);
+    zero_rank_if_zero_tile(Y.Z->d, Y.Z->blk2inad[by], ms * mr, *kdev, st);  // reading own-6
+    tag(8);
+    open_pre_skip(*kdev);
+    tag(14);
     double* Ny = ar.alloc((size_t)ms * mr);
     if (Y.trans) transpose_tile(Ny, ms, Nptr(Y.Z, by), lmax, ms, mr, st);
     else copy_cols(Ny, ms, Nptr(Y.Z, by), lmax, ms, dimc(mr), mr, st);
     *A = ar.alloc((size_t)mt * mr);
     hmul_dense(X.Z->d, X.trans, t, s, 0, Ny, ms, dimc(mr), mr, *A, mt, 1.0, 0.0, st);
     *B = ident;
-    set_int(*kdev, dimc(mr), st);
-    zero_rank_if_zero_tile(Y.Z->d, Y.Z->blk2inad[by], ms * mr, *kdev, st);  // reading own-6
     *lda = mt;
     *ldb = lmax;
     return mr;
@@ -396,6 +428,8 @@ struct Driver {
               Mark mk2(ar);
               double* A = ar.alloc((size_t)size(t) * rcap);
               double* B = ar.alloc((size_t)size(r) * rcap);
+              tag(0);
+              const size_t pre = exec_ctx()->begin_skip(tm.k);  // a rank-0 temporary adds nothing
               {
                 Group g;
                 stack_cols(A, size(t), size(t), nullptr, 0, nullptr, tm.A, tm.ma, T->lo[tm.ra] - T->lo[t], tm.ma,
@@ -403,7 +437,9 @@ struct Driver {
                 stack_cols(B, size(r), size(r), nullptr, 0, nullptr, tm.B, tm.mb, T->lo[tm.rb] - T->lo[r], tm.mb,
                            dimp(tm.k), rcap, st);
               }
+              tag(1);
               add(nullptr, t, r, A, size(t), B, size(r), tm.k, rcap, 1.0);
+              exec_ctx()->end_skip(pre, exec_big_items());
             }
           return;
         }
@@ -423,8 +459,12 @@ struct Driver {
     int lda, ldb;
     int* kdev;
     const bool dense_target = !tgt && Z->bt->kind[Z->bt->find(t, r)] == INADM;
+    pre_skip = NO_SKIP;
     const int kcap = factors(X, Y, t, s, r, &A, &lda, &B, &ldb, &kdev, dense_target);
+    const size_t ps = pre_skip;
+    pre_skip = NO_SKIP;
     if (kcap) add(tgt, t, r, A, lda, B, ldb, kdev, kcap, alpha);
+    if (ps != NO_SKIP) exec_ctx()->end_skip(ps, exec_big_items());
   }
 
   // ---- dense-right-hand-side substitutions with the factor (in place on B) ---------------------
@@ -488,9 +528,11 @@ struct Driver {
       int* kdev = ar.ialloc();
       double* Zs = ar.alloc((size_t)ms * rcap);
       double* Vt = ar.alloc((size_t)mt * rcap);
+      rank_if(kdev, Z->d.row.rank + t, Z->d.col.rank + s, st);  // rank 0 block -> nothing (oracle: S.size == 0)
+      tag(6);
+      const size_t pre = exec_ctx()->begin_skip(kdev);  // a rank-0 block needs no solve (reading R8)
       {
         Group g;  // the solves below touch Zs only
-        rank_if(kdev, Z->d.row.rank + t, Z->d.col.rank + s, st);  // rank 0 block -> nothing (oracle: S.size == 0)
         expand_basis(Z->d, Z->d.col, s, Zs, ms, st);
         expand_basis(Z->d, Z->d.row, t, Vt, mt, st);
       }
@@ -499,7 +541,9 @@ struct Driver {
       double* U = ar.alloc((size_t)mt * rcap);
       gemm(U, mt, Vt, mt, false, Sptr(Z, b), Z->d.rcap, false, dimc(mt), dimp(Z->d.col.rank + s),
            dimp(Z->d.row.rank + t), mt, rcap, rcap, 1.0, 0.0, st);
+      exec_ctx()->end_skip(pre, exec_big_items());
       zero_fill(Sptr(Z, b), (size_t)Z->d.rcap * Z->d.rcap, st);
+      tag(15);
       update(t, s, U, mt, Zs, ms, kdev, 1.0);
       return;
     }
@@ -532,9 +576,11 @@ struct Driver {
       int* kdev = ar.ialloc();
       double* Vt = ar.alloc((size_t)mt * rcap);
       double* Ws = ar.alloc((size_t)ms * rcap);
+      rank_if(kdev, Z->d.row.rank + t, Z->d.col.rank + s, st);
+      tag(6);
+      const size_t pre = exec_ctx()->begin_skip(kdev);
       {
         Group g;  // the solve below touches Vt only
-        rank_if(kdev, Z->d.row.rank + t, Z->d.col.rank + s, st);
         expand_basis(Z->d, Z->d.row, t, Vt, mt, st);
         expand_basis(Z->d, Z->d.col, s, Ws, ms, st);
       }
@@ -542,7 +588,9 @@ struct Driver {
       double* U = ar.alloc((size_t)mt * rcap);
       gemm(U, mt, Vt, mt, false, Sptr(Z, b), Z->d.rcap, false, dimc(mt), dimp(Z->d.col.rank + s),
            dimp(Z->d.row.rank + t), mt, rcap, rcap, 1.0, 0.0, st);
+      exec_ctx()->end_skip(pre, exec_big_items());
       zero_fill(Sptr(Z, b), (size_t)Z->d.rcap * Z->d.rcap, st);
+      tag(15);
       update(t, s, U, mt, Ws, ms, kdev, 1.0);
       return;
     }

@@ -102,9 +102,10 @@ def run_c3(N):
     w0 = time.perf_counter()
     t, bt = structure(c)
     st = time.perf_counter() - w0
-    Aop = P.h2_from_sparse(bt, c["A"], lower=False, rank_cap=32, update_cap=32)
-    Z = P.h2_from_sparse(bt, c["A"], lower=True, rank_cap=32, update_cap=32)
-    factor_and_pcg(c, bt, Z, Aop, 1e-4, f"C3 {N}^3", {"structure_s": st})
+    # 3D ranks exceed 32 ("larger ranks"): the largest stored capacity, 48 + 48
+    Aop = P.h2_from_sparse(bt, c["A"], lower=False, rank_cap=48, update_cap=48)
+    Z = P.h2_from_sparse(bt, c["A"], lower=True, rank_cap=48, update_cap=48)
+    factor_and_pcg(c, bt, Z, Aop, 1e-4, f"C3 {N}^3", {"structure_s": st, "rank_cap": 48})
 
 
 def run_c4(N, epss):
