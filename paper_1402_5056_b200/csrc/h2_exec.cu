@@ -36,7 +36,8 @@ constexpr int PR = 192;
 constexpr int RM = KC + 1;
 constexpr size_t SM_EXEC = (size_t)(3 * RM * KC + KC) * 8 + (KC + 8) * 4;  // max over items (SVD items)
 static_assert(SM_EXEC >= (size_t)((PR + 1) * KC + KC + 8) * 8 + (5 * 128 + PR) * 4, "smem (weights_cluster panel + block descriptors)");
-static_assert(SM_EXEC >= (size_t)((RCAP_MAX + 1) * RCAP_MAX + (PR + 1) * KC + KC + 8) * 8 + (5 * 128 + PR) * 4, "smem (weights path: B~ + weights_cluster)");
+static_assert(SM_EXEC >= (size_t)((PR + 1) * KC + KC + 8 + 1024 + 2 * (RCAP_MAX + 1) * RCAP_MAX) * 8 + 3 * 64 * 4, "smem (weights path: panel + G chain + path)");
+static_assert((5 * 128 + PR) * 4 <= 1024 * 8, "weights_cluster descriptors fit the spare area");
 static_assert(SM_EXEC >= (size_t)24000 * 8 + 9 * 128 * 4 + 16, "smem (couplings)");
 static_assert(SM_EXEC >= (size_t)(7 * (RCAP_MAX + 1) * RCAP_MAX + (2 * RCAP_MAX + 1) * RCAP_MAX + KC) * 8 + 5 * 64 * 4, "smem (rcache path)");
 static_assert(SM_EXEC >= (size_t)(3 * (RCAP_MAX + 1) + 2 * ar::C2_MS) * RCAP_MAX * 8, "smem (it_c2core)");

@@ -22,7 +22,8 @@ __device__ __forceinline__ bool inside(const DevSide& D, int t, int root) {
 }
 
 __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm, int mode,
-                                  const double* bp_sm = nullptr, int ldbp = 0);
+                                  const double* bp_sm = nullptr, int ldbp = 0, const int* fpc = nullptr,
+                                  const int* fpk = nullptr, int fL = 0);
 
 // ---- U0 + U1/U2 leaves + local weight stacks of the ancestors (all independent) ---------------
 __device__ void it_upd_ext_leaf(const MatDev& M, UpdArgs a_, int rl0, int nrl, int cl0, int ncl,
@@ -147,10 +148,10 @@ __device__ void it_upd_ext_level(const MatDev& M, UpdArgs a_, int bA, int nA, in
 // mode W_FULL: B~_t = R([local stack; B~_{t+} E~_t^T]) -> bw[t]
 // mode W_LOCAL: C_t = R(local stack) -> re[t]   (proper ancestors of t0 only: their re slot is free)
 // mode W_CHAIN: B~_t = R([C_t; B~_{t+} E_t^T])   -> bw[t]  (C_t from re[t])
-enum { W_FULL = 0, W_LOCAL = 1, W_CHAIN = 2 };
+enum { W_FULL = 0, W_LOCAL = 1, W_CHAIN = 2, W_FLAT = 3 };
 
 __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, int t, double* sm, int mode,
-                                  const double* bp_sm, int ldbp) {
+                                  const double* bp_sm, int ldbp, const int* fpc, const int* fpk, int fL) {
   const DevSide& A = rs ? M.row : M.col;
   const DevSide& B = rs ? M.col : M.row;
   const int a0 = rs ? a.t0 : a.s0, b0 = rs ? a.s0 : a.t0;
@@ -160,7 +161,7 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
   const int p = A.parent[t];
   const int asz = A.tsize[a0], bsz = B.tsize[b0];
   const int qb = mode == W_CHAIN ? 0 : A.bptr[t], qe = mode == W_CHAIN ? 0 : A.bptr[t + 1];
-  const int kp = (p >= 0 && mode != W_LOCAL) ? A.rank[p] : 0;
+  const int kp = (p >= 0 && mode != W_LOCAL && mode != W_FLAT) ? A.rank[p] : 0;
   const bool in_t = t >= a0 && t < a0 + asz;
   const int K = kt + (in_t ? k : 0);
   double* P = sm;                 // PR x KC panel
@@ -245,7 +246,40 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
       if (j < cnt) flush();  // block j does not fit: compress first
     }
   }
-  if (kp >= 0 && p >= 0 && mode != W_LOCAL) {
+  if (mode == W_FLAT) {
+    // the ancestors' local stacks, each carried down to t by its transfer chain:
+    // rows C_a G_a^T (G_a = E_t E_{t+} ... : k_t x k_a in bw[a], C_a in re[a]), zero on the k
+    // extension columns (E~_{t0} = [E_{t0}; 0]); same R-factor as the level-by-level chain
+    // B~_t = R([C_t; B~_{t+} E~_t^T]) (left orthogonal factors drop out), one QR instead of one per level
+    int l = fL - 1;
+    while (l >= 0) {
+      int r = rows, le = l;
+      while (le >= 0 && r + fpk[le] <= PR) r += fpk[le--];
+      if (le == l) {  // the next block does not fit: compress first
+        flush();
+        continue;
+      }
+      const int nr = r - rows;
+      for (int e = threadIdx.x; e < nr * K; e += NT) {
+        const int rr = e % nr, c = e / nr;
+        int b = l, off = 0;
+        while (rr >= off + fpk[b]) off += fpk[b--];
+        const int i = rr - off, kb = fpk[b];
+        double v = 0.0;
+        if (c < kt) {
+          const double* C = A.re + (size_t)fpc[b] * M.kcap * M.kcap;
+          const double* G = A.bw + (size_t)fpc[b] * M.kcap * M.kcap;
+          for (int j = 0; j < kb; ++j) v += C[i + j * M.kcap] * G[c + j * M.kcap];
+          fl += 2.0 * kb;
+        }
+        P[rows + rr + c * PRL] = v;
+      }
+      __syncthreads();
+      rows = r;
+      l = le;
+    }
+  }
+  if (kp >= 0 && p >= 0 && mode != W_LOCAL && mode != W_FLAT) {
     const bool in_p = p >= a0 && p < a0 + asz;
     const int Kp = kp + (in_p ? k : 0);
     if (Kp > 0) {
@@ -289,12 +323,13 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// U3 along pred(t0): B~_t = R([C_t; B~_{t+} E_t^T]) from the root down to the father of
-// t0 (C_t = R-factor of t's local stack, computed in parallel by the ext_leaf op into re[t]), then
-// t0 itself with its full stack (W_FULL).  The path comes from the leaf-ancestor table (one load
-// round), the ranks are loaded at once, B~ stays in shared memory from level to level, and C_t,
-// E_t of the next level are fetched with cp.async while the current level factorizes.  Same sums
-// and the same QR as weights_cluster(W_CHAIN) level by level.
+// U3 along pred(t0): B~_{t0} = R([local stack of t0; B~_{t0+} E~_{t0}^T]) with
+// B~_t = R([C_t; B~_{t+} E_t^T]) down the path (C_t = R-factor of t's local stack, computed in
+// parallel by the ext_leaf op into re[t]).  Unrolled, B~_{t0} is the R-factor of the local stack of
+// t0 stacked over C_a G_a^T for every proper ancestor a, G_a = E_{t0} E_{t0+} ... (the transfer chain
+// from t0 up to a): the same matrix up to left orthogonal factors, hence the same R-factor (rows up
+// to sign), with ONE QR instead of one QR per level.  The path comes from the leaf-ancestor table,
+// the ranks and the path's transfer matrices are loaded in one round each.
 __device__ void it_upd_weights_path(const MatDev& M, UpdArgs a_, int l0r, int l0c, int Lr, int Lc, int item_,
                                     double* smx_) {
   UpdArgs a = a_;
@@ -304,70 +339,69 @@ __device__ void it_upd_weights_path(const MatDev& M, UpdArgs a_, int l0r, int l0
   const DevSide& A = rs ? M.row : M.col;
   const int L = rs ? Lr : Lc;                  // level of t0: path = anc[0..L]
   const int32_t* anc = A.anc + (size_t)(rs ? l0r : l0c) * A.ancw;
-  constexpr int RC = RCAP_MAX, LB = RC + 1, LP = 2 * RC + 1;
-  double* Bsh = smx_;                          // B~ of the previous level (LB x RC)
-  double* Pn = Bsh + LB * RC;                  // chain panel ((2 RC) x RC, ld LP)
-  double* Cb[2] = {Pn + LP * RC, Pn + LP * RC + LB * RC};           // C_t double buffer
-  double* Eb[2] = {Cb[1] + LB * RC, Cb[1] + 2 * LB * RC};           // E_t double buffer
-  double* diag = Eb[1] + LB * RC;
-  int* pc = reinterpret_cast<int*>(diag + KC);  // path clusters (64)
-  int* pk = pc + 64;                            // their ranks
+  constexpr int RC = RCAP_MAX, LB = RC + 1;
+  // shared memory: [weights panel + descriptors | 1024 spare | G ping-pong (2 LB x RC) | path ints]
+  constexpr int GOFF = (PR + 1) * KC + KC + 8 + 1024;
+  int* pc = reinterpret_cast<int*>(smx_ + GOFF + 2 * LB * RC);  // path clusters (64)
+  int* pk = pc + 64;                                             // their ranks (64)
   for (int l = threadIdx.x; l <= L; l += NT) pc[l] = anc[l];
   __syncthreads();
   for (int l = threadIdx.x; l <= L; l += NT) pk[l] = A.rank[pc[l]];
   __syncthreads();
-  auto fetch = [&](int l, int buf) {  // C_t (K x K, ld kcap) and E_t (k_t x k_p, ld rcap) of level l
-    const int t = pc[l], kt = pk[l], kp = l > 0 ? pk[l - 1] : 0;
-    const double* C = A.re + (size_t)t * M.kcap * M.kcap;
-    const double* E = A.tr + (size_t)t * M.rcap * M.rcap;
-    for (int e = threadIdx.x; e < kt * kt; e += NT) cp_async8(Cb[buf] + (e % kt) + (e / kt) * LB, C + (e % kt) + (e / kt) * M.kcap);
-    for (int e = threadIdx.x; e < kt * kp; e += NT) cp_async8(Eb[buf] + (e % kt) + (e / kt) * LB, E + (e % kt) + (e / kt) * M.rcap);
-    cp_async_commit();
-  };
   double fl = 0.0;
-  int kb = 0;  // rank (rows = cols) of B~ in Bsh
-  if (L > 0) fetch(0, 0);
-  for (int l = 0; l < L; ++l) {
-    const int buf = l & 1;
-    if (l + 1 < L) {
-      fetch(l + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const int kt = pk[l], kp = l > 0 ? pk[l - 1] : 0;
-    // panel [C_t; B~_{t+} E_t^T]  (K = k_t: a proper ancestor is not extended)
-    for (int e = threadIdx.x; e < kt * kt; e += NT) Pn[(e % kt) + (e / kt) * LP] = Cb[buf][(e % kt) + (e / kt) * LB];
-    int rows = kt;
-    const int Kp = l > 0 ? kb : 0;
-    if (Kp > 0) {
-      for (int e = threadIdx.x; e < Kp * kt; e += NT) {
-        const int i = e % Kp, c = e / Kp;
-        double v = 0.0;
-        for (int j = 0; j < kp; ++j) v += Bsh[i + j * LB] * Eb[buf][c + j * LB];
-        Pn[rows + i + c * LP] = v;
+  // transfer chains G_l = E_{t0} E_{a_{L-1}} ... E_{a_{l+1}} (k_{t0} x k_l) for the proper ancestors
+  // a_l, bottom-up, into bw[a_l] (free: a proper ancestor's B~ is not needed, see W_FLAT); the E
+  // matrices of the whole path are staged in shared memory in one load round first
+  if (L > 0) {
+    double* stage = smx_;                       // (the weights panel, not used yet)
+    double* Gb[2] = {smx_ + GOFF, smx_ + GOFF + LB * RC};
+    int* eo = pk + 64;                           // staging offset of E_{a_l}, l = 1..L
+    if (threadIdx.x == 0) {
+      int o = 0;
+      for (int l = 1; l <= L; ++l) {
+        eo[l] = o;
+        o += pk[l] * pk[l - 1];
       }
-      fl += 2.0 * Kp * kp * kt;
-      rows += Kp;
+      eo[0] = o;  // total
     }
     __syncthreads();
-    if (rows > 0 && kt > 0) {
-      la::cta_qr_R(Pn, LP, rows, kt, diag, diag);
-      fl += hh_flops(rows, kt);
+    const bool staged = eo[0] <= (PR + 1) * KC;
+    if (staged) {
+      for (int l = 1; l <= L; ++l) {
+        const int kl = pk[l], kq = pk[l - 1];
+        const double* E = A.tr + (size_t)pc[l] * M.rcap * M.rcap;
+        for (int e = threadIdx.x; e < kl * kq; e += NT) stage[eo[l] + e] = E[(e % kl) + (e / kl) * M.rcap];
+      }
+      __syncthreads();
     }
-    const int mk = rows < kt ? rows : kt;
-    // B~_t (kt x kt, zero rows below min(rows, kt)) -> Bsh
-    for (int e = threadIdx.x; e < kt * kt; e += NT) {
-      const int i = e % kt, j = e / kt;
-      Bsh[i + j * LB] = i < mk ? Pn[i + j * LP] : 0.0;
+    auto Eel = [&](int l, int i, int j) -> double {  // E_{a_l}(i, j)
+      return staged ? stage[eo[l] + i + j * pk[l]] : A.tr[(size_t)pc[l] * M.rcap * M.rcap + i + j * M.rcap];
+    };
+    const int kt0 = pk[L];
+    int cur = 0;
+    for (int l = L - 1; l >= 0; --l) {
+      const int kl = pk[l], kn = pk[l + 1];
+      double* Gn = Gb[cur];
+      double* Gg = A.bw + (size_t)pc[l] * M.kcap * M.kcap;
+      for (int e = threadIdx.x; e < kt0 * kl; e += NT) {
+        const int i = e % kt0, j = e / kt0;
+        double v;
+        if (l == L - 1) {
+          v = Eel(L, i, j);  // G_{L-1} = E_{t0}
+        } else {
+          v = 0.0;
+          for (int q = 0; q < kn; ++q) v += Gb[cur ^ 1][i + q * LB] * Eel(l + 1, q, j);
+        }
+        Gn[i + j * LB] = v;
+        Gg[i + j * M.kcap] = v;
+      }
+      fl += 2.0 * kt0 * kn * kl;
+      cur ^= 1;
+      __syncthreads();
     }
-    kb = kt;
-    __syncthreads();
   }
-  // t0: full local stack + B~_{t0+} E~_{t0}^T (B~ of the father from shared memory)
-  double* rest = smx_ + LB * RC;  // weights_cluster's panel after Bsh
-  fl += weights_cluster(M, a, rs, pc[L], rest, W_FULL, L > 0 ? Bsh : nullptr, LB);
+  // t0: its full local stack + every ancestor's local stack carried down (one TSQR)
+  fl += weights_cluster(M, a, rs, pc[L], smx_, W_FLAT, nullptr, 0, pc, pk, L);
   if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_W_PATH, fl);
 }
 
@@ -405,6 +439,7 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
   long long c1;
   int p, sweeps;
   double* W = Bt;
+  const int path = (K <= m && m <= 16) ? 0 : (K <= 32 ? 1 : 2);  // profiling: which SVD variant
   if (K <= m && m <= 16) {  // K columns of length m <= 16 (no QR)
     // M = V B~^T (m x K) in Mm; one-sided Jacobi on M in registers of one warp (lane j owns
     // column j), W = M J = [sigma_j u_j] into Bt (free after the product)
@@ -490,6 +525,9 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
       atomicAdd(dbg + 4, (double)K);
       atomicAdd(dbg + 5, (double)m);
       atomicAdd(dbg + 6, (double)sweeps);
+      atomicAdd(dbg + 7 + path, 1.0);                        // calls per variant
+      atomicAdd(dbg + 10 + path, (double)(clock64() - c0));  // cycles per variant
+      if (kid == K_SVD_LEAF) atomicAdd(dbg + 13, 1.0);
     }
   }
 }
