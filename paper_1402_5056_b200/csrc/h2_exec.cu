@@ -39,7 +39,7 @@ static_assert(SM_EXEC >= (size_t)((PR + 1) * KC + KC + 8) * 8 + (5 * 128 + PR) *
 static_assert(SM_EXEC >= (size_t)((PR + 1) * KC + KC + 8 + 1024 + 2 * (RCAP_MAX + 1) * RCAP_MAX) * 8 + 3 * 64 * 4, "smem (weights path: panel + G chain + path)");
 static_assert((5 * 128 + PR) * 4 <= 1024 * 8, "weights_cluster descriptors fit the spare area");
 static_assert(SM_EXEC >= (size_t)24000 * 8 + 9 * 128 * 4 + 16, "smem (couplings)");
-static_assert(SM_EXEC >= (size_t)(7 * (RCAP_MAX + 1) * RCAP_MAX + (2 * RCAP_MAX + 1) * RCAP_MAX + KC) * 8 + 5 * 64 * 4, "smem (rcache path)");
+static_assert(SM_EXEC >= (size_t)((PR + 1) * RCAP_MAX + KC + 3 * (RCAP_MAX + 1) * RCAP_MAX) * 8 + 4 * 64 * 4, "smem (rcache items)");
 static_assert(SM_EXEC >= (size_t)(3 * (RCAP_MAX + 1) + 2 * ar::C2_MS) * RCAP_MAX * 8, "smem (it_c2core)");
 static_assert(SM_EXEC >= (size_t)(3 * (KC + 1) * KC + KC) * 8 + (KC + 8) * 4 && SM_EXEC >= (size_t)((2 * KC + 1) * KC + KC + 8) * 8, "smem");
 
@@ -582,7 +582,7 @@ cudaError_t launch_update(const h2_mat_* Z, const UpdArgs& a_in, cudaStream_t st
   const int nA = R->tsize[a.t0], nB = C->tsize[a.s0];
   c->emit(OP_UPD_COUPLE, nA + nB, &M, pu(a, nA, nB));   // U5
   c->emit(OP_UPD_INSTALL, nA + nB, &M, pu(a, nA, nB));  // U6
-  c->emit(OP_UPD_RCACHE, 2, &M, pu(a, rl0, cl0, Lr, Lc));  // R-factor caches on pred(t0), pred(s0)
+  c->emit(OP_UPD_RCACHE, Lr + Lc, &M, pu(a, rl0, cl0, Lr, Lc));  // R-factor caches on pred(t0), pred(s0): item per ancestor
   if (skip) c->end_skip(skip_at, g_big);
   return ac.done();
 }

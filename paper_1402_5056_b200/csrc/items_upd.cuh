@@ -781,108 +781,106 @@ __device__ void it_upd_install(const MatDev& M, UpdArgs a_, int nA, int nB, int 
 }
 
 // ---- memoised R-factors on pred(t0) ----------------------------------------------------------
-// rc[t] = R([rc[t1] E_t1; rc[t2] E_t2]) from the father of t0 up to the root (Alg. 16 recursion on the
-// changed path, reading R7).  The on-path son's R stays in shared memory from level to level; the
-// sibling's R and both transfer matrices of the next level arrive by cp.async while the current
-// level factorizes; the path, ranks and sons are loaded in three rounds up front.
+// rc[a] = R-factor of the nested basis V_a (Alg. 16 recursion, reading R7) for every proper ancestor
+// a = a_l of t0 (path a_0 = root ... a_L = t0, s_j = the sibling of a_j).  Unrolled down the path:
+//   V_a ~ [ rc[a_L] E_{a_L} T_L ; rc[s_L] E_{s_L} T_L ; ... ; rc[s_{l+1}] E_{s_{l+1}} T_{l+1} ]
+// (up to left orthogonal factors), T_{l+1} = I, T_{j+1} = E_{a_j} T_j the transfer chain from a_j up
+// to a.  So every ancestor is one independent item -- a chain of small products and ONE QR --
+// instead of a sequential chain of QRs from the father of t0 to the root.
 __device__ void it_upd_rcache_path(const MatDev& M, UpdArgs a_, int l0r, int l0c, int Lr, int Lc, int item_,
                                    double* smx_) {
   UpdArgs a = a_;
   if (a.kdev) a.k = *a.kdev;
   if (a.k <= 0) return;
-  const bool rs = item_ == 0;
+  const bool rs = item_ < Lr;
   const DevSide& D = rs ? M.row : M.col;
   const int L = rs ? Lr : Lc;
-  if (L == 0) return;
+  const int l = rs ? item_ : item_ - Lr;  // this item's ancestor level
   const int32_t* anc = D.anc + (size_t)(rs ? l0r : l0c) * D.ancw;
-  constexpr int RC = RCAP_MAX, LB = RC + 1, LP = 2 * RC + 1;
-  double* Ron = smx_;                                  // R of the on-path son (LB x RC)
-  double* Pn = Ron + LB * RC;                          // panel (2 RC x RC, ld LP)
-  double* Rb[2] = {Pn + LP * RC, Pn + LP * RC + LB * RC};  // sibling R (double buffer)
-  double* E0[2] = {Rb[1] + LB * RC, Rb[1] + 2 * LB * RC};  // E of son0
-  double* E1[2] = {E0[1] + LB * RC, E0[1] + 2 * LB * RC};  // E of son1
-  double* diag = E1[1] + LB * RC;
-  int* pc = reinterpret_cast<int*>(diag + KC);  // path clusters
-  int* pk = pc + 64;                            // their ranks
-  int* ps = pk + 64;                            // sibling of the on-path son at level l
-  int* psk = ps + 64;                           // its rank
-  int* pon0 = psk + 64;                         // 1 if the on-path son is son0
-  for (int l = threadIdx.x; l <= L; l += NT) pc[l] = anc[l];
+  constexpr int RC = RCAP_MAX, LB = RC + 1;
+  double* P = smx_;                        // panel (PR x RC, ld PRL)
+  double* diag = P + PRL * RC;
+  double* T[2] = {diag + KC, diag + KC + LB * RC};  // transfer chain ping-pong (k_j x k_l)
+  double* U = T[1] + LB * RC;              // E_s T (k_s x k_l)
+  int* pc = reinterpret_cast<int*>(U + LB * RC);  // path a_0..a_L
+  int* pk = pc + 64;                       // ranks
+  int* ps = pk + 64;                       // sibling s_j of a_j (j >= 1)
+  int* psk = ps + 64;                      // its rank
+  for (int j = threadIdx.x; j <= L; j += NT) pc[j] = anc[j];
   __syncthreads();
-  for (int l = threadIdx.x; l <= L; l += NT) {
-    pk[l] = D.rank[pc[l]];
-    if (l < L) {
-      const int s0 = D.son0[pc[l]], s1 = D.son1[pc[l]];
-      const bool on0 = s0 == pc[l + 1];
-      ps[l] = on0 ? s1 : s0;
-      pon0[l] = on0 ? 1 : 0;
+  for (int j = threadIdx.x; j <= L; j += NT) {
+    pk[j] = D.rank[pc[j]];
+    if (j > 0) {
+      const int par = pc[j - 1];
+      const int s0 = D.son0[par], s1 = D.son1[par];
+      ps[j] = s0 == pc[j] ? s1 : s0;
     }
   }
   __syncthreads();
-  for (int l = threadIdx.x; l < L; l += NT) psk[l] = D.rank[ps[l]];
+  for (int j = threadIdx.x + 1; j <= L; j += NT) psk[j] = D.rank[ps[j]];
   __syncthreads();
-  auto fetch = [&](int l, int buf) {  // level l: sibling R, E of both sons (k_son x k_t, ld rcap)
-    const int t = pc[l], kt = pk[l];
-    const int son_on = pc[l + 1], kon = pk[l + 1], sib = ps[l], ksib = psk[l];
-    const int c0 = pon0[l] ? son_on : sib, c1 = pon0[l] ? sib : son_on;
-    const int k0 = pon0[l] ? kon : ksib, k1 = pon0[l] ? ksib : kon;
-    const double* R = D.rc + (size_t)sib * M.rcap * M.rcap;
-    const double* Ea = D.tr + (size_t)c0 * M.rcap * M.rcap;
-    const double* Eb = D.tr + (size_t)c1 * M.rcap * M.rcap;
-    (void)t;
-    for (int e = threadIdx.x; e < ksib * ksib; e += NT)
-      cp_async8(Rb[buf] + (e % ksib) + (e / ksib) * LB, R + (e % ksib) + (e / ksib) * M.rcap);
-    for (int e = threadIdx.x; e < k0 * kt; e += NT)
-      cp_async8(E0[buf] + (e % k0) + (e / k0) * LB, Ea + (e % k0) + (e / k0) * M.rcap);
-    for (int e = threadIdx.x; e < k1 * kt; e += NT)
-      cp_async8(E1[buf] + (e % k1) + (e / k1) * LB, Eb + (e % k1) + (e / k1) * M.rcap);
-    cp_async_commit();
+  const int kl = pk[l];
+  int rows = 0;
+  double fl = 0.0;
+  // T_{l+1} = I (k_l x k_l)
+  for (int e = threadIdx.x; e < kl * kl; e += NT) T[0][(e % kl) + (e / kl) * LB] = (e % kl) == (e / kl) ? 1.0 : 0.0;
+  __syncthreads();
+  int cur = 0;
+  auto append = [&](const double* R, int kr, const double* E, int kp) {
+    // rows rc (kr x kr, upper triangular, ld rcap) * E (kr x kp, ld rcap) * T (kp x kl)
+    if (kr == 0 || kl == 0) return;
+    for (int e = threadIdx.x; e < kr * kl; e += NT) {  // U = E T
+      const int i = e % kr, c = e / kr;
+      double v = 0.0;
+      for (int q = 0; q < kp; ++q) v += E[i + q * M.rcap] * T[cur][q + c * LB];
+      U[i + c * LB] = v;
+    }
+    __syncthreads();
+    if (rows + kr > PR) {
+      la::cta_qr_R(P, PRL, rows, kl, diag, diag);
+      fl += hh_flops(rows, kl);
+      rows = rows < kl ? rows : kl;
+    }
+    for (int e = threadIdx.x; e < kr * kl; e += NT) {  // rows rc U
+      const int i = e % kr, c = e / kr;
+      double v = 0.0;
+      for (int q = i; q < kr; ++q) v += R[i + q * M.rcap] * U[q + c * LB];
+      P[rows + i + c * PRL] = v;
+    }
+    fl += 2.0 * kr * kp * kl + (double)kr * kr * kl;
+    rows += kr;
+    __syncthreads();
   };
-  // R of t0 (installed by the previous op) into Ron
-  {
-    const int kon = pk[L];
-    const double* R = D.rc + (size_t)pc[L] * M.rcap * M.rcap;
-    for (int e = threadIdx.x; e < kon * kon; e += NT) Ron[(e % kon) + (e / kon) * LB] = R[(e % kon) + (e / kon) * M.rcap];
-  }
-  fetch(L - 1, 0);
-  for (int l = L - 1, it = 0; l >= 0; --l, ++it) {
-    const int buf = it & 1;
-    if (l > 0) {
-      fetch(l - 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const int kt = pk[l], kon = pk[l + 1], ksib = psk[l];
-    const bool on0 = pon0[l] != 0;
-    int row0 = 0;
-    for (int q = 0; q < 2; ++q) {
-      const bool on = (q == 0) == on0;
-      const int kc = on ? kon : ksib;
-      const double* RC = on ? Ron : Rb[buf];
-      const double* E = q ? E1[buf] : E0[buf];
-      for (int e = threadIdx.x; e < kc * kt; e += NT) {
-        const int i = e % kc, j = e / kc;
+  for (int j = l + 1; j <= L; ++j) {
+    // the sibling of a_j, carried up to a_l
+    append(D.rc + (size_t)ps[j] * M.rcap * M.rcap, psk[j], D.tr + (size_t)ps[j] * M.rcap * M.rcap, pk[j - 1]);
+    if (j == L) {  // t0 itself (its R was installed by the previous op)
+      append(D.rc + (size_t)pc[L] * M.rcap * M.rcap, pk[L], D.tr + (size_t)pc[L] * M.rcap * M.rcap, pk[L - 1]);
+    } else {       // T_{j+1} = E_{a_j} T_j  (k_j x k_l)
+      const int kj = pk[j], kq = pk[j - 1];
+      const double* E = D.tr + (size_t)pc[j] * M.rcap * M.rcap;
+      for (int e = threadIdx.x; e < kj * kl; e += NT) {
+        const int i = e % kj, c = e / kj;
         double v = 0.0;
-        for (int p = i; p < kc; ++p) v += RC[i + p * LB] * E[p + j * LB];
-        Pn[row0 + i + j * LP] = v;
+        for (int q = 0; q < kq; ++q) v += E[i + q * M.rcap] * T[cur][q + c * LB];
+        T[cur ^ 1][i + c * LB] = v;
       }
-      row0 += kc;
+      fl += 2.0 * kj * kq * kl;
+      cur ^= 1;
+      __syncthreads();
     }
-    __syncthreads();
-    if (kt > 0) la::cta_qr_R(Pn, LP, row0, kt, diag, diag);
-    if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_RCACHE, hh_flops(row0, kt) + (double)row0 * row0 * kt);
-    double* RCg = D.rc + (size_t)pc[l] * M.rcap * M.rcap;
-    const int mk = row0 < kt ? row0 : kt;
-    for (int e = threadIdx.x; e < kt * kt; e += NT) {
-      const int i = e % kt, j = e / kt;
-      const double v = i < mk ? Pn[i + j * LP] : 0.0;
-      RCg[i + j * M.rcap] = v;
-      Ron[i + j * LB] = v;
-    }
-    __syncthreads();
   }
+  if (rows > 0 && kl > 0) {
+    la::cta_qr_R(P, PRL, rows, kl, diag, diag);
+    fl += hh_flops(rows, kl);
+  }
+  double* RCg = D.rc + (size_t)pc[l] * M.rcap * M.rcap;
+  const int mk = rows < kl ? rows : kl;
+  for (int e = threadIdx.x; e < kl * kl; e += NT) {
+    const int i = e % kl, j = e / kl;
+    RCg[i + j * M.rcap] = i < mk ? P[i + j * PRL] : 0.0;
+  }
+  if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_RCACHE, fl);
 }
 
 }  // namespace upd
