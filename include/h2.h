@@ -108,6 +108,16 @@ h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t k, double 
                             const double* X, int64_t ldx, const double* Y, int64_t ldy,
                             const h2_trunc* trunc, h2_stream stream);
 
+/* Batch recording (execution only, no change of the arithmetic): between h2_batch_begin(stream)
+ * and h2_batch_end(), h2_lowrank_update calls on that stream are recorded into one device op list
+ * that the executor runs in chunks (16,384 ops) while recording continues, instead of one executor
+ * launch per call; the result is bit-identical to unbatched calls (same ops, same order).  The
+ * caller keeps every X / Y alive and unchanged until the stream passes h2_batch_end.  Inside a
+ * batch only h2_lowrank_update (same stream) may be called; every other call returns H2_ERR_ARG.
+ * One open batch per host thread.  H2_ERR_ARG: nested begin / end without begin; H2_ERR_CUDA. */
+h2_status h2_batch_begin(h2_stream stream);
+h2_status h2_batch_end(void);
+
 /* y <- alpha op(Z) x + beta y (op = transpose ? Z^T : Z), x/y device vectors in ORIGINAL order
  * (forward transform, couplings, backward transform, nearfield). */
 h2_status h2_matvec(h2_mat Z, int32_t transpose, double alpha, const double* x, double beta, double* y,

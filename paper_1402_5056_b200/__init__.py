@@ -15,6 +15,8 @@ from .h2 import (  # noqa: F401
     h2_block_tree,
     h2_from_sparse,
     h2_lowrank_update,
+    h2_batch_begin,
+    h2_batch_end,
     h2_matvec,
     h2_addmul,
     h2_lr_factor,

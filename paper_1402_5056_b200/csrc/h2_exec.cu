@@ -381,6 +381,9 @@ void ExecCtx::end_skip(size_t at, int big_items) {
 void exec_begin(ExecCtx* ctx, cudaStream_t st) {
   ctx->st = st;
   ctx->ops.clear();
+  for (int i = 0; i < EXEC_MATS; ++i) ctx->mats[i] = nullptr;  // a reused context starts empty
+  ctx->hold = 0;
+  ctx->group = 0;
   g_ctx = ctx;
 }
 

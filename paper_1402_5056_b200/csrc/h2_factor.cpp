@@ -737,6 +737,10 @@ h2_status run_driver(h2_mat_* Z, const h2_trunc* trunc, h2_stream stream, int wh
 }  // namespace
 
 extern "C" h2_status h2_lr_factor(h2_mat A, h2_factor_kind kind, const h2_trunc* trunc, h2_stream stream) {
+  if (h2::batch_open()) {
+    h2::set_error("h2_lr_factor: not allowed inside h2_batch_begin/h2_batch_end");
+    return H2_ERR_ARG;
+  }
   if (!A) {
     h2::set_error("h2_lr_factor: NULL matrix");
     return H2_ERR_ARG;
@@ -759,6 +763,10 @@ extern "C" h2_status h2_lr_factor(h2_mat A, h2_factor_kind kind, const h2_trunc*
 }
 
 extern "C" h2_status h2_addmul(h2_mat Z, double alpha, h2_mat X, h2_mat Y, const h2_trunc* trunc, h2_stream stream) {
+  if (h2::batch_open()) {
+    h2::set_error("h2_addmul: not allowed inside h2_batch_begin/h2_batch_end");
+    return H2_ERR_ARG;
+  }
   if (!Z || !X || !Y) {
     h2::set_error("h2_addmul: NULL matrix");
     return H2_ERR_ARG;
@@ -784,6 +792,10 @@ extern "C" h2_status h2_addmul(h2_mat Z, double alpha, h2_mat X, h2_mat Y, const
 }
 
 extern "C" h2_status h2_solve(h2_mat F, double* x, int32_t nrhs, int64_t ldx, h2_stream stream) {
+  if (h2::batch_open()) {
+    h2::set_error("h2_solve: not allowed inside h2_batch_begin/h2_batch_end");
+    return H2_ERR_ARG;
+  }
   if (!F || !x) {
     h2::set_error("h2_solve: NULL argument");
     return H2_ERR_ARG;

@@ -12,9 +12,11 @@
 #include <cstring>
 #include <functional>
 #include <new>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "exec.h"
 #include "h2_internal.h"
 
 using namespace h2;
@@ -29,6 +31,11 @@ extern "C" const char* h2_last_error(void) { return g_last_error.c_str(); }
   do {                      \
     h2::set_error(msg);     \
     return code;            \
+  } while (0)
+// calls that read or launch on their own must not interleave with an open batch recording
+#define H2_NO_BATCH(name)                                                                          \
+  do {                                                                                             \
+    if (h2::batch_open()) H2_FAIL(H2_ERR_ARG, name ": not allowed inside h2_batch_begin/h2_batch_end"); \
   } while (0)
 
 #define CUDA_TRY(expr)                                                                      \
@@ -493,6 +500,7 @@ extern "C" h2_status h2_from_sparse(h2_btree bt, int64_t n, const int64_t* rowpt
 // ------------------------------------------------------------------------------------------------
 extern "C" h2_status h2_matvec(h2_mat Z, int32_t transpose, double alpha, const double* x, double beta,
                                double* y, h2_stream stream) {
+  H2_NO_BATCH("h2_matvec");
   if (!Z || !x || !y) H2_FAIL(H2_ERR_ARG, "h2_matvec: NULL argument");
   if (!std::isfinite(alpha) || !std::isfinite(beta)) H2_FAIL(H2_ERR_NONFINITE, "h2_matvec: non-finite scalar");
   CUDA_TRY(launch_matvec(Z, transpose ? 1 : 0, alpha, x, beta, y, (cudaStream_t)stream));
@@ -517,6 +525,8 @@ extern "C" h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t
   if (!(tc.rel_tol >= 0) || !(tc.abs_tol >= 0)) H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: negative tolerance");
   if (Z->lower && B->rt->lo[t0] < B->ct->lo[s0])
     H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: target block is not stored in H2_LOWER storage");
+  if (h2::batch_open() && h2::exec_ctx()->st != (cudaStream_t)stream)
+    H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: inside a batch every update must use the batch's stream");
   if (k == 0) return H2_OK;  // bit-identical
   h2_status st;
   if ((st = alloc_update_workspace(Z, Z->d.row)) != H2_OK) return st;
@@ -535,7 +545,11 @@ extern "C" h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t
   a.max_rank = tc.max_rank;
   a.kdev = nullptr;
   a.prof = nullptr;
-  CUDA_TRY(launch_update(Z, a, (cudaStream_t)stream));
+  try {
+    CUDA_TRY(launch_update(Z, a, (cudaStream_t)stream));
+  } catch (const std::exception& ex) {  // recording errors (e.g. too many matrices in one batch)
+    H2_FAIL(H2_ERR_ARG, std::string("h2_lowrank_update: ") + ex.what());
+  }
   if (B->kind[b0] != INADM) {  // the update may give the bases of T_{t0} / T_{s0} a non-zero rank
     for (int q = t0; q < t0 + B->rt->tsize[t0]; ++q) Z->nzr[q] = 1;
     for (int q = s0; q < s0 + B->ct->tsize[s0]; ++q) Z->nzc[q] = 1;
@@ -547,6 +561,7 @@ extern "C" h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t
 // Inspection
 // ------------------------------------------------------------------------------------------------
 extern "C" h2_status h2_ranks(h2_mat Z, int32_t* row_rank, int32_t* col_rank) {
+  H2_NO_BATCH("h2_ranks");
   if (!Z) H2_FAIL(H2_ERR_ARG, "h2_ranks: NULL matrix");
   CUDA_TRY(cudaDeviceSynchronize());
   if (row_rank)
@@ -557,6 +572,7 @@ extern "C" h2_status h2_ranks(h2_mat Z, int32_t* row_rank, int32_t* col_rank) {
 }
 
 extern "C" h2_status h2_check_device_flags(h2_mat Z, int32_t* flags) {
+  H2_NO_BATCH("h2_check_device_flags");
   if (!Z || !flags) H2_FAIL(H2_ERR_ARG, "h2_check_device_flags: NULL argument");
   CUDA_TRY(cudaDeviceSynchronize());
   int32_t f[3];
@@ -573,6 +589,7 @@ extern "C" h2_status h2_check_device_flags(h2_mat Z, int32_t* flags) {
 }
 
 extern "C" h2_status h2_stats(h2_mat Z, int64_t out[4]) {
+  H2_NO_BATCH("h2_stats");
   if (!Z || !out) H2_FAIL(H2_ERR_ARG, "h2_stats: NULL argument");
   for (int i = 0; i < 3; ++i) out[i] = Z->stats[i];
   int32_t nz = 0;
@@ -583,6 +600,7 @@ extern "C" h2_status h2_stats(h2_mat Z, int64_t out[4]) {
 }
 
 extern "C" h2_status h2_storage_report(h2_mat Z, int64_t scalars[4]) {
+  H2_NO_BATCH("h2_storage_report");
   if (!Z || !scalars) H2_FAIL(H2_ERR_ARG, "h2_storage_report: NULL argument");
   const h2_btree_* B = Z->bt;
   std::vector<int32_t> kr(Z->d.row.nclusters), kc(Z->d.col.nclusters);
@@ -606,6 +624,7 @@ extern "C" h2_status h2_storage_report(h2_mat Z, int64_t scalars[4]) {
 
 extern "C" h2_status h2_export(h2_mat Z, double* V, double* E, double* W, double* F, double* S, double* N,
                                int64_t sizes[6]) {
+  H2_NO_BATCH("h2_export");
   if (!Z || !sizes) H2_FAIL(H2_ERR_ARG, "h2_export: NULL argument");
   const h2_btree_* B = Z->bt;
   const h2_tree_* R = B->rt;
@@ -657,5 +676,29 @@ extern "C" h2_status h2_export(h2_mat Z, double* V, double* E, double* W, double
   sizes[3] = nF;
   sizes[4] = nS;
   sizes[5] = nN;
+  return H2_OK;
+}
+
+// ---- batch recording (include/h2.h) ----------------------------------------------------------
+namespace {
+thread_local h2::ExecCtx g_batch_ctx;
+thread_local bool g_batch_open = false;
+}  // namespace
+
+bool h2::batch_open() { return g_batch_open; }
+
+extern "C" h2_status h2_batch_begin(h2_stream stream) {
+  if (g_batch_open) H2_FAIL(H2_ERR_ARG, "h2_batch_begin: a batch is already open");
+  if (h2::exec_ctx()) H2_FAIL(H2_ERR_ARG, "h2_batch_begin: another recording is active");
+  h2::exec_begin(&g_batch_ctx, (cudaStream_t)stream);
+  g_batch_open = true;
+  return H2_OK;
+}
+
+extern "C" h2_status h2_batch_end(void) {
+  if (!g_batch_open) H2_FAIL(H2_ERR_ARG, "h2_batch_end: no open batch");
+  g_batch_open = false;
+  cudaError_t e = h2::exec_end();
+  if (e != cudaSuccess) H2_FAIL(H2_ERR_CUDA, std::string("h2_batch_end: ") + cudaGetErrorString(e));
   return H2_OK;
 }

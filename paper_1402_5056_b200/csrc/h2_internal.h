@@ -144,6 +144,8 @@ struct h2_mat_ {
 
 namespace h2 {
 void set_error(const std::string& msg);
+// true while an h2_batch_begin / h2_batch_end recording is open on this thread
+bool batch_open();
 
 // launchers (h2_matvec.cu)
 cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const double* x, double beta,

@@ -71,6 +71,10 @@ using namespace h2;
 
 extern "C" h2_status h2_pcg(h2_mat A, h2_mat F, const double* b, double* x, double tol, int32_t maxit,
                             int32_t* iters, double* relres, h2_stream stream) {
+  if (h2::batch_open()) {
+    h2::set_error("h2_pcg: not allowed inside h2_batch_begin/h2_batch_end");
+    return H2_ERR_ARG;
+  }
   if (!A || !F || !b || !x || !iters) {
     set_error("h2_pcg: NULL argument");
     return H2_ERR_ARG;

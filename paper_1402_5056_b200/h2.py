@@ -19,7 +19,7 @@ EXPORTED_SYMBOLS = [
     "h2_from_sparse", "h2_lowrank_update", "h2_matvec", "h2_addmul", "h2_lr_factor", "h2_solve",
     "h2_ranks", "h2_storage_report", "h2_export", "h2_check_device_flags",
     "h2_profile_enable", "h2_profile_read", "h2_profile_debug", "h2_profile_ops", "h2_stats", "h2_pcg", "h2_launch_count",
-    "h2_mat_destroy", "h2_last_error",
+    "h2_mat_destroy", "h2_last_error", "h2_batch_begin", "h2_batch_end",
 ]
 
 if not os.path.exists(_LIBPATH):
@@ -60,6 +60,8 @@ _sig = {
     "h2_profile_read": [_p, _p, _p, _p, _p, _p],
     "h2_mat_destroy": [_p],
     "h2_last_error": [],
+    "h2_batch_begin": [_p],
+    "h2_batch_end": [],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -219,7 +221,29 @@ def h2_lowrank_update(Z: Mat, t0: int, s0: int, X, Y, alpha: float = 1.0, trunc:
     tr = _ctrunc(trunc)
     _check(_lib.h2_lowrank_update(Z.h, int(t0), int(s0), int(k), float(alpha), _ptr(Xc), int(ldx), _ptr(Yc),
                                   int(ldy), C.byref(tr), _stream(stream)))
+    if _batch_keep is not None:  # deferred execution: the recorded pointers must stay valid
+        _batch_keep.append((X, Y, Xc, Yc))
     return Xc, Yc  # caller keeps them alive until the stream passes the call
+
+
+_batch_keep = None  # factor copies made by the binding while a batch is open (kept until h2_batch_end)
+
+
+def h2_batch_begin(stream=None):
+    """Record the following h2_lowrank_update calls (same stream) into one device op list.  The
+    column-major copies the binding makes of non-column-major factors are kept alive until
+    h2_batch_end (their memory can then only be reused by later work on the same stream)."""
+    global _batch_keep
+    _check(_lib.h2_batch_begin(_stream(stream)))
+    _batch_keep = []
+
+
+def h2_batch_end():
+    global _batch_keep
+    try:
+        _check(_lib.h2_batch_end())
+    finally:
+        _batch_keep = None
 
 
 def h2_matvec(Z: Mat, x, y=None, alpha: float = 1.0, beta: float = 0.0, transpose: bool = False, stream=None):

@@ -140,3 +140,42 @@ def test_mutation_is_detected():
     b = next(iter(k for k, v in OZ.S.items() if v.size))
     OZ.S[b] = OZ.S[b] + 1e-3
     assert operator_rel_diff(s["Z"], OZ, s["ot"].n) > 1e-9
+
+
+def test_batched_updates_bit_identical_and_guarded():
+    """h2_batch_begin/h2_batch_end records a whole dependent update stream into one op list: the
+    result is bit-identical to one call per update (same ops, same order) and to the oracle's
+    ranks; other calls inside a batch are refused (include/h2.h)."""
+    s = setup("C1")
+    ups = c1_stream(adm_targets(s["ot"], s["ob"]), 120, 8, seed=5)
+    trunc = P.Trunc(1e-12, 0.0, 16)
+    Zb = P.h2_from_sparse(s["bt"], s["c"]["A"], rank_cap=16, update_cap=32)
+    keep = [(_t(X), _t(Y)) for _, _, X, Y in ups]
+    torch.cuda.synchronize()
+    P.h2_batch_begin()
+    with pytest.raises(P.H2Error) as e:
+        P.h2_matvec(Zb, torch.zeros(s["ot"].n, dtype=torch.float64, device="cuda"))
+    assert e.value.status == "H2_ERR_ARG"
+    with pytest.raises(P.H2Error):
+        P.h2_batch_begin()
+    for (t0, s0, _, _), (X, Y) in zip(ups, keep):
+        P.h2_lowrank_update(Zb, t0, s0, X, Y, trunc=trunc)
+    P.h2_batch_end()
+    with pytest.raises(P.H2Error):
+        P.h2_batch_end()
+    Z1 = s["Z"]  # rank_cap 32 in setup: rebuild with the same capacities as Zb
+    Z1 = P.h2_from_sparse(s["bt"], s["c"]["A"], rank_cap=16, update_cap=32)
+    for (t0, s0, _, _), (X, Y) in zip(ups, keep):
+        P.h2_lowrank_update(Z1, t0, s0, X, Y, trunc=trunc)
+    kb, lb = P.h2_ranks(Zb)
+    k1, l1 = P.h2_ranks(Z1)
+    np.testing.assert_array_equal(kb, k1)
+    np.testing.assert_array_equal(lb, l1)
+    Xp = np.random.default_rng(2).standard_normal((s["ot"].n, 4))
+    np.testing.assert_array_equal(gpu_apply(Zb, Xp), gpu_apply(Z1, Xp))
+    up = Updater(s["OZ"], OTrunc(1e-12, 0.0, 16))
+    for t0, s0, X, Y in ups:
+        up(t0, s0, X, Y)
+    np.testing.assert_array_equal(kb, s["OZ"].k)
+    np.testing.assert_array_equal(lb, s["OZ"].l)
+    assert operator_rel_diff(Zb, s["OZ"], s["ot"].n) <= 1e-9
