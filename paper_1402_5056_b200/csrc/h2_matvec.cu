@@ -83,23 +83,32 @@ __device__ void mv_up(const MvArgs& a, int s, int lane) {
   }
   for (;;) {
     const int p = a.s_parent[s];
+    if (p < 0) return;
+    // the father's structure and transfer matrices are static: fetch them (ranks into registers,
+    // the F columns of this lane into L1) before the arrival handshake, so the climb step after it
+    // waits only for the sibling's coefficients
+    const int kp = a.s_rank[p];
+    const int sc0 = a.s_son0[p], sc1 = a.s_son1[p];
+    const int sk0 = a.s_rank[sc0], sk1 = a.s_rank[sc1];
+    for (int j = lane; j < kp; j += 32)
+      for (int q = 0; q < 2; ++q) {
+        const double* F = a.s_tr + (size_t)(q ? sc1 : sc0) * rcap * rcap + (size_t)j * rcap;
+        const int kc = q ? sk1 : sk0;
+        for (int i = 0; i < kc; i += 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(F + i));
+      }
     __threadfence();
     __syncwarp();
-    if (p < 0) {
-      return;
-    }
     int old = 0;
     if (lane == 0) old = atomicAdd(a.s_arrive + p, 1);
     old = __shfl_sync(FULL, old, 0);
     if (old == 0) return;  // first of the two sons: the sibling finishes the father
     if (lane == 0) a.s_arrive[p] = 0;
     __threadfence();
-    const int kp = a.s_rank[p];
     for (int j = lane; j < kp; j += 32) {
       double acc = 0.0;
       for (int q = 0; q < 2; ++q) {
-        const int c = q ? a.s_son1[p] : a.s_son0[p];
-        const int kc = a.s_rank[c];
+        const int c = q ? sc1 : sc0;
+        const int kc = q ? sk1 : sk0;
         const double* F = a.s_tr + (size_t)c * rcap * rcap;
         const double* xc = a.s_xh + (size_t)c * rcap;
         for (int i = 0; i < kc; ++i) acc += F[i + (size_t)j * rcap] * __ldcg(xc + i);
