@@ -131,6 +131,16 @@ h2_status h2_matvec(h2_mat Z, int32_t transpose, double alpha, const double* x, 
  * trees; Z must not alias X or Y.  Truncation of every update and temporary by *trunc. */
 h2_status h2_addmul(h2_mat Z, double alpha, h2_mat X, h2_mat Y, const h2_trunc* trunc, h2_stream stream);
 
+/* In-place approximate inverse A <- A^{-1} (Remark 1): block Gauss
+ * elimination over the cluster tree, C11 = A11^{-1}, B12 = C11 A12, B21 = A21 C11,
+ * S = A22 - A21 B12 (P:1382 prints A11: reading R20), C22 = S^{-1}, C12 = -B12 C22,
+ * C21 = -C22 B21, C11 = C11 - C12 B21 -- six h2_addmul-type products per level, truncated by
+ * *trunc; a leaf tile is inverted directly (Gauss-Jordan; a pivot |p| <= 1e-14 ||tile||_F is a
+ * breakdown, reported by h2_check_device_flags as H2_ERR_BREAKDOWN).  A: unfactored H2_FULL
+ * storage, shared row/column tree.  Allocates a scratch matrix of A's structure for B12 / B21 and
+ * synchronizes `stream` before releasing it. */
+h2_status h2_inverse(h2_mat A, const h2_trunc* trunc, h2_stream stream);
+
 /* In-place factorization:
  *   H2_CHOLESKY: A in H2_LOWER storage, symmetric positive definite; on return the
  *     stored lower triangle holds L (diagonal tiles lower-triangular) with A ~ L L^T;

@@ -14,6 +14,7 @@ PAPER §3 and §6 in the paper's order and notation:
            admissible-leaf case (not described in the paper, reading R8): S_b <- 0 and a local
            update with (V_t S_b, L^{-1} W_s) (resp. (L^{-1} V_t S_b, W_s))
   solve    vector forward/backward substitution with the factors (preconditioner of P:1440-1444)
+  inv      approximate inverse by block Gauss elimination, six products per level
   pcg      preconditioned CG [HEST52] to ||r||/||b|| < 1e-8 (reading R12)
   power    power iteration for ||I - A~^{-1} A|| (reading R11)
 
@@ -457,6 +458,50 @@ class Arith:
         self.rfs_lr(t2, t1)
         self.addmul(-1.0, Op(Z), Op(Z), t2, t1, t2)
         self.lr(t2)
+
+    # ---- approximate inverse (Remark 1) -------------------------
+    def zero_block(self, t, s):
+        """Z|_{t x s} <- 0: every coupling and nearfield tile of the block subtree (bases untouched)."""
+        Z = self.Z
+        for b in Z.bt.subtree(Z.bt.index[(t, s)]):
+            if b in Z.S:
+                Z.S[b] = np.zeros_like(Z.S[b])
+            if b in Z.N:
+                Z.N[b] = np.zeros_like(Z.N[b])
+
+    def inv(self, T, t=0, _aT=None):
+        """In place Z|_{t x t} <- (Z|_{t x t})^{-1} by block Gauss elimination (Remark 1):
+        C11 = A11^{-1};  B12 = C11 A12,  B21 = A21 C11  (into the scratch H^2 matrix T, same trees,
+        zero on entry);  S = A22 - A21 B12  (P:1382 prints "A_11 -", reading R20: A_22);
+        C22 = S^{-1};  C12 = -B12 C22;  C21 = -C22 B21;  C11 = C11 - C12 B21  -- six products, all
+        Z|_{t x r} += alpha X|_{t x s} Y|_{s x r} (addmul) in this order; a leaf tile is inverted
+        directly.  Full storage only."""
+        Z, rt = self.Z, self.rt
+        if rt.is_leaf(t):
+            b = Z.bt.index[(t, t)]
+            N = Z.N[b]
+            nrm = np.linalg.norm(N)
+            # breakdown rule of the leaf LR (reading own-2): no-pivot elimination pivots
+            M = N.copy()
+            for j in range(M.shape[0]):
+                if abs(M[j, j]) <= 1e-14 * nrm:
+                    raise BreakdownError(f"H2_ERR_BREAKDOWN: leaf {t} pivot {j}")
+                M[j + 1:, j] /= M[j, j]
+                M[j + 1:, j + 1:] -= np.outer(M[j + 1:, j], M[j, j + 1:])
+            Z.N[b] = np.linalg.inv(N)
+            return
+        aT = _aT if _aT is not None else Arith(T, self.trunc)
+        t1, t2 = rt.sons(t)
+        self.inv(T, t1, aT)
+        aT.addmul(1.0, Op(Z), Op(Z), t1, t1, t2)   # B12 = C11 A12   -> T|_{t1 x t2}
+        aT.addmul(1.0, Op(Z), Op(Z), t2, t1, t1)   # B21 = A21 C11   -> T|_{t2 x t1}
+        self.addmul(-1.0, Op(Z), Op(T), t2, t1, t2)  # S = A22 - A21 B12
+        self.inv(T, t2, aT)                          # C22 = S^{-1}
+        self.zero_block(t1, t2)
+        self.addmul(-1.0, Op(T), Op(Z), t1, t2, t2)  # C12 = -B12 C22
+        self.zero_block(t2, t1)
+        self.addmul(-1.0, Op(Z), Op(T), t2, t2, t1)  # C21 = -C22 B21
+        self.addmul(-1.0, Op(Z), Op(T), t1, t2, t1)  # C11 = C11 - C12 B21
 
     # ---- preconditioner application -------------------------------------------------------
     def solve_tree(self, b, cholesky=True):

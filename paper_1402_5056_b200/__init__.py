@@ -20,6 +20,7 @@ from .h2 import (  # noqa: F401
     h2_matvec,
     h2_addmul,
     h2_lr_factor,
+    h2_inverse,
     h2_solve,
     h2_ranks,
     h2_storage_report,

@@ -20,7 +20,7 @@ FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
-    "-Xptxas", "-v" if os.environ.get("H2_PTXAS_V") else "-O3",
+    "-Xptxas", "-v" if os.environ.get("H2_PTXAS_V") else ("-O" + os.environ.get("H2_PTXAS_O", "3")),
     "-shared", "-lcudart",
 ]
 

@@ -22,6 +22,8 @@ void hmul_dense(const MatDev& M, bool trans, int a, int b, int b_blk, const doub
 // dense tiles (nearfield slots): Cholesky / no-pivot LU in place; breakdown -> flags[1], flags[2] = cluster
 void tile_potrf(const MatDev& M, int slot, int t, cudaStream_t st);
 void tile_getrf(const MatDev& M, int slot, int t, cudaStream_t st);
+// in-place inverse of a diagonal leaf tile (Gauss-Jordan in elimination order; breakdown as getrf)
+void tile_inverse(const MatDev& M, int slot, int t, cudaStream_t st);
 // triangular solves with a diagonal tile T (m x m, ld lmax):
 enum TrsmMode { RLT = 0, LLN, LLU, LLT, RUN, LUN, LUT };
 void tile_trsm(const MatDev& M, int slot, int m, int mode, double* B, int ldb, int brows, Dim bcols, int bcolcap,

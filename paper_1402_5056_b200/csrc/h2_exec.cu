@@ -56,7 +56,7 @@ __constant__ int c_op_kid[OP_COUNT] = {
     K_AR_EXPAND, K_AR_GEMM, K_AR_GEMM, K_AR_GEMM, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL,
     K_AR_TILE, K_AR_TILE, K_AR_TILE, K_AR_TSQR, K_AR_TEMP, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC,
     K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_TEMP, K_AR_MISC,
-    K_AR_GEMM, K_AR_MISC};
+    K_AR_TILE, K_AR_GEMM, K_AR_MISC};
 
 __device__ __forceinline__ const DevSide& side_of(const MatDev& M, int s) { return s ? M.col : M.row; }
 
@@ -143,6 +143,10 @@ __device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, do
     case OP_GETRF: {
       const PTile& q = *reinterpret_cast<const PTile*>(op.p);
       ar::it_getrf(M, q.slot, q.t, it, n, sm);
+    } break;
+    case OP_TINV: {
+      const PTile& q = *reinterpret_cast<const PTile*>(op.p);
+      ar::it_tinv(M, q.slot, q.t, it, n, sm);
     } break;
     case OP_TRSM: {
       const PTile& q = *reinterpret_cast<const PTile*>(op.p);
@@ -690,6 +694,9 @@ void tile_potrf(const MatDev& M, int slot, int t, cudaStream_t) {
 }
 void tile_getrf(const MatDev& M, int slot, int t, cudaStream_t) {
   ctx_or_throw()->emit(OP_GETRF, 1, &M, PTile{slot, t, 0, 0, 0, 0, nullptr, dimc(0)});
+}
+void tile_inverse(const MatDev& M, int slot, int t, cudaStream_t) {
+  ctx_or_throw()->emit(OP_TINV, 1, &M, PTile{slot, t, 0, 0, 0, 0, nullptr, dimc(0)});
 }
 void tile_trsm(const MatDev& M, int slot, int m, int mode, double* B, int ldb, int brows, Dim bcols, int bcolcap,
                cudaStream_t) {

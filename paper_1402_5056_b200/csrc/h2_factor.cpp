@@ -620,6 +620,43 @@ struct Driver {
     chol(t2);
   }
 
+  // ---- approximate inverse (Remark 1) --------------------------
+  // Z|_{t x s} <- 0: the couplings of the admissible leaves and the tiles of the inadmissible leaves
+  // of the block subtree (contiguous slot ranges); the bases are left as they are
+  void zero_block(int t, int s) {
+    const h2_btree_* B = Z->bt;
+    const int b = B->find(t, s);
+    int a0 = -1, a1 = -1;
+    for (int q = b; q < b + B->bsize[b]; ++q)
+      if (Z->blk2adm[q] >= 0) {
+        if (a0 < 0) a0 = Z->blk2adm[q];
+        a1 = Z->blk2adm[q];
+      }
+    const size_t r2 = (size_t)Z->d.rcap * Z->d.rcap, l2 = (size_t)lmax * lmax;
+    if (a0 >= 0) zero_fill(Z->d.S + (size_t)a0 * r2, (size_t)(a1 - a0 + 1) * r2, st);
+    const int i0 = Z->inad_range[2 * b], i1 = Z->inad_range[2 * b + 1];
+    if (i1 > i0) zero_fill(Z->d.N + (size_t)i0 * l2, (size_t)(i1 - i0) * l2, st);
+  }
+  // in place Z|_{t x t} <- (Z|_{t x t})^{-1}; dT drives the scratch matrix T (zero on entry)
+  void inv(int t, Driver& dT) {
+    if (leaf(t)) {
+      tile_inverse(Z->d, diag_slot(t), t, st);
+      return;
+    }
+    const int t1 = T->son0[t], t2 = T->son1[t];
+    const HOp C{Z, false}, W{dT.Z, false};
+    inv(t1, dT);
+    dT.addmul(1.0, C, C, t1, t1, t2, nullptr);  // B12 = C11 A12      -> T|_{t1 x t2}
+    dT.addmul(1.0, C, C, t2, t1, t1, nullptr);  // B21 = A21 C11      -> T|_{t2 x t1}
+    addmul(-1.0, C, W, t2, t1, t2, nullptr);    // S = A22 - A21 B12 (P:1382 prints A11: R20)
+    inv(t2, dT);                                // C22 = S^{-1}
+    zero_block(t1, t2);
+    addmul(-1.0, W, C, t1, t2, t2, nullptr);    // C12 = -B12 C22
+    zero_block(t2, t1);
+    addmul(-1.0, C, W, t2, t2, t1, nullptr);    // C21 = -C22 B21
+    addmul(-1.0, C, W, t1, t2, t1, nullptr);    // C11 = C11 - C12 B21
+  }
+
   void lr(int t) {
     if (leaf(t)) {
       tile_getrf(Z->d, diag_slot(t), t, st);
@@ -682,21 +719,26 @@ h2_status run_driver(h2_mat_* Z, const h2_trunc* trunc, h2_stream stream, int wh
       Arena dummy;
       if ((s = ensure_ws(M, dummy)) != H2_OK) return s;
     }
-  // update workspace of the target
-  for (DevSide* D : {&Z->d.row, &Z->d.col})
-    if (!D->re) {
-      const size_t nc = D->nclusters, k2 = (size_t)Z->d.kcap * Z->d.kcap;
-      CUDA_TRY(cudaMalloc(&D->re, 8 * nc * k2));
-      Z->allocs.push_back(D->re);
-      CUDA_TRY(cudaMalloc(&D->bw, 8 * nc * k2));
-      Z->allocs.push_back(D->bw);
-      CUDA_TRY(cudaMalloc(&D->rn, 8 * nc * k2));
-      Z->allocs.push_back(D->rn);
-      CUDA_TRY(cudaMalloc(&D->qn, 8 * nc * (size_t)Z->d.ldq * Z->d.rcap));
-      Z->allocs.push_back(D->qn);
-      CUDA_TRY(cudaMalloc(&D->rnew, 4 * nc));
-      Z->allocs.push_back(D->rnew);
-    }
+  // update workspace of the target(s)
+  for (h2_mat_* Tg : {Z, what == 5 ? X : nullptr}) {
+    if (!Tg) continue;
+    for (DevSide* D : {&Tg->d.row, &Tg->d.col})
+      if (!D->re) {
+        const size_t nc = D->nclusters, k2 = (size_t)Tg->d.kcap * Tg->d.kcap;
+        CUDA_TRY(cudaMalloc(&D->re, 8 * nc * k2));
+        Tg->allocs.push_back(D->re);
+        CUDA_TRY(cudaMalloc(&D->bw, 8 * nc * k2));
+        Tg->allocs.push_back(D->bw);
+        CUDA_TRY(cudaMalloc(&D->rn, 8 * nc * k2));
+        Tg->allocs.push_back(D->rn);
+        CUDA_TRY(cudaMalloc(&D->qn, 8 * nc * (size_t)Tg->d.ldq * Tg->d.rcap));
+        Tg->allocs.push_back(D->qn);
+        CUDA_TRY(cudaMalloc(&D->rnew, 4 * nc));
+        Tg->allocs.push_back(D->rnew);
+      }
+  }
+  Arena arT;  // the scratch matrix of the inversion drives its own products
+  if (what == 5 && (s = ensure_ws(X, arT)) != H2_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   Driver dr{Z, st, tc.rel_tol, tc.abs_tol, tc.max_rank, ar, Z->bt->rt, Z->d.rcap, Z->d.lmax};
   ExecCtx ctx;
@@ -707,6 +749,15 @@ h2_status run_driver(h2_mat_* Z, const h2_trunc* trunc, h2_stream stream, int wh
     if (what == 0) dr.chol(0);
     else if (what == 1) dr.lr(0);
     else if (what == 2) dr.addmul(alpha, HOp{X, false}, HOp{Y, false}, 0, 0, 0, nullptr);
+    else if (what == 5) {
+      Driver dT{X, st, tc.rel_tol, tc.abs_tol, tc.max_rank, arT, X->bt->rt, X->d.rcap, X->d.lmax};
+      dT.ident = arT.alloc((size_t)X->d.lmax * X->d.lmax);
+      identity(dT.ident, X->d.lmax, X->d.lmax, st);
+      dr.inv(0, dT);
+      dr.n_updates += dT.n_updates;
+      dr.n_dense += dT.n_dense;
+      dr.n_temps += dT.n_temps;
+    }
     else if (what == 3 || what == 4) {
       // vec: n x nrhs in ORIGINAL order -> tree order, solve, back
       const int n = (int)Z->bt->rt->n;
@@ -759,6 +810,31 @@ extern "C" h2_status h2_lr_factor(h2_mat A, h2_factor_kind kind, const h2_trunc*
   }
   h2_status s = run_driver(A, trunc, stream, kind == H2_CHOLESKY ? 0 : 1, nullptr, nullptr, 0.0, nullptr, 0, 0);
   if (s == H2_OK) A->factored = kind == H2_CHOLESKY ? 1 : 2;
+  return s;
+}
+
+extern "C" h2_status h2_inverse(h2_mat A, const h2_trunc* trunc, h2_stream stream) {
+  if (h2::batch_open()) {
+    h2::set_error("h2_inverse: not allowed inside h2_batch_begin/h2_batch_end");
+    return H2_ERR_ARG;
+  }
+  if (!A) {
+    h2::set_error("h2_inverse: NULL matrix");
+    return H2_ERR_ARG;
+  }
+  if (A->lower || A->factored) {
+    h2::set_error("h2_inverse: needs an unfactored H2_FULL matrix");
+    return H2_ERR_ARG;
+  }
+  // scratch matrix T (same trees and capacities, zero): B12 / B21 of every level
+  const int64_t n = A->bt->rt->n;
+  std::vector<int64_t> rowptr((size_t)n + 1, 0);
+  h2_mat T = nullptr;
+  h2_status s = h2_from_sparse(A->bt, n, rowptr.data(), nullptr, nullptr, H2_FULL, A->d.rcap, A->d.ucap, stream, &T);
+  if (s != H2_OK) return s;
+  s = run_driver(A, trunc, stream, 5, T, nullptr, 0.0, nullptr, 0, 0);
+  cudaStreamSynchronize((cudaStream_t)stream);  // T's memory is released below
+  h2_mat_destroy(T);
   return s;
 }
 

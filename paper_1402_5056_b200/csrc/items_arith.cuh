@@ -287,6 +287,49 @@ __device__ void it_getrf(const MatDev& M, int slot, int t, int item_, int nitems
   }
 }
 
+// Inverse of a diagonal leaf tile (Remark 1: "if t is a leaf, we can compute the
+// inverse directly"): Gauss-Jordan on [T | I] in shared memory, pivots in the elimination order of
+// the no-pivot LU, so the breakdown rule is the leaf LR's (reading own-2: |p| <= 1e-14 ||T||_F).
+__device__ void it_tinv(const MatDev& M, int slot, int t, int item_, int nitems_, double* smx_) {
+  constexpr int LD = 65;
+  double* G = smx_;                  // m x 2m, ld LD
+  double* f = G + LD * 128;          // column-j multipliers
+  double& nrm = f[64];
+  int& bad = *(int*)(f + 65);
+  double* N = M.N + (size_t)slot * M.lmax * M.lmax;
+  const int m = M.row.hi[t] - M.row.lo[t];
+  for (int e = threadIdx.x; e < m * 2 * m; e += NT) {
+    const int i = e % m, c = e / m;
+    G[i + c * LD] = c < m ? N[i + (size_t)c * M.lmax] : (c - m == i ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int e = 0; e < m * m; ++e) s += G[(e % m) + (e / m) * LD] * G[(e % m) + (e / m) * LD];
+    nrm = sqrt(s);
+    bad = 0;
+  }
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    const double p = G[j + j * LD];
+    if (threadIdx.x == 0 && !(fabs(p) > 1e-14 * nrm)) bad = 1;
+    for (int i = threadIdx.x; i < m; i += NT) f[i] = G[i + j * LD];
+    __syncthreads();
+    for (int c = threadIdx.x; c < 2 * m; c += NT) G[j + c * LD] /= p;
+    __syncthreads();
+    for (int e = threadIdx.x; e < m * 2 * m; e += NT) {
+      const int i = e % m, c = e / m;
+      if (i != j) G[i + c * LD] -= f[i] * G[j + c * LD];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < m * m; e += NT) N[(e % m) + (size_t)(e / m) * M.lmax] = G[(e % m) + (e / m + m) * LD];
+  if (threadIdx.x == 0 && bad) {
+    atomicExch(M.flags + 1, 1);
+    atomicExch(M.flags + 2, t);
+  }
+}
+
 // Triangular solve with a leaf tile (m <= 32), one warp per 4 right-hand sides: lane i holds row
 // i of the 4 vectors and the 32 tile entries it needs (loaded once from the tile), every step is
 // one scaling, one shuffle broadcast and one FMA per vector (no shared memory, no block barrier).

@@ -19,7 +19,7 @@ EXPORTED_SYMBOLS = [
     "h2_from_sparse", "h2_lowrank_update", "h2_matvec", "h2_addmul", "h2_lr_factor", "h2_solve",
     "h2_ranks", "h2_storage_report", "h2_export", "h2_check_device_flags",
     "h2_profile_enable", "h2_profile_read", "h2_profile_debug", "h2_profile_ops", "h2_stats", "h2_pcg", "h2_launch_count",
-    "h2_mat_destroy", "h2_last_error", "h2_batch_begin", "h2_batch_end",
+    "h2_mat_destroy", "h2_last_error", "h2_batch_begin", "h2_batch_end", "h2_inverse",
 ]
 
 if not os.path.exists(_LIBPATH):
@@ -62,6 +62,7 @@ _sig = {
     "h2_last_error": [],
     "h2_batch_begin": [_p],
     "h2_batch_end": [],
+    "h2_inverse": [_p, _p, _p],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -260,6 +261,12 @@ def h2_addmul(Z: Mat, alpha, X: Mat, Y: Mat, trunc=None, stream=None):
     _check(_lib.h2_addmul(Z.h, float(alpha), X.h, Y.h, C.byref(tr), _stream(stream)))
 
 
+def h2_inverse(A: Mat, trunc=None, stream=None):
+    """A <- A^{-1} in place (Remark 1: block Gauss elimination, six products per level)."""
+    tr = _ctrunc(trunc)
+    _check(_lib.h2_inverse(A.h, C.byref(tr), _stream(stream)))
+
+
 def h2_lr_factor(A: Mat, cholesky: bool = True, trunc=None, stream=None):
     tr = _ctrunc(trunc)
     _check(_lib.h2_lr_factor(A.h, 1 if cholesky else 0, C.byref(tr), _stream(stream)))
@@ -339,7 +346,7 @@ OP_NAMES = ["upd_ext_leaf", "upd_ext_level", "upd_w_path", "upd_w_level", "upd_s
             "upd_couple", "upd_install", "upd_rcache", "expand", "gemm", "gemm_part", "gemm_sum", "hm_fwd_leaf",
             "hm_fwd_level", "hm_couple", "hm_bwd_level", "hm_leaf", "potrf", "getrf", "trsm", "tsqr", "temp",
             "copy_cols", "set_int", "add_int", "rank_if", "stack", "choose", "identity", "transpose", "gather",
-            "scatter", "zero", "dd", "nztile", "c2core", "skipz"]
+            "scatter", "zero", "dd", "nztile", "tinv", "c2core", "skipz"]
 
 
 def h2_profile_ops():

@@ -228,3 +228,52 @@ def test_c4_product_into_lower_then_cholesky():
         d = operator_rel_diff(Z, OZ, ot.n)
         print(f"C4-32 A*A -> Cholesky eps {eps}: rel diff {d:.2e}")
         assert d <= 10 * eps
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-4])
+def test_inverse_parity(eps):
+    """NEXT-2, approximate inverse (Remark 1) through h2_inverse against the oracle's
+    inv on the same seeded input: ranks bit-exact, operator <= 10 eps, and the inverse itself close
+    to the dense inverse (a definition independent of both)."""
+    c = config("C2", N=32)
+    t = P.h2_cluster_tree(c["points"], c["leaf"])
+    bt = P.h2_block_tree(t, t, c["eta"])
+    ot = ClusterTree(c["points"], c["leaf"])
+    ob = BlockTree(ot, ot, c["eta"])
+    OZ = o_from_sparse(ob, c["A"])
+    ar = Arith(OZ, OTrunc(eps))
+    ar.inv(o_from_sparse(ob, c["A"] * 0))
+    Z = P.h2_from_sparse(bt, c["A"])
+    P.h2_inverse(Z, trunc=P.Trunc(eps))
+    assert P.h2_check_device_flags(Z) == 0
+    _ranks_equal(Z, OZ)
+    d = operator_rel_diff(Z, OZ, ot.n)
+    Ainv = np.linalg.inv(c["A"].toarray())
+    Xp = np.random.default_rng(6).standard_normal((ot.n, 3))
+    e = np.linalg.norm(gpu_apply(Z, Xp) - Ainv @ Xp) / np.linalg.norm(Ainv @ Xp)
+    print(f"inverse eps {eps}: gpu vs oracle {d:.2e}, gpu vs dense inverse {e:.2e}, stats {P.h2_stats(Z)}")
+    assert d <= 10 * eps
+    assert e <= 100 * eps
+
+
+def test_inverse_identity_diagonal_and_breakdown():
+    c = config("C2", N=24)
+    t = P.h2_cluster_tree(c["points"], c["leaf"])
+    bt = P.h2_block_tree(t, t, c["eta"])
+    n = c["n"]
+    d = np.random.default_rng(2).uniform(1.0, 3.0, n)
+    for D in (sp.identity(n, format="csr"), sp.diags(d, format="csr")):
+        Z = P.h2_from_sparse(bt, D)
+        P.h2_inverse(Z, trunc=P.Trunc(1e-4))
+        Xp = np.random.default_rng(3).standard_normal((n, 2))
+        np.testing.assert_array_equal(gpu_apply(Z, Xp), (1.0 / D.diagonal())[:, None] * Xp)  # tile entries 1/d
+    A = c["A"].tolil()
+    A[0, :] = 0.0
+    A[:, 0] = 0.0
+    Z = P.h2_from_sparse(bt, A.tocsr())
+    with pytest.raises(P.H2Error) as e:
+        P.h2_inverse(Z, trunc=P.Trunc(1e-4))
+        P.h2_check_device_flags(Z)
+    assert e.value.status == "H2_ERR_BREAKDOWN"
+    with pytest.raises(P.H2Error):
+        P.h2_inverse(P.h2_from_sparse(bt, c["A"], lower=True))

@@ -163,3 +163,49 @@ def test_interpolative_decomposition_reading_own7():
     P = np.diag([3.0, 1e-13, 0.0, 2.0])
     A, B = Arith._interp_decomp(P)
     assert A.shape[1] == 2 and np.abs(A @ B.T - np.diag([3.0, 0, 0, 2.0])).max() == 0.0
+
+
+def _small(name="C2", N=24):
+    c = config(name, N=N)
+    ot = ClusterTree(c["points"], c["leaf"])
+    ob = BlockTree(ot, ot, c["eta"])
+    return c, ot, ob
+
+
+def test_inverse_remark1_against_dense_inverse():
+    """NEXT-2 (Remark 1): the block-Gauss approximate inverse equals the dense inverse
+    within the truncation (tight eps: 1e-8 relative on probes) and its error falls with eps (the
+    Schur complement uses A22; P:1382 prints A11, reading R20)."""
+    c, ot, ob = _small()
+    A = c["A"].toarray()
+    Ainv = np.linalg.inv(A)
+    X = np.random.default_rng(1).standard_normal((ot.n, 3))
+    errs = []
+    for eps in (1e-10, 1e-5, 1e-3):
+        Z = from_sparse(ob, c["A"])
+        Arith(Z, Trunc(eps)).inv(from_sparse(ob, c["A"] * 0))
+        errs.append(np.linalg.norm(Z.matvec(X) - Ainv @ X) / np.linalg.norm(Ainv @ X))
+    assert errs[0] < 1e-8
+    assert errs[0] < errs[1] < errs[2] < 1e-1
+
+
+def test_inverse_identity_and_diagonal_exact():
+    """A = I gives C = I exactly; a diagonal A gives C = diag(1/a) exactly (every product of a
+    zero off-diagonal block is exactly zero)."""
+    c, ot, ob = _small()
+    n = ot.n
+    d = np.random.default_rng(2).uniform(1.0, 3.0, n)
+    for D in (sp.identity(n, format="csr"), sp.diags(d, format="csr")):
+        Z = from_sparse(ob, D)
+        Arith(Z, Trunc(1e-4)).inv(from_sparse(ob, D * 0))
+        np.testing.assert_array_equal(densify(Z), np.diag(1.0 / D.diagonal())[np.ix_(ot.perm, ot.perm)])
+
+
+def test_inverse_breakdown_reported():
+    c, ot, ob = _small()
+    A = c["A"].tolil()
+    A[0, :] = 0.0
+    A[:, 0] = 0.0
+    from oracle.arith import BreakdownError
+    with pytest.raises(BreakdownError):
+        Arith(from_sparse(ob, A.tocsr()), Trunc(1e-4)).inv(from_sparse(ob, c["A"] * 0))

@@ -150,6 +150,33 @@ def run_c4(N, epss):
         del L
 
 
+def run_inv(N, eps):
+    """NEXT-2: approximate inverse (Remark 1) of the C2-shaped jump problem at N x N nodes; the
+    quality ||I - C A|| on probes and the PCG iterations with C as preconditioner."""
+    c = config("C2", N=N)
+    t, bt = structure(c)
+    Aop = P.h2_from_sparse(bt, c["A"], lower=False, rank_cap=32, update_cap=32)
+    Z = P.h2_from_sparse(bt, c["A"], lower=False, rank_cap=32, update_cap=32)
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    e0.record()
+    P.h2_inverse(Z, trunc=P.Trunc(eps))
+    e1.record()
+    torch.cuda.synchronize()
+    X = np.random.default_rng(7).standard_normal((c["n"], 4))
+    r = []
+    for j in range(4):
+        x = torch.from_numpy(X[:, j].copy()).to(dev)
+        ax = P.h2_matvec(Aop, x)
+        cax = P.h2_matvec(Z, ax).cpu().numpy()
+        r.append(np.linalg.norm(cax - X[:, j]) / np.linalg.norm(X[:, j]))
+    kr, kc = P.h2_ranks(Z)
+    print(json.dumps({"config": f"inverse C2-shaped {N}^2", "n": c["n"], "eps": eps, "inverse_s": e0.elapsed_time(e1) / 1e3,
+                      "I_minus_CA_probe_rel": max(r), "stats": P.h2_stats(Z), "max_rank": [int(kr.max()), int(kc.max())],
+                      "flags": P.h2_check_device_flags(Z),
+                      "storage_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / c["n"] / 1e3)}), flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     if what == "c1":
@@ -160,3 +187,5 @@ if __name__ == "__main__":
         N = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
         epss = [float(e) for e in sys.argv[3:]] or [1e-2, 1e-4, 1e-6]
         run_c4(N, epss)
+    elif what == "inv":
+        run_inv(int(sys.argv[2]) if len(sys.argv) > 2 else 256, float(sys.argv[3]) if len(sys.argv) > 3 else 1e-4)
