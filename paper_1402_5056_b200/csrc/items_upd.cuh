@@ -420,7 +420,10 @@ __device__ void it_upd_weights_level(const MatDev& M, UpdArgs a_, int bA, int nA
 // ---- U4 truncated nested basis --------------------------------------------------------------
 // Given V (m x K, ldv) in shared memory and B~_t, compute M = V B~^T, its SVD, the rank, Q and R_t.
 __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, int t, double* V, int ldv, int m,
-                         int K, double* sm_rest, int kid, double extra_flops) {
+                         int K, double* sm_rest, int kid, double extra_flops, const double* RV = nullptr) {
+  // RV (leaves): R-factor of V itself (V = Q_V R_V, computed by the extension op, ld kcap): then
+  // M = Q_V (R_V B~^T) and N = R_V B~^T (min(m,K) x K, a product of two triangles) replaces the
+  // Householder QR of M on the K <= 32 path -- the same singular values and right singular vectors
   // U4: left singular vectors / values of M = V B~^T (m x K).  K <= m <= 16: one-sided Jacobi
   // on M in registers of one warp.  K <= 32: Householder R of M, then the same on the
   // min(m, K) columns of R^T (length K), U Sigma = M Y Sigma^-1 (see below).  Otherwise: the SVD is taken
@@ -459,15 +462,26 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
     double* Rw = Bt;
     double* Y = Bt + 32 * RM;
     W = Bt + 64 * RM;
-    la::cta_copy(Rw, RM, Mm, RM, m, K);
-    __syncthreads();
-    la::cta_qr_R(Rw, RM, m, K, sig, (double*)order);
     const int pr = m < K ? m : K;
-    for (int e = threadIdx.x; e < K * pr; e += NT) {  // R^T (K x pr) into W's slot as the input
-      const int i = e % K, j = e / K;
-      W[i + j * RM] = j <= i ? Rw[j + i * RM] : 0.0;
+    if (RV) {
+      // N^T = B~ R_V^T (K x pr): N^T(i, j) = sum_q R_V(j, q) B~(i, q), both upper triangular
+      for (int e = threadIdx.x; e < K * pr; e += NT) {
+        const int i = e % K, j = e / K;
+        double v = 0.0;
+        for (int q = (i > j ? i : j); q < K; ++q) v += RV[j + (size_t)q * M.kcap] * Bt[i + q * RM];
+        W[i + j * RM] = v;
+      }
+      __syncthreads();
+    } else {
+      la::cta_copy(Rw, RM, Mm, RM, m, K);
+      __syncthreads();
+      la::cta_qr_R(Rw, RM, m, K, sig, (double*)order);
+      for (int e = threadIdx.x; e < K * pr; e += NT) {  // R^T (K x pr) into W's slot as the input
+        const int i = e % K, j = e / K;
+        W[i + j * RM] = j <= i ? Rw[j + i * RM] : 0.0;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     c1 = clock64();
     if (K <= 8) sweeps = la::warp_jacobi<8, false>(W, RM, K, pr, Y, RM, sig, order, scr);
     else if (K <= 16) sweeps = la::warp_jacobi<16, false>(W, RM, K, pr, Y, RM, sig, order, scr);
@@ -553,7 +567,7 @@ __device__ void it_upd_svd_leaf(const MatDev& M, UpdArgs a_, int rl0, int nrl, i
     V[i + j * RM] = j < kt ? Vb[i + (size_t)j * M.lmax] : al * Xf[off + i + (size_t)(j - kt) * ldx];
   }
   __syncthreads();
-  svd_core(M, a, D, t, V, RM, m, K, V + RM * KC, K_SVD_LEAF, 0.0);
+  svd_core(M, a, D, t, V, RM, m, K, V + RM * KC, K_SVD_LEAF, 0.0, D.re + (size_t)t * M.kcap * M.kcap);
 }
 
 __device__ void it_upd_svd_level(const MatDev& M, UpdArgs a_, int bA, int nA, int bB, int nB, int item_, int nitems_, double* smx_) {
