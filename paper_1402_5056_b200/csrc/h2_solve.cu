@@ -64,32 +64,40 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
   for (int p = 0; p < a.S.nl; ++p) {
     const int t = a.S.order[p];
     const int lo = a.lo[t], m = a.hi[t] - lo;
-    // ---- enter: yt_c = yh_c + E_c yt_father, top-down
-    for (int q = a.S.enter_ptr[p]; q < a.S.enter_ptr[p + 1]; ++q) {
-      const int c = a.S.enter[q];
-      const int kc = a.d_rank[c];
-      const int par = a.parent[c];
-      const int kp = par >= 0 ? a.d_rank[par] : 0;
-      const double* E = a.d_tr + (size_t)c * rc * rc;
-      for (int e = tid; e < kc * nr; e += SNT) {
-        const int i = e % kc, v = e / kc;
-        double acc = a.yh[((size_t)c * nr + v) * rc + i];
-        const double* yp = a.yt + ((size_t)par * nr + v) * rc;
-        for (int j = 0; j < kp; ++j) acc += E[i + (size_t)j * rc] * yp[j];
-        a.yt[((size_t)c * nr + v) * rc + i] = acc;
+    // ---- enter: yt_c = yh_c + E_c yt_father, top-down -- by warp 0 alone (a dependent chain of
+    // small products, __syncwarp between clusters) while warps 1..7 stage the diagonal tile and
+    // take the nearfield tiles: the two are independent
+    const int q_en0 = a.S.enter_ptr[p], q_en1 = a.S.enter_ptr[p + 1];
+    const bool split = q_en1 > q_en0;
+    if (warp == 0) {
+      for (int q = q_en0; q < q_en1; ++q) {
+        const int c = a.S.enter[q];
+        const int kc = a.d_rank[c];
+        const int par = a.parent[c];
+        const int kp = par >= 0 ? a.d_rank[par] : 0;
+        const double* E = a.d_tr + (size_t)c * rc * rc;
+        for (int e = lane; e < kc * nr; e += 32) {
+          const int i = e % kc, v = e / kc;
+          double acc = a.yh[((size_t)c * nr + v) * rc + i];
+          const double* yp = a.yt + ((size_t)par * nr + v) * rc;
+          for (int j = 0; j < kp; ++j) acc += E[i + (size_t)j * rc] * yp[j];
+          a.yt[((size_t)c * nr + v) * rc + i] = acc;
+        }
+        __syncwarp();
       }
-      __syncthreads();
     }
-    // ---- stage the diagonal tile; nearfield partial sums, warp w takes tiles w, w + 8, ...
-    {
+    // ---- stage the diagonal tile; nearfield partial sums, warp w takes tiles w, w + nw, ...
+    const int w0 = split ? 1 : 0, nw = 8 - w0;
+    if (tid >= 32 * w0) {
+      const int t0 = tid - 32 * w0, nth = SNT - 32 * w0;
       const double* D = a.N + (size_t)a.S.diag[p] * lmax * lmax;
-      for (int e = tid; e < m * m; e += SNT) T[(e % m) + (e / m) * TLD] = D[(e % m) + (size_t)(e / m) * lmax];
-      for (int i = tid; i < m; i += SNT) invd[i] = 1.0 / D[i + (size_t)i * lmax];
+      for (int e = t0; e < m * m; e += nth) T[(e % m) + (e / m) * TLD] = D[(e % m) + (size_t)(e / m) * lmax];
+      for (int i = t0; i < m; i += nth) invd[i] = 1.0 / D[i + (size_t)i * lmax];
     }
     double acc0[NRC], acc1[NRC];
 #pragma unroll
     for (int v = 0; v < NRC; ++v) acc0[v] = acc1[v] = 0.0;
-    for (int q = a.S.near_ptr[p] + warp; q < a.S.near_ptr[p + 1]; q += 8) {
+    for (int q = a.S.near_ptr[p] + warp - w0; warp >= w0 && q < a.S.near_ptr[p + 1]; q += nw) {
       const int slot = a.S.near_slot[q], s = a.S.near_src[q];
       const int los = a.lo[s], ms = a.hi[s] - los;
       const double* Tq = a.N + (size_t)slot * lmax * lmax;
