@@ -46,10 +46,12 @@ struct SweepArgs {
   const double *d_leafb, *d_tr;
   const double *Sc, *N;
   double* B;                  // n x nr (ld n), tree order: right-hand side in, solution out
+  double* prof;               // profiling: cycles per sweep phase (h2_profile_ops slots 40..44) or null
   double *xh, *yh, *yt;       // [cluster][nr][rcap]
 };
 
-constexpr size_t SWEEP_SMEM = sizeof(double) * (8 * 64 * NRC + 64 * NRC + 64 * TLD + 64);
+constexpr int WLD = 64;    // leading dimension of the staged leaf basis W_t
+constexpr size_t SWEEP_SMEM = sizeof(double) * (8 * 64 * NRC + 64 * NRC + 64 * TLD + 64 + WLD * 48);
 
 __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepArgs a) {
   extern __shared__ double smem[];
@@ -57,10 +59,19 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
   double* r = part + 8 * 64 * NRC;    // [rhs][row]
   double* T = r + 64 * NRC;           // diagonal tile, ld TLD
   double* invd = T + 64 * TLD;
+  double* Ws = invd + 64;             // W_t of the current leaf (m x k_t, ld WLD), staged during the solve
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nr = a.nr, rc = a.rcap, lmax = a.lmax;
   const int64_t n = a.n;
   const bool tr = a.mode == SW_LT;
+  long long ph[5] = {0, 0, 0, 0, 0}, c_prev = clock64();
+  auto tick = [&](int i) {
+    if (a.prof && tid == 0) {
+      const long long c = clock64();
+      ph[i] += c - c_prev;
+      c_prev = c;
+    }
+  };
   for (int p = 0; p < a.S.nl; ++p) {
     const int t = a.S.order[p];
     const int lo = a.lo[t], m = a.hi[t] - lo;
@@ -69,6 +80,12 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
     // take the nearfield tiles: the two are independent
     const int q_en0 = a.S.enter_ptr[p], q_en1 = a.S.enter_ptr[p + 1];
     const bool split = q_en1 > q_en0;
+    double b0[NRC], b1[NRC];  // warp 0: b|t, loaded first (consumed after the enter chain)
+#pragma unroll
+    for (int v = 0; v < NRC; ++v) {
+      b0[v] = (warp == 0 && split && v < nr && lane < m) ? a.B[lo + lane + (size_t)v * n] : 0.0;
+      b1[v] = (warp == 0 && split && v < nr && lane + 32 < m) ? a.B[lo + lane + 32 + (size_t)v * n] : 0.0;
+    }
     if (warp == 0) {
       for (int q = q_en0; q < q_en1; ++q) {
         const int c = a.S.enter[q];
@@ -97,6 +114,25 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
     double acc0[NRC], acc1[NRC];
 #pragma unroll
     for (int v = 0; v < NRC; ++v) acc0[v] = acc1[v] = 0.0;
+    if (warp == 0 && split) {
+      // the far-field part of the leaf, V_t yt_t (t entered last, just above), minus b|t as warp 0's
+      // share of the partial sums: the residual below only adds up shared memory
+      const int kt = a.d_rank[t];
+      const double* V = a.d_leafb + (size_t)a.d_leafidx[t] * lmax * rc;
+#pragma unroll
+      for (int v = 0; v < NRC; ++v) {
+        acc0[v] = -b0[v];
+        acc1[v] = -b1[v];
+        if (v < nr) {
+          const double* y = a.yt + ((size_t)t * nr + v) * rc;
+          for (int j = 0; j < kt; ++j) {
+            const double yj = y[j];
+            if (lane < m) acc0[v] += V[lane + (size_t)j * lmax] * yj;
+            if (lane + 32 < m) acc1[v] += V[lane + 32 + (size_t)j * lmax] * yj;
+          }
+        }
+      }
+    }
     for (int q = a.S.near_ptr[p] + warp - w0; warp >= w0 && q < a.S.near_ptr[p + 1]; q += nw) {
       const int slot = a.S.near_slot[q], s = a.S.near_src[q];
       const int los = a.lo[s], ms = a.hi[s] - los;
@@ -136,13 +172,15 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
       part[(warp * 64 + lane + 32) * NRC + v] = acc1[v];
     }
     __syncthreads();
+    tick(0);  // enter || diagonal tile + nearfield
     // ---- residual r = b|t - sum part - V_t yt_t
     {
-      const int kt = a.d_rank[t];
+      const bool vy = !split;  // V_t yt_t not yet in the partial sums (t always enters: never)
+      const int kt = vy ? a.d_rank[t] : 0;
       const double* V = a.d_leafb + (size_t)a.d_leafidx[t] * lmax * rc;
       for (int e = tid; e < m * nr; e += SNT) {
         const int i = e % m, v = e / m;
-        double acc = a.B[lo + i + (size_t)v * n];
+        double acc = vy ? a.B[lo + i + (size_t)v * n] : 0.0;  // (split: -b|t is in warp 0's part)
         for (int w = 0; w < 8; ++w) acc -= part[(w * 64 + i) * NRC + v];
         const double* y = a.yt + ((size_t)t * nr + v) * rc;
         for (int j = 0; j < kt; ++j) acc -= V[i + (size_t)j * lmax] * y[j];
@@ -150,7 +188,15 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
       }
     }
     __syncthreads();
-    // ---- diagonal tile solve, warp v = right-hand side v, lanes own rows (lane, lane + 32)
+    tick(1);  // residual
+    // ---- diagonal tile solve, warp v = right-hand side v, lanes own rows (lane, lane + 32); the
+    // other warps stage the leaf's source basis W_t for the forward transform that follows
+    const int kts = a.s_rank[t];
+    const bool wst = kts <= 48 && nr < 8;
+    if (warp >= nr && wst) {
+      const double* W = a.s_leafb + (size_t)a.s_leafidx[t] * lmax * rc;
+      for (int e = tid - 32 * nr; e < m * kts; e += SNT - 32 * nr) Ws[(e % m) + (e / m) * WLD] = W[(e % m) + (size_t)(e / m) * lmax];
+    }
     if (warp < nr && m <= 32) {  // operator row of this lane in registers: one shuffle + FMA per step
       const bool fwd = a.mode == SW_L, unit = a.unit != 0;
       double av[32];
@@ -197,6 +243,7 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
     __syncthreads();
     for (int e = tid; e < m * nr; e += SNT) a.B[lo + (e % m) + (size_t)(e / m) * n] = r[(e / m) * 64 + (e % m)];
     __syncthreads();
+    tick(2);  // diagonal solve + store
     // ---- completed source clusters, bottom-up: forward transform, then push into destinations
     for (int q = a.S.done_ptr[p]; q < a.S.done_ptr[p + 1]; ++q) {
       const int c = a.S.done[q];
@@ -206,7 +253,9 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
       for (int e = tid; e < kc * nr; e += SNT) {
         const int j = e % kc, v = e / kc;
         double acc = 0.0;
-        if (leaf) {  // c == t
+        if (leaf && wst) {  // c == t, W_t staged in shared memory
+          for (int i = 0; i < m; ++i) acc += Ws[i + j * WLD] * r[v * 64 + i];
+        } else if (leaf) {
           const double* W = a.s_leafb + (size_t)a.s_leafidx[c] * lmax * rc;
           for (int i = 0; i < m; ++i) acc += W[i + (size_t)j * lmax] * r[v * 64 + i];
         } else {
@@ -235,7 +284,13 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
       }
       __syncthreads();
     }
+    tick(3);  // forward transforms + pushes of the completed clusters
   }
+  if (a.prof && tid == 0)
+    for (int i = 0; i < 4; ++i) {
+      atomicAdd(a.prof + 4 * K_COUNT + 32 + 2 * (40 + i), (double)ph[i]);
+      atomicAdd(a.prof + 4 * K_COUNT + 32 + 2 * (40 + i) + 1, (double)a.S.nl);
+    }
 }
 
 __global__ void k_gather_cols(const double* __restrict__ x, int64_t ldx, const int64_t* __restrict__ perm,
@@ -372,6 +427,7 @@ cudaError_t solve_factored(h2_mat_* F, double* x, int nrhs, int64_t ldx, cudaStr
               k_gather_cols<<<cdiv(n * nr, 256), 256, 0, st>>>(x + v0 * ldx, ldx, M.row.perm, Bt, n, nr));
     for (int mo : modes) {
       SweepArgs a;
+      a.prof = prof_dev();
       a.S = F->sched[mo];
       a.mode = mo;
       a.unit = (mo == SW_L && !chol) ? 1 : 0;
