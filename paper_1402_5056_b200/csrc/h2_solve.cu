@@ -51,7 +51,7 @@ struct SweepArgs {
 };
 
 constexpr int WLD = 64;    // leading dimension of the staged leaf basis W_t
-constexpr size_t SWEEP_SMEM = sizeof(double) * (8 * 64 * NRC + 64 * NRC + 64 * TLD + 64 + WLD * 48);
+constexpr size_t SWEEP_SMEM = sizeof(double) * (8 * 64 * NRC + 64 * NRC + 64 * TLD + 64 + WLD * 48 + 48 * NRC);
 
 __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepArgs a) {
   extern __shared__ double smem[];
@@ -60,6 +60,7 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
   double* T = r + 64 * NRC;           // diagonal tile, ld TLD
   double* invd = T + 64 * TLD;
   double* Ws = invd + 64;             // W_t of the current leaf (m x k_t, ld WLD), staged during the solve
+  double* xs = Ws + WLD * 48;         // xhat of the cluster being completed (k_c x nr), for its pushes
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nr = a.nr, rc = a.rcap, lmax = a.lmax;
   const int64_t n = a.n;
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
           }
         }
         a.xh[((size_t)c * nr + v) * rc + j] = acc;
+        if (kc <= 48) xs[j + v * 48] = acc;
       }
       __syncthreads();
       for (int b = a.S.push_ptr[c] + warp; b < a.S.push_ptr[c + 1]; b += 8) {
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
         const double* Sa = a.Sc + (size_t)slot * rc * rc;
         for (int i = lane; i < kd; i += 32)
           for (int v = 0; v < nr; ++v) {
-            const double* x = a.xh + ((size_t)c * nr + v) * rc;
+            const double* x = kc <= 48 ? xs + v * 48 : a.xh + ((size_t)c * nr + v) * rc;
             double acc = 0.0;
             for (int j = 0; j < kc; ++j) acc += (tr ? Sa[j + (size_t)i * rc] : Sa[i + (size_t)j * rc]) * x[j];
             a.yh[((size_t)d * nr + v) * rc + i] += acc;
