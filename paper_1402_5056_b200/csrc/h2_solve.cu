@@ -175,13 +175,19 @@ __global__ void __launch_bounds__(SNT, 1) k_sweep(const __grid_constant__ SweepA
     __syncthreads();
     tick(0);  // enter || diagonal tile + nearfield
     // ---- residual r = b|t - sum part - V_t yt_t
-    {
-      const bool vy = !split;  // V_t yt_t not yet in the partial sums (t always enters: never)
-      const int kt = vy ? a.d_rank[t] : 0;
+    if (split) {  // -b|t and V_t yt_t are in warp 0's partial sums: shared memory only
+      for (int e = tid; e < m * nr; e += SNT) {
+        const int i = e % m, v = e / m;
+        double acc = 0.0;
+        for (int w = 0; w < 8; ++w) acc -= part[(w * 64 + i) * NRC + v];
+        r[v * 64 + i] = acc;
+      }
+    } else {  // (never: every leaf enters at its own step)
+      const int kt = a.d_rank[t];
       const double* V = a.d_leafb + (size_t)a.d_leafidx[t] * lmax * rc;
       for (int e = tid; e < m * nr; e += SNT) {
         const int i = e % m, v = e / m;
-        double acc = vy ? a.B[lo + i + (size_t)v * n] : 0.0;  // (split: -b|t is in warp 0's part)
+        double acc = a.B[lo + i + (size_t)v * n];
         for (int w = 0; w < 8; ++w) acc -= part[(w * 64 + i) * NRC + v];
         const double* y = a.yt + ((size_t)t * nr + v) * rc;
         for (int j = 0; j < kt; ++j) acc -= V[i + (size_t)j * lmax] * y[j];
