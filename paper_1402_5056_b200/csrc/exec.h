@@ -88,6 +88,7 @@ struct PGemm {
 };
 struct PHm {  // all H^2-block x dense items
   int dside, sside, a, b, trans, l0, base_lo, ldd, ldo;
+  int ident;  // D is the identity (ld ldd): products with D are column selections
   const double* D;
   double* xh;
   double* yh;

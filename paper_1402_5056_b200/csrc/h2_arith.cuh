@@ -16,7 +16,8 @@ void expand_basis(const MatDev& M, const DevSide& D, int t, double* out, int ld,
 // C (m x n) = alpha op(A) op(B) + beta C, dims on the device (caps on the host for grid sizes)
 void gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb, bool tb, Dim m, Dim n,
           Dim k, int mcap, int ncap, int kcap, double alpha, double beta, cudaStream_t st);
-// out (|a| x m) = beta out + op(Z)|_{a x b} D,  D: |b| x m  (H^2 block times dense, [BO10 Thm 3.42])
+// out (|a| x m) = beta out + op(Z)|_{a x b} D,  D: |b| x m  (H^2 block times dense, [BO10 Thm 3.42]);
+// b_blk = 1: D is the identity (its products are column selections, exact)
 void hmul_dense(const MatDev& M, bool trans, int a, int b, int b_blk, const double* D, int ldd, Dim m, int mcap,
                 double* out, int ldo, double alpha, double beta, cudaStream_t st);
 // dense tiles (nearfield slots): Cholesky / no-pivot LU in place; breakdown -> flags[1], flags[2] = cluster

@@ -117,7 +117,7 @@ __device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, do
     } break;
     case OP_HM_FWD_LEAF: {
       const PHm& q = *reinterpret_cast<const PHm*>(op.p);
-      ar::it_hm_fwd_leaf(M, side_of(M, q.sside), q.l0, q.base_lo, q.D, q.ldd, q.m, q.xh, it, n, sm);
+      ar::it_hm_fwd_leaf(M, side_of(M, q.sside), q.l0, q.base_lo, q.D, q.ldd, q.m, q.xh, q.ident, it, n, sm);
     } break;
     case OP_HM_FWD_LEVEL: {
       const PHm& q = *reinterpret_cast<const PHm*>(op.p);
@@ -134,7 +134,7 @@ __device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, do
     case OP_HM_LEAF: {
       const PHm& q = *reinterpret_cast<const PHm*>(op.p);
       ar::it_hm_leaf(M, side_of(M, q.dside), side_of(M, q.sside), q.l0, q.a, q.b, q.trans, q.D, q.ldd, q.m, q.yh,
-                     q.out, q.ldo, q.alpha, q.beta, it, n, sm);
+                     q.out, q.ldo, q.alpha, q.beta, q.ident, it, n, sm);
     } break;
     case OP_POTRF: {
       const PTile& q = *reinterpret_cast<const PTile*>(op.p);
@@ -643,7 +643,6 @@ void gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B
 
 void hmul_dense(const MatDev& M, bool trans, int a, int b, int b_blk, const double* D, int ldd, Dim m, int mcap,
                 double* out, int ldo, double alpha, double beta, cudaStream_t) {
-  (void)b_blk;
   (void)mcap;
   ExecCtx* c = ctx_or_throw();
   const DevSide& Dd = trans ? M.col : M.row;
@@ -665,6 +664,7 @@ void hmul_dense(const MatDev& M, bool trans, int a, int b, int b_blk, const doub
   h.m = m;
   h.alpha = alpha;
   h.beta = beta;
+  h.ident = b_blk;  // 1: D is the identity
   int l0, nl;
   leaf_range(Ts, b, &l0, &nl);
   h.l0 = l0;

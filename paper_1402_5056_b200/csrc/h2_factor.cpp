@@ -370,7 +370,7 @@ struct Driver {
       else copy_cols(*A, mt, Nptr(X.Z, bx), lmax, mt, dimc(ms), ms, st);
       *B = ar.alloc((size_t)mr * ms);
       const HOp Yt = Y.t();
-      hmul_dense(Y.Z->d, Yt.trans, r, s, 0, ident, lmax, dimc(ms), ms, *B, mr, 1.0, 0.0, st);
+      hmul_dense(Y.Z->d, Yt.trans, r, s, 1 /* D = I */, ident, lmax, dimc(ms), ms, *B, mr, 1.0, 0.0, st);
       *lda = mt;
       *ldb = mr;
       return ms;

@@ -104,7 +104,7 @@ constexpr int NPART = 64;
 // ---- H^2 block times dense --------------------------------------------------------------------
 // forward transform over T_b: leaves
 __device__ void it_hm_fwd_leaf(const MatDev& M, const DevSide& S, int l0, int base_lo, const double* D, int ldd,
-                                                    Dim md, double* xh, int item_, int nitems_, double* smx_) {
+                                                    Dim md, double* xh, int ident, int item_, int nitems_, double* smx_) {
   const int q = S.leaves[l0 + item_];
   const int m = md.v();
   const int rows = S.hi[q] - S.lo[q], kq = S.rank[q];
@@ -114,7 +114,12 @@ __device__ void it_hm_fwd_leaf(const MatDev& M, const DevSide& S, int l0, int ba
   for (int e = threadIdx.x; e < kq * m; e += NT) {
     const int j = e % kq, c = e / kq;
     double acc = 0.0;
-    for (int i = 0; i < rows; ++i) acc += W[i + j * M.lmax] * D[off + i + (size_t)c * ldd];
+    if (ident) {  // D = I: column c of D is e_c, W^T e_c = row (c - off) of W
+      const int i = c - off;
+      if (i >= 0 && i < rows) acc = W[i + j * M.lmax];
+    } else {
+      for (int i = 0; i < rows; ++i) acc += W[i + j * M.lmax] * D[off + i + (size_t)c * ldd];
+    }
     x[j + c * M.rcap] = acc;
   }
 }
@@ -181,7 +186,8 @@ __device__ void it_hm_bwd_level(const MatDev& M, const DevSide& D, int b0, Dim m
 
 __device__ void it_hm_leaf(const MatDev& M, const DevSide& Dd, const DevSide& Ds, int l0, int a, int b, int trans,
                                                 const double* D, int ldd, Dim md, const double* yh, double* out,
-                                                int ldo, double alpha, double beta, int item_, int nitems_, double* smx_) {
+                                                int ldo, double alpha, double beta, int ident, int item_, int nitems_,
+                                                double* smx_) {
   const int ap = Dd.leaves[l0 + item_];
   const int m = md.v();
   const int rows = Dd.hi[ap] - Dd.lo[ap], ka = Dd.rank[ap];
@@ -202,7 +208,13 @@ __device__ void it_hm_leaf(const MatDev& M, const DevSide& Dd, const DevSide& Ds
       if (bp < b || bp >= b + bsz) continue;
       const int rb = Ds.hi[bp] - Ds.lo[bp];
       const double* Na = M.N + (size_t)slot * M.lmax * M.lmax;
-      const double* x = D + (Ds.lo[bp] - Ds.lo[b]) + (size_t)c * ldd;
+      const int offb = Ds.lo[bp] - Ds.lo[b];
+      if (ident) {  // D = I: the tile's column (c - offb) (exact: the other terms are zero products)
+        const int jj = c - offb;
+        if (jj >= 0 && jj < rb) acc += trans ? Na[jj + i * M.lmax] : Na[i + jj * M.lmax];
+        continue;
+      }
+      const double* x = D + offb + (size_t)c * ldd;
       if (!trans)
         for (int j = 0; j < rb; ++j) acc += Na[i + j * M.lmax] * x[j];
       else
