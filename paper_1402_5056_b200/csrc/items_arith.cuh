@@ -709,9 +709,12 @@ __device__ void it_dd_compress(const MatDev& MX, const MatDev& MY, int slotx, in
                                int mt, int ms, int mr, double* A, int lda, double* B, int ldb, int* kout, double rel,
                                int item_, int nitems_, double* smx_) {
   constexpr int L = KC + 1;
-  double* P = smx_;        // mt x mr, QR in place
-  double* P0 = P + L * KC; // copy of P (original column order)
-  double* cn = P0 + L * KC;  // squared norms of the remaining rows, per (current) column
+  constexpr int TL = 65;   // staged tiles (<= 64 x 64)
+  double* P = smx_;        // mt x mr (mr <= 64 columns), QR in place
+  double* P0 = P + L * 64; // copy of P (original column order)
+  double* Xs = P0 + L * 64;  // op(X)|_{t x s}  (mt x ms, ld TL)
+  double* Ys = Xs + TL * 64; // op(Y)|_{s x r}  (ms x mr, ld TL)
+  double* cn = Ys + TL * 64; // squared norms of the remaining rows, per (current) column
   double* diag = cn + KC;    // R_jj
   double* red = diag + KC;   // [0] = |R_00|, [1] = |a_j|^2
   int* piv = (int*)(red + 8);
@@ -720,14 +723,21 @@ __device__ void it_dd_compress(const MatDev& MX, const MatDev& MY, int slotx, in
   const double* NY = MY.N + (size_t)sloty * MY.lmax * MY.lmax;
   const int lx = MX.lmax, ly = MY.lmax;
   const int tid = threadIdx.x, m = mt, n = mr;
+  // both tiles into shared memory in one load round (the product then reads shared memory only;
+  // the same sums in the same order as reading them from global memory)
+  for (int e = tid; e < m * ms; e += NT) {
+    const int i = e % m, q = e / m;
+    Xs[i + q * TL] = transx ? NX[q + i * lx] : NX[i + q * lx];
+  }
+  for (int e = tid; e < ms * n; e += NT) {
+    const int q = e % ms, j = e / ms;
+    Ys[q + j * TL] = transy ? NY[j + q * ly] : NY[q + j * ly];
+  }
+  __syncthreads();
   for (int e = tid; e < m * n; e += NT) {
     const int i = e % m, j = e / m;
     double acc = 0.0;
-    for (int q = 0; q < ms; ++q) {
-      const double x = transx ? NX[q + i * lx] : NX[i + q * lx];
-      const double y = transy ? NY[j + q * ly] : NY[q + j * ly];
-      acc += x * y;
-    }
+    for (int q = 0; q < ms; ++q) acc += Xs[i + q * TL] * Ys[q + j * TL];
     P[i + j * L] = acc;
     P0[i + j * L] = acc;
   }
