@@ -30,7 +30,7 @@ namespace {
 
 constexpr int NT = NTHREADS;
 constexpr int CL = 16;    // CTAs of the executor cluster (non-portable size 16; falls back to 8)
-constexpr int BIG = 1024;  // ops with more items run as a full-grid launch (64: +7 % at C2, launch gaps)
+constexpr int BIG = 64;    // ops with more items run as a full-grid launch (1024: -7 % at C2, but see DESIGN §2)
 constexpr int KC = KCAP_MAX;
 constexpr int PR = 192;
 constexpr int RM = KC + 1;
@@ -49,6 +49,7 @@ struct ExecParams {
   int begin, end;
   double* prof;   // profiling counters (h2_prof) or nullptr
   double* gpart;  // partial sums of long-inner-dimension GEMMs
+  int fence;      // H2_EXEC_FENCE=1: a gpu-scope fence after every cluster barrier (diagnostic)
   MatDev mats[EXEC_MATS];
 };
 
@@ -264,7 +265,10 @@ __global__ void __launch_bounds__(NT, 1) k_exec_cluster(const __grid_constant__ 
     }
     // barrier.cluster.arrive (release) / wait (acquire) at cluster scope: this op's global-memory
     // results are visible to every CTA of the cluster afterwards
-    if (op.barrier & 1) cl.sync();
+    if (op.barrier & 1) {
+      cl.sync();
+      if (P.fence) __threadfence();
+    }
     if (timing) {
       const int kid = c_op_kid[op.code];
       const double dt = (double)(gtimer() - t0);
@@ -440,6 +444,8 @@ cudaError_t exec_flush() {
   P.ops = g_dops;
   P.prof = prof_dev();
   P.gpart = g_gpart;
+  static const int fence_mode = getenv("H2_EXEC_FENCE") ? atoi(getenv("H2_EXEC_FENCE")) : 0;
+  P.fence = fence_mode;
   for (int i = 0; i < EXEC_MATS; ++i) {
     if (c->mats[i]) P.mats[i] = *c->mats[i];
     else std::memset(&P.mats[i], 0, sizeof(MatDev));
