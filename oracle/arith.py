@@ -167,6 +167,13 @@ class Arith:
     def _factors(self, X: Op, Y: Op, t, s, r, dense_target=False):
         """Low-rank factors A, B with X|_{t x s} Y|_{s x r} = A B^T (Case 2; R23)."""
         kx, ky = X.kind(t, s), Y.kind(s, r)
+        # reading own-6: a contribution one of whose factors is an exactly zero dense tile adds
+        # nothing and is skipped -- in every branch, also when the other factor is admissible (the
+        # tiles of the factor that never receive fill stay exactly zero; P:505-509 leaves the
+        # construction of the Case-2 factors open)
+        if (kx == INADM and X.dense(t, s) is not None and not X.dense(t, s).any()) or \
+           (ky == INADM and Y.dense(s, r) is not None and not Y.dense(s, r).any()):
+            return np.zeros((self.rt.size(t), 0)), np.zeros((self.rt.size(r), 0))
         if kx == ADM and ky == ADM:
             Sx, Sy = X.coupling(t, s), Y.coupling(s, r)
             Vx, Wy = X.row_basis(t), Y.col_basis(r)
@@ -190,11 +197,6 @@ class Arith:
                 return np.zeros((self.rt.size(t), 0)), np.zeros((Wy.shape[0], 0))
             A = X.mul_dense(t, s, Y.row_basis(s) @ Sy)
             return A, Wy
-        # reading own-6: a contribution whose dense factor tile is exactly zero adds nothing and is
-        # skipped (the tiles of the factor that never receive fill stay exactly zero)
-        if (kx == INADM and X.dense(t, s) is not None and not X.dense(t, s).any()) or \
-           (ky == INADM and Y.dense(s, r) is not None and not Y.dense(s, r).any()):
-            return np.zeros((self.rt.size(t), 0)), np.zeros((self.rt.size(r), 0))
         if kx == INADM and ky == INADM and not dense_target:
             # reading own-7: both factors dense leaf blocks, low-rank target (P:505-509 leaves the factorization
             # open): interpolative decomposition of P = X_ts Y_sr by column-pivoted QR,

@@ -11,7 +11,7 @@ import scipy.sparse as sp
 
 from inputs import config
 from inputs.updates import c0_global_factors, mixed_stream
-from oracle.structure import ClusterTree, BlockTree, ADM
+from oracle.structure import ClusterTree, BlockTree, ADM, INADM
 from oracle.h2 import from_sparse
 from oracle.update import Updater, Trunc
 from oracle.dense import densify
@@ -209,3 +209,69 @@ def test_inverse_breakdown_reported():
     from oracle.arith import BreakdownError
     with pytest.raises(BreakdownError):
         Arith(from_sparse(ob, A.tocsr()), Trunc(1e-4)).inv(from_sparse(ob, c["A"] * 0))
+
+
+def test_lr_substitutions_invert_the_represented_factors():
+    """Arith.lsolve(unit) / usolve / utsolve and solve_tree(cholesky=False) solve with the
+    triangular matrices the factored H^2 matrix represents: L = unit-lower part, R = upper part of
+    densify(Z) (a truncated LR at eps = 1e-4 after the C0 rank-8 update, so the blocks have
+    non-zero ranks).  Reference: dense triangular solves of the densified factors."""
+    from scipy.linalg import solve_triangular
+    c, rt, bt, Z = _c0()
+    n = rt.n
+    X, Y = c0_global_factors(n)
+    Xt, Yt = X[rt.perm], Y[rt.perm]
+    up = Updater(Z, Trunc(1e-4))
+    for b in bt.adm:
+        t0, s0 = int(bt.t[b]), int(bt.s[b])
+        up(t0, s0, Xt[rt.lo[t0]:rt.hi[t0]], Yt[rt.lo[s0]:rt.hi[s0]], alpha=1.0 / n)
+    ar = Arith(Z, Trunc(1e-4))
+    ar.lr()
+    assert Z.k.max() > 0 and Z.l.max() > 0
+    D = densify(Z)
+    L = np.tril(D, -1) + np.eye(n)
+    R = np.triu(D)
+    B = np.random.default_rng(21).standard_normal((n, 3))
+    for got, ref in ((ar.usolve(0, B), solve_triangular(R, B, lower=False)),
+                     (ar.utsolve(0, B), solve_triangular(R.T, B, lower=True)),
+                     (ar.lsolve(0, B, unit=True), solve_triangular(L, B, lower=True, unit_diagonal=True))):
+        assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref)
+    x = ar.solve_tree(B[:, 0], cholesky=False)
+    assert np.linalg.norm(L @ (R @ x) - B[:, 0]) <= 1e-10 * np.linalg.norm(B[:, 0])
+
+
+def test_zero_tile_factor_adds_nothing_reading_own6():
+    """own-6 in the mixed Case-2 branches: a product X|_{t x s} 0|_{s x r} (admissible block of an
+    H^2 matrix X with non-zero ranks times an exactly zero dense leaf tile), and 0|_{t x s} X|_{s x r},
+    leaves Z bit for bit unchanged and performs no local update -- the same decision the device
+    takes (h2_factor.cpp, zero_rank_if_zero_tile)."""
+    c, rt, bt, X = _c0()
+    targets = [(int(bt.t[b]), int(bt.s[b]), rt.size(bt.t[b]), rt.size(bt.s[b])) for b in range(bt.nblocks)]
+    ux = Updater(X, Trunc(1e-12))
+    for t0, s0, a, b in mixed_stream([tg for tg in targets if bt.kind[bt.index[tg[:2]]] == ADM], 40, 4, seed=5):
+        ux(t0, s0, a, b)
+    _, _, _, O = _c0(A=c["A"] * 0.0)
+    _, _, _, Z = _c0()
+    uz = Updater(Z, Trunc(1e-12))
+    for t0, s0, a, b in mixed_stream(targets, 6, 4, seed=6):
+        uz(t0, s0, a, b)
+    ox, oo = Op(X), Op(O)
+    n_cases = [0, 0]
+    for (t, s), bx in bt.index.items():
+        if bt.kind[bx] != ADM or X.k[t] == 0 or X.l[s] == 0:
+            continue
+        for r in range(rt.nclusters):
+            for case, (P, Q, a, b_, c_) in enumerate(((ox, oo, t, s, r), (oo, ox, r, t, s))):
+                if not all(blk in bt.index for blk in ((a, b_), (b_, c_), (a, c_))):
+                    continue
+                if (Q.kind(b_, c_) if case == 0 else P.kind(a, b_)) != INADM:  # the zero factor: a dense tile
+                    continue
+                before, k0, l0 = densify(Z), Z.k.copy(), Z.l.copy()
+                ar = Arith(Z, Trunc(1e-4))
+                ar.addmul(-1.0, P, Q, a, b_, c_)
+                assert ar.stats["updates"] == 0 and ar.stats["dense_adds"] == 0 and ar.stats["tmp_adds"] == 0
+                np.testing.assert_array_equal(densify(Z), before)
+                np.testing.assert_array_equal(Z.k, k0)
+                np.testing.assert_array_equal(Z.l, l0)
+                n_cases[case] += 1
+    assert min(n_cases) >= 3, n_cases

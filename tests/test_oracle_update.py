@@ -195,3 +195,16 @@ def test_c0_exact_rank8_pin():
         has_col = any(bt.col[p] for p in rt.pred(t))
         assert Z.k[t] == (8 if has_row else 0)
         assert Z.l[t] == (8 if has_col else 0)
+
+
+def test_transpose_matvec_nonzero_ranks():
+    """H.matvec_tree(transpose=True) with non-zero ranks equals densify(Z)^T x (P:1077-1081 with the
+    roles of the row and column bases swapped); also the plain product."""
+    c, rt, bt = _c0()
+    Z = from_sparse(bt, c["A"])
+    _random_updates(Z, bt, rt, Trunc(1e-6), 12, seed=31, check_o2=False)
+    assert Z.k.max() > 0 and Z.l.max() > 0
+    D = densify(Z)
+    x = stream(6).standard_normal((rt.n, 2))
+    np.testing.assert_allclose(Z.matvec_tree(x, transpose=True), D.T @ x, rtol=0, atol=1e-10 * np.abs(D.T @ x).max())
+    np.testing.assert_allclose(Z.matvec_tree(x), D @ x, rtol=0, atol=1e-10 * np.abs(D @ x).max())
