@@ -122,6 +122,15 @@ def run_gpu(args, rank, world):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     trunc = P.Trunc(EPS)
 
+    def check_step(Z, m=None, rel=None):
+        """A step counts only if the factorization is clean: no device flag (rank clamp, leaf
+        breakdown) and PCG converged to a finite residual (h2_pcg raises otherwise)."""
+        f = P.h2_check_device_flags(Z)
+        if f != 0:
+            raise P.H2Error(8, f"device flags {f} after the factorization")
+        if rel is not None and not (np.isfinite(rel) and rel < 1e-8):
+            raise P.H2Error(9, f"PCG relres {rel}")
+
     def fresh():
         t = time.perf_counter()
         Z = P.h2_from_sparse(bt, A, lower=True, rank_cap=32, update_cap=32)
@@ -129,10 +138,10 @@ def run_gpu(args, rank, world):
         return Z, time.perf_counter() - t
 
     prof = None
-    e2e = None
-    # ---- warm-up steps (the first one is profiled, the last one is the end-to-end measurement) ----
+    e2e_samples = []
+    # ---- warm-up steps (the first one is profiled, the others are end-to-end measurements) ----
     for w in range(args.warmup):
-        if w == args.warmup - 1:
+        if w >= 1:
             # e2e: host CSR -> h2_from_sparse (upload) -> factor -> PCG with b from pinned host -> x back
             bh = torch.from_numpy(b_host).pin_memory()
             xh = torch.empty(n, dtype=torch.float64).pin_memory()
@@ -145,23 +154,29 @@ def run_gpu(args, rank, world):
             xh.copy_(x, non_blocking=True)
             torch.cuda.synchronize()
             e2e_s = time.perf_counter() - te
-            nz = P.h2_stats(Z)["updates_nonzero"]
-            csr_bytes = A.indptr.nbytes + A.indices.nbytes + A.data.nbytes
-            e2e = {"value": nz / e2e_s, "unit": UNIT, "seconds": e2e_s, "h2d_bytes_per_step": int(csr_bytes + 8 * n),
-                   "d2h_bytes_per_step": int(8 * n),
-                   "path": "h2_from_sparse(host CSR) + h2_lr_factor + h2_pcg(b from pinned host) + x to host"}
+            check_step(Z)
+            e2e_samples.append((P.h2_stats(Z)["updates_nonzero"], e2e_s))
             del Z
             continue
         Z, _ = fresh()
-        if w == 0:
-            P.h2_profile_enable(True)
+        P.h2_profile_enable(True)
         P.h2_lr_factor(Z, cholesky=True, trunc=trunc)
         P.h2_pcg(Aop, Z, b, x, tol=1e-8)
         torch.cuda.synchronize()
-        if w == 0:
-            prof = P.h2_profile_read()
-            P.h2_profile_enable(False)
+        prof = P.h2_profile_read()
+        P.h2_profile_enable(False)
+        check_step(Z)
         del Z
+    e2e = None
+    if e2e_samples:
+        secs = sorted(t for _, t in e2e_samples)
+        med = secs[len(secs) // 2]
+        nz = e2e_samples[0][0]
+        csr_bytes = A.indptr.nbytes + A.indices.nbytes + A.data.nbytes
+        e2e = {"value": nz / med, "unit": UNIT, "seconds": med, "samples_s": [round(t, 3) for _, t in e2e_samples],
+               "h2d_bytes_per_step": int(csr_bytes + 8 * n), "d2h_bytes_per_step": int(8 * n),
+               "path": "h2_from_sparse(host CSR) + h2_lr_factor + h2_pcg(b from pinned host) + x to host; "
+                       "median over the non-profiled warm-up steps"}
     dist = None
     if world > 1:
         import torch.distributed as dist
@@ -169,7 +184,7 @@ def run_gpu(args, rank, world):
     torch.cuda.synchronize()
     clk_p, clk_f = _clock_sampler_start() if rank == 0 else (None, None)
     fact_ms, pcg_ms, nz_total, iters, rels, launches = 0.0, 0.0, 0, [], [], 0
-    stats = None
+    stats, failed, good = None, [], 0
     for j in range(args.steps):
         Z, fs = fresh()  # outside the timed events
         flush.fill_(float(j))  # L2 flush between timed steps
@@ -178,9 +193,16 @@ def run_gpu(args, rank, world):
         e0.record(cs)
         P.h2_lr_factor(Z, cholesky=True, trunc=trunc)
         e1.record(cs)
-        _, m, rel = P.h2_pcg(Aop, Z, b, x, tol=1e-8)
-        e2.record(cs)
-        torch.cuda.synchronize()
+        try:
+            _, m, rel = P.h2_pcg(Aop, Z, b, x, tol=1e-8)
+            e2.record(cs)
+            torch.cuda.synchronize()
+            check_step(Z, m, rel)
+        except P.H2Error as err:  # a failed step is dropped from the totals and reported
+            torch.cuda.synchronize()
+            failed.append({"step": j, "error": str(err)})
+            del Z
+            continue
         launches += P.h2_launch_count() - l0
         fact_ms += e0.elapsed_time(e1)
         pcg_ms += e1.elapsed_time(e2)
@@ -188,7 +210,8 @@ def run_gpu(args, rank, world):
         nz_total += stats["updates_nonzero"]
         iters.append(m)
         rels.append(rel)
-        if j == args.steps - 1:
+        good += 1
+        if good == 1:
             sto = P.h2_storage_report(Z)
             # matvecs (HBM-bound, both larger than L2): the factor L (~1.4 KB/DOF) and the sparse
             # input A in H^2 form (rank-0 bases; the matvec PCG applies every iteration)
@@ -216,36 +239,78 @@ def run_gpu(args, rank, world):
     clocks = _clock_sampler_stop(clk_p, clk_f, dev.index) if rank == 0 else None
     mv_bytes = 8.0 * float(sto.sum()) + 16.0 * n
     return dict(n=n, structure_s=structure_s, fact_ms=fact_ms, pcg_ms=pcg_ms, step_ms=step_ms, nz=nz_total,
+                good=good, failed=failed,
                 stats=stats, iters=iters, rels=rels, launches=launches, prof=prof, e2e=e2e, clocks=clocks,
                 sto=sto.tolist(), mv_ms=mv_ms, mv_bytes=mv_bytes, mvA_ms=mvA_ms, mvA_bytes=mvA_bytes)
 
 
-def oracle_sample(N, seed=0):
-    """The oracle (as it stands, single thread) on a bounded sample of the workload: the H^2
-    Cholesky + PCG of the same C2-shaped jump problem at N x N nodes."""
+def host_cpu():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
+class _Budget(Exception):
+    pass
+
+
+def oracle_setup(N, seed=0):
+    """The oracle's structure and rank-0 H^2 copy of the C2 jump problem (outside any timing)."""
+    from inputs import config
+    from oracle.structure import ClusterTree, BlockTree
+    import oracle.arith  # noqa: F401  (loads scipy.linalg's BLAS before the thread limit below)
     try:
         from threadpoolctl import threadpool_limits
-        threadpool_limits(1)
+        threadpool_limits(1)  # the oracle as it stands, on ONE host core (every loaded BLAS)
     except Exception:
         pass
-    from inputs import config
-    from inputs.rng import stream, RHS
-    from oracle.structure import ClusterTree, BlockTree
-    from oracle.h2 import from_sparse
-    from oracle.update import Trunc
-    from oracle.arith import Arith, pcg
     c = config("C2", N=N, seed=seed)
     ot = ClusterTree(c["points"], c["leaf"])
     ob = BlockTree(ot, ot, c["eta"])
-    OZ = from_sparse(ob, c["A"], lower=True)
-    ar = Arith(OZ, Trunc(EPS))
-    t0 = time.perf_counter()
-    ar.chol()
-    t1 = time.perf_counter()
-    b = stream(RHS).standard_normal(c["n"])
-    _, m, _ = pcg(lambda v: c["A"] @ v, lambda v: ar.solve(v), b)
-    t2 = time.perf_counter()
-    return dict(n=c["n"], updates=ar.stats["updates"], fact_s=t1 - t0, pcg_s=t2 - t1, m=m)
+    return c, ot, ob
+
+
+def oracle_sample(setup, budget_s):
+    """A bounded sample of the C2 workload on the oracle (as it stands, one thread): its H^2
+    Cholesky of the same n = N^2 jump problem, stopped after `budget_s` seconds of factorization.
+    The factorization order is the paper's (chol(t1) first), so the sample is the first part of
+    the very recursion the GPU runs.  Returns (local updates performed, seconds, finished)."""
+    from oracle.h2 import from_sparse
+    from oracle.update import Trunc
+    from oracle.arith import Arith
+    c, ot, ob = setup
+    Z = from_sparse(ob, c["A"], lower=True)
+
+    class Bounded(Arith):  # stops the recursion at the budget; the arithmetic is the oracle's
+        def _add(self, *a, **k):
+            if time.perf_counter() - self.t_start > budget_s:
+                raise _Budget()
+            return super()._add(*a, **k)
+
+    ar = Bounded(Z, Trunc(EPS))
+    ar.t_start = time.perf_counter()
+    done = True
+    try:
+        ar.chol()
+    except _Budget:
+        done = False
+    return ar.stats["updates"], time.perf_counter() - ar.t_start, done
+
+
+def full_size_oracle():
+    """The oracle's full C2 factorization as measured by tools/oracle_golden_c2.py (context)."""
+    p = os.path.join(ROOT, "tests", "golden", "c2_oracle_N512.json")
+    if not os.path.exists(p):
+        return None
+    g = json.load(open(p))
+    return {"fact_s": g["fact_s"], "updates": g["stats"]["updates"], "updates_per_s": g["stats"]["updates"] / g["fact_s"],
+            "host": g["host"], "note": "full n=262,144 oracle Cholesky, tools/oracle_golden_c2.py, build host"}
 
 
 def main():
@@ -255,7 +320,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--N", type=int, default=512, help="grid side (512: BASELINE C2, n = 262,144)")
-    ap.add_argument("--cpu-N", type=int, default=96, help="grid side of the oracle's bounded sample")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle factorization (cpu_baseline)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", 0))
@@ -268,25 +333,29 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        N = max(16, args.cpu_N // 2)
+        # each step: a bounded sample of the same C2 workload, sized so the whole run stays within a
+        # few minutes (the oracle needs ~515 s for the full factorization)
+        per_step = min(20.0, max(3.0, 150.0 / (args.steps + args.warmup)))
+        st = oracle_setup(args.N)
         for _ in range(args.warmup):
-            oracle_sample(16)
-        tot_u, tot_s, samples = 0, 0.0, []
+            oracle_sample(st, per_step)
+        tot_u, tot_s = 0, 0.0
         for _ in range(args.steps):
-            r = oracle_sample(N)
-            tot_u += r["updates"]
-            tot_s += r["fact_s"]
-            samples.append(r)
+            u, dt, _ = oracle_sample(st, per_step)
+            tot_u += u
+            tot_s += dt
         value = tot_u / tot_s
+        sample = (f"oracle (numpy/scipy, 1 thread) H2 Cholesky of the same C2 problem (n={args.N * args.N}), "
+                  f"each step the first {per_step:.1f} s of the factorization in the paper's order; "
+                  f"updates/s = local updates performed / factorization seconds")
         line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * sum(s["fact_s"] + s["pcg_s"] for s in samples) / len(samples),
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config,
-                "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                                 "sample": f"oracle H2 Cholesky + PCG of the C2-shaped jump problem at {N}x{N} nodes "
-                                           f"(n={N * N}) per step; updates/s over the factorization"},
-                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                "config": dict(config, sample_s_per_step=per_step),
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                                 "host": host_cpu()},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "full_size_oracle": full_size_oracle()}
         print(json.dumps(line))
         return
 
@@ -298,8 +367,12 @@ def main():
     res = run_gpu(args, rank, world)
     if rank != 0:
         return
+    if res["good"] == 0:
+        print(json.dumps({"metric": METRIC, "error": "every timed step failed", "failed_steps": res["failed"]}))
+        sys.exit(1)
     measured, fp = _peaks()
-    fact_s = res["fact_ms"] / 1e3 / args.steps
+    good = res["good"]
+    fact_s = res["fact_ms"] / 1e3 / good
     value = job_throughput(res["nz"], world, res["fact_ms"])
     prof = res["prof"] or {}
     # the executor kernel is the dominant kernel of the step (every op of the factorization runs in it)
@@ -312,17 +385,23 @@ def main():
             "peak_source": "profiles/fp64_peak.json (FP64 DFMA microbenchmark, measured)" if fp else
                            "B200 FP64 nominal 37 TFLOP/s (148 SMs x 64 DFMA/clk x 1.965 GHz)",
             "note": "latency-bound dependent chain of tiny dense problems (avg extended rank ~6); see DESIGN.md"}
+    tr = os.path.join(ROOT, "profiles", "r02", "exec_traffic.json")
+    if os.path.exists(tr):
+        t = json.load(open(tr))
+        roof["traffic"] = t.get("dram_bytes_per_launch")
+        roof["traffic_source"] = t.get("source")
     if roof["achieved"] is not None:
         roof["frac"] = roof["achieved"] / roof["peak"]
     mv_gbs = res["mv_bytes"] / (res["mv_ms"] / 1e3) / 1e9
     hbm = measured.get("hbm_gbs", 6650.0)
-    cpu = oracle_sample(args.cpu_N)
+    cpu_u, cpu_s, _ = oracle_sample(oracle_setup(args.N), args.cpu_budget)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": res["step_ms"] / args.steps, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": res["step_ms"] / good, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
         "setup_s": fact_s, "setup_s_paper_l9_opteron": 28.7,
-        "pcg": {"iterations": res["iters"], "relres": res["rels"], "ms": res["pcg_ms"] / args.steps},
+        "steps_valid": good, "failed_steps": res["failed"],
+        "pcg": {"iterations": res["iters"], "relres": res["rels"], "ms": res["pcg_ms"] / good},
         "structure_s": res["structure_s"],
         "updates": res["stats"],
         "storage_KB_per_dof": 8.0 * sum(res["sto"]) / res["n"] / 1e3,
@@ -333,14 +412,18 @@ def main():
                      "bytes": res["mvA_bytes"], "peak": hbm,
                      "frac": res["mvA_bytes"] / (res["mvA_ms"] / 1e3) / 1e9 / hbm, "bound": "hbm",
                      "of": "input A (H2 form, the PCG operator)"},
-        "cpu_baseline": {"value": cpu["updates"] / cpu["fact_s"], "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"oracle H2 Cholesky of the C2-shaped jump problem at {args.cpu_N}x{args.cpu_N} "
-                                   f"nodes (n={cpu['n']}): {cpu['updates']} updates in {cpu['fact_s']:.1f} s, "
-                                   f"PCG m={cpu['m']} (numpy, 1 thread)"},
+        "cpu_baseline": {"value": cpu_u / cpu_s, "unit": UNIT, "cores": 1, "kind": "oracle", "host": host_cpu(),
+                         "sample": f"oracle (numpy/scipy, 1 thread) H2 Cholesky of the same C2 problem "
+                                   f"(n={res['n']}), stopped after {cpu_s:.1f} s: {cpu_u} local updates "
+                                   f"(the first part of the factorization in the paper's order)",
+                         "full_size_oracle": full_size_oracle()},
         "e2e": res["e2e"],
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
-        "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 2)} for k, v in prof.items()},
+        "executor_ops": {k: {"ops": v["launches"], "ms": round(v["ms"], 2)} for k, v in prof.items()
+                         if k not in ("k_matvec", "k_solve_sweep")},
+        "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 2)} for k, v in prof.items()
+                    if k in ("k_matvec", "k_solve_sweep")},
     }
     print(json.dumps(line))
 

@@ -44,7 +44,8 @@ typedef enum {
   H2_ERR_BREAKDOWN = 5, /* dense leaf pivot breakdown (message names the cluster and pivot)     */
   H2_ERR_NOMEM = 6,     /* device allocation failed / capacity exceeded                         */
   H2_ERR_CUDA = 7,      /* a CUDA runtime error                                                 */
-  H2_ERR_UNSUPPORTED = 8 /* operation not available in this build                               */
+  H2_ERR_UNSUPPORTED = 8, /* operation not available in this build                              */
+  H2_ERR_NOCONV = 9     /* an iteration (h2_pcg) reached maxit without meeting its tolerance    */
 } h2_status;
 
 /* TruncationControl (reading SURVEY R5): a cluster keeps
@@ -160,7 +161,9 @@ h2_status h2_solve(h2_mat F, double* x, int32_t nrhs, int64_t ldx, h2_stream str
  * preconditioner ((L L^T)^{-1} or (L R)^{-1} via h2_solve), x0 = 0, stops when ||r||/||b|| < tol
  * or after maxit iterations.  b, x: device vectors of length n in ORIGINAL order.  *iters receives
  * the number of A-applications, *relres (may be NULL) the final relative residual.  Synchronizes
- * the stream once per iteration (residual norm). */
+ * the stream once per iteration (residual norm).  A non-finite residual (a NaN/Inf in A, F or b)
+ * stops the iteration at once with H2_ERR_NONFINITE; maxit iterations without ||r||/||b|| < tol
+ * return H2_ERR_NOCONV (*iters / *relres are set in both cases). */
 h2_status h2_pcg(h2_mat A, h2_mat F, const double* b, double* x, double tol, int32_t maxit, int32_t* iters,
                  double* relres, h2_stream stream);
 

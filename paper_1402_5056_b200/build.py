@@ -34,17 +34,36 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = True) -> str:
+    """Compile every source to an object in parallel (the executor translation unit dominates),
+    then link the shared library."""
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
-    if verbose:
-        print(" ".join(cmd), flush=True)
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in FLAGS if f not in ("-shared", "-lcudart")]
+    jobs = []
+    for f in SOURCES:
+        obj = os.path.join(objdir, f + ".o")
+        cmd = [NVCC, *compile_flags, "-c", "-o", obj, os.path.join(CSRC, f)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        jobs.append((f, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+    failed = False
+    for f, obj, pr in jobs:
+        out, _ = pr.communicate()
+        if pr.returncode != 0:
+            failed = True
+            sys.stderr.write(out)
+        elif verbose and out:
+            sys.stderr.write(out)
+    if failed:
+        raise RuntimeError("nvcc failed building libh2b200.so")
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-lcudart", "-o", LIB + ".tmp",
+           *[obj for _, obj, _ in jobs]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libh2b200.so")
-    if verbose and (r.stdout or r.stderr):
-        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed linking libh2b200.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

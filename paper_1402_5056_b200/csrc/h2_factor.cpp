@@ -678,8 +678,10 @@ h2_status ensure_ws(h2_mat_* Z, Arena& ar) {
     if (!D->hx) {
       CUDA_TRY(cudaMalloc(&D->hx, sizeof(double) * (size_t)D->nclusters * M.rcap * KC));
       Z->allocs.push_back(D->hx);
+      h2::poison(D->hx, sizeof(double) * (size_t)D->nclusters * M.rcap * KC);
       CUDA_TRY(cudaMalloc(&D->hy, sizeof(double) * (size_t)D->nclusters * M.rcap * KC));
       Z->allocs.push_back(D->hy);
+      h2::poison(D->hy, sizeof(double) * (size_t)D->nclusters * M.rcap * KC);
     }
   }
   if (!Z->ws) {
@@ -687,6 +689,7 @@ h2_status ensure_ws(h2_mat_* Z, Arena& ar) {
     Z->ws_cap = 24 * n * (size_t)KC + ((size_t)1 << 22);
     CUDA_TRY(cudaMalloc(&Z->ws, sizeof(double) * Z->ws_cap));
     Z->allocs.push_back(Z->ws);
+    h2::poison(Z->ws, sizeof(double) * Z->ws_cap);
     Z->iws_cap = 1 << 20;
     CUDA_TRY(cudaMalloc(&Z->iws, sizeof(int) * Z->iws_cap));
     Z->allocs.push_back(Z->iws);
@@ -727,12 +730,16 @@ h2_status run_driver(h2_mat_* Z, const h2_trunc* trunc, h2_stream stream, int wh
         const size_t nc = D->nclusters, k2 = (size_t)Tg->d.kcap * Tg->d.kcap;
         CUDA_TRY(cudaMalloc(&D->re, 8 * nc * k2));
         Tg->allocs.push_back(D->re);
+        h2::poison(D->re, 8 * nc * k2);
         CUDA_TRY(cudaMalloc(&D->bw, 8 * nc * k2));
         Tg->allocs.push_back(D->bw);
+        h2::poison(D->bw, 8 * nc * k2);
         CUDA_TRY(cudaMalloc(&D->rn, 8 * nc * k2));
         Tg->allocs.push_back(D->rn);
+        h2::poison(D->rn, 8 * nc * k2);
         CUDA_TRY(cudaMalloc(&D->qn, 8 * nc * (size_t)Tg->d.ldq * Tg->d.rcap));
         Tg->allocs.push_back(D->qn);
+        h2::poison(D->qn, 8 * nc * (size_t)Tg->d.ldq * Tg->d.rcap);
         CUDA_TRY(cudaMalloc(&D->rnew, 4 * nc));
         Tg->allocs.push_back(D->rnew);
       }

@@ -250,12 +250,22 @@ extern "C" void h2_btree_destroy(h2_btree bt) { delete bt; }
 // ------------------------------------------------------------------------------------------------
 // Device storage
 // ------------------------------------------------------------------------------------------------
+namespace h2 {
+void poison(void* p, size_t bytes) {
+  static const bool on = getenv("H2_POISON") && atoi(getenv("H2_POISON")) != 0;
+  if (on && p && bytes) cudaMemset(p, 0xFF, bytes);
+}
+}  // namespace h2
+
 template <class T>
 static cudaError_t dalloc(h2_mat_* Z, T** p, size_t count) {
   *p = nullptr;
   if (count == 0) count = 1;
   cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
-  if (e == cudaSuccess) Z->allocs.push_back((void*)*p);
+  if (e == cudaSuccess) {
+    Z->allocs.push_back((void*)*p);
+    if (sizeof(T) == 8) h2::poison(*p, count * sizeof(T));
+  }
   return e;
 }
 

@@ -144,6 +144,9 @@ struct h2_mat_ {
 
 namespace h2 {
 void set_error(const std::string& msg);
+// H2_POISON=1 (diagnostic): fill a fresh FP64 workspace with NaN bytes (0xFF) instead of leaving
+// it uninitialised, so that any read of never-written memory shows up as a NaN in the result
+void poison(void* p, size_t bytes);
 // true while an h2_batch_begin / h2_batch_end recording is open on this thread
 bool batch_open();
 

@@ -151,6 +151,11 @@ extern "C" h2_status h2_pcg(h2_mat A, h2_mat F, const double* b, double* x, doub
     k_update_xr<<<g, PB, 0, st>>>(x, r, p, q, rz, pq, n);
     dot(r, r, rr);
     rel = std::sqrt(host(rr)) / nb;
+    if (!std::isfinite(rel)) {  // NaN / Inf in the factor, the operator or b: never "converges"
+      set_error("h2_pcg: non-finite residual at iteration " + std::to_string(m));
+      status = H2_ERR_NONFINITE;
+      break;
+    }
     if (rel < tol) break;
     count_launch(1);
     k_copy<<<g, PB, 0, st>>>(z, r, n, 1.0);
@@ -167,6 +172,10 @@ extern "C" h2_status h2_pcg(h2_mat A, h2_mat F, const double* b, double* x, doub
   if (status == H2_OK && (e = cudaGetLastError()) != cudaSuccess) {
     set_error(std::string("h2_pcg: ") + cudaGetErrorString(e));
     return H2_ERR_CUDA;
+  }
+  if (status == H2_OK && !(rel < tol)) {
+    set_error("h2_pcg: no convergence in " + std::to_string(m) + " iterations (relres " + std::to_string(rel) + ")");
+    return H2_ERR_NOCONV;
   }
   return status;
 }

@@ -70,7 +70,8 @@ for _name, _args in _sig.items():
     _f.restype = None if _name.endswith("_destroy") else (C.c_char_p if _name == "h2_last_error" else C.c_int)
 
 STATUS = {0: "H2_OK", 1: "H2_ERR_ARG", 2: "H2_ERR_SHAPE", 3: "H2_ERR_STRUCTURE", 4: "H2_ERR_NONFINITE",
-          5: "H2_ERR_BREAKDOWN", 6: "H2_ERR_NOMEM", 7: "H2_ERR_CUDA", 8: "H2_ERR_UNSUPPORTED"}
+          5: "H2_ERR_BREAKDOWN", 6: "H2_ERR_NOMEM", 7: "H2_ERR_CUDA", 8: "H2_ERR_UNSUPPORTED",
+          9: "H2_ERR_NOCONV"}
 
 
 class H2Error(RuntimeError):
@@ -346,7 +347,7 @@ OP_NAMES = ["upd_ext_leaf", "upd_ext_level", "upd_w_path", "upd_w_level", "upd_s
             "upd_couple", "upd_install", "upd_rcache", "expand", "gemm", "gemm_part", "gemm_sum", "hm_fwd_leaf",
             "hm_fwd_level", "hm_couple", "hm_bwd_level", "hm_leaf", "potrf", "getrf", "trsm", "tsqr", "temp",
             "copy_cols", "set_int", "add_int", "rank_if", "stack", "choose", "identity", "transpose", "gather",
-            "scatter", "zero", "dd", "nztile", "tinv", "c2core", "skipz"]
+            "scatter", "zero", "dd", "nztile", "tinv", "c2core", "skipz", "hm_small"]
 
 
 def h2_profile_ops():

@@ -6,7 +6,7 @@ import pytest
 import scipy.sparse as sp
 
 from inputs import config
-from inputs.rng import stream, RHS, POWER
+from inputs.rng import stream, probes, RHS, POWER
 from inputs.updates import c0_global_factors, mixed_stream
 from oracle.structure import ClusterTree, BlockTree
 from oracle.h2 import from_sparse as o_from_sparse
@@ -37,7 +37,7 @@ def _gpu_solve(Z, b):
     return x.cpu().numpy()
 
 
-@pytest.mark.parametrize("name,N", [("C0", None), ("C2", 64), ("C3", 12)])
+@pytest.mark.parametrize("name,N", [("C0", None), ("C2", 64), ("C3", 12), ("C2", 128), ("C2", 256)])
 def test_cholesky_parity(name, N):
     eps = 1e-4
     s = setup(name, N, lower=True)
@@ -50,6 +50,9 @@ def test_cholesky_parity(name, N):
     d = operator_rel_diff(Z, OZ, s["ot"].n)
     print(f"{name} Cholesky: L operator rel diff {d:.2e}, stats {P.h2_stats(Z)} oracle {ar.stats}")
     assert d <= 10 * eps
+    # the same local updates are performed: the device's non-zero-rank updates are exactly the
+    # oracle's (reading own-3 / own-6 on both sides)
+    assert P.h2_stats(Z)["updates_nonzero"] == ar.stats["updates"]
     # solves, PCG iterations and the convergence factor
     n = s["ot"].n
     b = stream(RHS).standard_normal(n)
@@ -277,3 +280,98 @@ def test_inverse_identity_diagonal_and_breakdown():
     assert e.value.status == "H2_ERR_BREAKDOWN"
     with pytest.raises(P.H2Error):
         P.h2_inverse(P.h2_from_sparse(bt, c["A"], lower=True))
+
+
+def test_device_pcg_parity_and_guards():
+    """h2_pcg (the call the bench times) against the oracle's pcg with the oracle's factor on the
+    same seeded b (reading R12): iterations +-1, the residual of the device's x checked on the host
+    with the sparse A; a NaN in b stops at once with H2_ERR_NONFINITE, maxit = 1 returns
+    H2_ERR_NOCONV."""
+    eps = 1e-4
+    s = setup("C2", 64, lower=True)
+    OZ, Z, A = s["OZ"], s["Z"], s["c"]["A"]
+    n = s["ot"].n
+    ar = Arith(OZ, OTrunc(eps))
+    ar.chol()
+    P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps))
+    Aop = P.h2_from_sparse(s["bt"], A, lower=False)
+    b = stream(RHS).standard_normal(n)
+    _, m_o, _ = pcg(lambda v: A @ v, lambda v: ar.solve(v), b)
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    _, m_g, rel = P.h2_pcg(Aop, Z, _t(b), x, tol=1e-8)
+    xh = x.cpu().numpy()
+    res = np.linalg.norm(b - A @ xh) / np.linalg.norm(b)
+    print(f"device PCG m {m_g} (oracle {m_o}), relres {rel:.2e}, host residual {res:.2e}")
+    assert abs(m_g - m_o) <= 1 and rel < 1e-8 and res < 2e-8
+    bn = b.copy()
+    bn[7] = np.nan
+    with pytest.raises(P.H2Error) as e:
+        P.h2_pcg(Aop, Z, _t(bn), x, tol=1e-8)
+    assert e.value.status == "H2_ERR_NONFINITE"
+    with pytest.raises(P.H2Error) as e:
+        P.h2_pcg(Aop, Z, _t(b), x, tol=1e-8, maxit=1)
+    assert e.value.status == "H2_ERR_NOCONV"
+
+
+def _c2_factor(N, lower=True):
+    c = config("C2", N=N)
+    t = P.h2_cluster_tree(c["points"], c["leaf"])
+    bt = P.h2_block_tree(t, t, c["eta"])
+    Z = P.h2_from_sparse(bt, c["A"], lower=lower, rank_cap=32, update_cap=32)
+    P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(1e-4))
+    return c, bt, Z
+
+
+def test_c2_headline_parity_against_full_size_oracle():
+    """North_star target (X1): the H^2 Cholesky of the n = 262,144 jump problem (BASELINE.json
+    configs[2]; workload P:1397-1409, Table 1 row l=9 at P:1423) against the oracle's result at
+    the same size, written by tools/oracle_golden_c2.py (oracle/ and inputs/ only): ranks
+    bit-exact, update count equal, L on 4 seeded probes <= 10 eps, PCG iterations +-1 and
+    Err = ||I - (LL^T)^{-1} A|| by power iteration within 1e-2 relative."""
+    import json
+    import os
+    gdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    g = np.load(os.path.join(gdir, "c2_oracle_N512.npz"))
+    meta = json.load(open(os.path.join(gdir, "c2_oracle_N512.json")))
+    eps = 1e-4
+    c, bt, Z = _c2_factor(512)
+    n = c["n"]
+    assert P.h2_check_device_flags(Z) == 0
+    kr, kc = P.h2_ranks(Z)
+    np.testing.assert_array_equal(kr, g["ranks_row"])
+    np.testing.assert_array_equal(kc, g["ranks_col"])
+    assert P.h2_stats(Z)["updates_nonzero"] == meta["stats"]["updates"]
+    Xp = probes(n, 4).T
+    yg = gpu_apply(Z, Xp)
+    yo = g["probes_out"].astype(np.float64)
+    d = np.linalg.norm(yg - yo) / np.linalg.norm(yo)
+    assert d <= 10 * eps, d
+    A = c["A"]
+    Aop = P.h2_from_sparse(bt, A, lower=False)
+    b = stream(RHS).standard_normal(n)
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    _, m_g, rel = P.h2_pcg(Aop, Z, _t(b), x, tol=1e-8)
+    assert abs(m_g - int(g["pcg_m"])) <= 1 and rel < 1e-8
+    e_g = power_error(lambda v: A @ v, lambda v: _gpu_solve(Z, v), stream(POWER).standard_normal(n))
+    e_o = float(g["err"])
+    print(f"C2 512^2: L rel diff {d:.2e} (float32 golden), PCG m {m_g} (oracle {int(g['pcg_m'])}), "
+          f"Err {e_g:.5f} (oracle {e_o:.5f})")
+    assert abs(e_g - e_o) <= 1e-2 * e_o
+
+
+@pytest.mark.parametrize("N,runs", [(256, 10)])
+def test_cholesky_bit_identical_reruns(N, runs):
+    """Determinism: the factorization of the same input, repeated on fresh
+    copies, gives bit-identical ranks, counts and operator every time."""
+    ref = None
+    for r in range(runs):
+        c, bt, Z = _c2_factor(N)
+        assert P.h2_check_device_flags(Z) == 0
+        kr, kc = P.h2_ranks(Z)
+        y = gpu_apply(Z, probes(c["n"], 2).T)
+        fp = (kr.tobytes(), kc.tobytes(), tuple(P.h2_stats(Z).values()), y.tobytes())
+        assert np.isfinite(y).all()
+        if ref is None:
+            ref = fp
+        assert fp == ref, f"run {r} differs from run 0"
+        del Z

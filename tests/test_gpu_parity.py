@@ -109,6 +109,17 @@ def test_c1_fixed_rank_chain(ku):
     print(f"C1 k_u={ku} worst rel diff", w)
 
 
+@pytest.mark.parametrize("ku", [4, 8, 16, 32])
+def test_c1_protocol_full_length(ku):
+    """C1 protocol at its full length (R16): 10,000 seeded random updates per k_u at
+    fixed rank 16 on the 128 x 128 Laplacian, ranks bit-exact and operator <= 1e-9 at every
+    1,000-update checkpoint (BASELINE.json configs[1])."""
+    s = setup("C1")
+    ups = c1_stream(adm_targets(s["ot"], s["ob"]), 10000, ku, seed=0)
+    w = _run_pair(s, ups, P.Trunc(1e-12, 0.0, 16), check_every=1000, tol=1e-9)
+    print(f"C1 protocol k_u={ku}: 10,000 updates, worst rel diff at the checkpoints {w:.2e}")
+
+
 def test_update_global_root_and_edge_cases():
     s = setup("C0")
     Z, ot = s["Z"], s["ot"]
