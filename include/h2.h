@@ -191,6 +191,18 @@ h2_status h2_storage_report(h2_mat Z, int64_t scalars[4]);
 h2_status h2_export(h2_mat Z, double* V, double* E, double* W, double* F, double* S, double* N,
                     int64_t sizes[6]);
 
+/* h2_import (test-only): the inverse of h2_export.  Builds a matrix of block tree
+ * bt from host arrays in exactly h2_export's tight layouts: row_rank / col_rank (one int per
+ * cluster, <= rank_cap), V / W (leaf bases in leaf order, |t| x k_t), E / F (transfers of clusters
+ * 1..nclusters-1, k_t x k_parent), S (couplings of the stored admissible blocks in DFS order,
+ * k_t x l_s), N (stored nearfield tiles in DFS order).  The memoised R-factors of the nested bases
+ * (reading R7) are recomputed from the imported bases (Alg. 16), so later updates see
+ * the same state as on the exporting side.  Arrays may be NULL when they would be empty.  Errors:
+ * H2_ERR_SHAPE (rank above rank_cap), H2_ERR_NONFINITE, H2_ERR_ARG, as h2_from_sparse. */
+h2_status h2_import(h2_btree bt, const int32_t* row_rank, const int32_t* col_rank, const double* V, const double* E,
+                    const double* W, const double* F, const double* S, const double* N, h2_storage storage,
+                    int32_t rank_cap, int32_t update_cap, h2_stream stream, h2_mat* out);
+
 /* Device-side status word: nonzero if a device kernel hit a rank above rank_cap (clamped) since
  * the last call; the flag is cleared.  Synchronizes the stream. */
 h2_status h2_check_device_flags(h2_mat Z, int32_t* flags);

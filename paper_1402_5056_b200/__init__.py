@@ -25,6 +25,7 @@ from .h2 import (  # noqa: F401
     h2_ranks,
     h2_storage_report,
     h2_export,
+    h2_import,
     h2_check_device_flags,
     h2_profile_enable,
     h2_profile_read,

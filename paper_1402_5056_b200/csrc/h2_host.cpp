@@ -689,6 +689,138 @@ extern "C" h2_status h2_export(h2_mat Z, double* V, double* E, double* W, double
   return H2_OK;
 }
 
+// ---- import (test-only, the inverse of h2_export) ---------------------------------------------
+namespace {
+// R-factor (k x k upper triangle, rows beyond min(rows, k) zero, ld ldr) of the rows x k matrix A
+// (column-major, ld lda) by Householder reflections: the memoised R of a nested basis (reading R7)
+void host_qr_R(std::vector<double> A, int rows, int k, int lda, double* R, int ldr) {
+  const int p = std::min(rows, k);
+  for (int j = 0; j < p; ++j) {
+    double nrm = 0.0;
+    for (int i = j; i < rows; ++i) nrm += A[i + (size_t)j * lda] * A[i + (size_t)j * lda];
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0) continue;
+    const double a0 = A[j + (size_t)j * lda];
+    const double alpha = a0 > 0 ? -nrm : nrm;
+    std::vector<double> v(rows - j);
+    v[0] = a0 - alpha;
+    for (int i = j + 1; i < rows; ++i) v[i - j] = A[i + (size_t)j * lda];
+    double vv = 0.0;
+    for (double x : v) vv += x * x;
+    if (vv == 0.0) continue;
+    for (int c = j; c < k; ++c) {
+      double d = 0.0;
+      for (int i = j; i < rows; ++i) d += v[i - j] * A[i + (size_t)c * lda];
+      const double f = 2.0 * d / vv;
+      for (int i = j; i < rows; ++i) A[i + (size_t)c * lda] -= f * v[i - j];
+    }
+  }
+  for (int c = 0; c < k; ++c)
+    for (int i = 0; i < k; ++i) R[i + (size_t)c * ldr] = (i <= c && i < p) ? A[i + (size_t)c * lda] : 0.0;
+}
+}  // namespace
+
+extern "C" h2_status h2_import(h2_btree bt, const int32_t* row_rank, const int32_t* col_rank, const double* V,
+                               const double* E, const double* W, const double* F, const double* S, const double* N,
+                               h2_storage storage, int32_t rank_cap, int32_t update_cap, h2_stream stream,
+                               h2_mat* out) {
+  if (!out) H2_FAIL(H2_ERR_ARG, "h2_import: out is NULL");
+  *out = nullptr;
+  if (!bt || !row_rank || !col_rank) H2_FAIL(H2_ERR_ARG, "h2_import: NULL argument");
+  const h2_tree_* R = bt->rt;
+  const h2_tree_* C = bt->ct;
+  for (int t = 0; t < R->nclusters; ++t)
+    if (row_rank[t] < 0 || row_rank[t] > rank_cap) H2_FAIL(H2_ERR_SHAPE, "h2_import: row rank outside [0, rank_cap]");
+  for (int t = 0; t < C->nclusters; ++t)
+    if (col_rank[t] < 0 || col_rank[t] > rank_cap) H2_FAIL(H2_ERR_SHAPE, "h2_import: column rank outside [0, rank_cap]");
+  // the rank-0 structure (empty CSR), then the blocks
+  std::vector<int64_t> rowptr((size_t)R->n + 1, 0);
+  h2_mat Z = nullptr;
+  h2_status st = h2_from_sparse(bt, R->n, rowptr.data(), nullptr, nullptr, storage, rank_cap, update_cap, stream, &Z);
+  if (st != H2_OK) return st;
+  MatDev& M = Z->d;
+  const size_t r2 = (size_t)M.rcap * M.rcap;
+  int64_t pV = 0, pE = 0, pS = 0, pN = 0;
+  auto take = [](const double* src, int64_t& pos, double* dst, int rows, int cols, int ld) {
+    for (int j = 0; j < cols; ++j)
+      for (int i = 0; i < rows; ++i) dst[i + (size_t)j * ld] = src[pos++];
+  };
+  for (int side = 0; side < 2; ++side) {
+    const h2_tree_* T = side ? C : R;
+    const int32_t* k = side ? col_rank : row_rank;
+    const double* Lsrc = side ? W : V;
+    const double* Tsrc = side ? F : E;
+    DevSide& D = side ? M.col : M.row;
+    std::vector<double> leafb((size_t)D.nleaves * M.lmax * M.rcap, 0.0), tr((size_t)T->nclusters * r2, 0.0);
+    std::vector<double> rc((size_t)T->nclusters * r2, 0.0);
+    pV = 0;
+    pE = 0;
+    for (size_t q = 0; q < T->leaves.size(); ++q) {
+      const int t = T->leaves[q];
+      if (k[t] && !Lsrc) { h2_mat_destroy(Z); H2_FAIL(H2_ERR_ARG, "h2_import: NULL leaf basis"); }
+      take(Lsrc, pV, &leafb[q * M.lmax * M.rcap], T->hi[t] - T->lo[t], k[t], M.lmax);
+    }
+    for (int t = 1; t < T->nclusters; ++t) {
+      if (k[t] * k[T->parent[t]] && !Tsrc) { h2_mat_destroy(Z); H2_FAIL(H2_ERR_ARG, "h2_import: NULL transfers"); }
+      take(Tsrc, pE, &tr[(size_t)t * r2], k[t], k[T->parent[t]], M.rcap);
+    }
+    // memoised R-factors of the nested bases, bottom-up (Alg. 16; reading R7)
+    for (int t = T->nclusters - 1; t >= 0; --t) {
+      const int kt = k[t];
+      if (!kt) continue;
+      if (T->son0[t] < 0) {
+        const int m = T->hi[t] - T->lo[t];
+        const size_t q = (size_t)T->leaf_index[t];
+        std::vector<double> A(&leafb[q * M.lmax * M.rcap], &leafb[q * M.lmax * M.rcap] + (size_t)M.lmax * M.rcap);
+        host_qr_R(A, m, kt, M.lmax, &rc[(size_t)t * r2], M.rcap);
+      } else {
+        const int c0 = T->son0[t], c1 = T->son1[t], rows = k[c0] + k[c1];
+        std::vector<double> A((size_t)std::max(rows, 1) * kt, 0.0);
+        int r0 = 0;
+        for (int c : {c0, c1}) {  // R_c E_c  (k_c x k_t)
+          for (int j = 0; j < kt; ++j)
+            for (int i = 0; i < k[c]; ++i) {
+              double v = 0.0;
+              for (int p = 0; p < k[c]; ++p) v += rc[(size_t)c * r2 + i + (size_t)p * M.rcap] * tr[(size_t)c * r2 + p + (size_t)j * M.rcap];
+              A[r0 + i + (size_t)j * std::max(rows, 1)] = v;
+            }
+          r0 += k[c];
+        }
+        host_qr_R(A, rows, kt, std::max(rows, 1), &rc[(size_t)t * r2], M.rcap);
+      }
+    }
+    CUDA_TRY(cudaMemcpy(D.leafb, leafb.data(), leafb.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(D.tr, tr.data(), tr.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(D.rc, rc.data(), rc.size() * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(D.rank, k, sizeof(int32_t) * T->nclusters, cudaMemcpyHostToDevice));
+    std::vector<char>& nz = side ? Z->nzc : Z->nzr;
+    for (int t = 0; t < T->nclusters; ++t) nz[t] = k[t] != 0;
+  }
+  if (M.nadm) {
+    if (!S) { h2_mat_destroy(Z); H2_FAIL(H2_ERR_ARG, "h2_import: NULL couplings"); }
+    std::vector<double> hS((size_t)M.nadm * r2, 0.0);
+    for (int a = 0; a < M.nadm; ++a) {
+      const int b = Z->adm_blk[a];
+      take(S, pS, &hS[a * r2], row_rank[bt->t[b]], col_rank[bt->s[b]], M.rcap);
+    }
+    CUDA_TRY(cudaMemcpy(M.S, hS.data(), hS.size() * 8, cudaMemcpyHostToDevice));
+  }
+  if (M.ninad) {
+    if (!N) { h2_mat_destroy(Z); H2_FAIL(H2_ERR_ARG, "h2_import: NULL nearfield"); }
+    std::vector<double> hN((size_t)M.ninad * M.lmax * M.lmax, 0.0);
+    for (int a = 0; a < M.ninad; ++a) {
+      const int b = Z->inad_blk[a];
+      take(N, pN, &hN[(size_t)a * M.lmax * M.lmax], R->hi[bt->t[b]] - R->lo[bt->t[b]],
+           C->hi[bt->s[b]] - C->lo[bt->s[b]], M.lmax);
+      for (int64_t e = pN - (int64_t)(R->hi[bt->t[b]] - R->lo[bt->t[b]]) * (C->hi[bt->s[b]] - C->lo[bt->s[b]]); e < pN; ++e)
+        if (!std::isfinite(N[e])) { h2_mat_destroy(Z); H2_FAIL(H2_ERR_NONFINITE, "h2_import: non-finite nearfield entry"); }
+    }
+    CUDA_TRY(cudaMemcpy(M.N, hN.data(), hN.size() * 8, cudaMemcpyHostToDevice));
+  }
+  *out = Z;
+  return H2_OK;
+}
+
 // ---- batch recording (include/h2.h) ----------------------------------------------------------
 namespace {
 thread_local h2::ExecCtx g_batch_ctx;

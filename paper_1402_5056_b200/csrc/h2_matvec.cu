@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <unordered_map>
 
 #include "h2_internal.h"
 
@@ -52,6 +54,7 @@ struct MvArgs {
   const double* x;
   double* y;
   double alpha, beta;
+  int* sync;  // fused kernel: [0] forward done, [1] warps done with the couplings, [2] blocks exited
 };
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -83,7 +86,14 @@ __device__ void mv_up(const MvArgs& a, int s, int lane) {
   }
   for (;;) {
     const int p = a.s_parent[s];
-    if (p < 0) return;
+    if (p < 0) {  // s is the root: every forward coefficient is final (fused kernel: release them)
+      if (a.sync) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicExch(a.sync, 1);
+      }
+      return;
+    }
     // the father's structure and transfer matrices are static: fetch them (ranks into registers,
     // the F columns of this lane into L1) before the arrival handshake, so the climb step after it
     // waits only for the sibling's coefficients
@@ -217,14 +227,14 @@ __device__ void mv_couple(const MvArgs& a, int t, int lane) {
       if (!a.transpose) {
 #pragma unroll 8
         for (int j = 0; j < ks; ++j) {
-          const double xj = xs[j];
+          const double xj = __ldcg(xs + j);
           if (r < kt) y0 += Sa[r + (size_t)j * rcap] * xj;
           if (r + 32 < kt) y1 += Sa[r + 32 + (size_t)j * rcap] * xj;
         }
       } else {
 #pragma unroll 8
         for (int j = 0; j < ks; ++j) {
-          const double xj = xs[j];
+          const double xj = __ldcg(xs + j);
           if (r < kt) y0 += Sa[j + (size_t)r * rcap] * xj;
           if (r + 32 < kt) y1 += Sa[j + (size_t)(r + 32) * rcap] * xj;
         }
@@ -254,8 +264,8 @@ __device__ __forceinline__ void walk_levels(const MvArgs& a, int c0, int c1, int
     const int c = __shfl_sync(FULL, L < 32 ? c0 : c1, L & 31);
     const int kc = __shfl_sync(FULL, L < 32 ? k0 : k1, L & 31);
     const double* yc = a.d_xh + (size_t)c * rcap;
-    double n0 = lane < kc ? yc[lane] : 0.0;
-    double n1 = lane + 32 < kc ? yc[lane + 32] : 0.0;
+    double n0 = lane < kc ? __ldcg(yc + lane) : 0.0;
+    double n1 = lane + 32 < kc ? __ldcg(yc + lane + 32) : 0.0;
     if (kprev > 0 && kc > 0) {
       const double* E = a.d_tr + (size_t)c * rcap * rcap;
 #pragma unroll 4
@@ -271,12 +281,12 @@ __device__ __forceinline__ void walk_levels(const MvArgs& a, int c0, int c1, int
   }
 }
 
-__device__ void mv_walk(const MvArgs& a, int lane) {
+__device__ void mv_walk(const MvArgs& a, int lane, int group) {
   __shared__ double ysh[64];
   __shared__ int sh[2];  // common prefix length, rank at its end
   const int rcap = a.rcap, lmax = a.lmax, aw = a.d_ancw;
   const int warp = threadIdx.x >> 5;
-  const int lf = blockIdx.x * 8, ll = min(lf + 8, a.d_nleaves) - 1;  // first / last leaf ordinal
+  const int lf = group * 8, ll = min(lf + 8, a.d_nleaves) - 1;  // first / last leaf ordinal
   if (warp == 0) {
     const int32_t* pf = a.d_anc + (size_t)lf * aw;
     const int32_t* pl = a.d_anc + (size_t)ll * aw;
@@ -318,8 +328,16 @@ __device__ void mv_walk(const MvArgs& a, int lane) {
     if (lane < m) a0 += V[lane + (size_t)j * lmax] * yj;
     if (lane + 32 < m) a1 += V[lane + 32 + (size_t)j * lmax] * yj;
   }
-  if (lane < m) a.y[a.d_perm[lo + lane]] += a.alpha * a0;
-  if (lane + 32 < m) a.y[a.d_perm[lo + lane + 32]] += a.alpha * a1;
+  // y was written by another warp (nearfield phase, maybe on another SM in the fused kernel): read
+  // it through L2, never from a possibly stale L1 line
+  if (lane < m) {
+    double* yo = a.y + a.d_perm[lo + lane];
+    *yo = __ldcg(yo) + a.alpha * a0;
+  }
+  if (lane + 32 < m) {
+    double* yo = a.y + a.d_perm[lo + lane + 32];
+    *yo = __ldcg(yo) + a.alpha * a1;
+  }
 }
 
 __global__ void __launch_bounds__(256, 4) k_matvec_near(const __grid_constant__ MvArgs a) {
@@ -338,7 +356,46 @@ __global__ void __launch_bounds__(256) k_matvec_couple(const __grid_constant__ M
 }
 
 __global__ void __launch_bounds__(256) k_matvec_walk(const __grid_constant__ MvArgs a) {
-  mv_walk(a, threadIdx.x & 31);
+  mv_walk(a, threadIdx.x & 31, blockIdx.x);
+}
+
+// ---- the whole far + near field in ONE persistent (cooperative) launch --------------------------
+// Every warp: (A) forward transform of its source leaves with the climb (the warp completing the
+// root publishes sync[0]); (B) the nearfield of its destination leaves, y = alpha N x + beta y --
+// the bulk of the bytes streams while the climb's latency chain finishes elsewhere; (C) once the
+// forward coefficients are final, the couplings of its destination clusters (sync[1] counts the
+// warps done); (D) once every coupling is in, each CTA walks its groups of 8 leaves and adds
+// alpha V_t yhat_t.  The CTAs are co-resident (cooperative launch), so the two spin-waits cannot
+// deadlock; the last CTA to leave resets the counters for the next product.
+__device__ __forceinline__ void spin_until(const int* p, int v) {
+  while (*(volatile const int*)p < v) __nanosleep(64);
+  __threadfence();
+}
+
+__global__ void __launch_bounds__(256, 2) k_matvec_fused(const __grid_constant__ MvArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (int)(gridDim.x * (blockDim.x >> 5));
+  const int w0 = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  for (int w = w0; w < a.s_nleaves; w += nw) mv_up(a, a.s_leaves[w], lane);
+  for (int w = w0; w < a.d_nleaves; w += nw) mv_leaf_near(a, a.d_leaves[w], lane);
+  spin_until(a.sync, 1);
+  for (int w = w0; w < a.d_nclusters; w += nw) mv_couple(a, w, lane);
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) atomicAdd(a.sync + 1, 1);
+  spin_until(a.sync + 1, nw);
+  const int ngroups = (a.d_nleaves + 7) / 8;
+  for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    mv_walk(a, lane, g);
+    __syncthreads();  // the shared path prefix of the next group
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(a.sync + 2, 1) == (int)gridDim.x - 1) {
+    a.sync[0] = 0;
+    a.sync[1] = 0;
+    a.sync[2] = 0;
+    __threadfence();
+  }
 }
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
@@ -399,15 +456,45 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   // the far field contributes only if some row and some column basis may have a non-zero rank
   const bool far = std::find(Z->nzr.begin(), Z->nzr.end(), 1) != Z->nzr.end() &&
                    std::find(Z->nzc.begin(), Z->nzc.end(), 1) != Z->nzc.end();
+  a.sync = nullptr;
   if (!far) {
     H2_LAUNCH(K_MV, st, k_matvec_near<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
     return cudaGetLastError();
   }
+  // one cooperative launch (k_matvec_fused) only on request (H2_MV_FUSED=1): measured 334 us for
+  // the C2 factor L against 167 us for the four-launch path below -- a persistent grid of 2 CTAs
+  // per SM serialises the latency-bound climb / coupling / walk work that the separate launches
+  // spread over 8-16k warps
+  static const bool fused_on = getenv("H2_MV_FUSED") && atoi(getenv("H2_MV_FUSED")) != 0;
+  static int fused_grid = -1;
+  static std::unordered_map<cudaStream_t, int*> syncs;  // counters per stream (products on one stream are ordered)
+  cudaError_t e;
+  if (fused_on && fused_grid < 0) {
+    int dev = 0, nsm = 0, per = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_matvec_fused, 256, 0);
+    fused_grid = coop ? nsm * std::min(per, 2) : 0;
+    cudaGetLastError();
+  }
+  if (fused_on && fused_grid > 0) {
+    int*& sync = syncs[st];
+    if (!sync) {
+      if ((e = cudaMalloc(&sync, 4 * sizeof(int)))) return e;
+      if ((e = cudaMemset(sync, 0, 4 * sizeof(int)))) return e;
+    }
+    a.sync = sync;
+    void* args[] = {(void*)&a};
+    H2_LAUNCH(K_MV, st, e = cudaLaunchCooperativeKernel((const void*)k_matvec_fused, dim3(fused_grid), dim3(256), args, 0, st));
+    if (e) return e;
+    return cudaGetLastError();
+  }
+  a.sync = nullptr;
   // the nearfield stream (the bulk of the bytes) runs on a second stream, concurrently with the
   // forward transform and the couplings; the backward walk adds V_t yhat_t after both
   static cudaStream_t s2 = nullptr;
   static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaError_t e;
   if (!s2) {
     if ((e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming))) return e;

@@ -103,24 +103,108 @@ constexpr int NPART = 64;
 
 // ---- H^2 block times dense --------------------------------------------------------------------
 // forward transform over T_b: leaves
-__device__ void it_hm_fwd_leaf(const MatDev& M, const DevSide& S, int l0, int base_lo, const double* D, int ldd,
-                                                    Dim md, double* xh, int ident, int item_, int nitems_, double* smx_) {
-  const int q = S.leaves[l0 + item_];
-  const int m = md.v();
-  const int rows = S.hi[q] - S.lo[q], kq = S.rank[q];
+// Every output entry of the five phases is one inline function, shared by the per-phase items
+// below and by the fused small-subtree item (it_hm_small): both compute the same sums in the same
+// order, so the two schedules are bit-identical.
+__device__ __forceinline__ double hm_fwd_leaf_entry(const MatDev& M, const DevSide& S, int q, int base_lo,
+                                                    const double* D, int ldd, int ident, int j, int c) {
+  const int rows = S.hi[q] - S.lo[q];
   const double* W = S.leafb + (size_t)S.leafidx[q] * M.lmax * M.rcap;
   const int off = S.lo[q] - base_lo;
+  double acc = 0.0;
+  if (ident) {  // D = I: column c of D is e_c, W^T e_c = row (c - off) of W
+    const int i = c - off;
+    if (i >= 0 && i < rows) acc = W[i + j * M.lmax];
+  } else {
+    for (int i = 0; i < rows; ++i) acc += W[i + j * M.lmax] * D[off + i + (size_t)c * ldd];
+  }
+  return acc;
+}
+
+__device__ __forceinline__ double hm_fwd_level_entry(const MatDev& M, const DevSide& S, const double* xh, int s, int j,
+                                                     int c) {
+  double acc = 0.0;
+  for (int q = 0; q < 2; ++q) {
+    const int sq = q ? S.son1[s] : S.son0[s];
+    const int kq = S.rank[sq];
+    const double* F = S.tr + (size_t)sq * M.rcap * M.rcap;
+    const double* xq = xh + (size_t)sq * M.rcap * KC;
+    for (int i = 0; i < kq; ++i) acc += F[i + j * M.rcap] * xq[i + c * M.rcap];
+  }
+  return acc;
+}
+
+__device__ __forceinline__ double hm_couple_entry(const MatDev& M, const DevSide& Dd, const DevSide& Ds, int ap, int b,
+                                                  int bsz, int trans, const double* xh, int i, int c) {
+  double acc = 0.0;
+  for (int q = Dd.bptr[ap]; q < Dd.bptr[ap + 1]; ++q) {
+    const int slot = Dd.bidx[q];
+    const int bp = trans ? M.adm_t[slot] : M.adm_s[slot];
+    if (bp < b || bp >= b + bsz) continue;
+    const int kb = Ds.rank[bp];
+    const double* Sa = M.S + (size_t)slot * M.rcap * M.rcap;
+    const double* x = xh + (size_t)bp * M.rcap * KC + c * M.rcap;
+    if (!trans)
+      for (int j = 0; j < kb; ++j) acc += Sa[i + j * M.rcap] * x[j];
+    else
+      for (int j = 0; j < kb; ++j) acc += Sa[j + i * M.rcap] * x[j];
+  }
+  return acc;
+}
+
+__device__ __forceinline__ double hm_bwd_level_entry(const MatDev& M, const DevSide& D, const double* yh, int t, int i,
+                                                     int c) {
+  const int p = D.parent[t], kp = D.rank[p];
+  const double* E = D.tr + (size_t)t * M.rcap * M.rcap;
+  const double* yp = yh + (size_t)p * M.rcap * KC;
+  double acc = yh[(size_t)t * M.rcap * KC + i + c * M.rcap];
+  for (int j = 0; j < kp; ++j) acc += E[i + j * M.rcap] * yp[j + c * M.rcap];
+  return acc;
+}
+
+__device__ __forceinline__ void hm_leaf_entry(const MatDev& M, const DevSide& Dd, const DevSide& Ds, int ap, int a,
+                                              int b, int bsz, int trans, const double* D, int ldd, const double* yh,
+                                              double* out, int ldo, double alpha, double beta, int ident, int i,
+                                              int c) {
+  const int ka = Dd.rank[ap];
+  const int offo = Dd.lo[ap] - Dd.lo[a];
+  const double* V = Dd.leafb + (size_t)Dd.leafidx[ap] * M.lmax * M.rcap;
+  const double* y = yh + (size_t)ap * M.rcap * KC;
+  const int32_t* np = trans ? M.ntptr : M.nptr;
+  const int32_t* ni = trans ? M.ntidx : M.nidx;
+  const int32_t* part = trans ? M.in_t : M.in_s;
+  double acc = 0.0;
+  for (int j = 0; j < ka; ++j) acc += V[i + j * M.lmax] * y[j + c * M.rcap];
+  for (int q = np[ap]; q < np[ap + 1]; ++q) {
+    const int slot = ni[q];
+    const int bp = part[slot];
+    if (bp < b || bp >= b + bsz) continue;
+    const int rb = Ds.hi[bp] - Ds.lo[bp];
+    const double* Na = M.N + (size_t)slot * M.lmax * M.lmax;
+    const int offb = Ds.lo[bp] - Ds.lo[b];
+    if (ident) {  // D = I: the tile's column (c - offb) (exact: the other terms are zero products)
+      const int jj = c - offb;
+      if (jj >= 0 && jj < rb) acc += trans ? Na[jj + i * M.lmax] : Na[i + jj * M.lmax];
+      continue;
+    }
+    const double* x = D + offb + (size_t)c * ldd;
+    if (!trans)
+      for (int j = 0; j < rb; ++j) acc += Na[i + j * M.lmax] * x[j];
+    else
+      for (int j = 0; j < rb; ++j) acc += Na[j + i * M.lmax] * x[j];
+  }
+  double* o = out + offo + i + (size_t)c * ldo;
+  *o = beta == 0.0 ? alpha * acc : beta * *o + alpha * acc;
+}
+
+__device__ void it_hm_fwd_leaf(const MatDev& M, const DevSide& S, int l0, int base_lo, const double* D, int ldd,
+                               Dim md, double* xh, int ident, int item_, int nitems_, double* smx_) {
+  const int q = S.leaves[l0 + item_];
+  const int m = md.v(), kq = S.rank[q];
   double* x = xh + (size_t)q * M.rcap * KC;
   for (int e = threadIdx.x; e < kq * m; e += NT) {
     const int j = e % kq, c = e / kq;
-    double acc = 0.0;
-    if (ident) {  // D = I: column c of D is e_c, W^T e_c = row (c - off) of W
-      const int i = c - off;
-      if (i >= 0 && i < rows) acc = W[i + j * M.lmax];
-    } else {
-      for (int i = 0; i < rows; ++i) acc += W[i + j * M.lmax] * D[off + i + (size_t)c * ldd];
-    }
-    x[j + c * M.rcap] = acc;
+    x[j + c * M.rcap] = hm_fwd_leaf_entry(M, S, q, base_lo, D, ldd, ident, j, c);
   }
 }
 
@@ -131,97 +215,145 @@ __device__ void it_hm_fwd_level(const MatDev& M, const DevSide& S, int b0, Dim m
   double* x = xh + (size_t)s * M.rcap * KC;
   for (int e = threadIdx.x; e < ks * m; e += NT) {
     const int j = e % ks, c = e / ks;
-    double acc = 0.0;
-    for (int q = 0; q < 2; ++q) {
-      const int sq = q ? S.son1[s] : S.son0[s];
-      const int kq = S.rank[sq];
-      const double* F = S.tr + (size_t)sq * M.rcap * M.rcap;
-      const double* xq = xh + (size_t)sq * M.rcap * KC;
-      for (int i = 0; i < kq; ++i) acc += F[i + j * M.rcap] * xq[i + c * M.rcap];
-    }
-    x[j + c * M.rcap] = acc;
+    x[j + c * M.rcap] = hm_fwd_level_entry(M, S, xh, s, j, c);
   }
 }
 
 // couplings: CTA per cluster a' of T_a (dst side): yhat_{a'} = sum_{(a',b') adm, b' in T_b} S_op xhat_{b'}
 __device__ void it_hm_couple(const MatDev& M, const DevSide& Dd, const DevSide& Ds, int a, int b, int trans, Dim md,
-                                                  const double* xh, double* yh, int item_, int nitems_, double* smx_) {
+                             const double* xh, double* yh, int item_, int nitems_, double* smx_) {
   const int ap = a + item_;
   const int m = md.v(), ka = Dd.rank[ap];
   const int bsz = Ds.tsize[b];
   double* y = yh + (size_t)ap * M.rcap * KC;
   for (int e = threadIdx.x; e < ka * m; e += NT) {
     const int i = e % ka, c = e / ka;
-    double acc = 0.0;
-    for (int q = Dd.bptr[ap]; q < Dd.bptr[ap + 1]; ++q) {
-      const int slot = Dd.bidx[q];
-      const int bp = trans ? M.adm_t[slot] : M.adm_s[slot];
-      if (bp < b || bp >= b + bsz) continue;
-      const int kb = Ds.rank[bp];
-      const double* Sa = M.S + (size_t)slot * M.rcap * M.rcap;
-      const double* x = xh + (size_t)bp * M.rcap * KC + c * M.rcap;
-      if (!trans)
-        for (int j = 0; j < kb; ++j) acc += Sa[i + j * M.rcap] * x[j];
-      else
-        for (int j = 0; j < kb; ++j) acc += Sa[j + i * M.rcap] * x[j];
-    }
-    y[i + c * M.rcap] = acc;
+    y[i + c * M.rcap] = hm_couple_entry(M, Dd, Ds, ap, b, bsz, trans, xh, i, c);
   }
 }
 
 __device__ void it_hm_bwd_level(const MatDev& M, const DevSide& D, int b0, Dim md, double* yh, int item_, int nitems_, double* smx_) {
   const int t = D.bfs[b0 + item_];
-  const int p = D.parent[t];
-  const int m = md.v(), kt = D.rank[t], kp = D.rank[p];
-  const double* E = D.tr + (size_t)t * M.rcap * M.rcap;
+  const int m = md.v(), kt = D.rank[t];
   double* y = yh + (size_t)t * M.rcap * KC;
-  const double* yp = yh + (size_t)p * M.rcap * KC;
   for (int e = threadIdx.x; e < kt * m; e += NT) {
     const int i = e % kt, c = e / kt;
-    double acc = y[i + c * M.rcap];
-    for (int j = 0; j < kp; ++j) acc += E[i + j * M.rcap] * yp[j + c * M.rcap];
-    y[i + c * M.rcap] = acc;
+    y[i + c * M.rcap] = hm_bwd_level_entry(M, D, yh, t, i, c);
   }
 }
 
 __device__ void it_hm_leaf(const MatDev& M, const DevSide& Dd, const DevSide& Ds, int l0, int a, int b, int trans,
-                                                const double* D, int ldd, Dim md, const double* yh, double* out,
-                                                int ldo, double alpha, double beta, int ident, int item_, int nitems_,
-                                                double* smx_) {
+                           const double* D, int ldd, Dim md, const double* yh, double* out, int ldo, double alpha,
+                           double beta, int ident, int item_, int nitems_, double* smx_) {
   const int ap = Dd.leaves[l0 + item_];
   const int m = md.v();
-  const int rows = Dd.hi[ap] - Dd.lo[ap], ka = Dd.rank[ap];
-  const int offo = Dd.lo[ap] - Dd.lo[a];
+  const int rows = Dd.hi[ap] - Dd.lo[ap];
   const int bsz = Ds.tsize[b];
-  const double* V = Dd.leafb + (size_t)Dd.leafidx[ap] * M.lmax * M.rcap;
-  const double* y = yh + (size_t)ap * M.rcap * KC;
-  const int32_t* np = trans ? M.ntptr : M.nptr;
-  const int32_t* ni = trans ? M.ntidx : M.nidx;
-  const int32_t* part = trans ? M.in_t : M.in_s;
   for (int e = threadIdx.x; e < rows * m; e += NT) {
     const int i = e % rows, c = e / rows;
-    double acc = 0.0;
-    for (int j = 0; j < ka; ++j) acc += V[i + j * M.lmax] * y[j + c * M.rcap];
-    for (int q = np[ap]; q < np[ap + 1]; ++q) {
-      const int slot = ni[q];
-      const int bp = part[slot];
-      if (bp < b || bp >= b + bsz) continue;
-      const int rb = Ds.hi[bp] - Ds.lo[bp];
-      const double* Na = M.N + (size_t)slot * M.lmax * M.lmax;
-      const int offb = Ds.lo[bp] - Ds.lo[b];
-      if (ident) {  // D = I: the tile's column (c - offb) (exact: the other terms are zero products)
-        const int jj = c - offb;
-        if (jj >= 0 && jj < rb) acc += trans ? Na[jj + i * M.lmax] : Na[i + jj * M.lmax];
-        continue;
-      }
-      const double* x = D + offb + (size_t)c * ldd;
-      if (!trans)
-        for (int j = 0; j < rb; ++j) acc += Na[i + j * M.lmax] * x[j];
-      else
-        for (int j = 0; j < rb; ++j) acc += Na[j + i * M.lmax] * x[j];
+    hm_leaf_entry(M, Dd, Ds, ap, a, b, bsz, trans, D, ldd, yh, out, ldo, alpha, beta, ident, i, c);
+  }
+}
+
+// ---- H^2 block times dense for SMALL block subtrees in one item ----------------------------------
+// out = beta out + alpha op(Z)|_{a x b} D when T_a and T_b have at most HM_SMALL clusters: the five
+// phases above (forward leaves, forward levels bottom-up, couplings, backward levels top-down,
+// leaves) run in one CTA with block barriers between dependent levels instead of one op (and one
+// cluster barrier) per phase and level.  Within a phase the (cluster, entry) pairs of all clusters
+// of the level are flattened over the CTA's threads.  Same entry functions: bit-identical.
+constexpr int HM_SMALL = 31;  // clusters per subtree (16 leaves, 5 levels)
+
+// list the clusters of T_r (ids r .. r + tsize - 1) at tree level L (L < 0: all; L = 99: the
+// leaves) with their entry counts (rows x m) into cl[] / pre[] (exclusive prefix sums); thread 0
+__device__ __forceinline__ int hm_list(const DevSide& D, int r, int L, int m, bool use_rank, int* cl, int* pre) {
+  int n = 0, tot = 0;
+  const int e = r + D.tsize[r];
+  for (int q = r; q < e; ++q) {
+    const bool take = L < 0 || (L == 99 ? D.son0[q] < 0 : D.level[q] == L);
+    if (!take) continue;
+    cl[n] = q;
+    pre[n] = tot;
+    tot += (use_rank ? D.rank[q] : D.hi[q] - D.lo[q]) * m;
+    ++n;
+  }
+  pre[n] = tot;
+  return n;
+}
+
+// the listed cluster that owns flattened entry e (last i with pre[i] <= e)
+__device__ __forceinline__ int hm_owner(const int* pre, int n, int e) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ void it_hm_small(const MatDev& M, const DevSide& Dd, const DevSide& Ds, int a, int b, int trans,
+                            const double* D, int ldd, Dim md, double* xh, double* yh, double* out, int ldo,
+                            double alpha, double beta, int ident, double* smx_) {
+  int* cl = reinterpret_cast<int*>(smx_);  // listed clusters (<= HM_SMALL)
+  int* pre = cl + 64;                      // entry prefix sums
+  int* info = pre + 65;                    // [0] count, [2] deepest level in T_b, [3] in T_a
+  const int m = md.v();
+  const int base_lo = Ds.lo[b];
+  const int bsz = Ds.tsize[b];
+  if (threadIdx.x == 0) {
+    int lb = 0, la = 0;
+    for (int q = b; q < b + bsz; ++q) lb = max(lb, Ds.level[q]);
+    for (int q = a; q < a + Dd.tsize[a]; ++q) la = max(la, Dd.level[q]);
+    info[2] = lb;
+    info[3] = la;
+  }
+  __syncthreads();
+  const int Lb = info[2], La = info[3], lvb = Ds.level[b], lva = Dd.level[a];
+  // forward transform, bottom-up over T_b (a leaf from D, an internal cluster from its sons)
+  for (int L = Lb; L >= lvb; --L) {
+    if (threadIdx.x == 0) info[0] = hm_list(Ds, b, L, m, true, cl, pre);
+    __syncthreads();
+    const int n = info[0];
+    for (int e = threadIdx.x; e < pre[n]; e += NT) {
+      const int i = hm_owner(pre, n, e), q = cl[i], kq = Ds.rank[q], x0 = e - pre[i];
+      const int j = x0 % kq, c = x0 / kq;
+      xh[(size_t)q * M.rcap * KC + j + c * M.rcap] = Ds.son0[q] < 0
+          ? hm_fwd_leaf_entry(M, Ds, q, base_lo, D, ldd, ident, j, c)
+          : hm_fwd_level_entry(M, Ds, xh, q, j, c);
     }
-    double* o = out + offo + i + (size_t)c * ldo;
-    *o = beta == 0.0 ? alpha * acc : beta * *o + alpha * acc;
+    __syncthreads();
+  }
+  // couplings for every cluster of T_a
+  if (threadIdx.x == 0) info[0] = hm_list(Dd, a, -1, m, true, cl, pre);
+  __syncthreads();
+  {
+    const int n = info[0];
+    for (int e = threadIdx.x; e < pre[n]; e += NT) {
+      const int i = hm_owner(pre, n, e), ap = cl[i], ka = Dd.rank[ap], x0 = e - pre[i];
+      const int ii = x0 % ka, c = x0 / ka;
+      yh[(size_t)ap * M.rcap * KC + ii + c * M.rcap] = hm_couple_entry(M, Dd, Ds, ap, b, bsz, trans, xh, ii, c);
+    }
+  }
+  __syncthreads();
+  // backward transform, top-down below a
+  for (int L = lva + 1; L <= La; ++L) {
+    if (threadIdx.x == 0) info[0] = hm_list(Dd, a, L, m, true, cl, pre);
+    __syncthreads();
+    const int n = info[0];
+    for (int e = threadIdx.x; e < pre[n]; e += NT) {
+      const int i = hm_owner(pre, n, e), t = cl[i], kt = Dd.rank[t], x0 = e - pre[i];
+      const int ii = x0 % kt, c = x0 / kt;
+      yh[(size_t)t * M.rcap * KC + ii + c * M.rcap] = hm_bwd_level_entry(M, Dd, yh, t, ii, c);
+    }
+    __syncthreads();
+  }
+  // leaves of T_a
+  if (threadIdx.x == 0) info[0] = hm_list(Dd, a, 99, m, false, cl, pre);
+  __syncthreads();
+  const int n = info[0];
+  for (int e = threadIdx.x; e < pre[n]; e += NT) {
+    const int i = hm_owner(pre, n, e), ap = cl[i], rows = Dd.hi[ap] - Dd.lo[ap], x0 = e - pre[i];
+    hm_leaf_entry(M, Dd, Ds, ap, a, b, bsz, trans, D, ldd, yh, out, ldo, alpha, beta, ident, x0 % rows, x0 / rows);
   }
 }
 

@@ -19,7 +19,7 @@ EXPORTED_SYMBOLS = [
     "h2_from_sparse", "h2_lowrank_update", "h2_matvec", "h2_addmul", "h2_lr_factor", "h2_solve",
     "h2_ranks", "h2_storage_report", "h2_export", "h2_check_device_flags",
     "h2_profile_enable", "h2_profile_read", "h2_profile_debug", "h2_profile_ops", "h2_stats", "h2_pcg", "h2_launch_count",
-    "h2_mat_destroy", "h2_last_error", "h2_batch_begin", "h2_batch_end", "h2_inverse",
+    "h2_mat_destroy", "h2_last_error", "h2_batch_begin", "h2_batch_end", "h2_inverse", "h2_import",
 ]
 
 if not os.path.exists(_LIBPATH):
@@ -63,6 +63,7 @@ _sig = {
     "h2_batch_begin": [_p],
     "h2_batch_end": [],
     "h2_inverse": [_p, _p, _p],
+    "h2_import": [_p, _p, _p, _p, _p, _p, _p, _p, _p, C.c_int, _i32, _i32, _p, C.POINTER(_p)],
 }
 for _name, _args in _sig.items():
     _f = getattr(_lib, _name)
@@ -314,6 +315,18 @@ def h2_export(Z: Mat):
     _check(_lib.h2_export(Z.h, *[_ptr(b) for b in bufs], _ptr(sizes)))
     kr, kc = h2_ranks(Z)
     return dict(zip(["V", "E", "W", "F", "S", "N"], bufs), k=kr, l=kc)
+
+
+def h2_import(bt: BlockTree, rep: dict, lower: bool = False, rank_cap: int = 32, update_cap: int = 32,
+              stream=None) -> Mat:
+    """The inverse of h2_export: rep = dict(k, l, V, E, W, F, S, N) in h2_export's layouts."""
+    kr = np.ascontiguousarray(rep["k"], dtype=np.int32)
+    kc = np.ascontiguousarray(rep["l"], dtype=np.int32)
+    arrs = [np.ascontiguousarray(rep[x], dtype=np.float64) for x in ("V", "E", "W", "F", "S", "N")]
+    h = _p()
+    _check(_lib.h2_import(bt.h, _ptr(kr), _ptr(kc), *[_ptr(a) if a.size else None for a in arrs],
+                          1 if lower else 0, int(rank_cap), int(update_cap), _stream(stream), C.byref(h)))
+    return Mat(h.value, bt, lower, rank_cap, update_cap)
 
 
 def h2_profile_enable(on: bool = True):
