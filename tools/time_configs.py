@@ -85,6 +85,23 @@ def run_c1(count):
     print(json.dumps(out), flush=True)
 
 
+def matvec_gbps(Z, n, reps=20):
+    """Algorithmic bytes (8 per stored scalar + 16 n) / median time of h2_matvec."""
+    x = torch.randn(n, dtype=torch.float64, device=dev)
+    y = torch.empty_like(x)
+    for _ in range(3):
+        P.h2_matvec(Z, x, y)
+    evs = [(ev(), ev()) for _ in range(reps)]
+    for a, b in evs:
+        a.record()
+        P.h2_matvec(Z, x, y)
+        b.record()
+    torch.cuda.synchronize()
+    ms = sorted(a.elapsed_time(b) for a, b in evs)[reps // 2]
+    byt = 8.0 * float(P.h2_storage_report(Z).sum()) + 16.0 * n
+    return {"ms": ms, "MB": byt / 1e6, "GBps": byt / ms / 1e6}
+
+
 def factor_and_pcg(c, bt, Z, Aop, eps, label, extra):
     e0, e1, e2 = ev(), ev(), ev()
     torch.cuda.synchronize()
@@ -100,7 +117,8 @@ def factor_and_pcg(c, bt, Z, Aop, eps, label, extra):
     out = {"config": label, "n": c["n"], "eps": eps, "setup_s": e0.elapsed_time(e1) / 1e3,
            "pcg_iterations": m, "pcg_relres": rel, "pcg_s": e1.elapsed_time(e2) / 1e3, "stats": P.h2_stats(Z),
            "max_rank": [int(kr.max()), int(kc.max())], "flags": P.h2_check_device_flags(Z),
-           "storage_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / c["n"] / 1e3)}
+           "storage_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / c["n"] / 1e3),
+           "matvec_factor": matvec_gbps(Z, c["n"])}
     out.update(extra)
     print(json.dumps(out), flush=True)
 
@@ -141,12 +159,14 @@ def run_c4(N, epss):
     ref = c["A"] @ (c["A"] @ xv)
     prod = {"product_s": prod_s, "product_stats": P.h2_stats(Z),
             "product_rel_err": float(np.linalg.norm(zx - ref) / np.linalg.norm(ref)),
-            "product_storage_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / c["n"] / 1e3)}
+            "product_storage_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / c["n"] / 1e3),
+            "matvec_product": matvec_gbps(Z, c["n"])}
     print(json.dumps({"config": f"C4 {N}^2 A*A", "n": c["n"], "structure_s": st, **prod}), flush=True)
     del Z
     for eps in epss:
-        L = P.h2_from_sparse(bt, c["A"], lower=True, rank_cap=32, update_cap=32)
-        factor_and_pcg(c, bt, L, Aop, eps, f"C4 {N}^2 Cholesky of A", {})
+        cap = 32 if eps >= 1e-4 else 48  # tighter truncation, larger ranks
+        L = P.h2_from_sparse(bt, c["A"], lower=True, rank_cap=cap, update_cap=cap)
+        factor_and_pcg(c, bt, L, Aop, eps, f"C4 {N}^2 Cholesky of A", {"rank_cap": cap})
         del L
 
 
