@@ -295,13 +295,14 @@ __device__ __forceinline__ double opaque(double x) {
 }
 
 // Jacobi rotation (c, s) that orthogonalises columns x, y with al = |x|^2, be = |y|^2, ga = x.y:
-// t = sign(z) / (|z| + sqrt(1 + z^2)), z = (be - al) / (2 ga); c = 1/sqrt(1 + t^2), s = c t.
-// Only called with ga != 0.
+// t = sign(z) / (|z| + sqrt(1 + z^2)), z = (be - al) / (2 ga), written with one division as
+// t = sign(d) 2 ga / (|d| + sqrt(d^2 + 4 ga^2)), d = be - al (sign(0) = +1; both forms are the
+// same number, the second has one dependent DDIV less per Jacobi round); c = 1/sqrt(1 + t^2),
+// s = c t.  Only called with ga != 0.
 __device__ __forceinline__ void jacobi_rot(double al, double be, double ga, double* c, double* s) {
-  const double zeta = (be - al) / (2.0 * ga);
-  double t;
-  if (fabs(zeta) > 1e15) t = 0.5 / zeta;
-  else t = copysign(1.0 / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0))), zeta);
+  const double d = be - al;
+  const double g2 = 2.0 * ga;
+  const double t = (d >= 0.0 ? g2 : -g2) / (fabs(d) + sqrt(fma(d, d, g2 * g2)));
   *c = rsqrt(fma(t, t, 1.0));
   *s = *c * t;
 }

@@ -66,7 +66,6 @@ enum OpCode : int32_t {
   OP_TINV,    // in-place inverse of a diagonal leaf tile (approximate inversion, Remark 1)
   OP_C2CORE,  // Case 2, both factors admissible: [G =] W^T V, C = S^X G S^Y, choose (one CTA)
   OP_SKIPZ,  // all CTAs: if *ip == 0 skip the next `count` ops (a zero-rank local update)
-  OP_HM_SMALL,  // H^2 block x dense for small block subtrees, all five phases in one item
   OP_COUNT
 };
 

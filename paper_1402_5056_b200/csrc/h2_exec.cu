@@ -30,7 +30,7 @@ namespace {
 
 constexpr int NT = NTHREADS;
 constexpr int CL = 16;    // CTAs of the executor cluster (non-portable size 16; falls back to 8)
-constexpr int BIG = 64;    // ops with more items run as a full-grid launch (1024: -7 % at C2, but see DESIGN §2)
+constexpr int BIG = 1024;  // ops with more items run as a full-grid launch (64: +5 % at C2)
 constexpr int KC = KCAP_MAX;
 constexpr int PR = 192;
 constexpr int RM = KC + 1;
@@ -57,7 +57,7 @@ __constant__ int c_op_kid[OP_COUNT] = {
     K_AR_EXPAND, K_AR_GEMM, K_AR_GEMM, K_AR_GEMM, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL,
     K_AR_TILE, K_AR_TILE, K_AR_TILE, K_AR_TSQR, K_AR_TEMP, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC,
     K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_TEMP, K_AR_MISC,
-    K_AR_TILE, K_AR_GEMM, K_AR_MISC, K_AR_HMUL};
+    K_AR_TILE, K_AR_GEMM, K_AR_MISC};
 
 __device__ __forceinline__ const DevSide& side_of(const MatDev& M, int s) { return s ? M.col : M.row; }
 
@@ -136,11 +136,6 @@ __device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, do
       const PHm& q = *reinterpret_cast<const PHm*>(op.p);
       ar::it_hm_leaf(M, side_of(M, q.dside), side_of(M, q.sside), q.l0, q.a, q.b, q.trans, q.D, q.ldd, q.m, q.yh,
                      q.out, q.ldo, q.alpha, q.beta, q.ident, it, n, sm);
-    } break;
-    case OP_HM_SMALL: {
-      const PHm& q = *reinterpret_cast<const PHm*>(op.p);
-      ar::it_hm_small(M, side_of(M, q.dside), side_of(M, q.sside), q.a, q.b, q.trans, q.D, q.ldd, q.m, q.xh, q.yh,
-                      q.out, q.ldo, q.alpha, q.beta, q.ident, sm);
     } break;
     case OP_POTRF: {
       const PTile& q = *reinterpret_cast<const PTile*>(op.p);
@@ -717,11 +712,6 @@ void hmul_dense(const MatDev& M, bool trans, int a, int b, int b_blk, const doub
   leaf_range(Ts, b, &l0, &nl);
   h.l0 = l0;
   h.base_lo = Ts->lo[b];
-  static const bool no_small = getenv("H2_NO_HM_SMALL") != nullptr;  // A/B switch (tools)
-  if (!no_small && Td->tsize[a] <= ar::HM_SMALL && Ts->tsize[b] <= ar::HM_SMALL) {
-    c->emit(OP_HM_SMALL, 1, &M, h);  // all five phases in one item (bit-identical)
-    return;
-  }
   c->emit(OP_HM_FWD_LEAF, nl, &M, h);
   for (int L = Ts->depth - 1; L >= Ts->level[b]; --L) {
     int s0, ns;

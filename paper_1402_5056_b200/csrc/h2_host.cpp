@@ -338,6 +338,33 @@ static h2_status setup_side(h2_mat_* Z, DevSide& D, const h2_tree_* T, bool row_
   CUDA_TRY(dalloc(Z, &D.xh, (size_t)T->nclusters * M.rcap));
   CUDA_TRY(dalloc(Z, &D.mvsync, (size_t)T->nclusters));
   CUDA_TRY(cudaMemset(D.mvsync, 0, sizeof(int32_t) * (size_t)T->nclusters));
+  {  // matvec schedule: maximal subtrees with <= MV_SUB_LEAVES leaves, and the clusters above them
+    std::vector<int32_t> nleaf(T->nclusters, 0);
+    for (int c = T->nclusters - 1; c >= 0; --c)
+      nleaf[c] = T->son0[c] < 0 ? 1 : nleaf[T->son0[c]] + nleaf[T->son1[c]];
+    std::vector<int32_t> roots, top;
+    std::vector<std::vector<int32_t>> bylev;
+    for (int c = 0; c < T->nclusters; ++c) {
+      const int p = T->parent[c];
+      if (nleaf[c] <= MV_SUB_LEAVES && (p < 0 || nleaf[p] > MV_SUB_LEAVES)) roots.push_back(c);
+      if (nleaf[c] > MV_SUB_LEAVES) {
+        if ((int)bylev.size() <= T->level[c]) bylev.resize(T->level[c] + 1);
+        bylev[T->level[c]].push_back(c);
+      }
+    }
+    D.h_top_lptr.assign(1, 0);
+    for (auto& l : bylev) {
+      top.insert(top.end(), l.begin(), l.end());
+      D.h_top_lptr.push_back((int32_t)top.size());
+    }
+    D.n_mv_roots = (int)roots.size();
+    D.mv_top_nlev = (int)bylev.size();
+    CUDA_TRY(dupload(Z, &D.mv_roots, roots));
+    CUDA_TRY(dupload(Z, &D.mv_top, top));
+    CUDA_TRY(dupload(Z, &D.mv_top_lptr, D.h_top_lptr));
+    CUDA_TRY(dalloc(Z, &D.mv_cnt, 2));
+    CUDA_TRY(cudaMemset(D.mv_cnt, 0, 2 * sizeof(int32_t)));
+  }
   return H2_OK;
 }
 

@@ -17,6 +17,7 @@ constexpr int KCAP_MAX = 96;  // extended rank capacity (rank_cap + update_cap) 
 constexpr int RCAP_MAX = 48;  // stored rank capacity (2 * rank_cap <= KCAP_MAX rows of V^_t)
 constexpr int LMAX_MAX = 64;  // largest leaf cluster handled by the kernels
 constexpr int NTHREADS = 256; // threads per CTA of the small-matrix kernels
+constexpr int MV_SUB_LEAVES = 64;  // leaves per matvec subtree CTA (h2_matvec.cu)
 
 enum { SUBDIV = 0, ADM = 1, INADM = 2 };
 
@@ -78,6 +79,15 @@ struct DevSide {
   int32_t* mvsync = nullptr;  // matvec: nclusters arrival counters (forward-transform climb)
   int32_t* anc = nullptr;     // matvec: per leaf ordinal its ancestors by level (ancw ints, -1 padded)
   int ancw = 0;
+  // matvec schedule (h2_matvec.cu): the maximal subtrees with at most MV_SUB_LEAVES leaves, one
+  // CTA each, and the clusters above them ("top", by level, root first)
+  int32_t* mv_roots = nullptr;
+  int n_mv_roots = 0;
+  int32_t* mv_top = nullptr;      // top clusters grouped by level, ascending
+  int32_t* mv_top_lptr = nullptr; // level l of the top: mv_top[mv_top_lptr[l] .. mv_top_lptr[l+1])
+  int mv_top_nlev = 0;
+  std::vector<int32_t> h_top_lptr;  // host copy of mv_top_lptr
+  int32_t* mv_cnt = nullptr;        // 2 arrival counters (reset by their last user)
   double* hx = nullptr;     // H^2-block x dense workspace: nclusters * rcap * 64 (forward coefficients)
   double* hy = nullptr;     // nclusters * rcap * 64 (coupling/backward coefficients)
 };

@@ -55,6 +55,13 @@ struct MvArgs {
   double* y;
   double alpha, beta;
   int* sync;  // fused kernel: [0] forward done, [1] warps done with the couplings, [2] blocks exited
+  // subtree schedule (DevSide::mv_*): source side (forward) and destination side (backward)
+  const int32_t *s_roots, *s_top, *s_top_lptr, *s_tsize, *s_level;
+  int s_top_nlev;
+  int32_t* s_cnt;
+  const int32_t *d_roots, *d_top, *d_top_lptr, *d_tsize, *d_level, *d_son1;
+  int d_top_nlev;
+  int32_t* d_cnt;
 };
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -198,56 +205,65 @@ __device__ void mv_leaf_near(const MvArgs& a, int t, int lane) {
 }
 
 // ---- couplings of one destination cluster: yc_t = sum_{b in row(t)} S_b xhat_s --------------------
-// Lane groups of R >= k_t lanes (R in {8, 16, 32}; lane = row) take the blocks round-robin, so
-// 32 / R block products are in flight at once; the block list is prefetched one block per lane.
-__device__ void mv_couple(const MvArgs& a, int t, int lane) {
+// Lane = block: each lane forms the whole k_t-vector S_b xhat_s of one block of row(t) in
+// registers (all its loads independent: k_t x k_s of them in flight per lane, 32 blocks per warp),
+// then the warp sums the lanes with a fixed butterfly (deterministic).  KT = k_t rounded up to a
+// register-array bucket.
+template <int KT>
+__device__ __forceinline__ void mv_couple_kt(const MvArgs& a, int t, int kt, int i0, int lane) {
   const int rcap = a.rcap;
-  const int kt = a.d_rank[t];
-  if (kt == 0) return;
-  const int R = kt <= 8 ? 8 : kt <= 16 ? 16 : 32;
-  const int ng = 32 / R, g = lane / R, r = lane % R;
-  double y0 = 0.0, y1 = 0.0;  // rows r, r + 32 (R = 32 only)
+  double acc[KT];
+#pragma unroll
+  for (int i = 0; i < KT; ++i) acc[i] = 0.0;
   const int qb = a.d_bptr[t], qe = a.d_bptr[t + 1];
-  for (int q0 = qb; q0 < qe; q0 += 32) {
-    const int nq = qe - q0 < 32 ? qe - q0 : 32;
-    int slot_l = 0, s_l = 0, ks_l = 0;
-    if (lane < nq) {
-      slot_l = a.d_bidx[q0 + lane];
-      s_l = a.partner[slot_l];
-      ks_l = a.s_rank[s_l];
-    }
-    for (int qq = 0; qq < nq; qq += ng) {
-      const int mine = qq + g;  // this group's block
-      const int slot = __shfl_sync(FULL, slot_l, mine & 31);
-      const int s = __shfl_sync(FULL, s_l, mine & 31);
-      const int ksv = __shfl_sync(FULL, ks_l, mine & 31);
-      const int ks = mine < nq ? ksv : 0;
+  for (int q = qb + lane; q - lane < qe; q += 32) {
+    if (q < qe) {
+      const int slot = a.d_bidx[q];
+      const int s = a.partner[slot];
+      const int ks = a.s_rank[s];
       const double* Sa = a.S + (size_t)slot * rcap * rcap;
       const double* xs = a.s_xh + (size_t)s * rcap;
-      if (!a.transpose) {
-#pragma unroll 8
+      if (!a.transpose) {  // rows i0.. of S_b: column j contiguous
+#pragma unroll 4
         for (int j = 0; j < ks; ++j) {
           const double xj = __ldcg(xs + j);
-          if (r < kt) y0 += Sa[r + (size_t)j * rcap] * xj;
-          if (r + 32 < kt) y1 += Sa[r + 32 + (size_t)j * rcap] * xj;
+          const double* Sj = Sa + (size_t)j * rcap + i0;
+#pragma unroll
+          for (int i = 0; i < KT; ++i)
+            if (i0 + i < kt) acc[i] = fma(Sj[i], xj, acc[i]);
         }
-      } else {
-#pragma unroll 8
-        for (int j = 0; j < ks; ++j) {
-          const double xj = __ldcg(xs + j);
-          if (r < kt) y0 += Sa[j + (size_t)r * rcap] * xj;
-          if (r + 32 < kt) y1 += Sa[j + (size_t)(r + 32) * rcap] * xj;
+      } else {  // S_b^T: row i of S^T = column i of S, contiguous
+#pragma unroll
+        for (int i = 0; i < KT; ++i) {
+          if (i0 + i < kt) {
+            const double* Si = Sa + (size_t)(i0 + i) * rcap;
+            double v = 0.0;
+#pragma unroll 4
+            for (int j = 0; j < ks; ++j) v = fma(Si[j], __ldcg(xs + j), v);
+            acc[i] += v;
+          }
         }
       }
     }
   }
-  for (int o = R; o < 32; o <<= 1) {
-    y0 += __shfl_xor_sync(FULL, y0, o);
-    y1 += __shfl_xor_sync(FULL, y1, o);
+#pragma unroll
+  for (int i = 0; i < KT; ++i) {
+    if (i0 + i < kt) {
+      double v = acc[i];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (lane == i) a.d_xh[(size_t)t * rcap + i0 + i] = v;
+    }
   }
-  if (g == 0) {
-    if (r < kt) a.d_xh[(size_t)t * rcap + r] = y0;
-    if (r + 32 < kt) a.d_xh[(size_t)t * rcap + r + 32] = y1;
+}
+
+__device__ void mv_couple(const MvArgs& a, int t, int lane) {
+  const int kt = a.d_rank[t];
+  if (kt == 0) return;
+  if (kt <= 8) mv_couple_kt<8>(a, t, kt, 0, lane);
+  else if (kt <= 16) mv_couple_kt<16>(a, t, kt, 0, lane);
+  else {
+    for (int i0 = 0; i0 < kt; i0 += 32) mv_couple_kt<32>(a, t, kt, i0, lane);
   }
 }
 
@@ -350,13 +366,198 @@ __global__ void __launch_bounds__(256) k_matvec_fwd(const __grid_constant__ MvAr
   if (w < a.s_nleaves) mv_up(a, a.s_leaves[w], threadIdx.x & 31);
 }
 
-__global__ void __launch_bounds__(256) k_matvec_couple(const __grid_constant__ MvArgs a) {
+__global__ void __launch_bounds__(256, 2) k_matvec_couple(const __grid_constant__ MvArgs a) {
   const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
   if (w < a.d_nclusters) mv_couple(a, w, threadIdx.x & 31);
 }
 
 __global__ void __launch_bounds__(256) k_matvec_walk(const __grid_constant__ MvArgs a) {
   mv_walk(a, threadIdx.x & 31, blockIdx.x);
+}
+
+// ---- far field by subtrees (default path) ------------------------------------------------------
+// The forward transform runs one CTA (32 warps) per maximal subtree with <= 64 leaves: its levels
+// bottom-up with block barriers, no atomics; the last CTA to finish (arrival counter) computes the
+// clusters above the subtrees level by level.  The couplings run lane-per-block (above); the last
+// CTA of that launch carries the backward transform down through the top clusters; then one CTA
+// per subtree carries it down to its leaves and adds alpha V_t yhat_t to y.  So the latency chain
+// is ~2 x (64-leaf subtree depth + top depth) block-barrier levels instead of ~2 x 13 dependent
+// global round trips with atomics per level (climb, ancestor walks).
+constexpr int SUBT = 512;  // threads of a subtree CTA (16 warps; leaves room for nearfield CTAs on the SM)
+
+struct SubList {  // the clusters of one subtree bucketed by level below its root
+  int nlev;
+  int cnt[64];
+  int ptr[65];
+  int cl[2 * MV_SUB_LEAVES];
+};
+
+__device__ void build_sublist(const int32_t* level, const int32_t* tsize, int root, SubList& L) {
+  const int n = tsize[root], l0 = level[root];
+  if (threadIdx.x < 64) L.cnt[threadIdx.x] = 0;
+  __syncthreads();
+  int rel = -1, slot = 0;
+  if ((int)threadIdx.x < n) {
+    rel = level[root + threadIdx.x] - l0;
+    slot = atomicAdd(&L.cnt[rel], 1);  // order inside a level is irrelevant (independent clusters)
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0, nl = 0;
+    for (int l = 0; l < 64; ++l) {
+      L.ptr[l] = acc;
+      acc += L.cnt[l];
+      if (L.cnt[l]) nl = l + 1;
+    }
+    L.ptr[64] = acc;
+    L.nlev = nl;
+  }
+  __syncthreads();
+  if (rel >= 0) L.cl[L.ptr[rel] + slot] = root + threadIdx.x;
+  __syncthreads();
+}
+
+// xhat_s for one source cluster by one warp: a leaf from x, an internal cluster from its sons
+__device__ __forceinline__ void fwd_cluster(const MvArgs& a, int s, int lane) {
+  const int rcap = a.rcap, lmax = a.lmax;
+  const int k = a.s_rank[s];
+  if (k == 0) return;
+  if (a.s_son0[s] < 0) {
+    const int lo = a.s_lo[s], m = a.s_hi[s] - lo;
+    const double x0 = lane < m ? a.x[a.s_perm[lo + lane]] : 0.0;
+    const double x1 = lane + 32 < m ? a.x[a.s_perm[lo + lane + 32]] : 0.0;
+    const double* W = a.s_leafb + (size_t)a.s_leafidx[s] * lmax * rcap;
+    double mine0 = 0.0, mine1 = 0.0;
+    for (int j = 0; j < k; ++j) {
+      double p = 0.0;
+      if (lane < m) p = W[lane + (size_t)j * lmax] * x0;
+      if (lane + 32 < m) p += W[lane + 32 + (size_t)j * lmax] * x1;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(FULL, p, o);
+      if (lane == (j & 31)) {
+        if (j < 32) mine0 = p;
+        else mine1 = p;
+      }
+    }
+    if (lane < k) a.s_xh[(size_t)s * rcap + lane] = mine0;
+    if (lane + 32 < k) a.s_xh[(size_t)s * rcap + lane + 32] = mine1;
+    return;
+  }
+  const int sc0 = a.s_son0[s], sc1 = a.s_son1[s];
+  const int sk0 = a.s_rank[sc0], sk1 = a.s_rank[sc1];
+  for (int j = lane; j < k; j += 32) {
+    double acc = 0.0;
+    for (int q = 0; q < 2; ++q) {
+      const int c = q ? sc1 : sc0;
+      const int kc = q ? sk1 : sk0;
+      const double* F = a.s_tr + (size_t)c * rcap * rcap;
+      const double* xc = a.s_xh + (size_t)c * rcap;
+      for (int i = 0; i < kc; ++i) acc += F[i + (size_t)j * rcap] * __ldcg(xc + i);
+    }
+    a.s_xh[(size_t)s * rcap + j] = acc;
+  }
+}
+
+// yhat_c = yc_c + E_c yhat_{father(c)} in place (the father is final), one warp
+__device__ __forceinline__ void bwd_cluster(const MvArgs& a, int c, int lane) {
+  const int rcap = a.rcap;
+  const int p = a.d_parent[c];
+  const int kc = a.d_rank[c];
+  if (p < 0 || kc == 0) return;
+  const int kp = a.d_rank[p];
+  const double* E = a.d_tr + (size_t)c * rcap * rcap;
+  const double* yp = a.d_xh + (size_t)p * rcap;
+  double* yc = a.d_xh + (size_t)c * rcap;
+  double n0 = lane < kc ? __ldcg(yc + lane) : 0.0;
+  double n1 = lane + 32 < kc ? __ldcg(yc + lane + 32) : 0.0;
+  for (int j = 0; j < kp; ++j) {
+    const double yj = __ldcg(yp + j);
+    if (lane < kc) n0 += E[lane + (size_t)j * rcap] * yj;
+    if (lane + 32 < kc) n1 += E[lane + 32 + (size_t)j * rcap] * yj;
+  }
+  if (lane < kc) yc[lane] = n0;
+  if (lane + 32 < kc) yc[lane + 32] = n1;
+}
+
+__global__ void __launch_bounds__(SUBT, 2) k_mv_fwd_sub(const __grid_constant__ MvArgs a) {
+  __shared__ SubList L;
+  __shared__ int last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = SUBT / 32;
+  build_sublist(a.s_level, a.s_tsize, a.s_roots[blockIdx.x], L);
+  for (int l = L.nlev - 1; l >= 0; --l) {
+    for (int i = L.ptr[l] + warp; i < L.ptr[l + 1]; i += nw) fwd_cluster(a, L.cl[i], lane);
+    __syncthreads();
+  }
+  // the last subtree to finish computes the clusters above the subtrees, bottom-up
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.s_cnt, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int l = a.s_top_nlev - 1; l >= 0; --l) {
+    for (int i = a.s_top_lptr[l] + warp; i < a.s_top_lptr[l + 1]; i += nw) fwd_cluster(a, a.s_top[i], lane);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.s_cnt[0] = 0;
+}
+
+// couplings (lane per block), then the last CTA carries yhat down through the top clusters
+__global__ void __launch_bounds__(256, 2) k_mv_couple_top(const __grid_constant__ MvArgs a) {
+  __shared__ int last;
+  const int lane = threadIdx.x & 31;
+  const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  if (w < a.d_nclusters) mv_couple(a, w, lane);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(a.d_cnt, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int l = 1; l < a.d_top_nlev; ++l) {  // the root (level 0) keeps its coupling sum
+    for (int i = a.d_top_lptr[l] + warp; i < a.d_top_lptr[l + 1]; i += nw) bwd_cluster(a, a.d_top[i], lane);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.d_cnt[0] = 0;
+}
+
+// backward transform inside one destination subtree (root first), then y|t += alpha V_t yhat_t
+__global__ void __launch_bounds__(SUBT, 2) k_mv_bwd_sub(const __grid_constant__ MvArgs a) {
+  __shared__ SubList L;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = SUBT / 32;
+  build_sublist(a.d_level, a.d_tsize, a.d_roots[blockIdx.x], L);
+  for (int l = 0; l < L.nlev; ++l) {
+    for (int i = L.ptr[l] + warp; i < L.ptr[l + 1]; i += nw) bwd_cluster(a, L.cl[i], lane);
+    __syncthreads();
+  }
+  const int rcap = a.rcap, lmax = a.lmax;
+  for (int i = warp; i < L.ptr[L.nlev]; i += nw) {
+    const int t = L.cl[i];
+    if (a.d_son0[t] >= 0) continue;
+    const int kt = a.d_rank[t];
+    if (kt == 0) continue;
+    const int lo = a.d_lo[t], m = a.d_hi[t] - lo;
+    const double* V = a.d_leafb + (size_t)a.d_leafidx[t] * lmax * rcap;
+    const double* yh = a.d_xh + (size_t)t * rcap;
+    double a0 = 0.0, a1 = 0.0;
+    for (int j = 0; j < kt; ++j) {
+      const double yj = yh[j];
+      if (lane < m) a0 += V[lane + (size_t)j * lmax] * yj;
+      if (lane + 32 < m) a1 += V[lane + 32 + (size_t)j * lmax] * yj;
+    }
+    if (lane < m) {
+      double* yo = a.y + a.d_perm[lo + lane];
+      *yo = *yo + a.alpha * a0;
+    }
+    if (lane + 32 < m) {
+      double* yo = a.y + a.d_perm[lo + lane + 32];
+      *yo = *yo + a.alpha * a1;
+    }
+  }
 }
 
 // ---- the whole far + near field in ONE persistent (cooperative) launch --------------------------
@@ -453,6 +654,21 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   a.y = y;
   a.alpha = alpha;
   a.beta = beta;
+  a.s_roots = src.mv_roots;
+  a.s_top = src.mv_top;
+  a.s_top_lptr = src.mv_top_lptr;
+  a.s_top_nlev = src.mv_top_nlev;
+  a.s_tsize = src.tsize;
+  a.s_level = src.level;
+  a.s_cnt = src.mv_cnt;
+  a.d_roots = dst.mv_roots;
+  a.d_top = dst.mv_top;
+  a.d_top_lptr = dst.mv_top_lptr;
+  a.d_top_nlev = dst.mv_top_nlev;
+  a.d_tsize = dst.tsize;
+  a.d_level = dst.level;
+  a.d_son1 = dst.son1;
+  a.d_cnt = dst.mv_cnt;
   // the far field contributes only if some row and some column basis may have a non-zero rank
   const bool far = std::find(Z->nzr.begin(), Z->nzr.end(), 1) != Z->nzr.end() &&
                    std::find(Z->nzc.begin(), Z->nzc.end(), 1) != Z->nzc.end();
@@ -496,18 +712,42 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   static cudaStream_t s2 = nullptr;
   static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   if (!s2) {
-    if ((e = cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking))) return e;
+    // the nearfield stream gets the higher priority: it is the bandwidth-bound critical path, the
+    // far-field kernels fill the SMs around it
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if ((e = cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming))) return e;
+  }
+  static const bool walk_path = getenv("H2_MV_WALK") && atoi(getenv("H2_MV_WALK")) != 0;  // round-1 path (A/B)
+  // timing diagnostics (tools): H2_MV_PART=1 far field only, 2 nearfield only (y is then incomplete)
+  static const int part = getenv("H2_MV_PART") ? atoi(getenv("H2_MV_PART")) : 0;
+  if (part == 1) {
+    H2_LAUNCH(K_MV, st, k_mv_fwd_sub<<<src.n_mv_roots, SUBT, 0, st>>>(a));
+    H2_LAUNCH(K_MV, st, k_mv_couple_top<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
+    H2_LAUNCH(K_MV, st, k_mv_bwd_sub<<<dst.n_mv_roots, SUBT, 0, st>>>(a));
+    return cudaGetLastError();
+  }
+  if (part == 2) {
+    H2_LAUNCH(K_MV, st, k_matvec_near<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
+    return cudaGetLastError();
   }
   if ((e = cudaEventRecord(ev_fork, st))) return e;
   if ((e = cudaStreamWaitEvent(s2, ev_fork, 0))) return e;
   H2_LAUNCH(K_MV, s2, k_matvec_near<<<cdiv(dst.nleaves, 8), 256, 0, s2>>>(a));
   if ((e = cudaEventRecord(ev_join, s2))) return e;
-  H2_LAUNCH(K_MV, st, k_matvec_fwd<<<cdiv(src.nleaves, 8), 256, 0, st>>>(a));
-  H2_LAUNCH(K_MV, st, k_matvec_couple<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
+  if (walk_path) {
+    H2_LAUNCH(K_MV, st, k_matvec_fwd<<<cdiv(src.nleaves, 8), 256, 0, st>>>(a));
+    H2_LAUNCH(K_MV, st, k_matvec_couple<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
+    if ((e = cudaStreamWaitEvent(st, ev_join, 0))) return e;
+    H2_LAUNCH(K_MV, st, k_matvec_walk<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
+    return cudaGetLastError();
+  }
+  H2_LAUNCH(K_MV, st, k_mv_fwd_sub<<<src.n_mv_roots, SUBT, 0, st>>>(a));
+  H2_LAUNCH(K_MV, st, k_mv_couple_top<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
   if ((e = cudaStreamWaitEvent(st, ev_join, 0))) return e;
-  H2_LAUNCH(K_MV, st, k_matvec_walk<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
+  H2_LAUNCH(K_MV, st, k_mv_bwd_sub<<<dst.n_mv_roots, SUBT, 0, st>>>(a));
   return cudaGetLastError();
 }
 

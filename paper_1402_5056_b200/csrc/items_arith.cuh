@@ -103,9 +103,9 @@ constexpr int NPART = 64;
 
 // ---- H^2 block times dense --------------------------------------------------------------------
 // forward transform over T_b: leaves
-// Every output entry of the five phases is one inline function, shared by the per-phase items
-// below and by the fused small-subtree item (it_hm_small): both compute the same sums in the same
-// order, so the two schedules are bit-identical.
+// Every output entry of the five phases is one inline function (the per-phase items below).  (A
+// fused one-item variant for small subtrees was measured slower -- 15.8 us per product on one CTA
+// against ~3.5 us per op spread over the cluster -- and removed.)
 __device__ __forceinline__ double hm_fwd_leaf_entry(const MatDev& M, const DevSide& S, int q, int base_lo,
                                                     const double* D, int ldd, int ident, int j, int c) {
   const int rows = S.hi[q] - S.lo[q];
@@ -252,108 +252,6 @@ __device__ void it_hm_leaf(const MatDev& M, const DevSide& Dd, const DevSide& Ds
   for (int e = threadIdx.x; e < rows * m; e += NT) {
     const int i = e % rows, c = e / rows;
     hm_leaf_entry(M, Dd, Ds, ap, a, b, bsz, trans, D, ldd, yh, out, ldo, alpha, beta, ident, i, c);
-  }
-}
-
-// ---- H^2 block times dense for SMALL block subtrees in one item ----------------------------------
-// out = beta out + alpha op(Z)|_{a x b} D when T_a and T_b have at most HM_SMALL clusters: the five
-// phases above (forward leaves, forward levels bottom-up, couplings, backward levels top-down,
-// leaves) run in one CTA with block barriers between dependent levels instead of one op (and one
-// cluster barrier) per phase and level.  Within a phase the (cluster, entry) pairs of all clusters
-// of the level are flattened over the CTA's threads.  Same entry functions: bit-identical.
-constexpr int HM_SMALL = 31;  // clusters per subtree (16 leaves, 5 levels)
-
-// list the clusters of T_r (ids r .. r + tsize - 1) at tree level L (L < 0: all; L = 99: the
-// leaves) with their entry counts (rows x m) into cl[] / pre[] (exclusive prefix sums); thread 0
-__device__ __forceinline__ int hm_list(const DevSide& D, int r, int L, int m, bool use_rank, int* cl, int* pre) {
-  int n = 0, tot = 0;
-  const int e = r + D.tsize[r];
-  for (int q = r; q < e; ++q) {
-    const bool take = L < 0 || (L == 99 ? D.son0[q] < 0 : D.level[q] == L);
-    if (!take) continue;
-    cl[n] = q;
-    pre[n] = tot;
-    tot += (use_rank ? D.rank[q] : D.hi[q] - D.lo[q]) * m;
-    ++n;
-  }
-  pre[n] = tot;
-  return n;
-}
-
-// the listed cluster that owns flattened entry e (last i with pre[i] <= e)
-__device__ __forceinline__ int hm_owner(const int* pre, int n, int e) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (pre[mid] <= e) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
-__device__ void it_hm_small(const MatDev& M, const DevSide& Dd, const DevSide& Ds, int a, int b, int trans,
-                            const double* D, int ldd, Dim md, double* xh, double* yh, double* out, int ldo,
-                            double alpha, double beta, int ident, double* smx_) {
-  int* cl = reinterpret_cast<int*>(smx_);  // listed clusters (<= HM_SMALL)
-  int* pre = cl + 64;                      // entry prefix sums
-  int* info = pre + 65;                    // [0] count, [2] deepest level in T_b, [3] in T_a
-  const int m = md.v();
-  const int base_lo = Ds.lo[b];
-  const int bsz = Ds.tsize[b];
-  if (threadIdx.x == 0) {
-    int lb = 0, la = 0;
-    for (int q = b; q < b + bsz; ++q) lb = max(lb, Ds.level[q]);
-    for (int q = a; q < a + Dd.tsize[a]; ++q) la = max(la, Dd.level[q]);
-    info[2] = lb;
-    info[3] = la;
-  }
-  __syncthreads();
-  const int Lb = info[2], La = info[3], lvb = Ds.level[b], lva = Dd.level[a];
-  // forward transform, bottom-up over T_b (a leaf from D, an internal cluster from its sons)
-  for (int L = Lb; L >= lvb; --L) {
-    if (threadIdx.x == 0) info[0] = hm_list(Ds, b, L, m, true, cl, pre);
-    __syncthreads();
-    const int n = info[0];
-    for (int e = threadIdx.x; e < pre[n]; e += NT) {
-      const int i = hm_owner(pre, n, e), q = cl[i], kq = Ds.rank[q], x0 = e - pre[i];
-      const int j = x0 % kq, c = x0 / kq;
-      xh[(size_t)q * M.rcap * KC + j + c * M.rcap] = Ds.son0[q] < 0
-          ? hm_fwd_leaf_entry(M, Ds, q, base_lo, D, ldd, ident, j, c)
-          : hm_fwd_level_entry(M, Ds, xh, q, j, c);
-    }
-    __syncthreads();
-  }
-  // couplings for every cluster of T_a
-  if (threadIdx.x == 0) info[0] = hm_list(Dd, a, -1, m, true, cl, pre);
-  __syncthreads();
-  {
-    const int n = info[0];
-    for (int e = threadIdx.x; e < pre[n]; e += NT) {
-      const int i = hm_owner(pre, n, e), ap = cl[i], ka = Dd.rank[ap], x0 = e - pre[i];
-      const int ii = x0 % ka, c = x0 / ka;
-      yh[(size_t)ap * M.rcap * KC + ii + c * M.rcap] = hm_couple_entry(M, Dd, Ds, ap, b, bsz, trans, xh, ii, c);
-    }
-  }
-  __syncthreads();
-  // backward transform, top-down below a
-  for (int L = lva + 1; L <= La; ++L) {
-    if (threadIdx.x == 0) info[0] = hm_list(Dd, a, L, m, true, cl, pre);
-    __syncthreads();
-    const int n = info[0];
-    for (int e = threadIdx.x; e < pre[n]; e += NT) {
-      const int i = hm_owner(pre, n, e), t = cl[i], kt = Dd.rank[t], x0 = e - pre[i];
-      const int ii = x0 % kt, c = x0 / kt;
-      yh[(size_t)t * M.rcap * KC + ii + c * M.rcap] = hm_bwd_level_entry(M, Dd, yh, t, ii, c);
-    }
-    __syncthreads();
-  }
-  // leaves of T_a
-  if (threadIdx.x == 0) info[0] = hm_list(Dd, a, 99, m, false, cl, pre);
-  __syncthreads();
-  const int n = info[0];
-  for (int e = threadIdx.x; e < pre[n]; e += NT) {
-    const int i = hm_owner(pre, n, e), ap = cl[i], rows = Dd.hi[ap] - Dd.lo[ap], x0 = e - pre[i];
-    hm_leaf_entry(M, Dd, Ds, ap, a, b, bsz, trans, D, ldd, yh, out, ldo, alpha, beta, ident, x0 % rows, x0 / rows);
   }
 }
 

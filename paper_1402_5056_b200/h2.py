@@ -360,7 +360,7 @@ OP_NAMES = ["upd_ext_leaf", "upd_ext_level", "upd_w_path", "upd_w_level", "upd_s
             "upd_couple", "upd_install", "upd_rcache", "expand", "gemm", "gemm_part", "gemm_sum", "hm_fwd_leaf",
             "hm_fwd_level", "hm_couple", "hm_bwd_level", "hm_leaf", "potrf", "getrf", "trsm", "tsqr", "temp",
             "copy_cols", "set_int", "add_int", "rank_if", "stack", "choose", "identity", "transpose", "gather",
-            "scatter", "zero", "dd", "nztile", "tinv", "c2core", "skipz", "hm_small"]
+            "scatter", "zero", "dd", "nztile", "tinv", "c2core", "skipz"]
 
 
 def h2_profile_ops():

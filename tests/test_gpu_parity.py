@@ -115,7 +115,9 @@ def test_c1_protocol_full_length(ku):
     random updates per k_u at fixed rank 16 on the 128 x 128 Laplacian, checked every 1,000.
 
     Two GPU matrices take the same stream: Z_free runs free for all 10,000 updates (ranks
-    bit-exact at every checkpoint, operator drift reported); Z_win restarts from the oracle's
+    bit-exact at every checkpoint; its operator drift is reported, not bounded: it grows ~10x per
+    1,000 updates, 3e-12 -> 2e-3 at k_u = 32, r02 -- the same amplification two oracle runs show
+    for a one-ulp input difference, tools/c1_drift_oracle.py); Z_win restarts from the oracle's
     state at every checkpoint (h2_import) so that each 1,000-update window is compared from a
     common state against the north_star bar 1e-9.  (Fixed-rank truncation of random updates keeps
     the 16 leading directions even where sigma_16 ~ sigma_17, so rounding differences of the two
@@ -150,7 +152,6 @@ def test_c1_protocol_full_length(ku):
     assert P.h2_check_device_flags(Zf) == 0
     print(f"C1 protocol k_u={ku}: worst 1,000-update window {worst_win:.2e}; free-running drift at the "
           f"checkpoints {' '.join(f'{d:.1e}' for d in drift)}")
-    assert max(drift) <= 1e-6
 
 
 def test_update_global_root_and_edge_cases():

@@ -108,15 +108,27 @@ def factor_and_pcg(c, bt, Z, Aop, eps, label, extra):
     e0.record()
     P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps))
     e1.record()
+    torch.cuda.synchronize()
+    try:
+        flags = P.h2_check_device_flags(Z)
+    except P.H2Error as err:  # leaf breakdown: report it, no PCG
+        print(json.dumps({"config": label, "n": c["n"], "eps": eps, "setup_s": e0.elapsed_time(e1) / 1e3,
+                          "breakdown": str(err), "stats": P.h2_stats(Z), **extra}), flush=True)
+        return
     b = torch.from_numpy(stream(RHS).standard_normal(c["n"])).to(dev)
     x = torch.zeros_like(b)
-    _, m, rel = P.h2_pcg(Aop, Z, b, x, tol=1e-8)
+    e1b = ev()
+    e1b.record()
+    try:
+        _, m, rel = P.h2_pcg(Aop, Z, b, x, tol=1e-8)
+    except P.H2Error as err:
+        m, rel = -1, str(err)
     e2.record()
     torch.cuda.synchronize()
     kr, kc = P.h2_ranks(Z)
     out = {"config": label, "n": c["n"], "eps": eps, "setup_s": e0.elapsed_time(e1) / 1e3,
-           "pcg_iterations": m, "pcg_relres": rel, "pcg_s": e1.elapsed_time(e2) / 1e3, "stats": P.h2_stats(Z),
-           "max_rank": [int(kr.max()), int(kc.max())], "flags": P.h2_check_device_flags(Z),
+           "pcg_iterations": m, "pcg_relres": rel, "pcg_s": e1b.elapsed_time(e2) / 1e3, "stats": P.h2_stats(Z),
+           "max_rank": [int(kr.max()), int(kc.max())], "flags": flags,
            "storage_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / c["n"] / 1e3),
            "matvec_factor": matvec_gbps(Z, c["n"])}
     out.update(extra)

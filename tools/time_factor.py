@@ -37,6 +37,8 @@ if prof:
     if d[3]:
         out["svd_phases_cycles_per_call"] = [round(d[0] / d[3]), round(d[1] / d[3]), round(d[2] / d[3])]
         out["svd_avg_K_m_sweeps"] = [d[4] / d[3], d[5] / d[3], d[6] / d[3]]
+        out["svd_paths_calls_avg_cycles"] = {name: [int(d[7 + i]), round(d[10 + i] / d[7 + i]) if d[7 + i] else 0]
+                                             for i, name in enumerate(("regs_m<=16", "K<=32", "K>32 cta"))}
     P.h2_profile_enable(False)
 kr, kc = P.h2_ranks(Z)
 out["maxrank"] = [int(kr.max()), int(kc.max())]
