@@ -254,7 +254,8 @@ class Arith:
             if target is None:
                 kz = int(self.Z.bt.kind[self.Z.bt.index[(t, r)]])
                 if kz == ADM:
-                    temps = {(t2, r2): RkTemp(rt, t2, r2, self.trunc)
+                    ttr = self.trunc.relative() if self.trunc.blockwise else self.trunc  # one block: relative
+                    temps = {(t2, r2): RkTemp(rt, t2, r2, ttr)
                              for t2 in rt.sons_plus(t) for r2 in rt.sons_plus(r)}
                     self.stats["temporaries"] += len(temps)
                     for s2 in rt.sons_plus(s):

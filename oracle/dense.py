@@ -50,8 +50,9 @@ def densify(Z) -> np.ndarray:
     return D
 
 
-def block_row(D, Z, t, row_side=True):
-    """Z~_t: stored admissible blocks (t*, s), t* in pred(t), restricted to rows t."""
+def block_row(D, Z, t, row_side=True, blockwise=False):
+    """Z~_t: stored admissible blocks (t*, s), t* in pred(t), restricted to rows t.
+    blockwise (NEXT-1): each block scaled by 1 / ||D|_{t* x s}||_F (the whole block's norm)."""
     rt, ct, bt = Z.rt, Z.ct, Z.bt
     tree = rt if row_side else ct
     blocks = bt.row if row_side else bt.col
@@ -62,10 +63,18 @@ def block_row(D, Z, t, row_side=True):
                 continue
             if row_side:
                 s = bt.s[b]
-                cols.append(D[rt.lo[t]:rt.hi[t], ct.lo[s]:ct.hi[s]])
+                blk = D[rt.lo[t]:rt.hi[t], ct.lo[s]:ct.hi[s]]
+                full = D[rt.lo[tp]:rt.hi[tp], ct.lo[s]:ct.hi[s]]
             else:
                 r = bt.t[b]
-                cols.append(D[rt.lo[r]:rt.hi[r], ct.lo[t]:ct.hi[t]].T)
+                blk = D[rt.lo[r]:rt.hi[r], ct.lo[t]:ct.hi[t]].T
+                full = D[rt.lo[r]:rt.hi[r], ct.lo[tp]:ct.hi[tp]]
+            if blockwise:
+                nrm = np.linalg.norm(full)
+                if nrm == 0.0:
+                    continue
+                blk = blk / nrm
+            cols.append(blk)
     if not cols:
         return np.zeros((tree.size(t), 0))
     return np.hstack(cols)
@@ -75,7 +84,7 @@ def _dense_bases(D, Z, root, row_side, trunc):
     tree = Z.rt if row_side else Z.ct
     Q, r, sig = {}, {}, {}
     for t in reversed(tree.subtree(root)):
-        Zt = block_row(D, Z, t, row_side)
+        Zt = block_row(D, Z, t, row_side, getattr(trunc, "blockwise", False))
         if tree.is_leaf(t):
             P = np.eye(tree.size(t))
         else:

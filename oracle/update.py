@@ -30,19 +30,34 @@ from .h2 import H2
 @dataclass
 class Trunc:
     """TruncationControl.  rank r = #{sigma_i > max(rel_tol*sigma_1, abs_tol)},
-    capped by max_rank (<= 0: unbounded).  SURVEY R5."""
+    capped by max_rank (<= 0: unbounded).  SURVEY R5.
+
+    blockwise=True (DESIGN reading own-10): "block-relative accuracy eps^"
+    (P:874-879): the weight matrices carry the factor 1/||G~_b||_F for every block b
+    (weighting factors in B_{t,s}), so their singular values are measured in units of
+    the blocks' own norms, and the rank is r = #{sigma_i > max(rel_tol, abs_tol)} -- an ABSOLUTE
+    threshold eps^ = rel_tol on the weighted matrix.  Low-rank temporaries (one block each) keep
+    the relative rule (relative())."""
     rel_tol: float = 1e-4
     abs_tol: float = 0.0
     max_rank: int = 0
+    blockwise: bool = False
 
     def rank(self, sig: np.ndarray) -> int:
         if sig.size == 0 or sig[0] <= 0.0:
             return 0
-        thr = max(self.rel_tol * sig[0], self.abs_tol)
+        if self.blockwise:
+            thr = max(self.rel_tol, self.abs_tol)
+        else:
+            thr = max(self.rel_tol * sig[0], self.abs_tol)
         r = int(np.count_nonzero(sig > thr))
         if self.max_rank > 0:
             r = min(r, self.max_rank)
         return r
+
+    def relative(self) -> "Trunc":
+        """The plain relative rule with the same tolerance (temporaries of the product)."""
+        return Trunc(self.rel_tol, self.abs_tol, self.max_rank)
 
 
 FIXED16 = Trunc(rel_tol=1e-12, abs_tol=0.0, max_rank=16)  # SURVEY R5/R16 fixed-rank mode
@@ -152,8 +167,11 @@ def _ext_rfactors(side: _Side):
     return R
 
 
-def _weights(side: _Side, other: _Side, R_other_ext, other_cache: RCache):
-    """U3: weight matrices B~_t for t in pred(t0) u T_{t0}."""
+def _weights(side: _Side, other: _Side, R_other_ext, other_cache: RCache, blockwise: bool = False,
+             R_own_ext=None, own_cache: RCache = None):
+    """U3: weight matrices B~_t for t in pred(t0) u T_{t0}.
+    blockwise: every block's rows R_{W,s} S~_b^T carry the weight 1/||G~_b||_F, where
+    ||G~_b||_F = ||R_{V,t} S~_b R_{W,s}^T||_F (R-factors of the current / extended bases, R7)."""
     tr = side.tree
     B = {}
     order = tr.pred(side.root)[:-1] + side.sub  # father before son
@@ -176,7 +194,14 @@ def _weights(side: _Side, other: _Side, R_other_ext, other_cache: RCache):
                 assert not in_s, "block of an ancestor inside the partner subtree cannot be a leaf"
                 St = S
                 RB = other_cache.get(s)
-            rows.append(RB @ St.T)
+            blk = RB @ St.T
+            if blockwise:
+                RV = R_own_ext[t] if in_t else own_cache.get(t)
+                nrm = np.linalg.norm(blk @ RV.T)
+                if nrm == 0.0:
+                    continue  # a zero block adds nothing to the weights
+                blk = blk / nrm
+            rows.append(blk)
         p = tr.parent[t]
         if p >= 0:
             rows.append(B[p] @ side.Eext(t).T)
@@ -232,8 +257,9 @@ def local_update(Z: H2, t0: int, s0: int, X: np.ndarray, Y: np.ndarray, trunc: T
     RVe = _ext_rfactors(row)
     RWe = _ext_rfactors(col)
     # U3
-    Brow = _weights(row, col, RWe, rcache_col)
-    Bcol = _weights(col, row, RVe, rcache_row)
+    bw = trunc.blockwise
+    Brow = _weights(row, col, RWe, rcache_col, bw, RVe, rcache_row)
+    Bcol = _weights(col, row, RVe, rcache_row, bw, RWe, rcache_col)
     # U4
     Qr, Rr, rr, sr = _truncated_basis(row, Brow, trunc)
     Qc, Rc, rc, sc = _truncated_basis(col, Bcol, trunc)

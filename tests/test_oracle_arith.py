@@ -275,3 +275,21 @@ def test_zero_tile_factor_adds_nothing_reading_own6():
                 np.testing.assert_array_equal(Z.l, l0)
                 n_cases[case] += 1
     assert min(n_cases) >= 3, n_cases
+
+
+def test_cholesky_blockwise_truncation():
+    """NEXT-1: the H^2 Cholesky with blockwise-relative truncation (own-10; temporaries keep the
+    relative rule): at a tight eps^ it reproduces the dense Cholesky, at a loose one the factor
+    still preconditions CG."""
+    c, rt, bt, Z = _c0(lower=True)
+    A = c["A"]
+    Ad = A.toarray()[rt.perm][:, rt.perm]
+    ar = Arith(Z, Trunc(1e-12, blockwise=True))
+    ar.chol()
+    assert np.abs(np.tril(densify(Z)) - np.linalg.cholesky(Ad)).max() / np.abs(Ad).max() < 1e-9
+    c, rt, bt, Z = _c0(lower=True)
+    ar = Arith(Z, Trunc(1e-3, blockwise=True))
+    ar.chol()
+    b = np.random.default_rng(4).standard_normal(A.shape[0])
+    _, m, rel = pcg(lambda v: A @ v, lambda v: ar.solve(v), b)
+    assert rel < 1e-8 and m <= 12

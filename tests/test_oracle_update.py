@@ -208,3 +208,48 @@ def test_transpose_matvec_nonzero_ranks():
     x = stream(6).standard_normal((rt.n, 2))
     np.testing.assert_allclose(Z.matvec_tree(x, transpose=True), D.T @ x, rtol=0, atol=1e-10 * np.abs(D.T @ x).max())
     np.testing.assert_allclose(Z.matvec_tree(x), D @ x, rtol=0, atol=1e-10 * np.abs(D @ x).max())
+
+
+@pytest.mark.parametrize("eps", [1e-2, 1e-4])
+def test_blockwise_o1_equals_o2(eps):
+    """NEXT-1 (reading own-10): the blockwise-relative weights in the paper's nested recursion (O1)
+    equal the dense definition -- SVDs of the block rows with every block scaled by 1 / its
+    Frobenius norm, absolute threshold eps^ (O2) -- in ranks and result."""
+    c, rt, bt = _c0()
+    Z = from_sparse(bt, c["A"])
+    worst = _random_updates(Z, bt, rt, Trunc(eps, blockwise=True), 24, seed=17)
+    assert worst < 1e-12
+
+
+def test_blockwise_error_bound_per_block():
+    """The point of blockwise-relative truncation: after a local update every
+    admissible block keeps its own relative accuracy, ||G_b - G~_b||_2 <= 2 (depth + 1) eps^ ||G_b||_F
+    (row and column truncation, each accumulating at most depth + 1 levels), whatever the blocks'
+    magnitudes -- here blocks scaled over eight orders of magnitude."""
+    c, rt, bt = _c0()
+    Z = from_sparse(bt, c["A"])
+    eps = 1e-3
+    up = Updater(Z, Trunc(1e-13))
+    rng = np.random.default_rng(3)
+    for b in bt.adm:  # build blocks of wildly different size: exact (tight truncation)
+        t0, s0 = int(bt.t[b]), int(bt.s[b])
+        scale = 10.0 ** rng.uniform(-4, 4)
+        up(t0, s0, scale * rng.standard_normal((rt.size(t0), 3)), rng.standard_normal((rt.size(s0), 3)))
+    depth = max(rt.level)
+    b0 = next(b for b in range(bt.nblocks) if bt.kind[b] == 0 and rt.size(bt.t[b]) >= 128)
+    t0, s0 = int(bt.t[b0]), int(bt.s[b0])
+    X = rng.standard_normal((rt.size(t0), 4))
+    Y = rng.standard_normal((rt.size(s0), 4))
+    exact = densify(Z)
+    exact[rt.lo[t0]:rt.hi[t0], rt.lo[s0]:rt.hi[s0]] += X @ Y.T
+    Updater(Z, Trunc(eps, blockwise=True))(t0, s0, X, Y)
+    got = densify(Z)
+    worst = 0.0
+    for b in bt.adm:
+        t, s = int(bt.t[b]), int(bt.s[b])
+        G = exact[rt.lo[t]:rt.hi[t], rt.lo[s]:rt.hi[s]]
+        if not G.any():
+            continue
+        err = np.linalg.norm(got[rt.lo[t]:rt.hi[t], rt.lo[s]:rt.hi[s]] - G, 2) / np.linalg.norm(G)
+        worst = max(worst, err)
+    assert 0.0 < worst <= 2 * (depth + 1) * eps, worst
