@@ -50,11 +50,20 @@ typedef enum {
 
 /* TruncationControl (reading SURVEY R5): a cluster keeps
  *   r = #{ sigma_i > max(rel_tol * sigma_1, abs_tol) },  r <= max_rank (max_rank <= 0: unbounded),
- * of the singular values of its weighted basis V~_t B~_t^T. sigma_1 = 0 gives r = 0. */
+ * of the singular values of its weighted basis V~_t B~_t^T. sigma_1 = 0 gives r = 0.
+ * blockwise != 0 (DESIGN reading own-10): the paper's "block-relative accuracy
+ * eps^" ("weighting factors in the matrices B_{t,s} ... to ensure blockwise relative
+ * error bounds"): every block b = (t, s) enters the weight stacks of the local update
+ * with the factor 1 / ||R_{V,t} S~_b R_{W,s}^T||_F (the block's Frobenius norm, from the R-factors
+ * of the current / extended bases) and a cluster keeps r = #{ sigma_i > max(rel_tol, abs_tol) }
+ * -- an ABSOLUTE threshold eps^ = rel_tol on the weighted matrix.  The low-rank temporaries of the
+ * product (one block each) keep the relative rule.  (The field occupies what was
+ * padding: sizeof(h2_trunc) is unchanged; callers must zero-initialise the struct.) */
 typedef struct {
   double rel_tol;
   double abs_tol;
   int32_t max_rank;
+  int32_t blockwise;
 } h2_trunc;
 
 typedef enum { H2_FULL = 0, H2_LOWER = 1 } h2_storage; /* LOWER: blocks with t-range >= s-range */

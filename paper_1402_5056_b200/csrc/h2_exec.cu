@@ -37,7 +37,7 @@ constexpr int RM = KC + 1;
 constexpr size_t SM_EXEC = (size_t)(3 * RM * KC + KC) * 8 + (KC + 8) * 4;  // max over items (SVD items)
 static_assert(SM_EXEC >= (size_t)((PR + 1) * KC + KC + 8) * 8 + (5 * 128 + PR) * 4, "smem (weights_cluster panel + block descriptors)");
 static_assert(SM_EXEC >= (size_t)((PR + 1) * KC + KC + 8 + 1024 + 2 * (RCAP_MAX + 1) * RCAP_MAX) * 8 + 3 * 64 * 4, "smem (weights path: panel + G chain + path)");
-static_assert((5 * 128 + PR) * 4 <= 1024 * 8, "weights_cluster descriptors fit the spare area");
+static_assert((5 * 128 + PR) * 4 + 128 * 8 <= 1024 * 8, "weights_cluster descriptors fit the spare area");
 static_assert(SM_EXEC >= (size_t)24000 * 8 + 9 * 128 * 4 + 16, "smem (couplings)");
 static_assert(SM_EXEC >= (size_t)(2 * (KC + 1) * 64 + 2 * 65 * 64 + 2 * KC + 8) * 8 + 2 * KC * 4 + 64, "smem (dd_compress)");
 static_assert(SM_EXEC >= (size_t)((PR + 1) * RCAP_MAX + KC + 3 * (RCAP_MAX + 1) * RCAP_MAX) * 8 + 4 * 64 * 4, "smem (rcache items)");

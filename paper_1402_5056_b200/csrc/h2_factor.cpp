@@ -104,6 +104,7 @@ struct Driver {
   cudaStream_t st;
   double rel, abs_tol;
   int max_rank;
+  int blockwise;  // h2_trunc.blockwise: local updates weight block-relative; temporaries keep the relative rule
   Arena& ar;
   const h2_tree_* T;  // the (shared) cluster tree
   int rcap, lmax;
@@ -153,6 +154,7 @@ struct Driver {
     a.rel_tol = rel;
     a.abs_tol = abs_tol;
     a.max_rank = max_rank;
+    a.blockwise = blockwise;
     a.prof = nullptr;
     cudaError_t e = launch_update(Z, a, st);
     if (e != cudaSuccess) throw std::runtime_error(std::string("h2 update launch: ") + cudaGetErrorString(e));
@@ -713,7 +715,7 @@ h2_status run_driver(h2_mat_* Z, const h2_trunc* trunc, h2_stream stream, int wh
     h2::set_error("leaf clusters larger than 64 are not supported");
     return H2_ERR_ARG;
   }
-  const h2_trunc tc = trunc ? *trunc : h2_trunc{1e-4, 0.0, 0};
+  const h2_trunc tc = trunc ? *trunc : h2_trunc{1e-4, 0.0, 0, 0};
   Arena ar;
   h2_status s;
   if ((s = ensure_ws(Z, ar)) != H2_OK) return s;
@@ -747,7 +749,7 @@ h2_status run_driver(h2_mat_* Z, const h2_trunc* trunc, h2_stream stream, int wh
   Arena arT;  // the scratch matrix of the inversion drives its own products
   if (what == 5 && (s = ensure_ws(X, arT)) != H2_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  Driver dr{Z, st, tc.rel_tol, tc.abs_tol, tc.max_rank, ar, Z->bt->rt, Z->d.rcap, Z->d.lmax};
+  Driver dr{Z, st, tc.rel_tol, tc.abs_tol, tc.max_rank, tc.blockwise != 0, ar, Z->bt->rt, Z->d.rcap, Z->d.lmax};
   ExecCtx ctx;
   exec_begin(&ctx, st);  // the recursion records ops; the device executor runs them (exec.h)
   try {
@@ -757,7 +759,7 @@ h2_status run_driver(h2_mat_* Z, const h2_trunc* trunc, h2_stream stream, int wh
     else if (what == 1) dr.lr(0);
     else if (what == 2) dr.addmul(alpha, HOp{X, false}, HOp{Y, false}, 0, 0, 0, nullptr);
     else if (what == 5) {
-      Driver dT{X, st, tc.rel_tol, tc.abs_tol, tc.max_rank, arT, X->bt->rt, X->d.rcap, X->d.lmax};
+      Driver dT{X, st, tc.rel_tol, tc.abs_tol, tc.max_rank, tc.blockwise != 0, arT, X->bt->rt, X->d.rcap, X->d.lmax};
       dT.ident = arT.alloc((size_t)X->d.lmax * X->d.lmax);
       identity(dT.ident, X->d.lmax, X->d.lmax, st);
       dr.inv(0, dT);

@@ -558,7 +558,7 @@ extern "C" h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t
   if (k > 0 && (!X || !Y)) H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: NULL factor");
   const int mt = B->rt->hi[t0] - B->rt->lo[t0], ms = B->ct->hi[s0] - B->ct->lo[s0];
   if (k > 0 && (ldx < mt || ldy < ms)) H2_FAIL(H2_ERR_SHAPE, "h2_lowrank_update: leading dimension too small");
-  h2_trunc tc = trunc ? *trunc : h2_trunc{1e-4, 0.0, 0};
+  h2_trunc tc = trunc ? *trunc : h2_trunc{1e-4, 0.0, 0, 0};
   if (!(tc.rel_tol >= 0) || !(tc.abs_tol >= 0)) H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: negative tolerance");
   if (Z->lower && B->rt->lo[t0] < B->ct->lo[s0])
     H2_FAIL(H2_ERR_ARG, "h2_lowrank_update: target block is not stored in H2_LOWER storage");
@@ -580,6 +580,7 @@ extern "C" h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t
   a.rel_tol = tc.rel_tol;
   a.abs_tol = tc.abs_tol;
   a.max_rank = tc.max_rank;
+  a.blockwise = tc.blockwise != 0;
   a.kdev = nullptr;
   a.prof = nullptr;
   try {

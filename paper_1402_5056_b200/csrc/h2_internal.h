@@ -103,6 +103,7 @@ struct UpdArgs {
   double alpha;
   double rel_tol, abs_tol;
   int max_rank;
+  int blockwise;  // h2_trunc.blockwise (reading own-10): block-relative weighting, absolute threshold
   double* prof;  // device flop/byte counters (profiling) or nullptr
   const int* kdev;  // if set, the update rank is read from device memory (internal callers)
 };

@@ -175,6 +175,10 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
   int* d_rc = d_ls + NBD;
   int* d_off = d_rc + NBD;
   int* rowblk = d_off + NBD;      // PR: panel row -> descriptor
+  double* d_nrm = reinterpret_cast<double*>(rowblk + PR);  // NBD: ||G~_b||_F (blockwise weighting)
+  // blockwise (reading own-10): R-factor of this cluster's own (extended) basis
+  const double* RVo = in_t ? A.re + (size_t)t * M.kcap * M.kcap : A.rc + (size_t)t * M.rcap * M.rcap;
+  const int ldRV = in_t ? M.kcap : M.rcap;
   int rows = 0;
   double fl = 0.0;
   auto flush = [&]() {
@@ -241,6 +245,31 @@ __device__ double weights_cluster(const MatDev& M, const UpdArgs& a, bool rs, in
         P[rr + c * PRL] = v;
       }
       __syncthreads();
+      if (a.blockwise) {
+        // every block's rows carry the weight 1 / ||G~_b||_F,  G~_b^T = (R_B S~^T) R_V^T
+        // (d_rc[b] x K; R_V upper triangular).  One warp per block, fixed summation order.
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int b = j + warp; b < je; b += NT / 32) {
+          const int nrb = d_rc[b], ob = d_off[b];
+          double sq = 0.0;
+          for (int e = lane; e < nrb * K; e += 32) {
+            const int i = e % nrb, cp = e / nrb;
+            double g = 0.0;
+            for (int c = cp; c < K; ++c) g += P[ob + i + c * PRL] * RVo[cp + (size_t)c * ldRV];
+            sq += g * g;
+          }
+          for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+          if (lane == 0) d_nrm[b] = sqrt(sq);
+        }
+        fl += (double)nr * K * K;
+        __syncthreads();
+        for (int e = threadIdx.x; e < nr * K; e += NT) {
+          const int rr = rows + e % nr, c = e / nr;
+          const double nb = d_nrm[rowblk[rr]];
+          P[rr + c * PRL] = nb > 0.0 ? P[rr + c * PRL] / nb : 0.0;  // a zero block adds nothing
+        }
+        __syncthreads();
+      }
       rows = r;
       j = je;
       if (j < cnt) flush();  // block j does not fit: compress first
@@ -512,7 +541,10 @@ __device__ void svd_core(const MatDev& M, const UpdArgs& a, const DevSide& D, in
   int& clamped = scr[2];
   if (threadIdx.x == 0) clamped = 0;
   __syncthreads();
-  const int r = la::trunc_rank(sig, order, p, a.rel_tol, a.abs_tol, a.max_rank, M.rcap, &clamped);
+  // blockwise: an absolute threshold eps^ = rel_tol on the block-relative weighted matrix
+  const int r = a.blockwise
+                    ? la::trunc_rank(sig, order, p, 0.0, fmax(a.rel_tol, a.abs_tol), a.max_rank, M.rcap, &clamped)
+                    : la::trunc_rank(sig, order, p, a.rel_tol, a.abs_tol, a.max_rank, M.rcap, &clamped);
   double* Q = Mm;
   // Q(:, q) = W(:, order[q]) / sigma
   for (int e = threadIdx.x; e < m * r; e += NT) {

@@ -104,19 +104,21 @@ def _stream(stream):
 
 @dataclass
 class Trunc:
-    """h2_trunc (reading SURVEY R5)."""
+    """h2_trunc (reading SURVEY R5; blockwise: P:874-879, reading own-10)."""
     rel_tol: float = 1e-4
     abs_tol: float = 0.0
     max_rank: int = 0
+    blockwise: bool = False
 
 
 class _CTrunc(C.Structure):
-    _fields_ = [("rel_tol", C.c_double), ("abs_tol", C.c_double), ("max_rank", C.c_int32)]
+    _fields_ = [("rel_tol", C.c_double), ("abs_tol", C.c_double), ("max_rank", C.c_int32),
+                ("blockwise", C.c_int32)]
 
 
 def _ctrunc(tr):
     tr = tr or Trunc()
-    return _CTrunc(float(tr.rel_tol), float(tr.abs_tol), int(tr.max_rank))
+    return _CTrunc(float(tr.rel_tol), float(tr.abs_tol), int(tr.max_rank), int(bool(tr.blockwise)))
 
 
 class Tree:

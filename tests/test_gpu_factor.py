@@ -79,6 +79,27 @@ def test_cholesky_parity(name, N, cap):
     assert abs(e_g - e_o) <= 1e-2 * max(e_o, 1e-12) + 1e-12
 
 
+@pytest.mark.parametrize("name,N,eps", [("C0", None, 1e-3), ("C2", 64, 1e-3), ("C2", 128, 1e-2)])
+def test_cholesky_blockwise_parity(name, N, eps):
+    """NEXT-1: the H^2 Cholesky with block-relative truncation eps^ (P:1408-1409, reading own-10;
+    temporaries keep the relative rule): ranks and update counts bit-exact, operator <= 10 eps^,
+    PCG iterations +-1."""
+    s = setup(name, N, lower=True)
+    OZ, Z, A = s["OZ"], s["Z"], s["c"]["A"]
+    ar = Arith(OZ, OTrunc(eps, blockwise=True))
+    ar.chol()
+    P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps, blockwise=True))
+    assert P.h2_check_device_flags(Z) == 0
+    _ranks_equal(Z, OZ)
+    assert P.h2_stats(Z)["updates_nonzero"] == ar.stats["updates"]
+    d = operator_rel_diff(Z, OZ, s["ot"].n)
+    b = stream(RHS).standard_normal(s["ot"].n)
+    _, m_o, _ = pcg(lambda v: A @ v, lambda v: ar.solve(v), b)
+    _, m_g, rel = pcg(lambda v: A @ v, lambda v: _gpu_solve(Z, v), b)
+    print(f"{name} blockwise Cholesky eps^={eps}: rel diff {d:.2e}, max rank {OZ.k.max()}, m gpu {m_g} oracle {m_o}")
+    assert d <= 10 * eps and rel < 1e-8 and abs(m_g - m_o) <= 1
+
+
 def test_lr_parity_c0_rank8():
     """C0 protocol (R15): rank-8 update with alpha = 1/n on every admissible leaf, then LR."""
     eps = 1e-4

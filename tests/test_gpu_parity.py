@@ -49,7 +49,7 @@ def test_matvec_from_sparse(name, N):
 def _run_pair(s, updates, trunc, check_every=1, tol=None, alpha=1.0):
     """Apply the same update sequence to the oracle and the GPU; compare ranks and operators."""
     OZ, ot, Z = s["OZ"], s["ot"], s["Z"]
-    up = Updater(OZ, OTrunc(trunc.rel_tol, trunc.abs_tol, trunc.max_rank))
+    up = Updater(OZ, OTrunc(trunc.rel_tol, trunc.abs_tol, trunc.max_rank, blockwise=trunc.blockwise))
     worst = 0.0
     keep = []
     for i, (t0, s0, X, Y) in enumerate(updates):
@@ -74,6 +74,23 @@ def test_update_mixed_targets_c0_adaptive():
     w = _run_pair(s, ups, P.Trunc(1e-4), tol=10 * 1e-4)
     print("C0 mixed adaptive worst rel diff", w)
     assert w < 1e-9  # observed agreement (the bar above is 10 eps)
+
+
+@pytest.mark.parametrize("eps", [1e-2, 1e-4])
+def test_update_blockwise_relative_truncation(eps):
+    """NEXT-1 (reading own-10): block-relative weighting of the weight
+    stacks and the absolute threshold eps^ -- ranks bit-exact after every update, operator <= 10 eps^.
+    The factors are scaled per update over eight orders of magnitude, so the rule differs from
+    the plain relative one (which would drop the small blocks)."""
+    s = setup("C0")
+    rng = np.random.default_rng(11)
+    ups = [(t0, s0, X * 10.0 ** rng.uniform(-4, 4), Y)
+           for t0, s0, X, Y in mixed_stream(all_targets(s["ot"], s["ob"]), 40, kmax=8, seed=7)]
+    w = _run_pair(s, ups, P.Trunc(eps, blockwise=True), tol=10 * eps)
+    print(f"C0 blockwise eps^={eps}: worst rel diff {w:.2e}, max rank {P.h2_ranks(s['Z'])[0].max()}")
+    s2 = setup("C0")
+    _run_pair(s2, ups, P.Trunc(eps), check_every=40)
+    assert (P.h2_ranks(s2["Z"])[0] != P.h2_ranks(s["Z"])[0]).any(), "the blockwise rule changed nothing"
 
 
 def test_update_exact_no_truncation():

@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
     python bench.py --warmup 3 --steps 1 --cpu-budget 2 > gpurun_out/ncu_launches_bench.log 2>&1
 # full capture of the fused matvec of the C2 factor L (3 launches after warm-up)
-ncu --set full --clock-control none --import-source on -k regex:k_matvec -s 20 -c 2 -o gpurun_out/prof_matvec \
+ncu --set full --clock-control none --import-source on -k "regex:k_m(atvec|v_)" -s 24 -c 8 -o gpurun_out/prof_matvec \
     python tools/time_matvec.py 512 factor > gpurun_out/ncu_mv.log 2>&1
 # full capture of one executor launch inside the C2 factorization (traffic)
 ncu --set full --clock-control none --import-source on -k regex:k_exec_cluster -s 200 -c 1 -o gpurun_out/prof_exec \
