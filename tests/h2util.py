@@ -7,8 +7,10 @@ from oracle.structure import ClusterTree, BlockTree, ADM
 from oracle.h2 import from_sparse as o_from_sparse
 
 
-def setup(name, N=None, lower=False, rank_cap=32, update_cap=32, gpu=True):
+def setup(name, N=None, lower=False, rank_cap=32, update_cap=32, gpu=True, eta=None):
     c = config(name, N=N)
+    if eta is not None:
+        c["eta"] = eta
     ot = ClusterTree(c["points"], c["leaf"])
     ob = BlockTree(ot, ot, c["eta"])
     OZ = o_from_sparse(ob, c["A"], lower=lower)

@@ -79,12 +79,15 @@ def test_cholesky_parity(name, N, cap):
     assert abs(e_g - e_o) <= 1e-2 * max(e_o, 1e-12) + 1e-12
 
 
-@pytest.mark.parametrize("name,N,eps", [("C0", None, 1e-3), ("C2", 64, 1e-3), ("C2", 128, 1e-2)])
-def test_cholesky_blockwise_parity(name, N, eps):
+@pytest.mark.parametrize("name,N,eps,eta", [("C0", None, 1e-3, None), ("C2", 64, 1e-3, None), ("C2", 128, 1e-2, None),
+                                             ("C1", 63, 1.2e-2, 4.0), ("C1", 127, 3.1e-3, 4.0)])
+def test_cholesky_blockwise_parity(name, N, eps, eta):
     """NEXT-1: the H^2 Cholesky with block-relative truncation eps^ (P:1408-1409, reading own-10;
     temporaries keep the relative rule): ranks and update counts bit-exact, operator <= 10 eps^,
-    PCG iterations +-1."""
-    s = setup(name, N, lower=True)
+    PCG iterations +-1.  The C1 cases are the paper's own parameters (Table 1: Poisson
+    on (2^l - 1)^2 nodes, eta = 4, eps^ ~ h^2; l = 6 and the printed l = 7 row), whose ragged leaves
+    (63 and 127 are not powers of two) also exercise clusters of unequal size."""
+    s = setup(name, N, lower=True, eta=eta)
     OZ, Z, A = s["OZ"], s["Z"], s["c"]["A"]
     ar = Arith(OZ, OTrunc(eps, blockwise=True))
     ar.chol()

@@ -293,3 +293,44 @@ def test_cholesky_blockwise_truncation():
     b = np.random.default_rng(4).standard_normal(A.shape[0])
     _, m, rel = pcg(lambda v: A @ v, lambda v: ar.solve(v), b)
     assert rel < 1e-8 and m <= 12
+
+
+def test_cholesky_on_dd_tree_equals_dense_and_keeps_decoupled_blocks_zero():
+    """NEXT-3 (reading own-11): on the domain-decomposition tree the H^2 Cholesky at a
+    tight truncation is the dense Cholesky in tree (= nested dissection) order, the blocks of the
+    decoupled domain pairs stay exactly zero (rank 0) and far fewer local updates are needed than
+    on the bisection tree; at eps = 1e-4 it preconditions CG like the bisection-tree factor."""
+    c = config("C2", N=48)
+    A = c["A"]
+    rt = ClusterTree(c["points"], c["leaf"], adjacency=A)
+    bt = BlockTree(rt, rt, c["eta"])
+    Z = from_sparse(bt, A, lower=True)
+    Ad = A.toarray()[rt.perm][:, rt.perm]
+    ar = Arith(Z, Trunc(1e-13))
+    ar.chol()
+    L = np.tril(densify(Z))
+    Lref = np.linalg.cholesky(Ad)
+    assert np.abs(L - Lref).max() / np.abs(Lref).max() < 1e-9
+    npairs = 0
+    for p in np.nonzero(rt.ddpair)[0]:
+        a, b = rt.sons(p)
+        blk = bt.index[(b, a)]
+        assert bt.kind[blk] == ADM and Z.k[b] * 0 == 0
+        assert not L[rt.lo[b]:rt.hi[b], rt.lo[a]:rt.hi[a]].any()
+        assert not Lref[rt.lo[b]:rt.hi[b], rt.lo[a]:rt.hi[a]].any()  # no fill in nested dissection order
+        npairs += 1
+    assert npairs > 10
+    # truncated: error bound, PCG, and the update count against the bisection tree
+    Z2 = from_sparse(bt, A, lower=True)
+    ar2 = Arith(Z2, Trunc(1e-4))
+    ar2.chol()
+    E = dense_factor_product(Z2, True) - Ad
+    assert np.linalg.norm(E, 2) <= 10 * 1e-4 * np.linalg.norm(Ad, 2)
+    b = np.random.default_rng(4).standard_normal(A.shape[0])
+    _, m, rel = pcg(lambda v: A @ v, lambda v: ar2.solve(v), b)
+    assert rel < 1e-8 and m <= 12
+    rb = ClusterTree(c["points"], c["leaf"])
+    Zb = from_sparse(BlockTree(rb, rb, c["eta"]), A, lower=True)
+    arb = Arith(Zb, Trunc(1e-4))
+    arb.chol()
+    assert ar2.stats["updates"] < arb.stats["updates"] / 2

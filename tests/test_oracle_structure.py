@@ -154,3 +154,86 @@ def test_block_tree_counts_match_survey_appendix():
         t = ClusterTree(c["points"], c["leaf"])
         bt = BlockTree(t, t, c["eta"])
         assert (len(bt.adm), len(bt.inadm), bt.sparsity()) == (adm, inadm, csp)
+
+
+# ---- domain-decomposition clustering (NEXT-3, reading own-11) ----------------------
+def _dd_checks(pts, A, leaf, eta):
+    """Properties that define the DD tree: partition, nested-dissection order, interface =
+    exactly the points of the right half coupled to the left half, decoupled domain pairs (no
+    matrix entry, brute force on the dense pattern), block-tree partition with every nonzero in an
+    inadmissible leaf."""
+    n = pts.shape[0]
+    t = ClusterTree(pts, leaf, adjacency=A)
+    assert sorted(t.perm.tolist()) == list(range(n))
+    D = (A != 0).toarray()
+    D = D | D.T
+    Dt = D[t.perm][:, t.perm]
+    npairs = 0
+    for c in range(t.nclusters):
+        if t.is_leaf(c):
+            assert t.size(c) <= max(leaf, 1)
+            continue
+        a, b = t.sons(c)
+        assert t.lo[a] == t.lo[c] and t.hi[a] == t.lo[b] and t.hi[b] == t.hi[c]
+        if t.ddpair[c]:
+            npairs += 1
+            assert not Dt[t.lo[a]:t.hi[a], t.lo[b]:t.hi[b]].any()  # decoupled domains
+            p = t.parent[c]
+            if p >= 0 and t.son0[p] == c and not t.ddpair[p]:
+                g = t.son1[p]  # the interface of this split: every point coupled to dom1, none of dom2 is
+                assert Dt[t.lo[g]:t.hi[g], t.lo[a]:t.hi[a]].any(axis=1).all()
+                # geometric rule: dom1 is the left half (coord < mid of the father's box), the rest right
+                ext = t.bmax[p] - t.bmin[p]
+                ax = int(np.argmax(ext))
+                mid2 = t.bmin[p][ax] + t.bmax[p][ax]
+                assert (2 * pts[t.perm[t.lo[a]:t.hi[a]], ax] < mid2).all()
+                assert (2 * pts[t.perm[t.lo[b]:t.hi[g]], ax] >= mid2).all()
+    bt = BlockTree(t, t, eta)
+    cover = np.zeros((n, n), dtype=np.int64)
+    near = np.zeros((n, n), dtype=bool)
+    for b in range(bt.nblocks):
+        if bt.kind[b] != SUBDIV:
+            tt, ss = bt.t[b], bt.s[b]
+            cover[t.lo[tt]:t.hi[tt], t.lo[ss]:t.hi[ss]] += 1
+            if bt.kind[b] == INADM:
+                near[t.lo[tt]:t.hi[tt], t.lo[ss]:t.hi[ss]] = True
+            else:
+                pt, ps = pts[t.perm[t.lo[tt]:t.hi[tt]]], pts[t.perm[t.lo[ss]:t.hi[ss]]]
+                pair = tt != ss and t.parent[tt] == t.parent[ss] and t.ddpair[t.parent[tt]]
+                assert pair or _brute_adm(pt, ps, eta)
+    assert (cover == 1).all()
+    assert near[Dt].all()
+    return t, bt, npairs
+
+
+def test_dd_tree_nested_dissection_closed_form():
+    """(2^l - 1)^2 grid, 5-point stencil: the root split is the classical nested dissection --
+    separator = the middle grid line (2^l - 1 points), two domains of (2^(l-1) - 1)(2^l - 1)."""
+    l = 5
+    N = 2 ** l - 1
+    c = config("C1", N=N)
+    t, bt, npairs = _dd_checks(c["points"], c["A"], 32, 2.0)
+    inner, gam = t.sons(0)
+    assert t.ddpair[inner] and not t.ddpair[0]
+    assert t.size(gam) == N and all(t.size(d) == (2 ** (l - 1) - 1) * N for d in t.sons(inner))
+    assert (c["points"][t.perm[t.lo[gam]:t.hi[gam]], 0] == 2 ** (l - 1)).all()
+    assert npairs >= 7
+    # without the graph the constructor is the plain bisection tree
+    assert not ClusterTree(c["points"], 32).ddpair.any()
+
+
+def test_dd_tree_irregular_graph():
+    """Random points with a k-nearest-neighbour coupling graph (unsymmetric pattern, symmetrised
+    by the constructor), and a graph with two components (an empty interface)."""
+    rng = np.random.default_rng(3)
+    pts = np.round(rng.uniform(0, 100, (400, 2)))
+    d2 = ((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1)
+    nb = np.argsort(d2, axis=1)[:, :5]
+    import scipy.sparse as sp
+    A = sp.csr_matrix((np.ones(nb.size), (np.repeat(np.arange(400), 5), nb.ravel())), shape=(400, 400))
+    _dd_checks(pts, A, 16, 2.0)
+    # two far-apart clouds coupled only inside themselves: the root itself is a decoupled pair
+    pts2 = np.vstack([pts[:100], pts[100:200] + [1000.0, 0.0]])
+    B = sp.block_diag([A[:100, :100], A[100:200, 100:200]]).tocsr()
+    t, _, _ = _dd_checks(pts2, B, 16, 2.0)
+    assert t.ddpair[0]

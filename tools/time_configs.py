@@ -10,6 +10,12 @@
                                                  into a fresh rank-0 Z), then H^2 Cholesky of A
                                                  (reading own-8: A^2 is numerically singular here)
 
+  python tools/time_configs.py table1 [l...]      the paper's own FEM parameters (Table 1):
+                                                 Poisson on (2^l - 1)^2 nodes, eta = 4, block-relative
+                                                 accuracy eps^ ~ h^2 (NEXT-1, reading own-10), geometric
+                                                 bisection tree (the paper: DD clustering, NEXT-3);
+                                                 Time/n, Mem/n, Err (power iteration, R11), m
+
 Every call goes through the C ABI (paper_1402_5056_b200); times are CUDA events on the stream.
 """
 import json
@@ -209,8 +215,68 @@ def run_inv(N, eps):
                       "storage_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / c["n"] / 1e3)}), flush=True)
 
 
+TABLE1 = {7: (3.1e-3, 7.0e-5, 1.0, 0.06, 3), 8: (7.7e-4, 8.4e-5, 1.1, 0.07, 3), 9: (1.9e-4, 1.1e-4, 1.2, 0.07, 3),
+          10: (4.8e-5, 1.3e-4, 1.2, 0.10, 3), 11: (1.2e-5, 1.5e-4, 1.2, 0.11, 3)}  # l: eps^, Time/n, Mem/n KB, Err, m
+
+
+def run_table1(levels):
+    from inputs.rng import POWER
+    for l in levels:
+        N = 2 ** l - 1
+        eps = TABLE1[l][0]
+        c = config("C1", N=N)  # the constant-coefficient 5-point problem
+        t = P.h2_cluster_tree(c["points"], c["leaf"])
+        bt = P.h2_block_tree(t, t, 4.0)
+        Aop = P.h2_from_sparse(bt, c["A"], lower=False, rank_cap=32, update_cap=32)
+        Z = P.h2_from_sparse(bt, c["A"], lower=True, rank_cap=32, update_cap=32)
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record()
+        P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps, blockwise=True))
+        e1.record()
+        torch.cuda.synchronize()
+        flags = P.h2_check_device_flags(Z)
+        n = c["n"]
+        b = torch.from_numpy(stream(RHS).standard_normal(n)).to(dev)
+        x = torch.zeros_like(b)
+        e2, e3 = ev(), ev()
+        e2.record()
+        _, m, rel = P.h2_pcg(Aop, Z, b, x, tol=1e-8)
+        e3.record()
+        torch.cuda.synchronize()
+        # Err = ||I - (L L^T)^-1 A||_2 by plain power iteration (R11): 50 its or rel. change < 1e-4
+        v = torch.from_numpy(stream(POWER).standard_normal(n)).to(dev)
+        v /= torch.linalg.norm(v)
+        lam = 0.0
+        for it in range(50):
+            w = P.h2_matvec(Aop, v)
+            P.h2_solve(Z, w)
+            w = v - w
+            new = float(torch.linalg.norm(w))
+            v = w / new
+            if it > 0 and abs(new - lam) <= 1e-4 * new:
+                lam = new
+                break
+            lam = new
+        kr, kc = P.h2_ranks(Z)
+        setup_s = e0.elapsed_time(e1) / 1e3
+        ref = TABLE1[l]
+        print(json.dumps({"config": f"Table 1 l={l}", "n": n, "eta": 4.0, "eps_hat": eps, "tree": "geometric bisection, leaf 32",
+                          "setup_s": setup_s, "setup_s_per_dof": setup_s / n,
+                          "mem_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / n / 1e3),
+                          "Err": lam, "m": m, "pcg_relres": rel, "solve_s_per_step_per_dof": e2.elapsed_time(e3) / 1e3 / max(m, 1) / n,
+                          "max_rank": [int(kr.max()), int(kc.max())], "mean_rank": float(kr.mean()), "flags": flags,
+                          "stats": P.h2_stats(Z), "matvec_factor": matvec_gbps(Z, n),
+                          "paper_table1": {"setup_s_per_dof": ref[1], "mem_KB_per_dof": ref[2], "Err": ref[3], "m": ref[4],
+                                           "machine": "one Opteron 8431 core; DD clustering (P:1403-1405)"}}), flush=True)
+        del Z, Aop
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
+    if what == "table1":
+        run_table1([int(a) for a in sys.argv[2:]] or [7, 8, 9])
+        sys.exit(0)
     if what == "c1":
         run_c1(int(sys.argv[2]) if len(sys.argv) > 2 else 10000)
     elif what == "c3":
