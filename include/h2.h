@@ -77,6 +77,23 @@ typedef enum { H2_LR = 0, H2_CHOLESKY = 1 } h2_factor_kind;
  * pts: host, n x dim, row-major (point i at pts[i*dim .. i*dim+dim-1]); dim in {1,2,3}. */
 h2_status h2_cluster_tree(const double* pts, int64_t n, int32_t dim, int32_t leaf_size, h2_tree* out);
 
+/* Cluster tree by domain-decomposition clustering ("a domain
+ * decomposition cluster strategy similar to the one described in [GRKRLE05a]"; the paper gives no
+ * details: DESIGN reading own-11).  rowptr/colidx: host CSR pattern of the n x n matrix (taken
+ * symmetrically).  A DOMAIN cluster with more than 2 leaf_size points is bisected geometrically
+ * as in h2_cluster_tree into (left, right); the interface gamma = the points of `right` coupled
+ * to a point of `left`; dom1 = left, dom2 = right minus gamma; the ternary split becomes
+ * t -> (interior -> (dom1, dom2), gamma), i.e. the tree order is the nested dissection order.
+ * dom1/dom2 are DOMAIN clusters, gamma (an INTERFACE cluster) and small domains are bisected
+ * plainly; an empty gamma makes (left, right) itself a decoupled pair; an empty dom2 or an interior
+ * of <= leaf_size points gives a plain split.  h2_block_tree with this tree as rows AND columns
+ * makes the block of two decoupled domains an admissible leaf: it holds no matrix entry and the
+ * LR / Cholesky factorization in tree order creates none (its rank stays 0).
+ * h2_tree_ddpair: ddpair[t] = 1 iff the two sons of cluster t are decoupled domains (host, nclusters). */
+h2_status h2_cluster_tree_dd(const double* pts, int64_t n, int32_t dim, int32_t leaf_size, const int64_t* rowptr,
+                             const int32_t* colidx, h2_tree* out);
+h2_status h2_tree_ddpair(h2_tree tree, int8_t* ddpair);
+
 /* Export: perm[n]; lo/hi/son0/son1/level[nclusters] (son = -1 for leaves); any pointer may be
  * NULL.  *nclusters receives the count (call once with NULL arrays to size them). */
 h2_status h2_tree_export(h2_tree tree, int64_t* perm, int32_t* lo, int32_t* hi, int32_t* son0,

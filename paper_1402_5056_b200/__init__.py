@@ -12,6 +12,7 @@ from .h2 import (  # noqa: F401
     BlockTree,
     Mat,
     h2_cluster_tree,
+    h2_cluster_tree_dd,
     h2_block_tree,
     h2_from_sparse,
     h2_lowrank_update,

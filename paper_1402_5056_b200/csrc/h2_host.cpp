@@ -50,8 +50,14 @@ extern "C" const char* h2_last_error(void) { return g_last_error.c_str(); }
 // ------------------------------------------------------------------------------------------------
 // Cluster tree (binary P:331-332), geometric bisection per SURVEY R2.
 // ------------------------------------------------------------------------------------------------
-extern "C" h2_status h2_cluster_tree(const double* pts, int64_t n, int32_t dim, int32_t leaf_size,
-                                     h2_tree* out) {
+// gptr/gidx: nullptr (geometric bisection) or the symmetrised coupling graph in CSR form ->
+// domain-decomposition clustering (DESIGN reading own-11): a DOMAIN
+// cluster with more than 2 leaf_size points is bisected geometrically into (left, right), the
+// interface gamma = the points of `right` coupled to `left`, dom2 = right minus gamma, and the
+// ternary split of [GRKRLE05a] becomes t -> (interior -> (dom1, dom2), gamma): nested dissection
+// order.  ddpair[p] marks clusters whose two sons are decoupled domains.
+static h2_status build_cluster_tree(const double* pts, int64_t n, int32_t dim, int32_t leaf_size,
+                                    const int64_t* gptr, const int32_t* gidx, h2_tree* out) {
   if (!out) H2_FAIL(H2_ERR_ARG, "h2_cluster_tree: out is NULL");
   *out = nullptr;
   if (!pts || n <= 0 || dim < 1 || dim > 3 || leaf_size < 1)
@@ -66,10 +72,15 @@ extern "C" h2_status h2_cluster_tree(const double* pts, int64_t n, int32_t dim, 
   T->perm.resize(n);
   std::vector<int64_t> idx(n);
   for (int64_t i = 0; i < n; ++i) idx[i] = i;
+  std::vector<char> in_left(gptr ? n : 0, 0);
+  enum { DOMAIN = 0, INTERFACE = 1 };
 
-  std::function<int(std::vector<int64_t>&, int64_t, int, int)> build =
-      [&](std::vector<int64_t>& ids, int64_t start, int par, int lev) -> int {
+  // presplit: the interior cluster of a DD split (its sons are the two domains, given)
+  std::function<int(std::vector<int64_t>&, int64_t, int, int, int, std::vector<int64_t>*, std::vector<int64_t>*)> build =
+      [&](std::vector<int64_t>& ids, int64_t start, int par, int lev, int kind, std::vector<int64_t>* pre0,
+          std::vector<int64_t>* pre1) -> int {
     int cid = (int)T->lo.size();
+    T->ddpair.push_back(0);
     T->lo.push_back((int32_t)start);
     T->hi.push_back((int32_t)(start + (int64_t)ids.size()));
     T->son0.push_back(-1);
@@ -94,6 +105,17 @@ extern "C" h2_status h2_cluster_tree(const double* pts, int64_t n, int32_t dim, 
       for (size_t i = 0; i < ids.size(); ++i) T->perm[start + (int64_t)i] = ids[i];
       return cid;
     };
+    if (pre0) {
+      T->ddpair[cid] = 1;
+      ids.clear();
+      ids.shrink_to_fit();
+      const int64_t nl = (int64_t)pre0->size();
+      int c0 = build(*pre0, start, cid, lev + 1, DOMAIN, nullptr, nullptr);
+      int c1 = build(*pre1, start + nl, cid, lev + 1, DOMAIN, nullptr, nullptr);
+      T->son0[cid] = c0;
+      T->son1[cid] = c1;
+      return cid;
+    }
     if ((int64_t)ids.size() <= leaf_size) return make_leaf();
     int ax = 0;
     for (int d = 1; d < dim; ++d)
@@ -102,16 +124,45 @@ extern "C" h2_status h2_cluster_tree(const double* pts, int64_t n, int32_t dim, 
     std::vector<int64_t> left, right;
     for (int64_t q : ids) (2.0 * pts[q * dim + ax] < twomid ? left : right).push_back(q);
     if (left.empty() || right.empty()) return make_leaf();
+    const bool dd = gptr && kind == DOMAIN && (int64_t)ids.size() > 2 * (int64_t)leaf_size;
     ids.clear();
     ids.shrink_to_fit();
     int64_t nl = (int64_t)left.size();
-    int c0 = build(left, start, cid, lev + 1);
-    int c1 = build(right, start + nl, cid, lev + 1);
+    int c0, c1;
+    if (dd) {
+      for (int64_t q : left) in_left[q] = 1;
+      std::vector<int64_t> gam, d2;
+      for (int64_t q : right) {
+        bool coupled = false;
+        for (int64_t e = gptr[q]; e < gptr[q + 1] && !coupled; ++e) coupled = in_left[gidx[e]] != 0;
+        (coupled ? gam : d2).push_back(q);
+      }
+      for (int64_t q : left) in_left[q] = 0;
+      if (gam.empty()) {  // the halves are not coupled at all
+        T->ddpair[cid] = 1;
+        c0 = build(left, start, cid, lev + 1, DOMAIN, nullptr, nullptr);
+        c1 = build(right, start + nl, cid, lev + 1, DOMAIN, nullptr, nullptr);
+      } else if (d2.empty() || nl + (int64_t)d2.size() <= leaf_size) {  // no decoupling gained
+        c0 = build(left, start, cid, lev + 1, DOMAIN, nullptr, nullptr);
+        c1 = build(right, start + nl, cid, lev + 1, d2.empty() ? INTERFACE : DOMAIN, nullptr, nullptr);
+      } else {
+        right.clear();
+        right.shrink_to_fit();
+        std::vector<int64_t> inner(left);
+        inner.insert(inner.end(), d2.begin(), d2.end());
+        const int64_t ni = (int64_t)inner.size();
+        c0 = build(inner, start, cid, lev + 1, DOMAIN, &left, &d2);
+        c1 = build(gam, start + ni, cid, lev + 1, INTERFACE, nullptr, nullptr);
+      }
+    } else {
+      c0 = build(left, start, cid, lev + 1, kind, nullptr, nullptr);
+      c1 = build(right, start + nl, cid, lev + 1, kind, nullptr, nullptr);
+    }
     T->son0[cid] = c0;
     T->son1[cid] = c1;
     return cid;
   };
-  build(idx, 0, -1, 0);
+  build(idx, 0, -1, 0, gptr ? DOMAIN : INTERFACE, nullptr, nullptr);
   const int nc = (int)T->lo.size();
   T->nclusters = nc;
   T->depth = *std::max_element(T->level.begin(), T->level.end());
@@ -134,6 +185,43 @@ extern "C" h2_status h2_cluster_tree(const double* pts, int64_t n, int32_t dim, 
       T->leaves.push_back(t);
     }
   *out = T;
+  return H2_OK;
+}
+
+extern "C" h2_status h2_cluster_tree(const double* pts, int64_t n, int32_t dim, int32_t leaf_size,
+                                     h2_tree* out) {
+  return build_cluster_tree(pts, n, dim, leaf_size, nullptr, nullptr, out);
+}
+
+extern "C" h2_status h2_cluster_tree_dd(const double* pts, int64_t n, int32_t dim, int32_t leaf_size,
+                                        const int64_t* rowptr, const int32_t* colidx, h2_tree* out) {
+  if (!out) H2_FAIL(H2_ERR_ARG, "h2_cluster_tree_dd: out is NULL");
+  *out = nullptr;
+  if (!rowptr || !colidx || n <= 0) H2_FAIL(H2_ERR_ARG, "h2_cluster_tree_dd: need the CSR pattern of the matrix");
+  // symmetrised coupling graph (pattern of A + A^T, duplicates harmless)
+  std::vector<int64_t> gptr(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+      const int32_t j = colidx[e];
+      if (j < 0 || j >= n) H2_FAIL(H2_ERR_ARG, "h2_cluster_tree_dd: column index out of range");
+      gptr[i + 1]++;
+      gptr[j + 1]++;
+    }
+  for (int64_t i = 0; i < n; ++i) gptr[i + 1] += gptr[i];
+  std::vector<int32_t> gidx(gptr[n]);
+  std::vector<int64_t> fill(gptr.begin(), gptr.end() - 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+      const int32_t j = colidx[e];
+      gidx[fill[i]++] = j;
+      gidx[fill[j]++] = (int32_t)i;
+    }
+  return build_cluster_tree(pts, n, dim, leaf_size, gptr.data(), gidx.data(), out);
+}
+
+extern "C" h2_status h2_tree_ddpair(h2_tree tree, int8_t* ddpair) {
+  if (!tree || !ddpair) H2_FAIL(H2_ERR_ARG, "h2_tree_ddpair: NULL argument");
+  for (int t = 0; t < tree->nclusters; ++t) ddpair[t] = (int8_t)tree->ddpair[t];
   return H2_OK;
 }
 
@@ -195,8 +283,12 @@ extern "C" h2_status h2_block_tree(h2_tree rows, h2_tree cols, double eta, h2_bt
     B->sons.push_back({-1, -1, -1, -1});
     B->nsons.push_back(0);
     B->kind.push_back(SUBDIV);
+    // the two decoupled domains of a domain-decomposition split form an admissible (zero) block
+    // whatever their geometry (reading own-11); needs one tree for rows and columns
+    const bool ddzero = rows == cols && t != s && rows->parent[t] >= 0 && rows->parent[t] == cols->parent[s] &&
+                        rows->ddpair[rows->parent[t]];
     const double d2 = dist2(rows, t, cols, s);
-    if (d2 > 0.0 && std::max(diam2(rows, t), diam2(cols, s)) <= eta2 * d2) {
+    if (ddzero || (d2 > 0.0 && std::max(diam2(rows, t), diam2(cols, s)) <= eta2 * d2)) {
       B->kind[b] = ADM;
       return b;
     }

@@ -29,6 +29,7 @@ struct h2_tree_ {
   int nclusters = 0, depth = 0;
   std::vector<int64_t> perm;
   std::vector<int32_t> lo, hi, son0, son1, parent, level, tsize;
+  std::vector<char> ddpair;             // the two sons are decoupled domains (h2_cluster_tree_dd)
   std::vector<double> bmin, bmax;       // nclusters * dim
   std::vector<int32_t> bfs, level_ptr;  // clusters sorted by (level, id); level_ptr[depth+2]
   std::vector<int32_t> leaf_index;      // cluster -> leaf ordinal (or -1)

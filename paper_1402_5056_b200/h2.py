@@ -14,7 +14,7 @@ _LIBPATH = os.path.join(_HERE, os.environ.get("H2_LIB_NAME", "libh2b200.so"))  #
 
 # every symbol include/h2.h declares (checked by tests/test_abi.py)
 EXPORTED_SYMBOLS = [
-    "h2_cluster_tree", "h2_tree_export", "h2_tree_destroy",
+    "h2_cluster_tree", "h2_cluster_tree_dd", "h2_tree_ddpair", "h2_tree_export", "h2_tree_destroy",
     "h2_block_tree", "h2_btree_export", "h2_btree_destroy",
     "h2_from_sparse", "h2_lowrank_update", "h2_matvec", "h2_addmul", "h2_lr_factor", "h2_solve",
     "h2_ranks", "h2_storage_report", "h2_export", "h2_check_device_flags",
@@ -36,6 +36,8 @@ _p = C.c_void_p
 _i32, _i64, _f64 = C.c_int32, C.c_int64, C.c_double
 _sig = {
     "h2_cluster_tree": [_p, _i64, _i32, _i32, C.POINTER(_p)],
+    "h2_cluster_tree_dd": [_p, _i64, _i32, _i32, _p, _p, C.POINTER(_p)],
+    "h2_tree_ddpair": [_p, _p],
     "h2_tree_export": [_p, _p, _p, _p, _p, _p, _p, _p],
     "h2_tree_destroy": [_p],
     "h2_block_tree": [_p, _p, _f64, C.POINTER(_p)],
@@ -134,6 +136,8 @@ class Tree:
         self.lo, self.hi, self.son0, self.son1, self.level = (np.empty(self.nclusters, dtype=np.int32) for _ in range(5))
         _check(_lib.h2_tree_export(self.h, _ptr(self.perm), _ptr(self.lo), _ptr(self.hi), _ptr(self.son0),
                                    _ptr(self.son1), _ptr(self.level), C.byref(nc)))
+        self.ddpair = np.zeros(self.nclusters, dtype=np.int8)
+        _check(_lib.h2_tree_ddpair(self.h, _ptr(self.ddpair)))
 
     def size(self, t):
         return int(self.hi[t] - self.lo[t])
@@ -181,6 +185,21 @@ def h2_cluster_tree(points: np.ndarray, leaf_size: int) -> Tree:
         pts = pts[:, None]
     h = _p()
     _check(_lib.h2_cluster_tree(_ptr(pts), pts.shape[0], pts.shape[1], int(leaf_size), C.byref(h)))
+    return Tree(h.value, pts.shape[0])
+
+
+def h2_cluster_tree_dd(points: np.ndarray, leaf_size: int, A) -> Tree:
+    """Domain-decomposition cluster tree (NEXT-3); A: scipy.sparse matrix whose
+    pattern is the coupling graph (ORIGINAL order)."""
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    if pts.ndim == 1:
+        pts = pts[:, None]
+    A = A.tocsr()
+    rowptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
+    col = np.ascontiguousarray(A.indices, dtype=np.int32)
+    h = _p()
+    _check(_lib.h2_cluster_tree_dd(_ptr(pts), pts.shape[0], pts.shape[1], int(leaf_size), _ptr(rowptr), _ptr(col),
+                                   C.byref(h)))
     return Tree(h.value, pts.shape[0])
 
 

@@ -7,17 +7,18 @@ from oracle.structure import ClusterTree, BlockTree, ADM
 from oracle.h2 import from_sparse as o_from_sparse
 
 
-def setup(name, N=None, lower=False, rank_cap=32, update_cap=32, gpu=True, eta=None):
+def setup(name, N=None, lower=False, rank_cap=32, update_cap=32, gpu=True, eta=None, dd=False):
+    """dd: domain-decomposition cluster tree (NEXT-3) instead of geometric bisection."""
     c = config(name, N=N)
     if eta is not None:
         c["eta"] = eta
-    ot = ClusterTree(c["points"], c["leaf"])
+    ot = ClusterTree(c["points"], c["leaf"], adjacency=c["A"] if dd else None)
     ob = BlockTree(ot, ot, c["eta"])
     OZ = o_from_sparse(ob, c["A"], lower=lower)
     out = dict(c=c, ot=ot, ob=ob, OZ=OZ)
     if gpu:
         import paper_1402_5056_b200 as P
-        t = P.h2_cluster_tree(c["points"], c["leaf"])
+        t = P.h2_cluster_tree_dd(c["points"], c["leaf"], c["A"]) if dd else P.h2_cluster_tree(c["points"], c["leaf"])
         bt = P.h2_block_tree(t, t, c["eta"])
         Z = P.h2_from_sparse(bt, c["A"], lower=lower, rank_cap=rank_cap, update_cap=update_cap)
         out.update(t=t, bt=bt, Z=Z)

@@ -53,6 +53,41 @@ def test_structure_irregular_points_bit_exact():
         np.testing.assert_array_equal(bt.t, ob.t)
 
 
+@pytest.mark.parametrize("name,N", [("C1", 63), ("C2", 96), ("C3", 10)])
+def test_dd_structure_bit_exact_vs_oracle(name, N):
+    """Domain-decomposition cluster tree (NEXT-3, reading own-11) and its block tree."""
+    c = config(name, N=N)
+    t = P.h2_cluster_tree_dd(c["points"], c["leaf"], c["A"])
+    bt = P.h2_block_tree(t, t, c["eta"])
+    ot = ClusterTree(c["points"], c["leaf"], adjacency=c["A"])
+    ob = BlockTree(ot, ot, c["eta"])
+    np.testing.assert_array_equal(t.perm, ot.perm)
+    for a, b in ((t.lo, ot.lo), (t.hi, ot.hi), (t.son0, ot.son0), (t.son1, ot.son1), (t.level, ot.level),
+                 (t.ddpair, ot.ddpair)):
+        np.testing.assert_array_equal(a, b)
+    assert t.ddpair.sum() > 0
+    np.testing.assert_array_equal(bt.t, ob.t)
+    np.testing.assert_array_equal(bt.s, ob.s)
+    np.testing.assert_array_equal(bt.kind, ob.kind)
+
+
+def test_dd_structure_irregular_graph_bit_exact():
+    import scipy.sparse as sp
+    rng = np.random.default_rng(5)
+    pts = rng.integers(0, 80, size=(900, 2)).astype(float)
+    d2 = ((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1)
+    nb = np.argsort(d2, axis=1, kind="stable")[:, :4]
+    A = sp.csr_matrix((np.ones(nb.size), (np.repeat(np.arange(900), 4), nb.ravel())), shape=(900, 900))
+    t = P.h2_cluster_tree_dd(pts, 12, A)
+    ot = ClusterTree(pts, 12, adjacency=A)
+    np.testing.assert_array_equal(t.perm, ot.perm)
+    np.testing.assert_array_equal(t.ddpair, ot.ddpair)
+    bt = P.h2_block_tree(t, t, 1.5)
+    ob = BlockTree(ot, ot, 1.5)
+    np.testing.assert_array_equal(bt.kind, ob.kind)
+    np.testing.assert_array_equal(bt.t, ob.t)
+
+
 def test_argument_errors():
     with pytest.raises(P.H2Error) as e:
         P.h2_cluster_tree(np.zeros((0, 2)), 4)

@@ -103,6 +103,39 @@ def test_cholesky_blockwise_parity(name, N, eps, eta):
     assert d <= 10 * eps and rel < 1e-8 and abs(m_g - m_o) <= 1
 
 
+@pytest.mark.parametrize("name,N,eps,bw,eta", [("C2", 64, 1e-4, False, None), ("C2", 128, 1e-4, False, None),
+                                                ("C1", 127, 3.1e-3, True, 4.0), ("C3", 12, 1e-4, False, None),
+                                                ("C2", 256, 1e-4, False, None)])
+def test_cholesky_parity_dd_tree(name, N, eps, bw, eta):
+    """NEXT-3 (reading own-11): the H^2 Cholesky on the domain-decomposition cluster
+    tree (nested dissection order, unbalanced tree, leaves of unequal size, decoupled domain
+    blocks of rank zero): structure and ranks bit-exact, update counts equal, operator <= 10 eps,
+    solves, PCG iterations +-1.  The C1 case is the paper's Table-1 setting (l = 7: eta = 4,
+    block-relative eps^ = 3.1e-3)."""
+    s = setup(name, N, lower=True, eta=eta, dd=True)
+    OZ, Z, A, ot = s["OZ"], s["Z"], s["c"]["A"], s["ot"]
+    np.testing.assert_array_equal(s["t"].perm, ot.perm)
+    np.testing.assert_array_equal(s["bt"].kind, s["ob"].kind)
+    assert operator_rel_diff(Z, OZ, ot.n) <= 1e-13  # the rank-0 form on the unbalanced tree (matvec)
+    ar = Arith(OZ, OTrunc(eps, blockwise=bw))
+    ar.chol()
+    P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps, blockwise=bw))
+    assert P.h2_check_device_flags(Z) == 0
+    _ranks_equal(Z, OZ)
+    assert P.h2_stats(Z)["updates_nonzero"] == ar.stats["updates"]
+    d = operator_rel_diff(Z, OZ, ot.n)
+    b = stream(RHS).standard_normal(ot.n)
+    xs_g, xs_o = _gpu_solve(Z, b), ar.solve(b)
+    assert np.linalg.norm(xs_g - xs_o) / np.linalg.norm(xs_o) <= 10 * eps
+    _, m_o, _ = pcg(lambda v: A @ v, lambda v: ar.solve(v), b)
+    xg = _t(np.zeros(ot.n))
+    Aop = P.h2_from_sparse(s["bt"], A)
+    _, m_g, rel = P.h2_pcg(Aop, Z, _t(b), xg, tol=1e-8)
+    print(f"{name} N={N} DD tree: rel diff {d:.2e}, updates {ar.stats['updates']}, max rank {OZ.k.max()}, "
+          f"m gpu {m_g} oracle {m_o}, depth {ot.depth}")
+    assert d <= 10 * eps and rel < 1e-8 and abs(m_g - m_o) <= 1
+
+
 def test_lr_parity_c0_rank8():
     """C0 protocol (R15): rank-8 update with alpha = 1/n on every admissible leaf, then LR."""
     eps = 1e-4
