@@ -420,8 +420,11 @@ def main():
         "e2e": res["e2e"],
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
-        "executor_ops": {k: {"ops": v["launches"], "ms": round(v["ms"], 2)} for k, v in prof.items()
-                         if k not in ("k_matvec", "k_solve_sweep")},
+        # per op kind of the profiled warm-up step: op count, device time, counted FP64 flops and the
+        # rate they give (the ops are latency-bound: see DESIGN §4/§6)
+        "executor_ops": {k: {"ops": v["launches"], "ms": round(v["ms"], 2), "gflop": round(v["flops"] / 1e9, 3),
+                             "gflops_per_s": round(v["flops"] / max(v["ms"], 1e-9) / 1e6, 2)}
+                         for k, v in prof.items() if k not in ("k_matvec", "k_solve_sweep")},
         "kernels": {k: {"launches": v["launches"], "ms": round(v["ms"], 2)} for k, v in prof.items()
                     if k in ("k_matvec", "k_solve_sweep")},
     }

@@ -723,10 +723,10 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   static const bool walk_path = getenv("H2_MV_WALK") && atoi(getenv("H2_MV_WALK")) != 0;  // round-1 path (A/B)
   // timing diagnostics (tools): H2_MV_PART=1 far field only, 2 nearfield only (y is then incomplete)
   static const int part = getenv("H2_MV_PART") ? atoi(getenv("H2_MV_PART")) : 0;
-  if (part == 1) {
+  if (part == 1 || part == 3 || part == 4) {  // 3: forward only, 4: forward + couplings
     H2_LAUNCH(K_MV, st, k_mv_fwd_sub<<<src.n_mv_roots, SUBT, 0, st>>>(a));
-    H2_LAUNCH(K_MV, st, k_mv_couple_top<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
-    H2_LAUNCH(K_MV, st, k_mv_bwd_sub<<<dst.n_mv_roots, SUBT, 0, st>>>(a));
+    if (part != 3) H2_LAUNCH(K_MV, st, k_mv_couple_top<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
+    if (part == 1) H2_LAUNCH(K_MV, st, k_mv_bwd_sub<<<dst.n_mv_roots, SUBT, 0, st>>>(a));
     return cudaGetLastError();
   }
   if (part == 2) {

@@ -9,5 +9,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 ncu --set full --clock-control none --import-source on -k "regex:k_m(atvec|v_)" -s 24 -c 8 -o gpurun_out/prof_matvec \
     python tools/time_matvec.py 512 factor > gpurun_out/ncu_mv.log 2>&1
 # full capture of one executor launch inside the C2 factorization (traffic)
-ncu --set full --clock-control none --import-source on -k regex:k_exec_cluster -s 200 -c 1 -o gpurun_out/prof_exec \
+ncu --set full --clock-control none --import-source on -k regex:k_exec_cluster -s 10 -c 1 -o gpurun_out/prof_exec \
     python tools/time_factor.py 512 > gpurun_out/ncu_exec.log 2>&1
