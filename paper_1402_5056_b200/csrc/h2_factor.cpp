@@ -716,6 +716,10 @@ h2_status run_driver(h2_mat_* Z, const h2_trunc* trunc, h2_stream stream, int wh
     return H2_ERR_ARG;
   }
   const h2_trunc tc = trunc ? *trunc : h2_trunc{1e-4, 0.0, 0, 0};
+  if (what != 3 && what != 4) {  // everything but the solves changes the target (packed matvec copies)
+    Z->version++;
+    if (what == 5 && X) X->version++;
+  }
   Arena ar;
   h2_status s;
   if ((s = ensure_ws(Z, ar)) != H2_OK) return s;

@@ -371,6 +371,7 @@ static cudaError_t dupload(h2_mat_* Z, T** p, const std::vector<T>& v) {
 
 static void free_mat(h2_mat_* Z) {
   if (!Z) return;
+  h2::free_mvpack(Z);
   for (void* p : Z->allocs) cudaFree(p);
   delete Z;
 }
@@ -611,6 +612,7 @@ extern "C" h2_status h2_from_sparse(h2_btree bt, int64_t n, const int64_t* rowpt
   TRY_ALLOC(cudaMemset(M.S, 0, sizeof(double) * (size_t)M.nadm * M.rcap * M.rcap));
   TRY_ALLOC(dalloc(Z, &M.flags, 4));
   TRY_ALLOC(cudaMemset(M.flags, 0, 4 * sizeof(int32_t)));
+  if (getenv("H2_UPD_LOG")) TRY_ALLOC(dalloc(Z, &M.updlog, (size_t)3 << 21));
   TRY_ALLOC(dalloc(Z, &M.xt, n));
   TRY_ALLOC(dalloc(Z, &M.yt, n));
 #undef TRY_ALLOC
@@ -680,6 +682,7 @@ extern "C" h2_status h2_lowrank_update(h2_mat Z, int32_t t0, int32_t s0, int32_t
   } catch (const std::exception& ex) {  // recording errors (e.g. too many matrices in one batch)
     H2_FAIL(H2_ERR_ARG, std::string("h2_lowrank_update: ") + ex.what());
   }
+  Z->version++;
   if (B->kind[b0] != INADM) {  // the update may give the bases of T_{t0} / T_{s0} a non-zero rank
     for (int q = t0; q < t0 + B->rt->tsize[t0]; ++q) Z->nzr[q] = 1;
     for (int q = s0; q < s0 + B->ct->tsize[s0]; ++q) Z->nzc[q] = 1;
@@ -708,6 +711,17 @@ extern "C" h2_status h2_check_device_flags(h2_mat Z, int32_t* flags) {
   int32_t f[3];
   CUDA_TRY(cudaMemcpy(f, Z->d.flags, sizeof(f), cudaMemcpyDeviceToHost));
   CUDA_TRY(cudaMemset(Z->d.flags, 0, 3 * sizeof(int32_t)));  // flags[3] (update counter) is kept
+  if (Z->d.updlog && getenv("H2_UPD_LOG")) {  // diagnostic: the non-zero-rank updates in order, as text
+    int32_t cnt = 0;
+    CUDA_TRY(cudaMemcpy(&cnt, Z->d.flags + 3, sizeof(cnt), cudaMemcpyDeviceToHost));
+    cnt = std::min(cnt, 1 << 21);
+    std::vector<int32_t> lg((size_t)3 * cnt);
+    CUDA_TRY(cudaMemcpy(lg.data(), Z->d.updlog, sizeof(int32_t) * lg.size(), cudaMemcpyDeviceToHost));
+    if (FILE* f = fopen(getenv("H2_UPD_LOG"), "w")) {
+      for (int i = 0; i < cnt; ++i) fprintf(f, "%d %d %d\n", lg[3 * i], lg[3 * i + 1], lg[3 * i + 2]);
+      fclose(f);
+    }
+  }
   flags[0] = f[0] | (f[1] ? 2 : 0);
   if (f[1]) {
     char msg[160];

@@ -120,6 +120,7 @@ struct MatDev {
   int32_t *nptr = nullptr, *nidx = nullptr;    // inadmissible stored blocks per row leaf (CSR)
   int32_t *ntptr = nullptr, *ntidx = nullptr;  // inadmissible stored blocks per column leaf (CSR)
   int32_t* flags = nullptr;
+  int32_t* updlog = nullptr;  // diagnostic (H2_UPD_LOG): (t0, s0, k) of every non-zero-rank local update
   double *xt = nullptr, *yt = nullptr;  // tree-order vectors
 };
 
@@ -135,8 +136,21 @@ struct SolveSched {
   int32_t *push_ptr = nullptr, *push_slot = nullptr, *push_dst = nullptr;  // per source cluster
 };
 
+// Packed copies of the couplings and transfer matrices at the current ranks for the matvec
+// (h2_matvec.cu: ensure_packed), valid while version == h2_mat_::version.
+struct MvPack {
+  double* Sp = nullptr;
+  int64_t* Soff = nullptr;                 // nadm + 1
+  double* Tp[2] = {nullptr, nullptr};      // row / column side transfers
+  int64_t* Toff[2] = {nullptr, nullptr};   // nclusters + 1
+  size_t capS = 0, capT[2] = {0, 0};
+  long long version = -1;
+};
+
 struct h2_mat_ {
   h2_btree_* bt = nullptr;
+  long long version = 0;  // bumped by every call that changes ranks, bases or couplings
+  MvPack mvpack;
   bool lower = false;
   h2::MatDev d;
   std::vector<int32_t> adm_blk, inad_blk;  // slot -> block id (DFS order)
@@ -163,6 +177,7 @@ void poison(void* p, size_t bytes);
 bool batch_open();
 
 // launchers (h2_matvec.cu)
+void free_mvpack(h2_mat_* Z);
 cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const double* x, double beta,
                           double* y, cudaStream_t st);
 // sequential block substitution (h2_solve.cu): x (original order, n x nrhs, ld ldx) <- F^{-1} x

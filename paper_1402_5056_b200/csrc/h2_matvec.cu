@@ -5,19 +5,12 @@
 //   backward transform  yhat_{t'} += E_{t'} yhat_t  top-down; leaves y|t = V_t yhat_t
 //   nearfield           y|t += sum_{b=(t,s) inadmissible} N_b x|s
 //
-// Four launches on two streams (nearfield || forward transform + couplings, then the walk), no
-// grid-wide barrier, no spin-waits; a matrix whose bases all have rank 0 launches the nearfield only:
-//   k_matvec_near  warp per destination leaf: y|t = alpha sum_b N_b x|s + beta y|t (streams the
-//                  tiles, the bulk of the bytes) -- on a second stream, concurrently with:
-//   k_matvec_fwd   warp per source leaf: forward transform, then climb: the second of two siblings
-//                  to finish (arrival counter) computes the father, up to the root.  No waits.
-//   k_matvec_couple  warp per destination cluster: yc_t = sum_b S_b xhat_s.
-//   k_matvec_walk    warp per destination leaf: yhat along its ancestor path, root first
-//                    (yhat_c = yc_c + E_c yhat_father), then y|t += alpha V_t yhat_t; the path
-//                    prefix shared by a block's 8 leaves is walked once (shared memory).  No
-//                    level-by-level chain of launches or flags.
-// The arrival counters are reset by their last user.  Bytes are dominated by the nearfield tiles
-// (SURVEY §8(d)): lanes own rows, a 32-column panel is 32 coalesced 256 B streaming loads in flight.
+// Two streams: the nearfield kernel (the bulk of the bytes: warp per destination leaf, lanes own
+// rows, 16-column panels of coalesced 256 B streaming loads) runs on a second, high-priority
+// stream concurrently with the far-field chain
+//   k_mv_leaf_fwd -> k_mv_fwd_sub -> k_mv_couple_top -> k_mv_bwd_sub -> [join] -> k_mv_leaf_bwd
+// described below; a matrix whose bases all have rank 0 launches the nearfield kernel only.
+// No grid-wide barrier, no spin-waits; the arrival counters are reset by their last user.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -54,7 +47,6 @@ struct MvArgs {
   const double* x;
   double* y;
   double alpha, beta;
-  int* sync;  // fused kernel: [0] forward done, [1] warps done with the couplings, [2] blocks exited
   // subtree schedule (DevSide::mv_*): source side (forward) and destination side (backward)
   const int32_t *s_roots, *s_top, *s_top_lptr, *s_tsize, *s_level;
   int s_top_nlev;
@@ -62,79 +54,14 @@ struct MvArgs {
   const int32_t *d_roots, *d_top, *d_top_lptr, *d_tsize, *d_level, *d_son1;
   int d_top_nlev;
   int32_t* d_cnt;
+  // packed copies at the current ranks (MvPack): couplings (slot -> offset), transfers per side
+  const double* Sp;
+  const int64_t* Soff;
+  const double *s_Tp, *d_Tp;
+  const int64_t *s_Toff, *d_Toff;
 };
 
 constexpr unsigned FULL = 0xffffffffu;
-
-// ---- forward transform of one source leaf, then the climb ---------------------------------------
-__device__ void mv_up(const MvArgs& a, int s, int lane) {
-  const int rcap = a.rcap, lmax = a.lmax;
-  {
-    const int lo = a.s_lo[s], m = a.s_hi[s] - lo, k = a.s_rank[s];
-    if (k > 0) {
-      const double x0 = lane < m ? a.x[a.s_perm[lo + lane]] : 0.0;
-      const double x1 = lane + 32 < m ? a.x[a.s_perm[lo + lane + 32]] : 0.0;
-      const double* W = a.s_leafb + (size_t)a.s_leafidx[s] * lmax * rcap;
-      double mine0 = 0.0, mine1 = 0.0;
-      for (int j = 0; j < k; ++j) {
-        double p = 0.0;
-        if (lane < m) p = W[lane + (size_t)j * lmax] * x0;
-        if (lane + 32 < m) p += W[lane + 32 + (size_t)j * lmax] * x1;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(FULL, p, o);
-        if (lane == (j & 31)) {
-          if (j < 32) mine0 = p;
-          else mine1 = p;
-        }
-      }
-      if (lane < k) a.s_xh[(size_t)s * rcap + lane] = mine0;
-      if (lane + 32 < k) a.s_xh[(size_t)s * rcap + lane + 32] = mine1;
-    }
-  }
-  for (;;) {
-    const int p = a.s_parent[s];
-    if (p < 0) {  // s is the root: every forward coefficient is final (fused kernel: release them)
-      if (a.sync) {
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicExch(a.sync, 1);
-      }
-      return;
-    }
-    // the father's structure and transfer matrices are static: fetch them (ranks into registers,
-    // the F columns of this lane into L1) before the arrival handshake, so the climb step after it
-    // waits only for the sibling's coefficients
-    const int kp = a.s_rank[p];
-    const int sc0 = a.s_son0[p], sc1 = a.s_son1[p];
-    const int sk0 = a.s_rank[sc0], sk1 = a.s_rank[sc1];
-    for (int j = lane; j < kp; j += 32)
-      for (int q = 0; q < 2; ++q) {
-        const double* F = a.s_tr + (size_t)(q ? sc1 : sc0) * rcap * rcap + (size_t)j * rcap;
-        const int kc = q ? sk1 : sk0;
-        for (int i = 0; i < kc; i += 16) asm volatile("prefetch.global.L1 [%0];" ::"l"(F + i));
-      }
-    __threadfence();
-    __syncwarp();
-    int old = 0;
-    if (lane == 0) old = atomicAdd(a.s_arrive + p, 1);
-    old = __shfl_sync(FULL, old, 0);
-    if (old == 0) return;  // first of the two sons: the sibling finishes the father
-    if (lane == 0) a.s_arrive[p] = 0;
-    __threadfence();
-    for (int j = lane; j < kp; j += 32) {
-      double acc = 0.0;
-      for (int q = 0; q < 2; ++q) {
-        const int c = q ? sc1 : sc0;
-        const int kc = q ? sk1 : sk0;
-        const double* F = a.s_tr + (size_t)c * rcap * rcap;
-        const double* xc = a.s_xh + (size_t)c * rcap;
-        for (int i = 0; i < kc; ++i) acc += F[i + (size_t)j * rcap] * __ldcg(xc + i);
-      }
-      a.s_xh[(size_t)p * rcap + j] = acc;
-    }
-    s = p;
-  }
-}
 
 // ---- nearfield rows of a destination leaf: (a0, a1) += sum_b N_b x|s ----------------------------
 __device__ __forceinline__ void mv_near(const MvArgs& a, int t, int m, int lane, double& a0, double& a1) {
@@ -204,192 +131,42 @@ __device__ void mv_leaf_near(const MvArgs& a, int t, int lane) {
   }
 }
 
-// ---- couplings of one destination cluster: yc_t = sum_{b in row(t)} S_b xhat_s --------------------
-// Lane = block: each lane forms the whole k_t-vector S_b xhat_s of one block of row(t) in
-// registers (all its loads independent: k_t x k_s of them in flight per lane, 32 blocks per warp),
-// then the warp sums the lanes with a fixed butterfly (deterministic).  KT = k_t rounded up to a
-// register-array bucket.
-template <int KT>
-__device__ __forceinline__ void mv_couple_kt(const MvArgs& a, int t, int kt, int i0, int lane) {
-  const int rcap = a.rcap;
-  double acc[KT];
-#pragma unroll
-  for (int i = 0; i < KT; ++i) acc[i] = 0.0;
-  const int qb = a.d_bptr[t], qe = a.d_bptr[t + 1];
-  for (int q = qb + lane; q - lane < qe; q += 32) {
-    if (q < qe) {
-      const int slot = a.d_bidx[q];
-      const int s = a.partner[slot];
-      const int ks = a.s_rank[s];
-      const double* Sa = a.S + (size_t)slot * rcap * rcap;
-      const double* xs = a.s_xh + (size_t)s * rcap;
-      if (!a.transpose) {  // rows i0.. of S_b: column j contiguous
-#pragma unroll 4
-        for (int j = 0; j < ks; ++j) {
-          const double xj = __ldcg(xs + j);
-          const double* Sj = Sa + (size_t)j * rcap + i0;
-#pragma unroll
-          for (int i = 0; i < KT; ++i)
-            if (i0 + i < kt) acc[i] = fma(Sj[i], xj, acc[i]);
-        }
-      } else {  // S_b^T: row i of S^T = column i of S, contiguous
-#pragma unroll
-        for (int i = 0; i < KT; ++i) {
-          if (i0 + i < kt) {
-            const double* Si = Sa + (size_t)(i0 + i) * rcap;
-            double v = 0.0;
-#pragma unroll 4
-            for (int j = 0; j < ks; ++j) v = fma(Si[j], __ldcg(xs + j), v);
-            acc[i] += v;
-          }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < KT; ++i) {
-    if (i0 + i < kt) {
-      double v = acc[i];
-#pragma unroll
-      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-      if (lane == i) a.d_xh[(size_t)t * rcap + i0 + i] = v;
-    }
-  }
-}
-
-__device__ void mv_couple(const MvArgs& a, int t, int lane) {
-  const int kt = a.d_rank[t];
-  if (kt == 0) return;
-  if (kt <= 8) mv_couple_kt<8>(a, t, kt, 0, lane);
-  else if (kt <= 16) mv_couple_kt<16>(a, t, kt, 0, lane);
-  else {
-    for (int i0 = 0; i0 < kt; i0 += 32) mv_couple_kt<32>(a, t, kt, i0, lane);
-  }
-}
-
-// ---- backward transform along the path root -> leaf t, then y|t += alpha V_t yhat_t ---------------
-// yhat_c = yc_c + E_c yhat_{father(c)} level by level along the leaf's ancestor row (lane L holds the
-// cluster of level L).  The 8 leaves of a block are consecutive in DFS order, so their paths share
-// a prefix (the common ancestors of the first and the last leaf): warp 0 walks it once and leaves
-// yhat of the deepest common ancestor in shared memory, then every warp walks its own remainder.
-// No cross-block synchronisation.
-__device__ __forceinline__ void walk_levels(const MvArgs& a, int c0, int c1, int k0, int k1, int Lb, int Le,
-                                            int lane, double& y0, double& y1, int& kprev) {
-  const int rcap = a.rcap;
-  for (int L = Lb; L < Le; ++L) {
-    const int c = __shfl_sync(FULL, L < 32 ? c0 : c1, L & 31);
-    const int kc = __shfl_sync(FULL, L < 32 ? k0 : k1, L & 31);
-    const double* yc = a.d_xh + (size_t)c * rcap;
-    double n0 = lane < kc ? __ldcg(yc + lane) : 0.0;
-    double n1 = lane + 32 < kc ? __ldcg(yc + lane + 32) : 0.0;
-    if (kprev > 0 && kc > 0) {
-      const double* E = a.d_tr + (size_t)c * rcap * rcap;
-#pragma unroll 4
-      for (int j = 0; j < kprev; ++j) {
-        const double yj = __shfl_sync(FULL, j < 32 ? y0 : y1, j & 31);
-        if (lane < kc) n0 += E[lane + (size_t)j * rcap] * yj;
-        if (lane + 32 < kc) n1 += E[lane + 32 + (size_t)j * rcap] * yj;
-      }
-    }
-    y0 = n0;
-    y1 = n1;
-    kprev = kc;
-  }
-}
-
-__device__ void mv_walk(const MvArgs& a, int lane, int group) {
-  __shared__ double ysh[64];
-  __shared__ int sh[2];  // common prefix length, rank at its end
-  const int rcap = a.rcap, lmax = a.lmax, aw = a.d_ancw;
-  const int warp = threadIdx.x >> 5;
-  const int lf = group * 8, ll = min(lf + 8, a.d_nleaves) - 1;  // first / last leaf ordinal
-  if (warp == 0) {
-    const int32_t* pf = a.d_anc + (size_t)lf * aw;
-    const int32_t* pl = a.d_anc + (size_t)ll * aw;
-    const int f0 = lane < aw ? pf[lane] : -2, f1 = lane + 32 < aw ? pf[lane + 32] : -2;
-    const int l0 = lane < aw ? pl[lane] : -3, l1 = lane + 32 < aw ? pl[lane + 32] : -3;
-    const unsigned d0 = __ballot_sync(FULL, f0 != l0 || f0 < 0), d1 = __ballot_sync(FULL, f1 != l1 || f1 < 0);
-    const int Lc = d0 ? __ffs(d0) - 1 : (d1 ? 32 + __ffs(d1) - 1 : 64);  // first differing level
-    const int k0 = f0 >= 0 ? a.d_rank[f0] : 0, k1 = f1 >= 0 ? a.d_rank[f1] : 0;
-    double y0 = 0.0, y1 = 0.0;
-    int kprev = 0;
-    walk_levels(a, f0, f1, k0, k1, 0, Lc, lane, y0, y1, kprev);
-    if (lane < kprev) ysh[lane] = y0;
-    if (lane + 32 < kprev) ysh[lane + 32] = y1;
-    if (lane == 0) {
-      sh[0] = Lc;
-      sh[1] = kprev;
-    }
-  }
-  __syncthreads();
-  const int li = lf + warp;
-  if (li >= a.d_nleaves) return;
-  const int Lc = sh[0];
-  int kprev = sh[1];
-  double y0 = lane < kprev ? ysh[lane] : 0.0, y1 = lane + 32 < kprev ? ysh[lane + 32] : 0.0;
-  const int32_t* path = a.d_anc + (size_t)li * aw;
-  const int c0 = lane < aw ? path[lane] : -1;
-  const int c1 = lane + 32 < aw ? path[lane + 32] : -1;
-  const int nl = __popc(__ballot_sync(FULL, c0 >= 0)) + __popc(__ballot_sync(FULL, c1 >= 0));  // path length
-  const int k0 = c0 >= 0 ? a.d_rank[c0] : 0, k1 = c1 >= 0 ? a.d_rank[c1] : 0;
-  walk_levels(a, c0, c1, k0, k1, Lc, nl, lane, y0, y1, kprev);
-  const int t = __shfl_sync(FULL, (nl - 1) < 32 ? c0 : c1, (nl - 1) & 31);
-  const int kt = kprev;
-  if (kt == 0) return;
-  const int lo = a.d_lo[t], m = a.d_hi[t] - lo;
-  const double* V = a.d_leafb + (size_t)a.d_leafidx[t] * lmax * rcap;
-  double a0 = 0.0, a1 = 0.0;
-  for (int j = 0; j < kt; ++j) {
-    const double yj = __shfl_sync(FULL, j < 32 ? y0 : y1, j & 31);
-    if (lane < m) a0 += V[lane + (size_t)j * lmax] * yj;
-    if (lane + 32 < m) a1 += V[lane + 32 + (size_t)j * lmax] * yj;
-  }
-  // y was written by another warp (nearfield phase, maybe on another SM in the fused kernel): read
-  // it through L2, never from a possibly stale L1 line
-  if (lane < m) {
-    double* yo = a.y + a.d_perm[lo + lane];
-    *yo = __ldcg(yo) + a.alpha * a0;
-  }
-  if (lane + 32 < m) {
-    double* yo = a.y + a.d_perm[lo + lane + 32];
-    *yo = __ldcg(yo) + a.alpha * a1;
-  }
-}
-
 __global__ void __launch_bounds__(256, 4) k_matvec_near(const __grid_constant__ MvArgs a) {
-  const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
-  if (w < a.d_nleaves) mv_leaf_near(a, a.d_leaves[w], threadIdx.x & 31);
+  // grid-stride over the destination leaves: with the far field present the grid is 2 CTAs per SM,
+  // which leaves half of every SM to the far-field chain running concurrently
+  const int nw = (int)(gridDim.x * (blockDim.x >> 5));
+  for (int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w < a.d_nleaves; w += nw)
+    mv_leaf_near(a, a.d_leaves[w], threadIdx.x & 31);
 }
 
-__global__ void __launch_bounds__(256) k_matvec_fwd(const __grid_constant__ MvArgs a) {
-  const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
-  if (w < a.s_nleaves) mv_up(a, a.s_leaves[w], threadIdx.x & 31);
-}
 
-__global__ void __launch_bounds__(256, 2) k_matvec_couple(const __grid_constant__ MvArgs a) {
-  const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
-  if (w < a.d_nclusters) mv_couple(a, w, threadIdx.x & 31);
-}
-
-__global__ void __launch_bounds__(256) k_matvec_walk(const __grid_constant__ MvArgs a) {
-  mv_walk(a, threadIdx.x & 31, blockIdx.x);
-}
-
-// ---- far field by subtrees (default path) ------------------------------------------------------
-// The forward transform runs one CTA (32 warps) per maximal subtree with <= 64 leaves: its levels
-// bottom-up with block barriers, no atomics; the last CTA to finish (arrival counter) computes the
-// clusters above the subtrees level by level.  The couplings run lane-per-block (above); the last
-// CTA of that launch carries the backward transform down through the top clusters; then one CTA
-// per subtree carries it down to its leaves and adds alpha V_t yhat_t to y.  So the latency chain
-// is ~2 x (64-leaf subtree depth + top depth) block-barrier levels instead of ~2 x 13 dependent
-// global round trips with atomics per level (climb, ancestor walks).
-constexpr int SUBT = 512;  // threads of a subtree CTA (16 warps; leaves room for nearfield CTAs on the SM)
+// ---- far field -----------------------------------------------------------------------------------
+// Packed copies (MvPack, built once per matrix version by k_mv_pack): the couplings S_b (k_t x k_s,
+// ld k_t) and the transfer matrices (k_c x k_parent, ld k_c) stored contiguously at their current
+// ranks, so the far-field kernels read exactly the algorithmic bytes in coalesced bursts instead
+// of k-long column pieces of rank_cap^2 slots.
+//
+//   k_mv_leaf_fwd    warp per source leaf: xhat_s = W_s^T x|s                    (wide: the leaf bases
+//                    are the bulk of the forward transform's bytes)
+//   k_mv_fwd_sub     one CTA per maximal subtree of <= 64 leaves: the subtree's xhat (a contiguous
+//                    range of cluster ids) and its packed transfer matrices are staged in shared
+//                    memory, the internal levels run bottom-up from shared memory with block
+//                    barriers; the last CTA to finish computes the clusters above the subtrees
+//   k_mv_couple_top  warp per destination cluster: yc_t = sum_b S_b xhat_s from the packed
+//                    couplings (lanes = (row, column group), fixed reduction order); the last CTA
+//                    carries yhat down through the clusters above the subtrees
+//   k_mv_bwd_sub     one CTA per destination subtree: yhat top-down in shared memory
+//   k_mv_leaf_bwd    warp per destination leaf: y|t += alpha V_t yhat_t         (wide, after the
+//                    nearfield kernel on the second stream has written y)
+constexpr int SUBT = 512;        // threads of a subtree CTA
+constexpr int SUB_NC = 2 * MV_SUB_LEAVES;  // clusters of a subtree (<= 2 * 64 - 1)
+constexpr int SUB_TB = 12288;    // doubles of staged transfer matrices per subtree CTA (96 KB)
 
 struct SubList {  // the clusters of one subtree bucketed by level below its root
   int nlev;
   int cnt[64];
   int ptr[65];
-  int cl[2 * MV_SUB_LEAVES];
+  int cl[SUB_NC];
 };
 
 __device__ void build_sublist(const int32_t* level, const int32_t* tsize, int root, SubList& L) {
@@ -417,78 +194,140 @@ __device__ void build_sublist(const int32_t* level, const int32_t* tsize, int ro
   __syncthreads();
 }
 
-// xhat_s for one source cluster by one warp: a leaf from x, an internal cluster from its sons
-__device__ __forceinline__ void fwd_cluster(const MvArgs& a, int s, int lane) {
+// xhat_s = W_s^T x|s for one source leaf by one warp
+__device__ __forceinline__ void fwd_leaf(const MvArgs& a, int s, int lane) {
   const int rcap = a.rcap, lmax = a.lmax;
   const int k = a.s_rank[s];
   if (k == 0) return;
-  if (a.s_son0[s] < 0) {
-    const int lo = a.s_lo[s], m = a.s_hi[s] - lo;
-    const double x0 = lane < m ? a.x[a.s_perm[lo + lane]] : 0.0;
-    const double x1 = lane + 32 < m ? a.x[a.s_perm[lo + lane + 32]] : 0.0;
-    const double* W = a.s_leafb + (size_t)a.s_leafidx[s] * lmax * rcap;
-    double mine0 = 0.0, mine1 = 0.0;
-    for (int j = 0; j < k; ++j) {
-      double p = 0.0;
-      if (lane < m) p = W[lane + (size_t)j * lmax] * x0;
-      if (lane + 32 < m) p += W[lane + 32 + (size_t)j * lmax] * x1;
+  const int lo = a.s_lo[s], m = a.s_hi[s] - lo;
+  const double x0 = lane < m ? a.x[a.s_perm[lo + lane]] : 0.0;
+  const double x1 = lane + 32 < m ? a.x[a.s_perm[lo + lane + 32]] : 0.0;
+  const double* W = a.s_leafb + (size_t)a.s_leafidx[s] * lmax * rcap;
+  double mine0 = 0.0, mine1 = 0.0;
+  for (int j0 = 0; j0 < k; j0 += 4) {  // 4 columns per round: their loads and butterflies overlap
+    double p[4];
 #pragma unroll
-      for (int o = 16; o; o >>= 1) p += __shfl_xor_sync(FULL, p, o);
-      if (lane == (j & 31)) {
-        if (j < 32) mine0 = p;
-        else mine1 = p;
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u;
+      p[u] = 0.0;
+      if (j < k) {
+        if (lane < m) p[u] = W[lane + (size_t)j * lmax] * x0;
+        if (lane + 32 < m) p[u] += W[lane + 32 + (size_t)j * lmax] * x1;
       }
     }
-    if (lane < k) a.s_xh[(size_t)s * rcap + lane] = mine0;
-    if (lane + 32 < k) a.s_xh[(size_t)s * rcap + lane + 32] = mine1;
-    return;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) p[u] += __shfl_xor_sync(FULL, p[u], o);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u;
+      if (j < k && lane == (j & 31)) {
+        if (j < 32) mine0 = p[u];
+        else mine1 = p[u];
+      }
+    }
   }
+  if (lane < k) a.s_xh[(size_t)s * rcap + lane] = mine0;
+  if (lane + 32 < k) a.s_xh[(size_t)s * rcap + lane + 32] = mine1;
+}
+
+// xhat_s = sum over the sons c of F_c^T xhat_c (F_c: k_c x k_s, packed, ld k_c) by one warp.
+// xs(c): the sons' coefficients (shared memory inside a subtree, global above); tp: packed
+// transfers (shared memory copy with offset base `tb`, or global with tb = 0)
+template <class XS>
+__device__ __forceinline__ void fwd_internal(const MvArgs& a, int s, int lane, XS xs, const double* tp, int64_t tb,
+                                             double* out) {
+  const int k = a.s_rank[s];
+  if (k == 0) return;
   const int sc0 = a.s_son0[s], sc1 = a.s_son1[s];
   const int sk0 = a.s_rank[sc0], sk1 = a.s_rank[sc1];
+  const double* F0 = tp + (a.s_Toff[sc0] - tb);
+  const double* F1 = tp + (a.s_Toff[sc1] - tb);
+  const double* x0 = xs(sc0);
+  const double* x1 = xs(sc1);
   for (int j = lane; j < k; j += 32) {
     double acc = 0.0;
-    for (int q = 0; q < 2; ++q) {
-      const int c = q ? sc1 : sc0;
-      const int kc = q ? sk1 : sk0;
-      const double* F = a.s_tr + (size_t)c * rcap * rcap;
-      const double* xc = a.s_xh + (size_t)c * rcap;
-      for (int i = 0; i < kc; ++i) acc += F[i + (size_t)j * rcap] * __ldcg(xc + i);
-    }
-    a.s_xh[(size_t)s * rcap + j] = acc;
+    for (int i = 0; i < sk0; ++i) acc += F0[i + (size_t)j * sk0] * x0[i];
+    for (int i = 0; i < sk1; ++i) acc += F1[i + (size_t)j * sk1] * x1[i];
+    out[j] = acc;
   }
 }
 
-// yhat_c = yc_c + E_c yhat_{father(c)} in place (the father is final), one warp
-__device__ __forceinline__ void bwd_cluster(const MvArgs& a, int c, int lane) {
-  const int rcap = a.rcap;
+// yhat_c = yc_c + E_c yhat_father (E_c: k_c x k_p, packed, ld k_c), in place, one warp
+__device__ __forceinline__ void bwd_cluster(const MvArgs& a, int c, int lane, double* yc, const double* yp,
+                                            const double* tp, int64_t tb) {
   const int p = a.d_parent[c];
   const int kc = a.d_rank[c];
   if (p < 0 || kc == 0) return;
   const int kp = a.d_rank[p];
-  const double* E = a.d_tr + (size_t)c * rcap * rcap;
-  const double* yp = a.d_xh + (size_t)p * rcap;
-  double* yc = a.d_xh + (size_t)c * rcap;
-  double n0 = lane < kc ? __ldcg(yc + lane) : 0.0;
-  double n1 = lane + 32 < kc ? __ldcg(yc + lane + 32) : 0.0;
-  for (int j = 0; j < kp; ++j) {
-    const double yj = __ldcg(yp + j);
-    if (lane < kc) n0 += E[lane + (size_t)j * rcap] * yj;
-    if (lane + 32 < kc) n1 += E[lane + 32 + (size_t)j * rcap] * yj;
+  const double* E = tp + (a.d_Toff[c] - tb);
+  for (int i = lane; i < kc; i += 32) {
+    double v = yc[i];
+    for (int j = 0; j < kp; ++j) v += E[i + (size_t)j * kc] * yp[j];
+    yc[i] = v;
   }
-  if (lane < kc) yc[lane] = n0;
-  if (lane + 32 < kc) yc[lane + 32] = n1;
 }
 
-__global__ void __launch_bounds__(SUBT, 2) k_mv_fwd_sub(const __grid_constant__ MvArgs a) {
+__global__ void __launch_bounds__(256) k_mv_leaf_fwd(const __grid_constant__ MvArgs a) {
+  const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  if (w < a.s_nleaves) fwd_leaf(a, a.s_leaves[w], threadIdx.x & 31);
+}
+
+// stage the packed transfers of the clusters root+1 .. root+n-1 (contiguous) in shared memory
+__device__ __forceinline__ bool stage_transfers(const double* Tp, const int64_t* Toff, int root, int n, double* tbuf,
+                                                int64_t& tb) {
+  tb = Toff[root + 1 < root + n ? root + 1 : root];
+  const int64_t te = Toff[root + n];
+  const int64_t len = te - tb;
+  if (len > SUB_TB) return false;
+  for (int64_t e = threadIdx.x; e < len; e += blockDim.x) tbuf[e] = Tp[tb + e];
+  return true;
+}
+
+__global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ MvArgs a) {
+  extern __shared__ __align__(16) double dsm[];
   __shared__ SubList L;
   __shared__ int last;
+  const int rcap = a.rcap;
+  double* xs = dsm;                       // SUB_NC x rcap: xhat of the subtree's clusters
+  double* tbuf = dsm + (size_t)SUB_NC * rcap;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = SUBT / 32;
-  build_sublist(a.s_level, a.s_tsize, a.s_roots[blockIdx.x], L);
-  for (int l = L.nlev - 1; l >= 0; --l) {
-    for (int i = L.ptr[l] + warp; i < L.ptr[l + 1]; i += nw) fwd_cluster(a, L.cl[i], lane);
+  const int root = a.s_roots[blockIdx.x], n = a.s_tsize[root];
+  build_sublist(a.s_level, a.s_tsize, root, L);
+  if (n > 1) {
+    // the leaves' coefficients (k_mv_leaf_fwd) -- the subtree's xhat rows are contiguous in global
+    const double* xg = a.s_xh + (size_t)root * rcap;
+    for (int i = warp; i < n; i += nw) {
+      const int c = root + i;
+      if (a.s_son0[c] >= 0) continue;
+      const int k = a.s_rank[c];
+      for (int j = lane; j < k; j += 32) xs[(size_t)i * rcap + j] = __ldcg(xg + (size_t)i * rcap + j);
+    }
+    int64_t tb = 0;
+    const bool staged = stage_transfers(a.s_Tp, a.s_Toff, root, n, tbuf, tb);
     __syncthreads();
+    const double* tp = staged ? tbuf : a.s_Tp;
+    if (!staged) tb = 0;
+    auto xof = [&](int c) -> const double* { return xs + (size_t)(c - root) * rcap; };
+    for (int l = L.nlev - 2; l >= 0; --l) {
+      for (int i = L.ptr[l] + warp; i < L.ptr[l + 1]; i += nw) {
+        const int s = L.cl[i];
+        if (a.s_son0[s] >= 0) fwd_internal(a, s, lane, xof, tp, tb, xs + (size_t)(s - root) * rcap);
+      }
+      __syncthreads();
+    }
+    // publish the internal clusters' coefficients (the couplings read them from global)
+    for (int i = warp; i < n; i += nw) {
+      const int s = root + i;
+      if (a.s_son0[s] < 0) continue;
+      const int k = a.s_rank[s];
+      for (int j = lane; j < k; j += 32) a.s_xh[(size_t)s * rcap + j] = xs[(size_t)i * rcap + j];
+    }
   }
   // the last subtree to finish computes the clusters above the subtrees, bottom-up
+  __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     last = atomicAdd(a.s_cnt, 1) == (int)gridDim.x - 1;
@@ -496,19 +335,120 @@ __global__ void __launch_bounds__(SUBT, 2) k_mv_fwd_sub(const __grid_constant__ 
   __syncthreads();
   if (!last) return;
   __threadfence();
+  auto xg = [&](int c) -> const double* { return a.s_xh + (size_t)c * rcap; };
   for (int l = a.s_top_nlev - 1; l >= 0; --l) {
-    for (int i = a.s_top_lptr[l] + warp; i < a.s_top_lptr[l + 1]; i += nw) fwd_cluster(a, a.s_top[i], lane);
+    for (int i = a.s_top_lptr[l] + warp; i < a.s_top_lptr[l + 1]; i += nw) {
+      const int s = a.s_top[i];
+      // sons' coefficients through L2 (written by other CTAs / other warps of this one): one
+      // coalesced load per son, then broadcast by shuffles
+      const int k = a.s_rank[s];
+      if (k == 0) continue;
+      const int sc0 = a.s_son0[s], sc1 = a.s_son1[s];
+      const int sk0 = a.s_rank[sc0], sk1 = a.s_rank[sc1];
+      const double* F0 = a.s_Tp + a.s_Toff[sc0];
+      const double* F1 = a.s_Tp + a.s_Toff[sc1];
+      const double* x0 = xg(sc0);
+      const double* x1 = xg(sc1);
+      const double xa0 = lane < sk0 ? __ldcg(x0 + lane) : 0.0, xa1 = lane + 32 < sk0 ? __ldcg(x0 + lane + 32) : 0.0;
+      const double xb0 = lane < sk1 ? __ldcg(x1 + lane) : 0.0, xb1 = lane + 32 < sk1 ? __ldcg(x1 + lane + 32) : 0.0;
+      for (int j0 = 0; j0 < k; j0 += 32) {
+        const int j = j0 + lane;
+        double acc = 0.0;
+        for (int q = 0; q < sk0; ++q) {
+          const double xq = __shfl_sync(FULL, q < 32 ? xa0 : xa1, q & 31);
+          if (j < k) acc += F0[q + (size_t)j * sk0] * xq;
+        }
+        for (int q = 0; q < sk1; ++q) {
+          const double xq = __shfl_sync(FULL, q < 32 ? xb0 : xb1, q & 31);
+          if (j < k) acc += F1[q + (size_t)j * sk1] * xq;
+        }
+        if (j < k) a.s_xh[(size_t)s * rcap + j] = acc;
+      }
+    }
     __syncthreads();
   }
   if (threadIdx.x == 0) a.s_cnt[0] = 0;
 }
 
-// couplings (lane per block), then the last CTA carries yhat down through the top clusters
-__global__ void __launch_bounds__(256, 2) k_mv_couple_top(const __grid_constant__ MvArgs a) {
+// ---- couplings of one destination cluster from the packed S --------------------------------------
+// Descriptors of up to 32 blocks of row(t) are loaded at once (lane q: slot, offset, partner, its
+// rank), then the blocks are walked with shuffles, so the loads of consecutive blocks do not wait
+// for one another.  No transpose: lane = (row i, column group g), G = 32 / k_t groups share the
+// columns of a block; the groups are summed by a fixed sequence of shuffles.  Transpose: lane =
+// output column, each lane walks its contiguous column.
+template <bool TR>
+__device__ __forceinline__ void mv_couple_packed(const MvArgs& a, int t, int lane) {
+  const int rcap = a.rcap;
+  const int kt = a.d_rank[t];
+  if (kt == 0) return;
+  const int qb = a.d_bptr[t], qe = a.d_bptr[t + 1];
+  const int G = TR ? 1 : (kt >= 32 ? 1 : 32 / kt);
+  const int ig = TR ? lane : (kt >= 32 ? lane : lane % kt);
+  const int g = TR ? 0 : (kt >= 32 ? 0 : lane / kt);
+  const bool act = TR ? true : g < G;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int base = qb; base < qe; base += 32) {
+    const int cnt = qe - base < 32 ? qe - base : 32;
+    int d_s = 0, d_k = 0;
+    long long d_off = 0;
+    if (lane < cnt) {
+      const int slot = a.d_bidx[base + lane];
+      d_s = a.partner[slot];
+      d_k = a.s_rank[d_s];
+      d_off = a.Soff[slot];
+    }
+    for (int b = 0; b < cnt; ++b) {
+      const int s = __shfl_sync(FULL, d_s, b);
+      const int ks = __shfl_sync(FULL, d_k, b);
+      const long long off = __shfl_sync(FULL, d_off, b);
+      if (ks == 0) continue;
+      const double* Sa = a.Sp + off;
+      const double* xs = a.s_xh + (size_t)s * rcap;
+      if (!TR) {  // S_b: k_t x k_s, ld k_t; out[i] += sum_j S[i + j k_t] xhat_s[j]
+        if (act) {
+          for (int j = g; j < ks; j += G) {
+            const double xj = __ldcg(xs + j);
+            if (ig < kt) acc0 = fma(Sa[ig + (size_t)j * kt], xj, acc0);
+            if (ig + 32 < kt) acc1 = fma(Sa[ig + 32 + (size_t)j * kt], xj, acc1);
+          }
+        }
+      } else {    // S_b: k_s x k_t (rows = the partner's rank), ld k_s; out[j] += sum_i S[i + j k_s] xhat[i]
+        for (int q = 0; q < 2; ++q) {
+          const int j = lane + 32 * q;
+          if (j < kt) {
+            const double* Sj = Sa + (size_t)j * ks;
+            double v = 0.0;
+            for (int i = 0; i < ks; ++i) v = fma(Sj[i], __ldcg(xs + i), v);
+            if (q) acc1 += v;
+            else acc0 += v;
+          }
+        }
+      }
+    }
+  }
+  if (!TR && G > 1) {  // sum the column groups: lane i collects lanes i + g k_t, g = 1 .. G-1
+    double v = acc0;
+    for (int gg = 1; gg < G; ++gg) {
+      const double o = __shfl_sync(FULL, acc0, (ig + gg * kt) & 31);
+      if (g == 0) v += o;
+    }
+    acc0 = v;
+  }
+  if (g == 0 || TR) {
+    if (ig < kt) a.d_xh[(size_t)t * rcap + ig] = acc0;
+    if (ig + 32 < kt) a.d_xh[(size_t)t * rcap + ig + 32] = acc1;
+  }
+}
+
+// couplings, then the last CTA carries yhat down through the top clusters
+__global__ void __launch_bounds__(256, 4) k_mv_couple_top(const __grid_constant__ MvArgs a) {
   __shared__ int last;
   const int lane = threadIdx.x & 31;
   const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
-  if (w < a.d_nclusters) mv_couple(a, w, lane);
+  if (w < a.d_nclusters) {
+    if (a.transpose) mv_couple_packed<true>(a, w, lane);
+    else mv_couple_packed<false>(a, w, lane);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -517,94 +457,234 @@ __global__ void __launch_bounds__(256, 2) k_mv_couple_top(const __grid_constant_
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, rcap = a.rcap;
   for (int l = 1; l < a.d_top_nlev; ++l) {  // the root (level 0) keeps its coupling sum
-    for (int i = a.d_top_lptr[l] + warp; i < a.d_top_lptr[l + 1]; i += nw) bwd_cluster(a, a.d_top[i], lane);
+    for (int i = a.d_top_lptr[l] + warp; i < a.d_top_lptr[l + 1]; i += nw) {
+      const int c = a.d_top[i];
+      const int p = a.d_parent[c], kc = a.d_rank[c];
+      if (p < 0 || kc == 0) continue;
+      const int kp = a.d_rank[p];
+      const double* E = a.d_Tp + a.d_Toff[c];
+      const double* yp = a.d_xh + (size_t)p * rcap;
+      double* yc = a.d_xh + (size_t)c * rcap;
+      const double yp0 = lane < kp ? __ldcg(yp + lane) : 0.0, yp1 = lane + 32 < kp ? __ldcg(yp + lane + 32) : 0.0;
+      for (int r0 = 0; r0 < kc; r0 += 32) {
+        const int r = r0 + lane;
+        double v = r < kc ? __ldcg(yc + r) : 0.0;
+        for (int j = 0; j < kp; ++j) {
+          const double yj = __shfl_sync(FULL, j < 32 ? yp0 : yp1, j & 31);
+          if (r < kc) v += E[r + (size_t)j * kc] * yj;
+        }
+        if (r < kc) yc[r] = v;
+      }
+    }
     __syncthreads();
   }
   if (threadIdx.x == 0) a.d_cnt[0] = 0;
 }
 
-// backward transform inside one destination subtree (root first), then y|t += alpha V_t yhat_t
-__global__ void __launch_bounds__(SUBT, 2) k_mv_bwd_sub(const __grid_constant__ MvArgs a) {
+// backward transform inside one destination subtree (root first), in shared memory
+__global__ void __launch_bounds__(SUBT, 1) k_mv_bwd_sub(const __grid_constant__ MvArgs a) {
+  extern __shared__ __align__(16) double dsm[];
   __shared__ SubList L;
+  const int rcap = a.rcap;
+  double* ys = dsm;  // SUB_NC x rcap: yc / yhat of the subtree's clusters
+  double* tbuf = dsm + (size_t)SUB_NC * rcap;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = SUBT / 32;
-  build_sublist(a.d_level, a.d_tsize, a.d_roots[blockIdx.x], L);
-  for (int l = 0; l < L.nlev; ++l) {
-    for (int i = L.ptr[l] + warp; i < L.ptr[l + 1]; i += nw) bwd_cluster(a, L.cl[i], lane);
-    __syncthreads();
+  const int root = a.d_roots[blockIdx.x], n = a.d_tsize[root];
+  build_sublist(a.d_level, a.d_tsize, root, L);
+  double* yg = a.d_xh + (size_t)root * rcap;
+  for (int i = warp; i < n; i += nw) {
+    const int k = a.d_rank[root + i];
+    for (int j = lane; j < k; j += 32) ys[(size_t)i * rcap + j] = __ldcg(yg + (size_t)i * rcap + j);
   }
-  const int rcap = a.rcap, lmax = a.lmax;
-  for (int i = warp; i < L.ptr[L.nlev]; i += nw) {
-    const int t = L.cl[i];
-    if (a.d_son0[t] >= 0) continue;
-    const int kt = a.d_rank[t];
-    if (kt == 0) continue;
-    const int lo = a.d_lo[t], m = a.d_hi[t] - lo;
-    const double* V = a.d_leafb + (size_t)a.d_leafidx[t] * lmax * rcap;
-    const double* yh = a.d_xh + (size_t)t * rcap;
-    double a0 = 0.0, a1 = 0.0;
-    for (int j = 0; j < kt; ++j) {
-      const double yj = yh[j];
-      if (lane < m) a0 += V[lane + (size_t)j * lmax] * yj;
-      if (lane + 32 < m) a1 += V[lane + 32 + (size_t)j * lmax] * yj;
+  int64_t tb = 0;
+  const bool staged = n > 1 && stage_transfers(a.d_Tp, a.d_Toff, root, n, tbuf, tb);
+  __syncthreads();
+  const double* tp = staged ? tbuf : a.d_Tp;
+  if (!staged) tb = 0;
+  // the subtree's root: its father (if any) is a top cluster, final in global memory
+  if (warp == 0 && a.d_parent[root] >= 0) {
+    const int p = a.d_parent[root], kc = a.d_rank[root], kp = a.d_rank[p];
+    const double* E = a.d_Tp + a.d_Toff[root];
+    const double* yp = a.d_xh + (size_t)p * rcap;
+    for (int r = lane; r < kc; r += 32) {
+      double v = ys[r];
+      for (int j = 0; j < kp; ++j) v += E[r + (size_t)j * kc] * __ldcg(yp + j);
+      ys[r] = v;
     }
-    if (lane < m) {
-      double* yo = a.y + a.d_perm[lo + lane];
-      *yo = *yo + a.alpha * a0;
-    }
-    if (lane + 32 < m) {
-      double* yo = a.y + a.d_perm[lo + lane + 32];
-      *yo = *yo + a.alpha * a1;
-    }
-  }
-}
-
-// ---- the whole far + near field in ONE persistent (cooperative) launch --------------------------
-// Every warp: (A) forward transform of its source leaves with the climb (the warp completing the
-// root publishes sync[0]); (B) the nearfield of its destination leaves, y = alpha N x + beta y --
-// the bulk of the bytes streams while the climb's latency chain finishes elsewhere; (C) once the
-// forward coefficients are final, the couplings of its destination clusters (sync[1] counts the
-// warps done); (D) once every coupling is in, each CTA walks its groups of 8 leaves and adds
-// alpha V_t yhat_t.  The CTAs are co-resident (cooperative launch), so the two spin-waits cannot
-// deadlock; the last CTA to leave resets the counters for the next product.
-__device__ __forceinline__ void spin_until(const int* p, int v) {
-  while (*(volatile const int*)p < v) __nanosleep(64);
-  __threadfence();
-}
-
-__global__ void __launch_bounds__(256, 2) k_matvec_fused(const __grid_constant__ MvArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int nw = (int)(gridDim.x * (blockDim.x >> 5));
-  const int w0 = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
-  for (int w = w0; w < a.s_nleaves; w += nw) mv_up(a, a.s_leaves[w], lane);
-  for (int w = w0; w < a.d_nleaves; w += nw) mv_leaf_near(a, a.d_leaves[w], lane);
-  spin_until(a.sync, 1);
-  for (int w = w0; w < a.d_nclusters; w += nw) mv_couple(a, w, lane);
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) atomicAdd(a.sync + 1, 1);
-  spin_until(a.sync + 1, nw);
-  const int ngroups = (a.d_nleaves + 7) / 8;
-  for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
-    mv_walk(a, lane, g);
-    __syncthreads();  // the shared path prefix of the next group
   }
   __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(a.sync + 2, 1) == (int)gridDim.x - 1) {
-    a.sync[0] = 0;
-    a.sync[1] = 0;
-    a.sync[2] = 0;
-    __threadfence();
+  for (int l = 1; l < L.nlev; ++l) {
+    for (int i = L.ptr[l] + warp; i < L.ptr[l + 1]; i += nw) {
+      const int c = L.cl[i];
+      bwd_cluster(a, c, lane, ys + (size_t)(c - root) * rcap, ys + (size_t)(a.d_parent[c] - root) * rcap, tp, tb);
+    }
+    __syncthreads();
   }
+  // the leaves' yhat back to global for k_mv_leaf_bwd
+  for (int i = warp; i < n; i += nw) {
+    const int c = root + i;
+    if (a.d_son0[c] >= 0) continue;
+    const int k = a.d_rank[c];
+    for (int j = lane; j < k; j += 32) yg[(size_t)i * rcap + j] = ys[(size_t)i * rcap + j];
+  }
+}
+
+// y|t += alpha V_t yhat_t, warp per destination leaf
+__global__ void __launch_bounds__(256) k_mv_leaf_bwd(const __grid_constant__ MvArgs a) {
+  const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  if (w >= a.d_nleaves) return;
+  const int lane = threadIdx.x & 31;
+  const int t = a.d_leaves[w];
+  const int rcap = a.rcap, lmax = a.lmax;
+  const int kt = a.d_rank[t];
+  if (kt == 0) return;
+  const int lo = a.d_lo[t], m = a.d_hi[t] - lo;
+  const double* V = a.d_leafb + (size_t)a.d_leafidx[t] * lmax * rcap;
+  const double* yh = a.d_xh + (size_t)t * rcap;
+  const double yl0 = lane < kt ? __ldcg(yh + lane) : 0.0;
+  const double yl1 = lane + 32 < kt ? __ldcg(yh + lane + 32) : 0.0;
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+  for (int j = 0; j < kt; ++j) {
+    const double yj = __shfl_sync(FULL, j < 32 ? yl0 : yl1, j & 31);
+    if (lane < m) a0 += V[lane + (size_t)j * lmax] * yj;
+    if (lane + 32 < m) a1 += V[lane + 32 + (size_t)j * lmax] * yj;
+  }
+  if (lane < m) {
+    double* yo = a.y + a.d_perm[lo + lane];
+    *yo = __ldcg(yo) + a.alpha * a0;
+  }
+  if (lane + 32 < m) {
+    double* yo = a.y + a.d_perm[lo + lane + 32];
+    *yo = __ldcg(yo) + a.alpha * a1;
+  }
+}
+
+// ---- packing ------------------------------------------------------------------------------------
+struct PackArgs {
+  const int32_t *adm_t, *adm_s, *rrank, *crank, *rparent, *cparent;
+  const double *S, *rtr, *ctr;
+  double *Sp, *rTp, *cTp;
+  const int64_t *Soff, *rToff, *cToff;
+  int nadm, nr, nc, rcap;
+};
+
+__global__ void __launch_bounds__(256) k_mv_pack(const PackArgs p) {
+  const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  const int lane = threadIdx.x & 31;
+  const double* src;
+  double* dst;
+  int rows, cols;
+  if (w < p.nadm) {
+    rows = p.rrank[p.adm_t[w]];
+    cols = p.crank[p.adm_s[w]];
+    src = p.S + (size_t)w * p.rcap * p.rcap;
+    dst = p.Sp + p.Soff[w];
+  } else if (w < p.nadm + p.nr) {
+    const int c = w - p.nadm;
+    rows = p.rrank[c];
+    cols = p.rparent[c] >= 0 ? p.rrank[p.rparent[c]] : 0;
+    src = p.rtr + (size_t)c * p.rcap * p.rcap;
+    dst = p.rTp + p.rToff[c];
+  } else if (w < p.nadm + p.nr + p.nc) {
+    const int c = w - p.nadm - p.nr;
+    rows = p.crank[c];
+    cols = p.cparent[c] >= 0 ? p.crank[p.cparent[c]] : 0;
+    src = p.ctr + (size_t)c * p.rcap * p.rcap;
+    dst = p.cTp + p.cToff[c];
+  } else {
+    return;
+  }
+  for (int e = lane; e < rows * cols; e += 32) dst[e] = src[(e % rows) + (size_t)(e / rows) * p.rcap];
 }
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 }  // namespace
 
-cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const double* x, double beta, double* y,
+// (Re)build the packed copies of Z's couplings and transfer matrices at its current ranks.  Runs
+// once per matrix version (any mutating call bumps h2_mat_::version): ranks to the host (one
+// stream synchronisation), offsets by prefix sums, one packing kernel.
+static cudaError_t ensure_packed(h2_mat_* Z, cudaStream_t st) {
+  MvPack& K = Z->mvpack;
+  if (K.version == Z->version) return cudaSuccess;
+  const MatDev& M = Z->d;
+  cudaError_t e;
+  const int nr = M.row.nclusters, nc = M.col.nclusters;
+  std::vector<int32_t> kr(nr), kc(nc);
+  if ((e = cudaMemcpyAsync(kr.data(), M.row.rank, sizeof(int32_t) * nr, cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaMemcpyAsync(kc.data(), M.col.rank, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaStreamSynchronize(st))) return e;
+  const h2_btree_* B = Z->bt;
+  std::vector<int64_t> so(M.nadm + 1, 0), ro(nr + 1, 0), co(nc + 1, 0);
+  for (int a = 0; a < M.nadm; ++a) {
+    const int b = Z->adm_blk[a];
+    so[a + 1] = so[a] + (int64_t)kr[B->t[b]] * kc[B->s[b]];
+  }
+  for (int c = 0; c < nr; ++c) {
+    const int p = B->rt->parent[c];
+    ro[c + 1] = ro[c] + (p >= 0 ? (int64_t)kr[c] * kr[p] : 0);
+  }
+  for (int c = 0; c < nc; ++c) {
+    const int p = B->ct->parent[c];
+    co[c + 1] = co[c] + (p >= 0 ? (int64_t)kc[c] * kc[p] : 0);
+  }
+  auto grow = [&](double** p, size_t* cap, size_t need) -> cudaError_t {
+    if (*cap >= need && *p) return cudaSuccess;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = need + need / 8 + 1024;
+    return cudaMalloc((void**)p, *cap * sizeof(double));
+  };
+  if ((e = grow(&K.Sp, &K.capS, (size_t)so[M.nadm]))) return e;
+  if ((e = grow(&K.Tp[0], &K.capT[0], (size_t)ro[nr]))) return e;
+  if ((e = grow(&K.Tp[1], &K.capT[1], (size_t)co[nc]))) return e;
+  if (!K.Soff) {
+    if ((e = cudaMalloc((void**)&K.Soff, sizeof(int64_t) * (M.nadm + 1)))) return e;
+    if ((e = cudaMalloc((void**)&K.Toff[0], sizeof(int64_t) * (nr + 1)))) return e;
+    if ((e = cudaMalloc((void**)&K.Toff[1], sizeof(int64_t) * (nc + 1)))) return e;
+  }
+  if ((e = cudaMemcpyAsync(K.Soff, so.data(), sizeof(int64_t) * (M.nadm + 1), cudaMemcpyHostToDevice, st))) return e;
+  if ((e = cudaMemcpyAsync(K.Toff[0], ro.data(), sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice, st))) return e;
+  if ((e = cudaMemcpyAsync(K.Toff[1], co.data(), sizeof(int64_t) * (nc + 1), cudaMemcpyHostToDevice, st))) return e;
+  PackArgs p;
+  p.adm_t = M.adm_t;
+  p.adm_s = M.adm_s;
+  p.rrank = M.row.rank;
+  p.crank = M.col.rank;
+  p.rparent = M.row.parent;
+  p.cparent = M.col.parent;
+  p.S = M.S;
+  p.rtr = M.row.tr;
+  p.ctr = M.col.tr;
+  p.Sp = K.Sp;
+  p.rTp = K.Tp[0];
+  p.cTp = K.Tp[1];
+  p.Soff = K.Soff;
+  p.rToff = K.Toff[0];
+  p.cToff = K.Toff[1];
+  p.nadm = M.nadm;
+  p.nr = nr;
+  p.nc = nc;
+  p.rcap = M.rcap;
+  H2_LAUNCH(K_MV, st, k_mv_pack<<<cdiv((long long)M.nadm + nr + nc, 8), 256, 0, st>>>(p));
+  if ((e = cudaStreamSynchronize(st))) return e;  // the host offset vectors go out of scope
+  K.version = Z->version;
+  return cudaGetLastError();
+}
+
+void free_mvpack(h2_mat_* Z) {
+  MvPack& K = Z->mvpack;
+  for (void* p : {(void*)K.Sp, (void*)K.Tp[0], (void*)K.Tp[1], (void*)K.Soff, (void*)K.Toff[0], (void*)K.Toff[1]})
+    if (p) cudaFree(p);
+  K = MvPack();
+}
+
+cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const double* x, double beta, double* y,
                           cudaStream_t st) {
+  h2_mat_* Z = const_cast<h2_mat_*>(Zc);
   const MatDev& M = Z->d;
   const DevSide& src = transpose ? M.row : M.col;  // basis applied to x
   const DevSide& dst = transpose ? M.col : M.row;  // basis producing y
@@ -669,85 +749,73 @@ cudaError_t launch_matvec(const h2_mat_* Z, int transpose, double alpha, const d
   a.d_level = dst.level;
   a.d_son1 = dst.son1;
   a.d_cnt = dst.mv_cnt;
+  a.Sp = nullptr;
+  a.Soff = nullptr;
+  a.s_Tp = a.d_Tp = nullptr;
+  a.s_Toff = a.d_Toff = nullptr;
   // the far field contributes only if some row and some column basis may have a non-zero rank
   const bool far = std::find(Z->nzr.begin(), Z->nzr.end(), 1) != Z->nzr.end() &&
                    std::find(Z->nzc.begin(), Z->nzc.end(), 1) != Z->nzc.end();
-  a.sync = nullptr;
   if (!far) {
     H2_LAUNCH(K_MV, st, k_matvec_near<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
     return cudaGetLastError();
   }
-  // one cooperative launch (k_matvec_fused) only on request (H2_MV_FUSED=1): measured 334 us for
-  // the C2 factor L against 167 us for the four-launch path below -- a persistent grid of 2 CTAs
-  // per SM serialises the latency-bound climb / coupling / walk work that the separate launches
-  // spread over 8-16k warps
-  static const bool fused_on = getenv("H2_MV_FUSED") && atoi(getenv("H2_MV_FUSED")) != 0;
-  static int fused_grid = -1;
-  static std::unordered_map<cudaStream_t, int*> syncs;  // counters per stream (products on one stream are ordered)
   cudaError_t e;
-  if (fused_on && fused_grid < 0) {
-    int dev = 0, nsm = 0, per = 0, coop = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_matvec_fused, 256, 0);
-    fused_grid = coop ? nsm * std::min(per, 2) : 0;
-    cudaGetLastError();
-  }
-  if (fused_on && fused_grid > 0) {
-    int*& sync = syncs[st];
-    if (!sync) {
-      if ((e = cudaMalloc(&sync, 4 * sizeof(int)))) return e;
-      if ((e = cudaMemset(sync, 0, 4 * sizeof(int)))) return e;
-    }
-    a.sync = sync;
-    void* args[] = {(void*)&a};
-    H2_LAUNCH(K_MV, st, e = cudaLaunchCooperativeKernel((const void*)k_matvec_fused, dim3(fused_grid), dim3(256), args, 0, st));
-    if (e) return e;
-    return cudaGetLastError();
-  }
-  a.sync = nullptr;
-  // the nearfield stream (the bulk of the bytes) runs on a second stream, concurrently with the
-  // forward transform and the couplings; the backward walk adds V_t yhat_t after both
+  if ((e = ensure_packed(Z, st))) return e;
+  const MvPack& K = Z->mvpack;
+  a.Sp = K.Sp;
+  a.Soff = K.Soff;
+  a.s_Tp = K.Tp[transpose ? 0 : 1];
+  a.s_Toff = K.Toff[transpose ? 0 : 1];
+  a.d_Tp = K.Tp[transpose ? 1 : 0];
+  a.d_Toff = K.Toff[transpose ? 1 : 0];
+  // the far-field chain (latency-bound) runs on a high-priority side stream; the nearfield kernel
+  // (the bulk of the bytes) runs on the caller's stream with a grid of 2 CTAs per SM, so both are
+  // co-resident; the leaf backward transform adds V_t yhat_t after both
   static cudaStream_t s2 = nullptr;
   static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  static int nsm = 148;
   if (!s2) {
-    // the nearfield stream gets the higher priority: it is the bandwidth-bound critical path, the
-    // far-field kernels fill the SMs around it
-    int lo = 0, hi = 0;
+    int lo = 0, hi = 0, dev = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     if ((e = cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming))) return e;
+    const size_t sub_smem = sizeof(double) * ((size_t)SUB_NC * RCAP_MAX + SUB_TB);
+    if ((e = cudaFuncSetAttribute(k_mv_fwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem))) return e;
+    if ((e = cudaFuncSetAttribute(k_mv_bwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem))) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  static const bool walk_path = getenv("H2_MV_WALK") && atoi(getenv("H2_MV_WALK")) != 0;  // round-1 path (A/B)
-  // timing diagnostics (tools): H2_MV_PART=1 far field only, 2 nearfield only (y is then incomplete)
+  const size_t smem = sizeof(double) * ((size_t)SUB_NC * M.rcap + SUB_TB);
+  // timing diagnostics (tools): H2_MV_PART=1 far field only, 2 nearfield only, 3 / 4 / 5: the far
+  // field up to the forward transform / the couplings / the subtree backward transform (y is then
+  // incomplete); H2_MV_NEARGRID: CTAs per SM of the nearfield kernel (default 2)
   static const int part = getenv("H2_MV_PART") ? atoi(getenv("H2_MV_PART")) : 0;
-  if (part == 1 || part == 3 || part == 4) {  // 3: forward only, 4: forward + couplings
-    H2_LAUNCH(K_MV, st, k_mv_fwd_sub<<<src.n_mv_roots, SUBT, 0, st>>>(a));
-    if (part != 3) H2_LAUNCH(K_MV, st, k_mv_couple_top<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
-    if (part == 1) H2_LAUNCH(K_MV, st, k_mv_bwd_sub<<<dst.n_mv_roots, SUBT, 0, st>>>(a));
-    return cudaGetLastError();
-  }
+  static const int near_per_sm = getenv("H2_MV_NEARGRID") ? atoi(getenv("H2_MV_NEARGRID")) : 2;
+  const int near_grid = std::min(cdiv(dst.nleaves, 8), std::max(1, near_per_sm) * nsm);
   if (part == 2) {
-    H2_LAUNCH(K_MV, st, k_matvec_near<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
+    H2_LAUNCH(K_MV, st, k_matvec_near<<<near_grid, 256, 0, st>>>(a));
     return cudaGetLastError();
   }
-  if ((e = cudaEventRecord(ev_fork, st))) return e;
-  if ((e = cudaStreamWaitEvent(s2, ev_fork, 0))) return e;
-  H2_LAUNCH(K_MV, s2, k_matvec_near<<<cdiv(dst.nleaves, 8), 256, 0, s2>>>(a));
-  if ((e = cudaEventRecord(ev_join, s2))) return e;
-  if (walk_path) {
-    H2_LAUNCH(K_MV, st, k_matvec_fwd<<<cdiv(src.nleaves, 8), 256, 0, st>>>(a));
-    H2_LAUNCH(K_MV, st, k_matvec_couple<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
+  cudaStream_t sf = part == 0 ? s2 : st;  // the far-field chain
+  if (part == 0) {
+    if ((e = cudaEventRecord(ev_fork, st))) return e;
+    if ((e = cudaStreamWaitEvent(s2, ev_fork, 0))) return e;
+  }
+  H2_LAUNCH(K_MV, sf, k_mv_leaf_fwd<<<cdiv(src.nleaves, 8), 256, 0, sf>>>(a));
+  H2_LAUNCH(K_MV, sf, k_mv_fwd_sub<<<src.n_mv_roots, SUBT, smem, sf>>>(a));
+  if (part == 3) return cudaGetLastError();
+  H2_LAUNCH(K_MV, sf, k_mv_couple_top<<<cdiv(dst.nclusters, 8), 256, 0, sf>>>(a));
+  if (part == 4) return cudaGetLastError();
+  H2_LAUNCH(K_MV, sf, k_mv_bwd_sub<<<dst.n_mv_roots, SUBT, smem, sf>>>(a));
+  if (part == 5) return cudaGetLastError();
+  if (part == 0) {
+    if ((e = cudaEventRecord(ev_join, s2))) return e;
+    H2_LAUNCH(K_MV, st, k_matvec_near<<<near_grid, 256, 0, st>>>(a));
     if ((e = cudaStreamWaitEvent(st, ev_join, 0))) return e;
-    H2_LAUNCH(K_MV, st, k_matvec_walk<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
-    return cudaGetLastError();
   }
-  H2_LAUNCH(K_MV, st, k_mv_fwd_sub<<<src.n_mv_roots, SUBT, 0, st>>>(a));
-  H2_LAUNCH(K_MV, st, k_mv_couple_top<<<cdiv(dst.nclusters, 8), 256, 0, st>>>(a));
-  if ((e = cudaStreamWaitEvent(st, ev_join, 0))) return e;
-  H2_LAUNCH(K_MV, st, k_mv_bwd_sub<<<dst.n_mv_roots, SUBT, 0, st>>>(a));
+  H2_LAUNCH(K_MV, st, k_mv_leaf_bwd<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
   return cudaGetLastError();
 }
 

@@ -45,7 +45,14 @@ __device__ void it_upd_ext_leaf(const MatDev& M, UpdArgs a_, int rl0, int nrl, i
     if (a.prof && threadIdx.x == 0) atomicAdd(a.prof + 2 * K_W_PATH, fl);
     return;
   }
-  if (b == 0 && threadIdx.x == 0 && nrl + ncl > 0) atomicAdd(M.flags + 3, 1);  // non-zero-rank update count
+  if (b == 0 && threadIdx.x == 0 && nrl + ncl > 0) {
+    const int idx = atomicAdd(M.flags + 3, 1);  // non-zero-rank update count
+    if (M.updlog && idx < (1 << 21)) {
+      M.updlog[3 * idx] = a.t0;
+      M.updlog[3 * idx + 1] = a.s0;
+      M.updlog[3 * idx + 2] = a.k;
+    }
+  }
   if (b < nrl + ncl) {
     const bool rs = b < nrl;
     const DevSide& D = rs ? M.row : M.col;

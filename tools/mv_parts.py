@@ -6,9 +6,9 @@ import subprocess
 import sys
 
 N = sys.argv[1] if len(sys.argv) > 1 else "512"
-for name, env in (("full", {}), ("walk_r01", {"H2_MV_WALK": "1"}), ("far_only", {"H2_MV_PART": "1"}),
-                  ("near_only", {"H2_MV_PART": "2"}), ("fwd_only", {"H2_MV_PART": "3"}),
-                  ("fwd_couple", {"H2_MV_PART": "4"})):
+for name, env in (("full", {}), ("far_only", {"H2_MV_PART": "1"}), ("near_only", {"H2_MV_PART": "2"}),
+                  ("fwd_only", {"H2_MV_PART": "3"}), ("fwd_couple", {"H2_MV_PART": "4"}),
+                  ("fwd_couple_bwdsub", {"H2_MV_PART": "5"})):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "tools/time_matvec.py", N, "factor"], env=e, capture_output=True, text=True)
     line = [l for l in r.stdout.splitlines() if l.startswith("{")]
