@@ -229,8 +229,11 @@ h2_status h2_import(h2_btree bt, const int32_t* row_rank, const int32_t* col_ran
                     const double* W, const double* F, const double* S, const double* N, h2_storage storage,
                     int32_t rank_cap, int32_t update_cap, h2_stream stream, h2_mat* out);
 
-/* Device-side status word: nonzero if a device kernel hit a rank above rank_cap (clamped) since
- * the last call; the flag is cleared.  Synchronizes the stream. */
+/* Device-side status word since the last call (then cleared): bit 0 = a truncation hit a rank above
+ * rank_cap (clamped); bit 1 = a dense leaf breakdown (also returned as H2_ERR_BREAKDOWN); bit 2 =
+ * a contribution inside h2_addmul / h2_lr_factor / h2_inverse had a rank above update_cap and
+ * was dropped (the result is then wrong: re-run with a larger update_cap -- a dense x dense
+ * product of leaf tiles can reach rank = leaf size, reading own-7).  Synchronizes the stream. */
 h2_status h2_check_device_flags(h2_mat Z, int32_t* flags);
 
 /* Profiling hook (bench/test only; off by default).  h2_profile_enable(1) synchronizes the

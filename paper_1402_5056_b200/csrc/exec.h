@@ -66,6 +66,7 @@ enum OpCode : int32_t {
   OP_TINV,    // in-place inverse of a diagonal leaf tile (approximate inversion, Remark 1)
   OP_C2CORE,  // Case 2, both factors admissible: [G =] W^T V, C = S^X G S^Y, choose (one CTA)
   OP_SKIPZ,  // all CTAs: if *ip == 0 skip the next `count` ops (a zero-rank local update)
+  OP_KCHECK,  // *ip > rows (the update capacity): set the capacity flag and drop the contribution (*ip = 0)
   OP_COUNT
 };
 

@@ -39,6 +39,7 @@ void zero_rank_if_zero_tile(const MatDev& M, int slot, int count, int* kdev, cud
 // copy a (rows x cols) block with device column count into dst (zero-extended rows are the caller's)
 void copy_cols(double* dst, int ldd, const double* src, int lds, int rows, Dim cols, int colcap, cudaStream_t st);
 void set_int(int* p, Dim v, cudaStream_t st);
+void rank_check(const MatDev& M, int* kdev, int cap, cudaStream_t st);  // *kdev > cap: flag 4, *kdev = 0
 void rank_if(int* p, const int* a, const int* b, cudaStream_t st);  // *p = (*a>0 && *b>0) ? *b : 0
 void stack_cols(double* dst, int ldd, int rows, const double* T, int ldt, const int* kT, const double* Nw, int ldn,
                 int row_off, int rows_new, Dim knew, int colcap, cudaStream_t st);

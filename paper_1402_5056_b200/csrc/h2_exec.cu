@@ -57,7 +57,7 @@ __constant__ int c_op_kid[OP_COUNT] = {
     K_AR_EXPAND, K_AR_GEMM, K_AR_GEMM, K_AR_GEMM, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL, K_AR_HMUL,
     K_AR_TILE, K_AR_TILE, K_AR_TILE, K_AR_TSQR, K_AR_TEMP, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC,
     K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_MISC, K_AR_TEMP, K_AR_MISC,
-    K_AR_TILE, K_AR_GEMM, K_AR_MISC};
+    K_AR_TILE, K_AR_GEMM, K_AR_MISC, K_AR_MISC};
 
 __device__ __forceinline__ const DevSide& side_of(const MatDev& M, int s) { return s ? M.col : M.row; }
 
@@ -215,6 +215,13 @@ __device__ void dispatch(const ExecParams& P, const OpRec& op, int it, int n, do
       for (int e = threadIdx.x; e < q.rows; e += NT) any |= (T[e] != 0.0);
       any = __syncthreads_or(any);
       if (!any && threadIdx.x == 0) *q.ip = 0;
+    } break;
+    case OP_KCHECK: {  // a contribution whose device rank exceeds the update capacity: flag it, drop it
+      const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
+      if (threadIdx.x == 0 && *q.ip > q.rows) {
+        atomicOr(M.flags, 4);
+        *q.ip = 0;
+      }
     } break;
     case OP_ZERO: {
       const PMisc& q = *reinterpret_cast<const PMisc*>(op.p);
@@ -786,6 +793,12 @@ void add_int(int* p, Dim a, Dim b, cudaStream_t) {
   q.d1 = a;
   q.d2 = b;
   ctx_or_throw()->emit(OP_ADD_INT, 1, nullptr, q);
+}
+void rank_check(const MatDev& M, int* kdev, int cap, cudaStream_t) {
+  PMisc q = misc();
+  q.ip = kdev;
+  q.rows = cap;
+  ctx_or_throw()->emit(OP_KCHECK, 1, &M, q);
 }
 void rank_if(int* p, const int* a, const int* b, cudaStream_t) {
   PMisc q = misc();

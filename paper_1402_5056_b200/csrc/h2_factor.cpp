@@ -141,6 +141,10 @@ struct Driver {
 
   // ---- contributions -------------------------------------------------------------------------
   void update(int t, int r, const double* A, int lda, const double* B, int ldb, const int* kdev, double alpha) {
+    // a contribution's rank can reach the leaf size (dense x dense, reading own-7): if that may
+    // exceed the update capacity, check it on the device (flag 4 of h2_check_device_flags) instead
+    // of overrunning the extended-rank workspace
+    if (kdev && lmax > Z->d.ucap) rank_check(Z->d, const_cast<int*>(kdev), Z->d.ucap, st);
     UpdArgs a;
     a.t0 = t;
     a.s0 = r;

@@ -612,7 +612,7 @@ extern "C" h2_status h2_from_sparse(h2_btree bt, int64_t n, const int64_t* rowpt
   TRY_ALLOC(cudaMemset(M.S, 0, sizeof(double) * (size_t)M.nadm * M.rcap * M.rcap));
   TRY_ALLOC(dalloc(Z, &M.flags, 4));
   TRY_ALLOC(cudaMemset(M.flags, 0, 4 * sizeof(int32_t)));
-  if (getenv("H2_UPD_LOG")) TRY_ALLOC(dalloc(Z, &M.updlog, (size_t)3 << 21));
+  if (getenv("H2_UPD_LOG")) TRY_ALLOC(dalloc(Z, &M.updlog, (size_t)5 << 20));
   TRY_ALLOC(dalloc(Z, &M.xt, n));
   TRY_ALLOC(dalloc(Z, &M.yt, n));
 #undef TRY_ALLOC
@@ -714,11 +714,12 @@ extern "C" h2_status h2_check_device_flags(h2_mat Z, int32_t* flags) {
   if (Z->d.updlog && getenv("H2_UPD_LOG")) {  // diagnostic: the non-zero-rank updates in order, as text
     int32_t cnt = 0;
     CUDA_TRY(cudaMemcpy(&cnt, Z->d.flags + 3, sizeof(cnt), cudaMemcpyDeviceToHost));
-    cnt = std::min(cnt, 1 << 21);
-    std::vector<int32_t> lg((size_t)3 * cnt);
+    cnt = std::min(cnt, 1 << 20);
+    std::vector<int32_t> lg((size_t)5 * cnt);
     CUDA_TRY(cudaMemcpy(lg.data(), Z->d.updlog, sizeof(int32_t) * lg.size(), cudaMemcpyDeviceToHost));
     if (FILE* f = fopen(getenv("H2_UPD_LOG"), "w")) {
-      for (int i = 0; i < cnt; ++i) fprintf(f, "%d %d %d\n", lg[3 * i], lg[3 * i + 1], lg[3 * i + 2]);
+      for (int i = 0; i < cnt; ++i)
+        fprintf(f, "%d %d %d %d %d\n", lg[5 * i], lg[5 * i + 1], lg[5 * i + 2], lg[5 * i + 3], lg[5 * i + 4]);
       fclose(f);
     }
   }

@@ -141,9 +141,16 @@ struct SolveSched {
 struct MvPack {
   double* Sp = nullptr;
   int64_t* Soff = nullptr;                 // nadm + 1
-  double* Tp[2] = {nullptr, nullptr};      // row / column side transfers
+  double* Tp[2] = {nullptr, nullptr};      // row / column side transfers (k_c x k_p, ld k_c)
+  double* TpT[2] = {nullptr, nullptr};     // the same matrices transposed (k_p x k_c, ld k_p): forward transform
   int64_t* Toff[2] = {nullptr, nullptr};   // nclusters + 1
-  size_t capS = 0, capT[2] = {0, 0};
+  size_t capS = 0, capT[2] = {0, 0}, capTT[2] = {0, 0};
+  // per block of row(t) / col(s), in the order of DevSide::bidx: {offset in Sp, partner, partner's rank}
+  struct Desc {
+    long long off;
+    int partner, krank;
+  };
+  Desc* desc[2] = {nullptr, nullptr};
   long long version = -1;
 };
 

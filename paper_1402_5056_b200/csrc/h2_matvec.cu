@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <unordered_map>
 
@@ -59,7 +60,18 @@ struct MvArgs {
   const int64_t* Soff;
   const double *s_Tp, *d_Tp;
   const int64_t *s_Toff, *d_Toff;
+  int sub_tb;                // doubles of staged transfers per subtree CTA (shared memory budget)
+  const MvPack::Desc* desc;  // blocks of the destination clusters in d_bidx order
+  unsigned long long* dbg;  // H2_MV_DBG: globaltimer stamps of the far-field phases (diagnostic)
 };
+
+__device__ __forceinline__ void stamp(const MvArgs& a, int i) {
+  if (a.dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[i] = t;
+  }
+}
 
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -132,8 +144,8 @@ __device__ void mv_leaf_near(const MvArgs& a, int t, int lane) {
 }
 
 __global__ void __launch_bounds__(256, 4) k_matvec_near(const __grid_constant__ MvArgs a) {
-  // grid-stride over the destination leaves: with the far field present the grid is 2 CTAs per SM,
-  // which leaves half of every SM to the far-field chain running concurrently
+  // grid-stride over the destination leaves (the default grid has one warp per leaf; a grid of
+  // fewer CTAs per SM, H2_MV_NEARGRID, measured slower: 90 us against 66 us at 2 CTAs per SM)
   const int nw = (int)(gridDim.x * (blockDim.x >> 5));
   for (int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w < a.d_nleaves; w += nw)
     mv_leaf_near(a, a.d_leaves[w], threadIdx.x & 31);
@@ -160,21 +172,32 @@ __global__ void __launch_bounds__(256, 4) k_matvec_near(const __grid_constant__ 
 //                    nearfield kernel on the second stream has written y)
 constexpr int SUBT = 512;        // threads of a subtree CTA
 constexpr int SUB_NC = 2 * MV_SUB_LEAVES;  // clusters of a subtree (<= 2 * 64 - 1)
-constexpr int SUB_TB = 12288;    // doubles of staged transfer matrices per subtree CTA (96 KB)
+constexpr int SUB_SMEM = 220 * 1024;  // dynamic shared memory of a subtree CTA: coefficient rows + staged transfers
 
 struct SubList {  // the clusters of one subtree bucketed by level below its root
   int nlev;
   int cnt[64];
   int ptr[65];
   int cl[SUB_NC];
+  // structure of cluster root + i (contiguous ids: one coalesced load round), so that the level
+  // loops read shared memory only
+  int rk[SUB_NC], s0[SUB_NC], s1[SUB_NC], par[SUB_NC];
+  long long to[SUB_NC];
 };
 
-__device__ void build_sublist(const int32_t* level, const int32_t* tsize, int root, SubList& L) {
+__device__ void build_sublist(const int32_t* level, const int32_t* tsize, int root, SubList& L, const int32_t* rank,
+                              const int32_t* son0, const int32_t* son1, const int32_t* parent, const int64_t* Toff) {
   const int n = tsize[root], l0 = level[root];
   if (threadIdx.x < 64) L.cnt[threadIdx.x] = 0;
   __syncthreads();
   int rel = -1, slot = 0;
   if ((int)threadIdx.x < n) {
+    const int c = root + threadIdx.x;
+    L.rk[threadIdx.x] = rank[c];
+    L.s0[threadIdx.x] = son0[c];
+    L.s1[threadIdx.x] = son1[c];
+    L.par[threadIdx.x] = parent[c];
+    L.to[threadIdx.x] = Toff[c];
     rel = level[root + threadIdx.x] - l0;
     slot = atomicAdd(&L.cnt[rel], 1);  // order inside a level is irrelevant (independent clusters)
   }
@@ -204,10 +227,11 @@ __device__ __forceinline__ void fwd_leaf(const MvArgs& a, int s, int lane) {
   const double x1 = lane + 32 < m ? a.x[a.s_perm[lo + lane + 32]] : 0.0;
   const double* W = a.s_leafb + (size_t)a.s_leafidx[s] * lmax * rcap;
   double mine0 = 0.0, mine1 = 0.0;
-  for (int j0 = 0; j0 < k; j0 += 4) {  // 4 columns per round: their loads and butterflies overlap
-    double p[4];
+  constexpr int CB = 8;
+  for (int j0 = 0; j0 < k; j0 += CB) {  // 8 columns per round: their loads and butterflies overlap
+    double p[CB];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < CB; ++u) {
       const int j = j0 + u;
       p[u] = 0.0;
       if (j < k) {
@@ -218,10 +242,10 @@ __device__ __forceinline__ void fwd_leaf(const MvArgs& a, int s, int lane) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) p[u] += __shfl_xor_sync(FULL, p[u], o);
+      for (int u = 0; u < CB; ++u) p[u] += __shfl_xor_sync(FULL, p[u], o);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < CB; ++u) {
       const int j = j0 + u;
       if (j < k && lane == (j & 31)) {
         if (j < 32) mine0 = p[u];
@@ -233,57 +257,82 @@ __device__ __forceinline__ void fwd_leaf(const MvArgs& a, int s, int lane) {
   if (lane + 32 < k) a.s_xh[(size_t)s * rcap + lane + 32] = mine1;
 }
 
-// xhat_s = sum over the sons c of F_c^T xhat_c (F_c: k_c x k_s, packed, ld k_c) by one warp.
-// xs(c): the sons' coefficients (shared memory inside a subtree, global above); tp: packed
-// transfers (shared memory copy with offset base `tb`, or global with tb = 0)
-template <class XS>
-__device__ __forceinline__ void fwd_internal(const MvArgs& a, int s, int lane, XS xs, const double* tp, int64_t tb,
-                                             double* out) {
-  const int k = a.s_rank[s];
+// xhat_s = sum over the sons c of F_c^T xhat_c (F_c^T: k_s x k_c, packed transposed, ld k_s) by one warp, inside
+// a subtree: i = s - root; the sons of a binary preorder tree are i + 1 and the cluster after the
+// first son's subtree (L.s0 holds son0, son1 = father's other son: found via the parent array)
+__device__ __forceinline__ void fwd_internal(const SubList& L, int i, int i0, int i1, int lane, double* xs, int rcap,
+                                             const double* tp, int64_t tb) {
+  const int k = L.rk[i];
   if (k == 0) return;
-  const int sc0 = a.s_son0[s], sc1 = a.s_son1[s];
-  const int sk0 = a.s_rank[sc0], sk1 = a.s_rank[sc1];
-  const double* F0 = tp + (a.s_Toff[sc0] - tb);
-  const double* F1 = tp + (a.s_Toff[sc1] - tb);
-  const double* x0 = xs(sc0);
-  const double* x1 = xs(sc1);
-  for (int j = lane; j < k; j += 32) {
+  const int sk0 = L.rk[i0], sk1 = L.rk[i1];
+  const double* F0 = tp + (L.to[i0] - tb);
+  const double* F1 = tp + (L.to[i1] - tb);
+  const double* x0 = xs + (size_t)i0 * rcap;
+  const double* x1 = xs + (size_t)i1 * rcap;
+  for (int j = lane; j < k; j += 32) {  // F^T stored k x k_c (ld k): lanes read consecutive words
     double acc = 0.0;
-    for (int i = 0; i < sk0; ++i) acc += F0[i + (size_t)j * sk0] * x0[i];
-    for (int i = 0; i < sk1; ++i) acc += F1[i + (size_t)j * sk1] * x1[i];
-    out[j] = acc;
+    for (int q = 0; q < sk0; ++q) acc += F0[j + (size_t)q * k] * x0[q];
+    for (int q = 0; q < sk1; ++q) acc += F1[j + (size_t)q * k] * x1[q];
+    xs[(size_t)i * rcap + j] = acc;
   }
 }
 
 // yhat_c = yc_c + E_c yhat_father (E_c: k_c x k_p, packed, ld k_c), in place, one warp
-__device__ __forceinline__ void bwd_cluster(const MvArgs& a, int c, int lane, double* yc, const double* yp,
+__device__ __forceinline__ void bwd_cluster(const SubList& L, int i, int ip, int lane, double* ys, int rcap,
                                             const double* tp, int64_t tb) {
-  const int p = a.d_parent[c];
-  const int kc = a.d_rank[c];
-  if (p < 0 || kc == 0) return;
-  const int kp = a.d_rank[p];
-  const double* E = tp + (a.d_Toff[c] - tb);
-  for (int i = lane; i < kc; i += 32) {
-    double v = yc[i];
-    for (int j = 0; j < kp; ++j) v += E[i + (size_t)j * kc] * yp[j];
-    yc[i] = v;
+  const int kc = L.rk[i];
+  if (kc == 0) return;
+  const int kp = L.rk[ip];
+  const double* E = tp + (L.to[i] - tb);
+  double* yc = ys + (size_t)i * rcap;
+  const double* yp = ys + (size_t)ip * rcap;
+  for (int r = lane; r < kc; r += 32) {
+    double v = yc[r];
+    for (int j = 0; j < kp; ++j) v += E[r + (size_t)j * kc] * yp[j];
+    yc[r] = v;
   }
 }
 
 __global__ void __launch_bounds__(256) k_mv_leaf_fwd(const __grid_constant__ MvArgs a) {
+  if (blockIdx.x == 0) stamp(a, 0);
   const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
   if (w < a.s_nleaves) fwd_leaf(a, a.s_leaves[w], threadIdx.x & 31);
 }
 
-// stage the packed transfers of the clusters root+1 .. root+n-1 (contiguous) in shared memory
-__device__ __forceinline__ bool stage_transfers(const double* Tp, const int64_t* Toff, int root, int n, double* tbuf,
-                                                int64_t& tb) {
-  tb = Toff[root + 1 < root + n ? root + 1 : root];
-  const int64_t te = Toff[root + n];
-  const int64_t len = te - tb;
-  if (len > SUB_TB) return false;
-  for (int64_t e = threadIdx.x; e < len; e += blockDim.x) tbuf[e] = Tp[tb + e];
-  return true;
+// Stage the packed transfers of the clusters root+1 .. root+n-1 (contiguous, 16-byte aligned: every
+// packed matrix is padded to an even number of doubles) in shared memory with cp.async (16-byte
+// copies, all in flight at once, no registers); the caller does other work (the sublist), then
+// stage_wait.  `cap`: doubles of shared memory available behind the coefficient rows.
+struct StageRegs {
+  int64_t tb, len;
+  bool ok;
+};
+__device__ __forceinline__ void stage_load(const double* Tp, const int64_t* Toff, int root, int n, StageRegs& R,
+                                           double* tbuf, int cap) {
+  R.tb = Toff[root + 1 < root + n ? root + 1 : root];
+  R.len = Toff[root + n] - R.tb;
+  R.ok = n > 1 && R.len <= cap;
+  if (!R.ok) return;
+  const double* src = Tp + R.tb;
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(tbuf);
+  const int nv = (int)(R.len >> 1);  // len is even
+  for (int e = threadIdx.x; e < nv; e += blockDim.x)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * (unsigned)e), "l"(src + 2 * e));
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void stage_store(const StageRegs& R, double*) {
+  if (R.ok) asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// the first CTAs of a launch pull the packed transfers of the clusters above the subtrees into L2
+// (one cluster each), so that the last CTA's level-by-level pass over them hits L2
+__device__ __forceinline__ void prefetch_top(const double* Tp, const int64_t* Toff, const int32_t* top, int ntop) {
+  if ((int)blockIdx.x >= ntop) return;
+  const int c = top[blockIdx.x];
+  const char* b = reinterpret_cast<const char*>(Tp + Toff[c]);
+  const int64_t bytes = (Toff[c + 1] - Toff[c]) * 8;
+  for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += (int64_t)blockDim.x * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(b + o));
 }
 
 __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ MvArgs a) {
@@ -295,35 +344,40 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ 
   double* tbuf = dsm + (size_t)SUB_NC * rcap;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = SUBT / 32;
   const int root = a.s_roots[blockIdx.x], n = a.s_tsize[root];
-  build_sublist(a.s_level, a.s_tsize, root, L);
+  if (blockIdx.x == 0) stamp(a, 1);
+  unsigned long long t_in = 0, t_st = 0, t_lv = 0;
+  if (a.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_in));
+  StageRegs SR;
+  stage_load(a.s_Tp, a.s_Toff, root, n, SR, tbuf, a.sub_tb);
+  prefetch_top(a.s_Tp, a.s_Toff, a.s_top, a.s_top_lptr[a.s_top_nlev]);
+  build_sublist(a.s_level, a.s_tsize, root, L, a.s_rank, a.s_son0, a.s_son1, a.s_parent, a.s_Toff);
   if (n > 1) {
     // the leaves' coefficients (k_mv_leaf_fwd) -- the subtree's xhat rows are contiguous in global
     const double* xg = a.s_xh + (size_t)root * rcap;
     for (int i = warp; i < n; i += nw) {
-      const int c = root + i;
-      if (a.s_son0[c] >= 0) continue;
-      const int k = a.s_rank[c];
+      if (L.s0[i] >= 0) continue;
+      const int k = L.rk[i];
       for (int j = lane; j < k; j += 32) xs[(size_t)i * rcap + j] = __ldcg(xg + (size_t)i * rcap + j);
     }
-    int64_t tb = 0;
-    const bool staged = stage_transfers(a.s_Tp, a.s_Toff, root, n, tbuf, tb);
-    __syncthreads();
+    stage_store(SR, tbuf);
+    const bool staged = SR.ok;
+    const int64_t tb = staged ? SR.tb : 0;
     const double* tp = staged ? tbuf : a.s_Tp;
-    if (!staged) tb = 0;
-    auto xof = [&](int c) -> const double* { return xs + (size_t)(c - root) * rcap; };
+    __syncthreads();
+    if (a.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_st));
     for (int l = L.nlev - 2; l >= 0; --l) {
-      for (int i = L.ptr[l] + warp; i < L.ptr[l + 1]; i += nw) {
-        const int s = L.cl[i];
-        if (a.s_son0[s] >= 0) fwd_internal(a, s, lane, xof, tp, tb, xs + (size_t)(s - root) * rcap);
+      for (int q = L.ptr[l] + warp; q < L.ptr[l + 1]; q += nw) {
+        const int i = L.cl[q] - root;
+        if (L.s0[i] >= 0) fwd_internal(L, i, L.s0[i] - root, L.s1[i] - root, lane, xs, rcap, tp, tb);
       }
       __syncthreads();
     }
+    if (a.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_lv));
     // publish the internal clusters' coefficients (the couplings read them from global)
     for (int i = warp; i < n; i += nw) {
-      const int s = root + i;
-      if (a.s_son0[s] < 0) continue;
-      const int k = a.s_rank[s];
-      for (int j = lane; j < k; j += 32) a.s_xh[(size_t)s * rcap + j] = xs[(size_t)i * rcap + j];
+      if (L.s0[i] < 0) continue;
+      const int k = L.rk[i];
+      for (int j = lane; j < k; j += 32) a.s_xh[(size_t)(root + i) * rcap + j] = xs[(size_t)i * rcap + j];
     }
   }
   // the last subtree to finish computes the clusters above the subtrees, bottom-up
@@ -335,20 +389,57 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ 
   __syncthreads();
   if (!last) return;
   __threadfence();
-  auto xg = [&](int c) -> const double* { return a.s_xh + (size_t)c * rcap; };
+  if (a.dbg && threadIdx.x == 0) {
+    a.dbg[2] = t_in;
+    a.dbg[3] = t_st;
+    a.dbg[4] = t_lv;
+  }
+  stamp(a, 5);
+  // structure of the top clusters into shared memory (reusing the sublist arrays; <= SUB_NC - 1 of
+  // them: one per pair of subtrees at most), then the levels read only coefficients and transfers
+  const int ntop = a.s_top_lptr[a.s_top_nlev];
+  int* t_id = L.cl;      // cluster
+  int* t_k = L.rk;       // its rank
+  int* t_c0 = L.s0;      // sons
+  int* t_c1 = L.s1;
+  int* t_k0 = L.par;     // sons' ranks
+  int* t_k1 = L.cnt;     // (64 + 65 ints: cnt and ptr are adjacent)
+  long long* t_o0 = L.to;
+  long long* t_o1 = reinterpret_cast<long long*>(tbuf);
+  const bool cached = ntop <= SUB_NC && ntop <= 64 + 65;
+  if (cached) {
+    for (int i = threadIdx.x; i < ntop; i += SUBT) {
+      const int c = a.s_top[i];
+      const int c0 = a.s_son0[c], c1 = a.s_son1[c];
+      t_id[i] = c;
+      t_k[i] = a.s_rank[c];
+      t_c0[i] = c0;
+      t_c1[i] = c1;
+      t_k0[i] = a.s_rank[c0];
+      t_k1[i] = a.s_rank[c1];
+      t_o0[i] = a.s_Toff[c0];
+      t_o1[i] = a.s_Toff[c1];
+    }
+    __syncthreads();
+  }
   for (int l = a.s_top_nlev - 1; l >= 0; --l) {
-    for (int i = a.s_top_lptr[l] + warp; i < a.s_top_lptr[l + 1]; i += nw) {
-      const int s = a.s_top[i];
+    const int qb = a.s_top_lptr[l], qe = a.s_top_lptr[l + 1];
+    for (int i = qb + warp; i < qe; i += nw) {
+      int s, k, sc0, sc1, sk0, sk1;
+      long long o0, o1;
+      if (cached) {
+        s = t_id[i], k = t_k[i], sc0 = t_c0[i], sc1 = t_c1[i], sk0 = t_k0[i], sk1 = t_k1[i], o0 = t_o0[i], o1 = t_o1[i];
+      } else {
+        s = a.s_top[i], k = a.s_rank[s], sc0 = a.s_son0[s], sc1 = a.s_son1[s];
+        sk0 = a.s_rank[sc0], sk1 = a.s_rank[sc1], o0 = a.s_Toff[sc0], o1 = a.s_Toff[sc1];
+      }
+      if (k == 0) continue;
       // sons' coefficients through L2 (written by other CTAs / other warps of this one): one
       // coalesced load per son, then broadcast by shuffles
-      const int k = a.s_rank[s];
-      if (k == 0) continue;
-      const int sc0 = a.s_son0[s], sc1 = a.s_son1[s];
-      const int sk0 = a.s_rank[sc0], sk1 = a.s_rank[sc1];
-      const double* F0 = a.s_Tp + a.s_Toff[sc0];
-      const double* F1 = a.s_Tp + a.s_Toff[sc1];
-      const double* x0 = xg(sc0);
-      const double* x1 = xg(sc1);
+      const double* F0 = a.s_Tp + o0;
+      const double* F1 = a.s_Tp + o1;
+      const double* x0 = a.s_xh + (size_t)sc0 * rcap;
+      const double* x1 = a.s_xh + (size_t)sc1 * rcap;
       const double xa0 = lane < sk0 ? __ldcg(x0 + lane) : 0.0, xa1 = lane + 32 < sk0 ? __ldcg(x0 + lane + 32) : 0.0;
       const double xb0 = lane < sk1 ? __ldcg(x1 + lane) : 0.0, xb1 = lane + 32 < sk1 ? __ldcg(x1 + lane + 32) : 0.0;
       for (int j0 = 0; j0 < k; j0 += 32) {
@@ -356,11 +447,11 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ 
         double acc = 0.0;
         for (int q = 0; q < sk0; ++q) {
           const double xq = __shfl_sync(FULL, q < 32 ? xa0 : xa1, q & 31);
-          if (j < k) acc += F0[q + (size_t)j * sk0] * xq;
+          if (j < k) acc += F0[j + (size_t)q * k] * xq;
         }
         for (int q = 0; q < sk1; ++q) {
           const double xq = __shfl_sync(FULL, q < 32 ? xb0 : xb1, q & 31);
-          if (j < k) acc += F1[q + (size_t)j * sk1] * xq;
+          if (j < k) acc += F1[j + (size_t)q * k] * xq;
         }
         if (j < k) a.s_xh[(size_t)s * rcap + j] = acc;
       }
@@ -368,6 +459,7 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ 
     __syncthreads();
   }
   if (threadIdx.x == 0) a.s_cnt[0] = 0;
+  stamp(a, 6);
 }
 
 // ---- couplings of one destination cluster from the packed S --------------------------------------
@@ -391,28 +483,47 @@ __device__ __forceinline__ void mv_couple_packed(const MvArgs& a, int t, int lan
     const int cnt = qe - base < 32 ? qe - base : 32;
     int d_s = 0, d_k = 0;
     long long d_off = 0;
-    if (lane < cnt) {
-      const int slot = a.d_bidx[base + lane];
-      d_s = a.partner[slot];
-      d_k = a.s_rank[d_s];
-      d_off = a.Soff[slot];
+    if (lane < cnt) {  // one 16-byte descriptor per block (built with the packed copies)
+      const longlong2 dd = __ldg(reinterpret_cast<const longlong2*>(a.desc + base + lane));
+      d_off = dd.x;
+      d_s = (int)(dd.y & 0xffffffffll);
+      d_k = (int)(dd.y >> 32);
+      // all blocks of the batch in flight at once: the walk below then hits L2
+      const char* pb = reinterpret_cast<const char*>(a.Sp + d_off);
+      const int bytes = kt * d_k * 8;
+      for (int o = 0; o < bytes; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + o));
     }
-    for (int b = 0; b < cnt; ++b) {
-      const int s = __shfl_sync(FULL, d_s, b);
-      const int ks = __shfl_sync(FULL, d_k, b);
-      const long long off = __shfl_sync(FULL, d_off, b);
-      if (ks == 0) continue;
-      const double* Sa = a.Sp + off;
-      const double* xs = a.s_xh + (size_t)s * rcap;
-      if (!TR) {  // S_b: k_t x k_s, ld k_t; out[i] += sum_j S[i + j k_t] xhat_s[j]
-        if (act) {
-          for (int j = g; j < ks; j += G) {
+    if (!TR) {
+      // S_b: k_t x k_s, ld k_t; out[i] += sum_j S[i + j k_t] xhat_s[j].  Group g takes the blocks
+      // b = g, g + G, ...: G blocks are in flight per warp (a block's columns are independent loads)
+      const int rounds = (cnt + G - 1) / G;
+      for (int it = 0; it < rounds; ++it) {
+        const int b = it * G + g;
+        const bool ok = act && b < cnt;
+        const int bb = ok ? b : 0;
+        const int s = __shfl_sync(FULL, d_s, bb);
+        const int ks = __shfl_sync(FULL, d_k, bb);
+        const long long off = __shfl_sync(FULL, d_off, bb);
+        if (ok && ks > 0) {
+          const double* Sa = a.Sp + off;
+          const double* xs = a.s_xh + (size_t)s * rcap;
+#pragma unroll 4
+          for (int j = 0; j < ks; ++j) {
             const double xj = __ldcg(xs + j);
             if (ig < kt) acc0 = fma(Sa[ig + (size_t)j * kt], xj, acc0);
             if (ig + 32 < kt) acc1 = fma(Sa[ig + 32 + (size_t)j * kt], xj, acc1);
           }
         }
-      } else {    // S_b: k_s x k_t (rows = the partner's rank), ld k_s; out[j] += sum_i S[i + j k_s] xhat[i]
+      }
+    } else {
+      for (int b = 0; b < cnt; ++b) {
+        const int s = __shfl_sync(FULL, d_s, b);
+        const int ks = __shfl_sync(FULL, d_k, b);
+        const long long off = __shfl_sync(FULL, d_off, b);
+        if (ks == 0) continue;
+        const double* Sa = a.Sp + off;
+        const double* xs = a.s_xh + (size_t)s * rcap;
+        // S_b: k_s x k_t (rows = the partner's rank), ld k_s; out[j] += sum_i S[i + j k_s] xhat[i]
         for (int q = 0; q < 2; ++q) {
           const int j = lane + 32 * q;
           if (j < kt) {
@@ -445,6 +556,8 @@ __global__ void __launch_bounds__(256, 4) k_mv_couple_top(const __grid_constant_
   __shared__ int last;
   const int lane = threadIdx.x & 31;
   const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  if (blockIdx.x == 0) stamp(a, 7);
+  prefetch_top(a.d_Tp, a.d_Toff, a.d_top, a.d_top_lptr[a.d_top_nlev]);
   if (w < a.d_nclusters) {
     if (a.transpose) mv_couple_packed<true>(a, w, lane);
     else mv_couple_packed<false>(a, w, lane);
@@ -457,6 +570,7 @@ __global__ void __launch_bounds__(256, 4) k_mv_couple_top(const __grid_constant_
   __syncthreads();
   if (!last) return;
   __threadfence();
+  stamp(a, 8);
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, rcap = a.rcap;
   for (int l = 1; l < a.d_top_nlev; ++l) {  // the root (level 0) keeps its coupling sum
     for (int i = a.d_top_lptr[l] + warp; i < a.d_top_lptr[l + 1]; i += nw) {
@@ -481,6 +595,7 @@ __global__ void __launch_bounds__(256, 4) k_mv_couple_top(const __grid_constant_
     __syncthreads();
   }
   if (threadIdx.x == 0) a.d_cnt[0] = 0;
+  stamp(a, 9);
 }
 
 // backward transform inside one destination subtree (root first), in shared memory
@@ -492,48 +607,63 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_bwd_sub(const __grid_constant__ 
   double* tbuf = dsm + (size_t)SUB_NC * rcap;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = SUBT / 32;
   const int root = a.d_roots[blockIdx.x], n = a.d_tsize[root];
-  build_sublist(a.d_level, a.d_tsize, root, L);
+  if (blockIdx.x == 0) stamp(a, 10);
+  StageRegs SR;
+  stage_load(a.d_Tp, a.d_Toff, root, n, SR, tbuf, a.sub_tb);
+  // the root's father (a top cluster, final in global memory) and the root's own transfer matrix
+  const int pr = a.d_parent[root];
+  const int kpr = pr >= 0 ? a.d_rank[pr] : 0;
+  double ypr0 = 0.0, ypr1 = 0.0;
+  if (warp == 0 && pr >= 0) {
+    const double* yp = a.d_xh + (size_t)pr * rcap;
+    ypr0 = lane < kpr ? __ldcg(yp + lane) : 0.0;
+    ypr1 = lane + 32 < kpr ? __ldcg(yp + lane + 32) : 0.0;
+  }
+  build_sublist(a.d_level, a.d_tsize, root, L, a.d_rank, a.d_son0, a.d_son1, a.d_parent, a.d_Toff);
   double* yg = a.d_xh + (size_t)root * rcap;
   for (int i = warp; i < n; i += nw) {
-    const int k = a.d_rank[root + i];
+    const int k = L.rk[i];
     for (int j = lane; j < k; j += 32) ys[(size_t)i * rcap + j] = __ldcg(yg + (size_t)i * rcap + j);
   }
-  int64_t tb = 0;
-  const bool staged = n > 1 && stage_transfers(a.d_Tp, a.d_Toff, root, n, tbuf, tb);
-  __syncthreads();
+  stage_store(SR, tbuf);
+  const bool staged = SR.ok;
+  const int64_t tb = staged ? SR.tb : 0;
   const double* tp = staged ? tbuf : a.d_Tp;
-  if (!staged) tb = 0;
-  // the subtree's root: its father (if any) is a top cluster, final in global memory
-  if (warp == 0 && a.d_parent[root] >= 0) {
-    const int p = a.d_parent[root], kc = a.d_rank[root], kp = a.d_rank[p];
-    const double* E = a.d_Tp + a.d_Toff[root];
-    const double* yp = a.d_xh + (size_t)p * rcap;
-    for (int r = lane; r < kc; r += 32) {
-      double v = ys[r];
-      for (int j = 0; j < kp; ++j) v += E[r + (size_t)j * kc] * __ldcg(yp + j);
-      ys[r] = v;
+  __syncthreads();
+  if (warp == 0 && pr >= 0) {
+    const int kc = L.rk[0];
+    const double* E = a.d_Tp + L.to[0];
+    for (int r0 = 0; r0 < kc; r0 += 32) {
+      const int r = r0 + lane;
+      double v = r < kc ? ys[r] : 0.0;
+      for (int j = 0; j < kpr; ++j) {
+        const double yj = __shfl_sync(FULL, j < 32 ? ypr0 : ypr1, j & 31);
+        if (r < kc) v += E[r + (size_t)j * kc] * yj;
+      }
+      if (r < kc) ys[r] = v;
     }
   }
   __syncthreads();
   for (int l = 1; l < L.nlev; ++l) {
-    for (int i = L.ptr[l] + warp; i < L.ptr[l + 1]; i += nw) {
-      const int c = L.cl[i];
-      bwd_cluster(a, c, lane, ys + (size_t)(c - root) * rcap, ys + (size_t)(a.d_parent[c] - root) * rcap, tp, tb);
+    for (int q = L.ptr[l] + warp; q < L.ptr[l + 1]; q += nw) {
+      const int i = L.cl[q] - root;
+      bwd_cluster(L, i, L.par[i] - root, lane, ys, rcap, tp, tb);
     }
     __syncthreads();
   }
   // the leaves' yhat back to global for k_mv_leaf_bwd
   for (int i = warp; i < n; i += nw) {
-    const int c = root + i;
-    if (a.d_son0[c] >= 0) continue;
-    const int k = a.d_rank[c];
+    if (L.s0[i] >= 0) continue;
+    const int k = L.rk[i];
     for (int j = lane; j < k; j += 32) yg[(size_t)i * rcap + j] = ys[(size_t)i * rcap + j];
   }
+  if (blockIdx.x == 0) stamp(a, 11);
 }
 
 // y|t += alpha V_t yhat_t, warp per destination leaf
 __global__ void __launch_bounds__(256) k_mv_leaf_bwd(const __grid_constant__ MvArgs a) {
   const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
+  if (blockIdx.x == 0) stamp(a, 12);
   if (w >= a.d_nleaves) return;
   const int lane = threadIdx.x & 31;
   const int t = a.d_leaves[w];
@@ -566,7 +696,7 @@ __global__ void __launch_bounds__(256) k_mv_leaf_bwd(const __grid_constant__ MvA
 struct PackArgs {
   const int32_t *adm_t, *adm_s, *rrank, *crank, *rparent, *cparent;
   const double *S, *rtr, *ctr;
-  double *Sp, *rTp, *cTp;
+  double *Sp, *rTp, *cTp, *rTpT, *cTpT;
   const int64_t *Soff, *rToff, *cToff;
   int nadm, nr, nc, rcap;
 };
@@ -576,6 +706,7 @@ __global__ void __launch_bounds__(256) k_mv_pack(const PackArgs p) {
   const int lane = threadIdx.x & 31;
   const double* src;
   double* dst;
+  double* dstT = nullptr;
   int rows, cols;
   if (w < p.nadm) {
     rows = p.rrank[p.adm_t[w]];
@@ -588,16 +719,20 @@ __global__ void __launch_bounds__(256) k_mv_pack(const PackArgs p) {
     cols = p.rparent[c] >= 0 ? p.rrank[p.rparent[c]] : 0;
     src = p.rtr + (size_t)c * p.rcap * p.rcap;
     dst = p.rTp + p.rToff[c];
+    dstT = p.rTpT + p.rToff[c];
   } else if (w < p.nadm + p.nr + p.nc) {
     const int c = w - p.nadm - p.nr;
     rows = p.crank[c];
     cols = p.cparent[c] >= 0 ? p.crank[p.cparent[c]] : 0;
     src = p.ctr + (size_t)c * p.rcap * p.rcap;
     dst = p.cTp + p.cToff[c];
+    dstT = p.cTpT + p.cToff[c];
   } else {
     return;
   }
   for (int e = lane; e < rows * cols; e += 32) dst[e] = src[(e % rows) + (size_t)(e / rows) * p.rcap];
+  if (dstT)  // (cols x rows, ld cols)
+    for (int e = lane; e < rows * cols; e += 32) dstT[e] = src[(e / cols) + (size_t)(e % cols) * p.rcap];
 }
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
@@ -618,18 +753,19 @@ static cudaError_t ensure_packed(h2_mat_* Z, cudaStream_t st) {
   if ((e = cudaMemcpyAsync(kc.data(), M.col.rank, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost, st))) return e;
   if ((e = cudaStreamSynchronize(st))) return e;
   const h2_btree_* B = Z->bt;
+  auto even = [](int64_t v) { return (v + 1) & ~int64_t(1); };  // 16-byte aligned packed matrices
   std::vector<int64_t> so(M.nadm + 1, 0), ro(nr + 1, 0), co(nc + 1, 0);
   for (int a = 0; a < M.nadm; ++a) {
     const int b = Z->adm_blk[a];
-    so[a + 1] = so[a] + (int64_t)kr[B->t[b]] * kc[B->s[b]];
+    so[a + 1] = so[a] + even((int64_t)kr[B->t[b]] * kc[B->s[b]]);
   }
   for (int c = 0; c < nr; ++c) {
     const int p = B->rt->parent[c];
-    ro[c + 1] = ro[c] + (p >= 0 ? (int64_t)kr[c] * kr[p] : 0);
+    ro[c + 1] = ro[c] + (p >= 0 ? even((int64_t)kr[c] * kr[p]) : 0);
   }
   for (int c = 0; c < nc; ++c) {
     const int p = B->ct->parent[c];
-    co[c + 1] = co[c] + (p >= 0 ? (int64_t)kc[c] * kc[p] : 0);
+    co[c + 1] = co[c] + (p >= 0 ? even((int64_t)kc[c] * kc[p]) : 0);
   }
   auto grow = [&](double** p, size_t* cap, size_t need) -> cudaError_t {
     if (*cap >= need && *p) return cudaSuccess;
@@ -641,10 +777,30 @@ static cudaError_t ensure_packed(h2_mat_* Z, cudaStream_t st) {
   if ((e = grow(&K.Sp, &K.capS, (size_t)so[M.nadm]))) return e;
   if ((e = grow(&K.Tp[0], &K.capT[0], (size_t)ro[nr]))) return e;
   if ((e = grow(&K.Tp[1], &K.capT[1], (size_t)co[nc]))) return e;
+  if ((e = grow(&K.TpT[0], &K.capTT[0], (size_t)ro[nr]))) return e;
+  if ((e = grow(&K.TpT[1], &K.capTT[1], (size_t)co[nc]))) return e;
   if (!K.Soff) {
+    if ((e = cudaMalloc((void**)&K.desc[0], sizeof(MvPack::Desc) * (M.nadm + 1)))) return e;
+    if ((e = cudaMalloc((void**)&K.desc[1], sizeof(MvPack::Desc) * (M.nadm + 1)))) return e;
     if ((e = cudaMalloc((void**)&K.Soff, sizeof(int64_t) * (M.nadm + 1)))) return e;
     if ((e = cudaMalloc((void**)&K.Toff[0], sizeof(int64_t) * (nr + 1)))) return e;
     if ((e = cudaMalloc((void**)&K.Toff[1], sizeof(int64_t) * (nc + 1)))) return e;
+  }
+  // block descriptors in the order of DevSide::bidx (slots counting-sorted by cluster, setup_side)
+  std::vector<MvPack::Desc> dsc[2];
+  for (int side = 0; side < 2; ++side) {
+    const int ncl = side ? nc : nr;
+    std::vector<int32_t> ptr(ncl + 1, 0);
+    for (int a = 0; a < M.nadm; ++a) ptr[(side ? B->s[Z->adm_blk[a]] : B->t[Z->adm_blk[a]]) + 1]++;
+    for (int c = 0; c < ncl; ++c) ptr[c + 1] += ptr[c];
+    dsc[side].resize(M.nadm + 1);
+    for (int a = 0; a < M.nadm; ++a) {
+      const int b = Z->adm_blk[a];
+      const int own = side ? B->s[b] : B->t[b], other = side ? B->t[b] : B->s[b];
+      dsc[side][ptr[own]++] = MvPack::Desc{so[a], other, side ? kr[other] : kc[other]};
+    }
+    if ((e = cudaMemcpyAsync(K.desc[side], dsc[side].data(), sizeof(MvPack::Desc) * M.nadm, cudaMemcpyHostToDevice, st)))
+      return e;
   }
   if ((e = cudaMemcpyAsync(K.Soff, so.data(), sizeof(int64_t) * (M.nadm + 1), cudaMemcpyHostToDevice, st))) return e;
   if ((e = cudaMemcpyAsync(K.Toff[0], ro.data(), sizeof(int64_t) * (nr + 1), cudaMemcpyHostToDevice, st))) return e;
@@ -662,6 +818,8 @@ static cudaError_t ensure_packed(h2_mat_* Z, cudaStream_t st) {
   p.Sp = K.Sp;
   p.rTp = K.Tp[0];
   p.cTp = K.Tp[1];
+  p.rTpT = K.TpT[0];
+  p.cTpT = K.TpT[1];
   p.Soff = K.Soff;
   p.rToff = K.Toff[0];
   p.cToff = K.Toff[1];
@@ -677,7 +835,8 @@ static cudaError_t ensure_packed(h2_mat_* Z, cudaStream_t st) {
 
 void free_mvpack(h2_mat_* Z) {
   MvPack& K = Z->mvpack;
-  for (void* p : {(void*)K.Sp, (void*)K.Tp[0], (void*)K.Tp[1], (void*)K.Soff, (void*)K.Toff[0], (void*)K.Toff[1]})
+  for (void* p : {(void*)K.Sp, (void*)K.Tp[0], (void*)K.Tp[1], (void*)K.Soff, (void*)K.Toff[0], (void*)K.Toff[1],
+                  (void*)K.desc[0], (void*)K.desc[1], (void*)K.TpT[0], (void*)K.TpT[1]})
     if (p) cudaFree(p);
   K = MvPack();
 }
@@ -749,6 +908,8 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   a.d_level = dst.level;
   a.d_son1 = dst.son1;
   a.d_cnt = dst.mv_cnt;
+  a.dbg = nullptr;
+  a.desc = nullptr;
   a.Sp = nullptr;
   a.Soff = nullptr;
   a.s_Tp = a.d_Tp = nullptr;
@@ -765,13 +926,14 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   const MvPack& K = Z->mvpack;
   a.Sp = K.Sp;
   a.Soff = K.Soff;
-  a.s_Tp = K.Tp[transpose ? 0 : 1];
+  a.s_Tp = K.TpT[transpose ? 0 : 1];  // the forward transform applies F^T: transposed copies
   a.s_Toff = K.Toff[transpose ? 0 : 1];
   a.d_Tp = K.Tp[transpose ? 1 : 0];
   a.d_Toff = K.Toff[transpose ? 1 : 0];
-  // the far-field chain (latency-bound) runs on a high-priority side stream; the nearfield kernel
-  // (the bulk of the bytes) runs on the caller's stream with a grid of 2 CTAs per SM, so both are
-  // co-resident; the leaf backward transform adds V_t yhat_t after both
+  a.desc = K.desc[transpose ? 1 : 0];
+  // the far-field chain (latency-bound) runs on a high-priority side stream next to the nearfield
+  // kernel (the bulk of the bytes) on the caller's stream; the leaf backward transform adds
+  // V_t yhat_t after both
   static cudaStream_t s2 = nullptr;
   static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   static int nsm = 148;
@@ -781,23 +943,27 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
     if ((e = cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming))) return e;
-    const size_t sub_smem = sizeof(double) * ((size_t)SUB_NC * RCAP_MAX + SUB_TB);
-    if ((e = cudaFuncSetAttribute(k_mv_fwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem))) return e;
-    if ((e = cudaFuncSetAttribute(k_mv_bwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sub_smem))) return e;
+    if ((e = cudaFuncSetAttribute(k_mv_fwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB_SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_mv_bwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB_SMEM))) return e;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t smem = sizeof(double) * ((size_t)SUB_NC * M.rcap + SUB_TB);
+  const size_t smem = SUB_SMEM;
+  a.sub_tb = (int)(SUB_SMEM / sizeof(double)) - SUB_NC * M.rcap;
   // timing diagnostics (tools): H2_MV_PART=1 far field only, 2 nearfield only, 3 / 4 / 5: the far
   // field up to the forward transform / the couplings / the subtree backward transform (y is then
   // incomplete); H2_MV_NEARGRID: CTAs per SM of the nearfield kernel (default 2)
   static const int part = getenv("H2_MV_PART") ? atoi(getenv("H2_MV_PART")) : 0;
-  static const int near_per_sm = getenv("H2_MV_NEARGRID") ? atoi(getenv("H2_MV_NEARGRID")) : 2;
-  const int near_grid = std::min(cdiv(dst.nleaves, 8), std::max(1, near_per_sm) * nsm);
+  static const int near_per_sm = getenv("H2_MV_NEARGRID") ? atoi(getenv("H2_MV_NEARGRID")) : 0;
+  const int near_grid = near_per_sm > 0 ? std::min(cdiv(dst.nleaves, 8), near_per_sm * nsm) : cdiv(dst.nleaves, 8);
   if (part == 2) {
     H2_LAUNCH(K_MV, st, k_matvec_near<<<near_grid, 256, 0, st>>>(a));
     return cudaGetLastError();
   }
+  static unsigned long long* dbg = nullptr;
+  static const bool dbg_on = getenv("H2_MV_DBG") != nullptr;
+  if (dbg_on && !dbg) cudaMalloc((void**)&dbg, 16 * sizeof(unsigned long long));
+  a.dbg = dbg;
   cudaStream_t sf = part == 0 ? s2 : st;  // the far-field chain
   if (part == 0) {
     if ((e = cudaEventRecord(ev_fork, st))) return e;
@@ -816,6 +982,20 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
     if ((e = cudaStreamWaitEvent(st, ev_join, 0))) return e;
   }
   H2_LAUNCH(K_MV, st, k_mv_leaf_bwd<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
+  if (dbg_on) {  // diagnostic: phase stamps of this product, relative to the first kernel's start (us)
+    unsigned long long h[16];
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
+    static int calls = 0;
+    if (++calls % 16 == 0) {
+      const char* nm[13] = {"leaf_fwd start", "fwd_sub start", "last CTA in", "last CTA staged", "last CTA levels done",
+                            "last detected", "top fwd done", "couple start", "couple last detected", "top bwd done",
+                            "bwd_sub start", "bwd_sub cta0 end", "leaf_bwd start"};
+      fprintf(stderr, "[H2_MV_DBG]");
+      for (int i = 0; i < 13; ++i) fprintf(stderr, " %s %.1f;", nm[i], (double)((long long)h[i] - (long long)h[0]) / 1e3);
+      fprintf(stderr, "\n");
+    }
+  }
   return cudaGetLastError();
 }
 

@@ -47,10 +47,12 @@ __device__ void it_upd_ext_leaf(const MatDev& M, UpdArgs a_, int rl0, int nrl, i
   }
   if (b == 0 && threadIdx.x == 0 && nrl + ncl > 0) {
     const int idx = atomicAdd(M.flags + 3, 1);  // non-zero-rank update count
-    if (M.updlog && idx < (1 << 21)) {
-      M.updlog[3 * idx] = a.t0;
-      M.updlog[3 * idx + 1] = a.s0;
-      M.updlog[3 * idx + 2] = a.k;
+    if (M.updlog && idx < (1 << 20)) {
+      M.updlog[5 * idx] = a.t0;
+      M.updlog[5 * idx + 1] = a.s0;
+      M.updlog[5 * idx + 2] = a.k;
+      M.updlog[5 * idx + 3] = M.row.rank[a.t0];  // ranks before the update
+      M.updlog[5 * idx + 4] = M.col.rank[a.s0];
     }
   }
   if (b < nrl + ncl) {

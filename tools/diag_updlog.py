@@ -21,7 +21,7 @@ seq = []
 
 
 def rec(t, r, A, B, **k):
-    seq.append((t, r, A.shape[1], float(np.abs(A).max()), float(np.abs(B).max())))
+    seq.append((t, r, A.shape[1], int(s["OZ"].k[t]), int(s["OZ"].l[r]), float(np.abs(A).max()), float(np.abs(B).max())))
     return orig(t, r, A, B, **k)
 
 
@@ -53,7 +53,7 @@ P.h2_check_device_flags(s["Z"])
 g = [tuple(int(v) for v in l.split()) for l in open("/tmp/h2_updlog.txt")]
 print(name, N, "oracle", len(seq), "gpu", len(g))
 i = 0
-while i < min(len(seq), len(g)) and seq[i][:3] == g[i]:
+while i < min(len(seq), len(g)) and seq[i][:5] == g[i]:
     i += 1
 print("first difference at", i, "oracle", seq[i - 1:i + 3], "gpu", g[i - 1:i + 3])
 ot, ob = s["ot"], s["ob"]
