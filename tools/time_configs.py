@@ -219,20 +219,28 @@ TABLE1 = {7: (3.1e-3, 7.0e-5, 1.0, 0.06, 3), 8: (7.7e-4, 8.4e-5, 1.1, 0.07, 3), 
           10: (4.8e-5, 1.3e-4, 1.2, 0.10, 3), 11: (1.2e-5, 1.5e-4, 1.2, 0.11, 3)}  # l: eps^, Time/n, Mem/n KB, Err, m
 
 
-def run_table1(levels):
+def run_table1(levels, dd=False, jump=False):
+    """dd: the domain-decomposition cluster tree (NEXT-3, reading own-11) instead of geometric
+    bisection; jump: the C2 jump-coefficient problem at N = 512 with eta = 2, eps = 1e-4 relative
+    (the BASELINE C2 matrix on the DD tree) instead of the paper's Poisson settings."""
     from inputs.rng import POWER
     for l in levels:
         N = 2 ** l - 1
         eps = TABLE1[l][0]
         c = config("C1", N=N)  # the constant-coefficient 5-point problem (P:1399-1402)
-        t = P.h2_cluster_tree(c["points"], c["leaf"])
-        bt = P.h2_block_tree(t, t, 4.0)
+        eta, trunc = 4.0, P.Trunc(eps, abs_tol=1e-13 if dd else 0.0, blockwise=True)
+        if jump:
+            N = 2 ** l
+            c = config("C2", N=N)
+            eta, eps, trunc = 2.0, 1e-4, P.Trunc(1e-4, abs_tol=1e-13)
+        t = P.h2_cluster_tree_dd(c["points"], c["leaf"], c["A"]) if dd else P.h2_cluster_tree(c["points"], c["leaf"])
+        bt = P.h2_block_tree(t, t, eta)
         Aop = P.h2_from_sparse(bt, c["A"], lower=False, rank_cap=32, update_cap=32)
         Z = P.h2_from_sparse(bt, c["A"], lower=True, rank_cap=32, update_cap=32)
         torch.cuda.synchronize()
         e0, e1 = ev(), ev()
         e0.record()
-        P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps, blockwise=True))
+        P.h2_lr_factor(Z, cholesky=True, trunc=trunc)
         e1.record()
         torch.cuda.synchronize()
         flags = P.h2_check_device_flags(Z)
@@ -261,7 +269,10 @@ def run_table1(levels):
         kr, kc = P.h2_ranks(Z)
         setup_s = e0.elapsed_time(e1) / 1e3
         ref = TABLE1[l]
-        print(json.dumps({"config": f"Table 1 l={l}", "n": n, "eta": 4.0, "eps_hat": eps, "tree": "geometric bisection, leaf 32",
+        print(json.dumps({"config": ("C2 jump problem" if jump else f"Table 1 l={l}"), "n": n, "eta": eta, "eps_hat": eps,
+                          "truncation": "relative 1e-4 (+ abs 1e-13)" if jump else "block-relative (own-10)",
+                          "tree": ("domain decomposition (own-11)" if dd else "geometric bisection") + ", leaf 32",
+                          "clusters": int(t.nclusters), "blocks": int(bt.nblocks),
                           "setup_s": setup_s, "setup_s_per_dof": setup_s / n,
                           "mem_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / n / 1e3),
                           "Err": lam, "m": m, "pcg_relres": rel, "solve_s_per_step_per_dof": e2.elapsed_time(e3) / 1e3 / max(m, 1) / n,
@@ -272,10 +283,101 @@ def run_table1(levels):
         del Z, Aop
 
 
+TABLE2 = {11: (1.2e-4, 1.6e-4, 0.8, 0.05, 3), 12: (6.1e-5, 1.9e-4, 0.8, 0.03, 3), 13: (3.1e-5, 2.1e-4, 0.8, 0.03, 3),
+          14: (1.5e-5, 2.4e-4, 0.8, 0.02, 3), 15: (7.6e-6, 2.6e-4, 0.8, 0.02, 3), 16: (3.8e-6, 3.0e-4, 0.8, 0.02, 3)}
+
+
+def run_bem(levels):
+    """NEXT-4 (Table 2; reading own-12): single layer potential on the circle, n = 2^l
+    arcs, eta = 2, block-relative eps^ ~ h.  The H^2 matrix is built from the exact nearfield
+    entries by one h2_lowrank_update per admissible leaf (factors from inputs/bem.py, resident in
+    HBM before the clock starts), then factored (Cholesky, lower storage) and used in PCG."""
+    from inputs import bem
+    from inputs.rng import POWER
+    for l in levels:
+        n = 2 ** l
+        eps = TABLE2[l][0]
+        tr = P.Trunc(eps, blockwise=True)
+        t = P.h2_cluster_tree(bem.circle_points(n), 32)
+        bt = P.h2_block_tree(t, t, 2.0)
+        res = {}
+        mats = {}
+        for lower in (False, True):
+            w0 = time.perf_counter()
+            A_near, far = bem.pieces(n, t.perm, t.lo, t.hi, bt.t, bt.s, bt.kind, lower=lower)
+            gen_s = time.perf_counter() - w0
+            Z = P.h2_from_sparse(bt, A_near, lower=lower, rank_cap=32, update_cap=16)
+            Xs = [torch.from_numpy(np.asfortranarray(X)).to(dev) for _, _, X, _ in far]
+            Ys = [torch.from_numpy(np.asfortranarray(Y)).to(dev) for _, _, _, Y in far]
+            torch.cuda.synchronize()
+            e0, e1 = ev(), ev()
+            e0.record()
+            P.h2_batch_begin(torch.cuda.current_stream().cuda_stream)
+            for (t0, s0, _, _), X, Y in zip(far, Xs, Ys):
+                P.h2_lowrank_update(Z, t0, s0, X, Y, trunc=tr, stream=torch.cuda.current_stream().cuda_stream)
+            P.h2_batch_end()
+            e1.record()
+            torch.cuda.synchronize()
+            res["lower" if lower else "full"] = {"updates": len(far), "build_s": e0.elapsed_time(e1) / 1e3,
+                                                 "updates_per_s": len(far) / (e0.elapsed_time(e1) / 1e3), "generator_s": gen_s}
+            mats[lower] = Z
+            del Xs, Ys
+        Aop, Z = mats[False], mats[True]
+        # accuracy of the compressed operator against the exact circulant matrix (FFT product)
+        g = bem.first_row(n)
+        xv = np.random.default_rng(3).standard_normal(n)
+        ref = np.real(np.fft.ifft(np.fft.fft(g) * np.fft.fft(xv)))
+        yv = P.h2_matvec(Aop, torch.from_numpy(xv).to(dev)).cpu().numpy()
+        e0, e1 = ev(), ev()
+        e0.record()
+        P.h2_lr_factor(Z, cholesky=True, trunc=tr)
+        e1.record()
+        torch.cuda.synchronize()
+        flags = P.h2_check_device_flags(Z)
+        b = torch.from_numpy(stream(RHS).standard_normal(n)).to(dev)
+        x = torch.zeros_like(b)
+        e2, e3 = ev(), ev()
+        e2.record()
+        _, m, rel = P.h2_pcg(Aop, Z, b, x, tol=1e-8)
+        e3.record()
+        torch.cuda.synchronize()
+        v = torch.from_numpy(stream(POWER).standard_normal(n)).to(dev)
+        v /= torch.linalg.norm(v)
+        lam = 0.0
+        for it in range(50):
+            w = P.h2_matvec(Aop, v)
+            P.h2_solve(Z, w)
+            w = v - w
+            new = float(torch.linalg.norm(w))
+            v = w / new
+            if it > 0 and abs(new - lam) <= 1e-4 * new:
+                lam = new
+                break
+            lam = new
+        kr, kc = P.h2_ranks(Z)
+        setup_s = e0.elapsed_time(e1) / 1e3
+        ref2 = TABLE2[l]
+        print(json.dumps({"config": f"Table 2 l={l} (BEM single layer potential, circle r=1/2)", "n": n, "eta": 2.0, "eps_hat": eps,
+                          "compression_by_local_updates": res,
+                          "operator_rel_err_vs_exact": float(np.linalg.norm(yv - ref) / np.linalg.norm(ref)),
+                          "setup_s": setup_s, "setup_s_per_dof": setup_s / n,
+                          "mem_KB_per_dof": float(P.h2_storage_report(Z).sum() * 8 / n / 1e3),
+                          "Err": lam, "m": m, "pcg_relres": rel,
+                          "solve_s_per_step_per_dof": e2.elapsed_time(e3) / 1e3 / max(m, 1) / n,
+                          "max_rank": [int(kr.max()), int(kc.max())], "flags": flags, "stats": P.h2_stats(Z),
+                          "matvec_operator": matvec_gbps(Aop, n), "matvec_factor": matvec_gbps(Z, n),
+                          "paper_table2": {"setup_s_per_dof": ref2[1], "mem_KB_per_dof": ref2[2], "Err": ref2[3], "m": ref2[4],
+                                           "machine": "one Opteron 8431 core"}}), flush=True)
+        del mats, Aop, Z
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
-    if what == "table1":
-        run_table1([int(a) for a in sys.argv[2:]] or [7, 8, 9])
+    if what == "bem":
+        run_bem([int(a) for a in sys.argv[2:]] or [11, 13])
+        sys.exit(0)
+    if what in ("table1", "table1dd", "c2dd"):
+        run_table1([int(a) for a in sys.argv[2:]] or [7, 8, 9], dd=what != "table1", jump=what == "c2dd")
         sys.exit(0)
     if what == "c1":
         run_c1(int(sys.argv[2]) if len(sys.argv) > 2 else 10000)
