@@ -724,6 +724,11 @@ extern "C" h2_status h2_check_device_flags(h2_mat Z, int32_t* flags) {
     }
   }
   flags[0] = f[0] | (f[1] ? 2 : 0);
+  if (f[0] & 4) {  // reported first: a dropped contribution usually ends in a leaf breakdown as well
+    h2::set_error("a contribution's rank exceeded update_cap and was dropped: the result is invalid; "
+                  "rebuild the matrix with a larger update_cap (up to the leaf size)");
+    return H2_ERR_NOMEM;
+  }
   if (f[1]) {
     char msg[160];
     snprintf(msg, sizeof msg, "dense leaf breakdown (non-positive / tiny pivot) in the diagonal tile of cluster %d", f[2]);

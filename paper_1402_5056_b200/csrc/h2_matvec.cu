@@ -75,6 +75,13 @@ __device__ __forceinline__ void stamp(const MvArgs& a, int i) {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// Programmatic dependent launch (the far-field chain): a kernel launched with the attribute may
+// start while its predecessor in the stream still runs; pdl_wait() blocks until the predecessor
+// has completed and its memory is visible, pdl_trigger() lets the successor start launching.
+// Everything before pdl_wait() must not read what the predecessor writes.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- nearfield rows of a destination leaf: (a0, a1) += sum_b N_b x|s ----------------------------
 __device__ __forceinline__ void mv_near(const MvArgs& a, int t, int m, int lane, double& a0, double& a1) {
   const int lmax = a.lmax;
@@ -110,19 +117,48 @@ __device__ __forceinline__ void mv_near(const MvArgs& a, int t, int m, int lane,
           }
         }
       }
-    } else {  // y|t += N_b^T x|s: row `lane` of N_b^T is column `lane` of N_b
-      const int i1 = ms < 32 ? ms : 32;
-#pragma unroll 8
-      for (int i = 0; i < i1; ++i) {
-        const double xi = __shfl_sync(FULL, xs0, i);
-        if (lane < m) a0 += __ldg(Na + i + (size_t)lane * lmax) * xi;
-        if (lane + 32 < m) a1 += __ldg(Na + i + (size_t)(lane + 32) * lmax) * xi;
-      }
-#pragma unroll 8
-      for (int i = 32; i < ms; ++i) {
-        const double xi = __shfl_sync(FULL, xs1, i - 32);
-        if (lane < m) a0 += __ldg(Na + i + (size_t)lane * lmax) * xi;
-        if (lane + 32 < m) a1 += __ldg(Na + i + (size_t)(lane + 32) * lmax) * xi;
+    } else {
+      // y|t += N_b^T x|s with N_b stored |s| x |t|: y[j] = sum_i N[i, j] x[i].  Lanes own the rows i
+      // (coalesced 256 B column loads, 16-column panels as above); the 16 column sums over the 32
+      // lanes are formed by recursive halving (8 + 4 + 2 + 1 + 1 shuffles per panel): afterwards
+      // lane L holds the sum of panel column L >> 1, and lane L accumulates the panels with
+      // (panel & 1) == (L & 1): lane L owns output column 16 (L & 1) + (L >> 1) (+ 32 in a1).
+      const unsigned b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+      for (int j0 = 0; j0 < m; j0 += 16) {  // m = |t| output columns, ms = |s| rows
+        const double* Nj = Na + (size_t)j0 * lmax;
+        double v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          double p = 0.0;
+          if (j0 + j < m) {
+            if (lane < ms) p = __ldcs(Nj + lane + (size_t)j * lmax) * xs0;
+            if (lane + 32 < ms) p += __ldcs(Nj + lane + 32 + (size_t)j * lmax) * xs1;
+          }
+          v[j] = p;
+        }
+        double w8[8], w4[4], w2[2];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double mine = b4 ? v[k + 8] : v[k], other = b4 ? v[k] : v[k + 8];
+          w8[k] = mine + __shfl_xor_sync(FULL, other, 16);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double mine = b3 ? w8[k + 4] : w8[k], other = b3 ? w8[k] : w8[k + 4];
+          w4[k] = mine + __shfl_xor_sync(FULL, other, 8);
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const double mine = b2 ? w4[k + 2] : w4[k], other = b2 ? w4[k] : w4[k + 2];
+          w2[k] = mine + __shfl_xor_sync(FULL, other, 4);
+        }
+        double w1 = (b1 ? w2[1] : w2[0]) + __shfl_xor_sync(FULL, b1 ? w2[0] : w2[1], 2);
+        w1 += __shfl_xor_sync(FULL, w1, 1);
+        const int panel = j0 >> 4;
+        if ((panel & 1) == (lane & 1)) {
+          if (panel < 2) a0 += w1;
+          else a1 += w1;
+        }
       }
     }
   }
@@ -133,12 +169,14 @@ __device__ void mv_leaf_near(const MvArgs& a, int t, int lane) {
   const int lo = a.d_lo[t], m = a.d_hi[t] - lo;
   double a0 = 0.0, a1 = 0.0;
   mv_near(a, t, m, lane, a0, a1);
-  if (lane < m) {
-    const int64_t o = a.d_perm[lo + lane];
+  // no transpose: lane owns rows lane, lane + 32; transpose: columns c, c + 32 with c = 16 (lane & 1) + (lane >> 1)
+  const int c = a.transpose ? 16 * (lane & 1) + (lane >> 1) : lane;
+  if (c < m) {
+    const int64_t o = a.d_perm[lo + c];
     a.y[o] = a.beta == 0.0 ? a.alpha * a0 : a.alpha * a0 + a.beta * a.y[o];
   }
-  if (lane + 32 < m) {
-    const int64_t o = a.d_perm[lo + lane + 32];
+  if (c + 32 < m) {
+    const int64_t o = a.d_perm[lo + c + 32];
     a.y[o] = a.beta == 0.0 ? a.alpha * a1 : a.alpha * a1 + a.beta * a.y[o];
   }
 }
@@ -295,6 +333,7 @@ __device__ __forceinline__ void bwd_cluster(const SubList& L, int i, int ip, int
 
 __global__ void __launch_bounds__(256) k_mv_leaf_fwd(const __grid_constant__ MvArgs a) {
   if (blockIdx.x == 0) stamp(a, 0);
+  pdl_trigger();
   const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
   if (w < a.s_nleaves) fwd_leaf(a, a.s_leaves[w], threadIdx.x & 31);
 }
@@ -351,6 +390,8 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ 
   stage_load(a.s_Tp, a.s_Toff, root, n, SR, tbuf, a.sub_tb);
   prefetch_top(a.s_Tp, a.s_Toff, a.s_top, a.s_top_lptr[a.s_top_nlev]);
   build_sublist(a.s_level, a.s_tsize, root, L, a.s_rank, a.s_son0, a.s_son1, a.s_parent, a.s_Toff);
+  pdl_trigger();
+  pdl_wait();  // the leaves' coefficients (k_mv_leaf_fwd)
   if (n > 1) {
     // the leaves' coefficients (k_mv_leaf_fwd) -- the subtree's xhat rows are contiguous in global
     const double* xg = a.s_xh + (size_t)root * rcap;
@@ -558,6 +599,8 @@ __global__ void __launch_bounds__(256, 4) k_mv_couple_top(const __grid_constant_
   const int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5));
   if (blockIdx.x == 0) stamp(a, 7);
   prefetch_top(a.d_Tp, a.d_Toff, a.d_top, a.d_top_lptr[a.d_top_nlev]);
+  pdl_trigger();
+  pdl_wait();  // the forward coefficients (k_mv_fwd_sub)
   if (w < a.d_nclusters) {
     if (a.transpose) mv_couple_packed<true>(a, w, lane);
     else mv_couple_packed<false>(a, w, lane);
@@ -613,13 +656,14 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_bwd_sub(const __grid_constant__ 
   // the root's father (a top cluster, final in global memory) and the root's own transfer matrix
   const int pr = a.d_parent[root];
   const int kpr = pr >= 0 ? a.d_rank[pr] : 0;
+  build_sublist(a.d_level, a.d_tsize, root, L, a.d_rank, a.d_son0, a.d_son1, a.d_parent, a.d_Toff);
+  pdl_wait();  // the couplings and the top clusters' yhat (k_mv_couple_top)
   double ypr0 = 0.0, ypr1 = 0.0;
   if (warp == 0 && pr >= 0) {
     const double* yp = a.d_xh + (size_t)pr * rcap;
     ypr0 = lane < kpr ? __ldcg(yp + lane) : 0.0;
     ypr1 = lane + 32 < kpr ? __ldcg(yp + lane + 32) : 0.0;
   }
-  build_sublist(a.d_level, a.d_tsize, root, L, a.d_rank, a.d_son0, a.d_son1, a.d_parent, a.d_Toff);
   double* yg = a.d_xh + (size_t)root * rcap;
   for (int i = warp; i < n; i += nw) {
     const int k = L.rk[i];
@@ -969,12 +1013,31 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
     if ((e = cudaEventRecord(ev_fork, st))) return e;
     if ((e = cudaStreamWaitEvent(s2, ev_fork, 0))) return e;
   }
+  // the dependent kernels of the chain are launched programmatically (their prologues -- staging,
+  // sublists, prefetches -- overlap the predecessor's tail); H2_MV_NOPDL=1: plain launches (A/B)
+  static const bool pdl = !(getenv("H2_MV_NOPDL") && atoi(getenv("H2_MV_NOPDL")) != 0);
+  auto launch_dep = [&](auto kern, int grid, int block, size_t sm) -> cudaError_t {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = sf;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+  };
   H2_LAUNCH(K_MV, sf, k_mv_leaf_fwd<<<cdiv(src.nleaves, 8), 256, 0, sf>>>(a));
-  H2_LAUNCH(K_MV, sf, k_mv_fwd_sub<<<src.n_mv_roots, SUBT, smem, sf>>>(a));
+  H2_LAUNCH(K_MV, sf, e = launch_dep(k_mv_fwd_sub, src.n_mv_roots, SUBT, smem));
+  if (e) return e;
   if (part == 3) return cudaGetLastError();
-  H2_LAUNCH(K_MV, sf, k_mv_couple_top<<<cdiv(dst.nclusters, 8), 256, 0, sf>>>(a));
+  H2_LAUNCH(K_MV, sf, e = launch_dep(k_mv_couple_top, cdiv(dst.nclusters, 8), 256, 0));
+  if (e) return e;
   if (part == 4) return cudaGetLastError();
-  H2_LAUNCH(K_MV, sf, k_mv_bwd_sub<<<dst.n_mv_roots, SUBT, smem, sf>>>(a));
+  H2_LAUNCH(K_MV, sf, e = launch_dep(k_mv_bwd_sub, dst.n_mv_roots, SUBT, smem));
+  if (e) return e;
   if (part == 5) return cudaGetLastError();
   if (part == 0) {
     if ((e = cudaEventRecord(ev_join, s2))) return e;

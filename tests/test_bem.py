@@ -103,7 +103,7 @@ def test_bem_gpu_parity(n, eps, bw):
         ot, ob, OZ, A_near, far = _oracle_build(n, eps, lower=lower, bw=bw)
         np.testing.assert_array_equal(t.perm, ot.perm)
         np.testing.assert_array_equal(bt.kind, ob.kind)
-        Z = P.h2_from_sparse(bt, A_near, lower=lower, rank_cap=32, update_cap=16)
+        Z = P.h2_from_sparse(bt, A_near, lower=lower, rank_cap=32, update_cap=32)
         keep = [P.h2_lowrank_update(Z, t0, s0, _t(X), _t(Y), trunc=tr) for t0, s0, X, Y in far]
         kr, kc = P.h2_ranks(Z)
         np.testing.assert_array_equal(kr, OZ.k)

@@ -306,7 +306,7 @@ def run_bem(levels):
             w0 = time.perf_counter()
             A_near, far = bem.pieces(n, t.perm, t.lo, t.hi, bt.t, bt.s, bt.kind, lower=lower)
             gen_s = time.perf_counter() - w0
-            Z = P.h2_from_sparse(bt, A_near, lower=lower, rank_cap=32, update_cap=16)
+            Z = P.h2_from_sparse(bt, A_near, lower=lower, rank_cap=32, update_cap=32)
             Xs = [torch.from_numpy(np.asfortranarray(X)).to(dev) for _, _, X, _ in far]
             Ys = [torch.from_numpy(np.asfortranarray(Y)).to(dev) for _, _, _, Y in far]
             torch.cuda.synchronize()
