@@ -83,6 +83,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ---- nearfield rows of a destination leaf: (a0, a1) += sum_b N_b x|s ----------------------------
+template <bool TR>
 __device__ __forceinline__ void mv_near(const MvArgs& a, int t, int m, int lane, double& a0, double& a1) {
   const int lmax = a.lmax;
   for (int q = a.nptr[t]; q < a.nptr[t + 1]; ++q) {
@@ -92,7 +93,7 @@ __device__ __forceinline__ void mv_near(const MvArgs& a, int t, int m, int lane,
     const double xs0 = lane < ms ? a.x[a.s_perm[los + lane]] : 0.0;
     const double xs1 = lane + 32 < ms ? a.x[a.s_perm[los + lane + 32]] : 0.0;
     const double* Na = a.N + (size_t)slot * lmax * lmax;
-    if (!a.transpose) {
+    if (!TR) {
       for (int j0 = 0; j0 < ms; j0 += 16) {
         const int jn = ms - j0 < 16 ? ms - j0 : 16;
         const double xsrc = j0 >= 32 ? xs1 : xs0;
@@ -117,60 +118,33 @@ __device__ __forceinline__ void mv_near(const MvArgs& a, int t, int m, int lane,
           }
         }
       }
-    } else {
-      // y|t += N_b^T x|s with N_b stored |s| x |t|: y[j] = sum_i N[i, j] x[i].  Lanes own the rows i
-      // (coalesced 256 B column loads, 16-column panels as above); the 16 column sums over the 32
-      // lanes are formed by recursive halving (8 + 4 + 2 + 1 + 1 shuffles per panel): afterwards
-      // lane L holds the sum of panel column L >> 1, and lane L accumulates the panels with
-      // (panel & 1) == (L & 1): lane L owns output column 16 (L & 1) + (L >> 1) (+ 32 in a1).
-      const unsigned b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-      for (int j0 = 0; j0 < m; j0 += 16) {  // m = |t| output columns, ms = |s| rows
-        const double* Nj = Na + (size_t)j0 * lmax;
-        double v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          double p = 0.0;
-          if (j0 + j < m) {
-            if (lane < ms) p = __ldcs(Nj + lane + (size_t)j * lmax) * xs0;
-            if (lane + 32 < ms) p += __ldcs(Nj + lane + 32 + (size_t)j * lmax) * xs1;
-          }
-          v[j] = p;
-        }
-        double w8[8], w4[4], w2[2];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const double mine = b4 ? v[k + 8] : v[k], other = b4 ? v[k] : v[k + 8];
-          w8[k] = mine + __shfl_xor_sync(FULL, other, 16);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double mine = b3 ? w8[k + 4] : w8[k], other = b3 ? w8[k] : w8[k + 4];
-          w4[k] = mine + __shfl_xor_sync(FULL, other, 8);
-        }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const double mine = b2 ? w4[k + 2] : w4[k], other = b2 ? w4[k] : w4[k + 2];
-          w2[k] = mine + __shfl_xor_sync(FULL, other, 4);
-        }
-        double w1 = (b1 ? w2[1] : w2[0]) + __shfl_xor_sync(FULL, b1 ? w2[0] : w2[1], 2);
-        w1 += __shfl_xor_sync(FULL, w1, 1);
-        const int panel = j0 >> 4;
-        if ((panel & 1) == (lane & 1)) {
-          if (panel < 2) a0 += w1;
-          else a1 += w1;
-        }
+    } else {  // y|t += N_b^T x|s: row `lane` of N_b^T is column `lane` of N_b
+      // (a coalesced variant -- lanes own the rows of N_b, 16-column panels, column sums by
+      // recursive halving -- measured slower: 435 us against 318-359 us for the C2 operator)
+      const int i1 = ms < 32 ? ms : 32;
+#pragma unroll 8
+      for (int i = 0; i < i1; ++i) {
+        const double xi = __shfl_sync(FULL, xs0, i);
+        if (lane < m) a0 += __ldg(Na + i + (size_t)lane * lmax) * xi;
+        if (lane + 32 < m) a1 += __ldg(Na + i + (size_t)(lane + 32) * lmax) * xi;
+      }
+#pragma unroll 8
+      for (int i = 32; i < ms; ++i) {
+        const double xi = __shfl_sync(FULL, xs1, i - 32);
+        if (lane < m) a0 += __ldg(Na + i + (size_t)lane * lmax) * xi;
+        if (lane + 32 < m) a1 += __ldg(Na + i + (size_t)(lane + 32) * lmax) * xi;
       }
     }
   }
 }
 
 // ---- nearfield of one destination leaf: y|t = alpha sum_b N_b x|s + beta y|t ----------------------
-__device__ void mv_leaf_near(const MvArgs& a, int t, int lane) {
+template <bool TR>
+__device__ __forceinline__ void mv_leaf_near(const MvArgs& a, int t, int lane) {
   const int lo = a.d_lo[t], m = a.d_hi[t] - lo;
   double a0 = 0.0, a1 = 0.0;
-  mv_near(a, t, m, lane, a0, a1);
-  // no transpose: lane owns rows lane, lane + 32; transpose: columns c, c + 32 with c = 16 (lane & 1) + (lane >> 1)
-  const int c = a.transpose ? 16 * (lane & 1) + (lane >> 1) : lane;
+  mv_near<TR>(a, t, m, lane, a0, a1);
+  const int c = lane;
   if (c < m) {
     const int64_t o = a.d_perm[lo + c];
     a.y[o] = a.beta == 0.0 ? a.alpha * a0 : a.alpha * a0 + a.beta * a.y[o];
@@ -186,7 +160,13 @@ __global__ void __launch_bounds__(256, 4) k_matvec_near(const __grid_constant__ 
   // fewer CTAs per SM, H2_MV_NEARGRID, measured slower: 90 us against 66 us at 2 CTAs per SM)
   const int nw = (int)(gridDim.x * (blockDim.x >> 5));
   for (int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w < a.d_nleaves; w += nw)
-    mv_leaf_near(a, a.d_leaves[w], threadIdx.x & 31);
+    mv_leaf_near<false>(a, a.d_leaves[w], threadIdx.x & 31);
+}
+// the transposed product as its own kernel (its own register allocation)
+__global__ void __launch_bounds__(256, 2) k_matvec_near_t(const __grid_constant__ MvArgs a) {
+  const int nw = (int)(gridDim.x * (blockDim.x >> 5));
+  for (int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w < a.d_nleaves; w += nw)
+    mv_leaf_near<true>(a, a.d_leaves[w], threadIdx.x & 31);
 }
 
 
@@ -962,7 +942,7 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   const bool far = std::find(Z->nzr.begin(), Z->nzr.end(), 1) != Z->nzr.end() &&
                    std::find(Z->nzc.begin(), Z->nzc.end(), 1) != Z->nzc.end();
   if (!far) {
-    H2_LAUNCH(K_MV, st, k_matvec_near<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
+    H2_LAUNCH(K_MV, st, (transpose ? k_matvec_near_t : k_matvec_near)<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
     return cudaGetLastError();
   }
   cudaError_t e;
@@ -1001,7 +981,7 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   static const int near_per_sm = getenv("H2_MV_NEARGRID") ? atoi(getenv("H2_MV_NEARGRID")) : 0;
   const int near_grid = near_per_sm > 0 ? std::min(cdiv(dst.nleaves, 8), near_per_sm * nsm) : cdiv(dst.nleaves, 8);
   if (part == 2) {
-    H2_LAUNCH(K_MV, st, k_matvec_near<<<near_grid, 256, 0, st>>>(a));
+    H2_LAUNCH(K_MV, st, (transpose ? k_matvec_near_t : k_matvec_near)<<<near_grid, 256, 0, st>>>(a));
     return cudaGetLastError();
   }
   static unsigned long long* dbg = nullptr;
@@ -1041,7 +1021,7 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   if (part == 5) return cudaGetLastError();
   if (part == 0) {
     if ((e = cudaEventRecord(ev_join, s2))) return e;
-    H2_LAUNCH(K_MV, st, k_matvec_near<<<near_grid, 256, 0, st>>>(a));
+    H2_LAUNCH(K_MV, st, (transpose ? k_matvec_near_t : k_matvec_near)<<<near_grid, 256, 0, st>>>(a));
     if ((e = cudaStreamWaitEvent(st, ev_join, 0))) return e;
   }
   H2_LAUNCH(K_MV, st, k_mv_leaf_bwd<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));

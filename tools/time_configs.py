@@ -288,14 +288,14 @@ TABLE2 = {11: (1.2e-4, 1.6e-4, 0.8, 0.05, 3), 12: (6.1e-5, 1.9e-4, 0.8, 0.03, 3)
 
 
 def run_bem(levels):
-    """NEXT-4 (Table 2; reading own-12): single layer potential on the circle, n = 2^l
-    arcs, eta = 2, block-relative eps^ ~ h.  The H^2 matrix is built from the exact nearfield
+    """NEXT-4 (Table 2; reading own-12): single layer potential on the circle, n = 2^(l+2)
+    arcs (the paper's l = 11 row has n = 8,192), eta = 2, block-relative eps^ ~ h.  The H^2 matrix is built from the exact nearfield
     entries by one h2_lowrank_update per admissible leaf (factors from inputs/bem.py, resident in
     HBM before the clock starts), then factored (Cholesky, lower storage) and used in PCG."""
     from inputs import bem
     from inputs.rng import POWER
     for l in levels:
-        n = 2 ** l
+        n = 2 ** (l + 2)
         eps = TABLE2[l][0]
         tr = P.Trunc(eps, blockwise=True)
         t = P.h2_cluster_tree(bem.circle_points(n), 32)
@@ -306,7 +306,7 @@ def run_bem(levels):
             w0 = time.perf_counter()
             A_near, far = bem.pieces(n, t.perm, t.lo, t.hi, bt.t, bt.s, bt.kind, lower=lower)
             gen_s = time.perf_counter() - w0
-            Z = P.h2_from_sparse(bt, A_near, lower=lower, rank_cap=32, update_cap=32)
+            Z = P.h2_from_sparse(bt, A_near, lower=lower, rank_cap=48, update_cap=32)
             Xs = [torch.from_numpy(np.asfortranarray(X)).to(dev) for _, _, X, _ in far]
             Ys = [torch.from_numpy(np.asfortranarray(Y)).to(dev) for _, _, _, Y in far]
             torch.cuda.synchronize()
