@@ -455,8 +455,8 @@ static h2_status setup_side(h2_mat_* Z, DevSide& D, const h2_tree_* T, bool row_
     CUDA_TRY(dupload(Z, &D.mv_roots, roots));
     CUDA_TRY(dupload(Z, &D.mv_top, top));
     CUDA_TRY(dupload(Z, &D.mv_top_lptr, D.h_top_lptr));
-    CUDA_TRY(dalloc(Z, &D.mv_cnt, 2));
-    CUDA_TRY(cudaMemset(D.mv_cnt, 0, 2 * sizeof(int32_t)));
+    CUDA_TRY(dalloc(Z, &D.mv_cnt, 4));
+    CUDA_TRY(cudaMemset(D.mv_cnt, 0, 4 * sizeof(int32_t)));
   }
   return H2_OK;
 }

@@ -88,7 +88,8 @@ struct DevSide {
   int32_t* mv_top_lptr = nullptr; // level l of the top: mv_top[mv_top_lptr[l] .. mv_top_lptr[l+1])
   int mv_top_nlev = 0;
   std::vector<int32_t> h_top_lptr;  // host copy of mv_top_lptr
-  int32_t* mv_cnt = nullptr;        // 2 arrival counters (reset by their last user)
+  int32_t* mv_cnt = nullptr;        // [0] subtrees published, [1] top pass done (epoch counters, never reset); [2] couplings' arrival counter
+  unsigned mv_epoch = 0;            // products whose forward transform ran on this side
   double* hx = nullptr;     // H^2-block x dense workspace: nclusters * rcap * 64 (forward coefficients)
   double* hy = nullptr;     // nclusters * rcap * 64 (coupling/backward coefficients)
 };

@@ -60,6 +60,9 @@ struct MvArgs {
   const int64_t* Soff;
   const double *s_Tp, *d_Tp;
   const int64_t *s_Toff, *d_Toff;
+  int s_nroots;              // CTAs of k_mv_fwd_sub (subtrees of the source side)
+  unsigned s_epoch;          // products run on this source side so far + 1: the forward counters never reset
+  int same_tree;             // rows and columns share the cluster tree (levels comparable)
   int sub_tb;                // doubles of staged transfers per subtree CTA (shared memory budget)
   const MvPack::Desc* desc;  // blocks of the destination clusters in d_bidx order
   unsigned long long* dbg;  // H2_MV_DBG: globaltimer stamps of the far-field phases (diagnostic)
@@ -405,7 +408,9 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ 
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    last = atomicAdd(a.s_cnt, 1) == (int)gridDim.x - 1;
+    // [0] counts the published subtrees of all products (never reset): this product's go from
+    // (epoch - 1) n_roots to epoch n_roots
+    last = (unsigned)atomicAdd(a.s_cnt, 1) == a.s_epoch * (unsigned)gridDim.x - 1u;
   }
   __syncthreads();
   if (!last) return;
@@ -479,7 +484,10 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ 
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) a.s_cnt[0] = 0;
+  if (threadIdx.x == 0) {  // every forward coefficient is final: [1] = epoch
+    __threadfence();
+    atomicExch(a.s_cnt + 1, (int)a.s_epoch);
+  }
   stamp(a, 6);
 }
 
@@ -580,8 +588,17 @@ __global__ void __launch_bounds__(256, 4) k_mv_couple_top(const __grid_constant_
   if (blockIdx.x == 0) stamp(a, 7);
   prefetch_top(a.d_Tp, a.d_Toff, a.d_top, a.d_top_lptr[a.d_top_nlev]);
   pdl_trigger();
-  pdl_wait();  // the forward coefficients (k_mv_fwd_sub)
+  // The forward coefficients: a cluster below the top levels has only partners inside the
+  // subtrees, final once every subtree CTA of k_mv_fwd_sub has published ([0] == s_nroots); the
+  // others wait for the top pass of its last CTA ([1]).  So the bulk of the couplings overlaps
+  // the top forward pass.  (k_mv_fwd_sub's CTAs are all resident before this kernel may start --
+  // programmatic launch after their trigger, or a plain launch after their end: no deadlock.)
   if (w < a.d_nclusters) {
+    const bool low = a.same_tree && a.d_level[w] >= a.s_top_nlev;
+    const volatile int* flag = a.s_cnt + (low ? 0 : 1);
+    const unsigned need = low ? a.s_epoch * (unsigned)a.s_nroots : a.s_epoch;
+    while ((int)((unsigned)*flag - need) < 0) __nanosleep(200);
+    __threadfence();
     if (a.transpose) mv_couple_packed<true>(a, w, lane);
     else mv_couple_packed<false>(a, w, lane);
   }
@@ -931,7 +948,7 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   a.d_tsize = dst.tsize;
   a.d_level = dst.level;
   a.d_son1 = dst.son1;
-  a.d_cnt = dst.mv_cnt;
+  a.d_cnt = dst.mv_cnt + 2;  // [0], [1]: this side's forward epoch counters; [2]: the couplings' arrival counter
   a.dbg = nullptr;
   a.desc = nullptr;
   a.Sp = nullptr;
@@ -974,6 +991,9 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   }
   const size_t smem = SUB_SMEM;
   a.sub_tb = (int)(SUB_SMEM / sizeof(double)) - SUB_NC * M.rcap;
+  a.s_nroots = src.n_mv_roots;
+  a.s_epoch = ++const_cast<DevSide&>(src).mv_epoch;
+  a.same_tree = Z->bt->rt == Z->bt->ct ? 1 : 0;
   // timing diagnostics (tools): H2_MV_PART=1 far field only, 2 nearfield only, 3 / 4 / 5: the far
   // field up to the forward transform / the couplings / the subtree backward transform (y is then
   // incomplete); H2_MV_NEARGRID: CTAs per SM of the nearfield kernel (default 2)

@@ -135,3 +135,28 @@ def test_bem_gpu_parity(n, eps, bw):
     print(f"BEM n={n} eps={eps}: build diff {mats[False][2]:.2e}/{mats[True][2]:.2e}, factor diff {dL:.2e}, "
           f"max rank {OZL.k.max()}, PCG m gpu {m_g} oracle {m_o}")
     assert dL <= 10 * eps and rel < 1e-8 and abs(m_g - m_o) <= 1
+
+
+@pytest.mark.gpu
+def test_update_capacity_overrun_is_reported():
+    """A contribution inside the factorization whose rank exceeds update_cap (a dense x dense product
+    of 32-point leaves can reach rank 32, reading own-7) is dropped and reported (flag bit 2,
+    H2_ERR_NOMEM), not written past the extended-rank workspace."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1402_5056_b200 as P
+
+    n, eps = 1024, 1e-6
+    t = P.h2_cluster_tree(bem.circle_points(n), 32)
+    bt = P.h2_block_tree(t, t, 2.0)
+    A_near, far = bem.pieces(n, t.perm, t.lo, t.hi, bt.t, bt.s, bt.kind, lower=True)
+    Z = P.h2_from_sparse(bt, A_near, lower=True, rank_cap=32, update_cap=16)
+    keep = [P.h2_lowrank_update(Z, t0, s0, torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda(), trunc=P.Trunc(eps))
+            for t0, s0, X, Y in far]
+    assert P.h2_check_device_flags(Z) == 0
+    P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps))
+    with pytest.raises(P.H2Error) as e:
+        P.h2_check_device_flags(Z)
+    assert e.value.status == "H2_ERR_NOMEM" and "update_cap" in str(e.value)
+    del keep
