@@ -82,6 +82,28 @@ constexpr unsigned FULL = 0xffffffffu;
 // start while its predecessor in the stream still runs; pdl_wait() blocks until the predecessor
 // has completed and its memory is visible, pdl_trigger() lets the successor start launching.
 // Everything before pdl_wait() must not read what the predecessor writes.
+// Far-field operands (leaf bases, packed transfers and couplings: ~90 MB at C2) are loaded with the
+// L2 evict_last priority, the nearfield tiles (~340 MB per product) stream with evict_first
+// (__ldcs): across consecutive products of the same matrix the far field then stays resident in
+// the 126 MB L2 and its dependent round trips hit L2 instead of queueing behind the nearfield
+// stream in DRAM.  H2_MV_NOHINT=1 (compile-time -DH2_MV_NOHINT) disables the hint for A/B runs.
+__device__ __forceinline__ unsigned long long el_policy() {
+  unsigned long long pol = 0;
+#ifndef H2_MV_NOHINT
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  return pol;
+}
+__device__ __forceinline__ double ld_el(const double* p, unsigned long long pol) {
+#ifdef H2_MV_NOHINT
+  return *p;
+#else
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+#endif
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -165,6 +187,74 @@ __global__ void __launch_bounds__(256, 4) k_matvec_near(const __grid_constant__ 
   for (int w = (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)); w < a.d_nleaves; w += nw)
     mv_leaf_near<false>(a, a.d_leaves[w], threadIdx.x & 31);
 }
+// Nearfield with shared-memory staging (32-point leaves, no transpose): a persistent grid of ONE
+// small CTA per SM (NEAR_W warps, 16 KB of shared memory per warp); every warp streams the tiles
+// of its destination leaves through a two-slot ring with cp.async (an 8 KB tile = 16 16-byte
+// copies per lane), so NEAR_W x 16 KB are in flight per SM without holding registers or SM slots:
+// the far-field kernels could stay co-resident on every SM instead of waiting for nearfield CTAs
+// to retire (the register-panel kernel above needs 4 CTAs x 8 warps per SM and fills the register
+// file).  Measured slower (see the launcher) and therefore off by default: an experiment kept
+// for the next step (a deeper ring fed by bulk copies).  The slots' padding is zero and x_j = 0 beyond |s|,
+// so a tile is always multiplied as 32 x 32.
+constexpr int NEAR_W = 4;
+__global__ void __launch_bounds__(NEAR_W * 32, 1) k_matvec_near_s(const __grid_constant__ MvArgs a) {
+  extern __shared__ __align__(16) double nsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ring = nsm + (size_t)warp * 2048;
+  const unsigned rbase = (unsigned)__cvta_generic_to_shared(ring);
+  const int nwarps = (int)gridDim.x * NEAR_W;
+  for (int w = (int)blockIdx.x * NEAR_W + warp; w < a.d_nleaves; w += nwarps) {
+    const int t = a.d_leaves[w];
+    const int lo = a.d_lo[t], m = a.d_hi[t] - lo;
+    const int qb = a.nptr[t], qe = a.nptr[t + 1];
+    auto issue = [&](int q, int buf) {
+      const double* src = a.N + (size_t)a.nidx[q] * 1024;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = (u * 32 + lane) * 2;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(rbase + (unsigned)(buf * 1024 + e) * 8u), "l"(src + e));
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    auto loadx = [&](int q) -> double {
+      const int s = a.npartner[a.nidx[q]];
+      const int los = a.s_lo[s], ms = a.s_hi[s] - los;
+      return lane < ms ? a.x[a.s_perm[los + lane]] : 0.0;
+    };
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0, xcur = 0.0, xnext = 0.0;
+    if (qb < qe) {
+      issue(qb, 0);
+      xcur = loadx(qb);
+    }
+    for (int q = qb; q < qe; ++q) {
+      const int buf = (q - qb) & 1;
+      if (q + 1 < qe) {
+        issue(q + 1, buf ^ 1);
+        xnext = loadx(q + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncwarp();
+      const double* T = ring + buf * 1024 + lane;
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        acc0 = fma(T[(j + 0) * 32], __shfl_sync(FULL, xcur, j + 0), acc0);
+        acc1 = fma(T[(j + 1) * 32], __shfl_sync(FULL, xcur, j + 1), acc1);
+        acc2 = fma(T[(j + 2) * 32], __shfl_sync(FULL, xcur, j + 2), acc2);
+        acc3 = fma(T[(j + 3) * 32], __shfl_sync(FULL, xcur, j + 3), acc3);
+      }
+      __syncwarp();  // every lane is done with this slot before it is refilled
+      xcur = xnext;
+    }
+    if (lane < m) {
+      const double r = (acc0 + acc1) + (acc2 + acc3);
+      const int64_t o = a.d_perm[lo + lane];
+      a.y[o] = a.beta == 0.0 ? a.alpha * r : a.alpha * r + a.beta * a.y[o];
+    }
+  }
+}
+
 // the transposed product as its own kernel (its own register allocation)
 __global__ void __launch_bounds__(256, 2) k_matvec_near_t(const __grid_constant__ MvArgs a) {
   const int nw = (int)(gridDim.x * (blockDim.x >> 5));
@@ -248,6 +338,7 @@ __device__ __forceinline__ void fwd_leaf(const MvArgs& a, int s, int lane) {
   const double x1 = lane + 32 < m ? a.x[a.s_perm[lo + lane + 32]] : 0.0;
   const double* W = a.s_leafb + (size_t)a.s_leafidx[s] * lmax * rcap;
   double mine0 = 0.0, mine1 = 0.0;
+  const unsigned long long pol = el_policy();
   constexpr int CB = 8;
   for (int j0 = 0; j0 < k; j0 += CB) {  // 8 columns per round: their loads and butterflies overlap
     double p[CB];
@@ -256,8 +347,8 @@ __device__ __forceinline__ void fwd_leaf(const MvArgs& a, int s, int lane) {
       const int j = j0 + u;
       p[u] = 0.0;
       if (j < k) {
-        if (lane < m) p[u] = W[lane + (size_t)j * lmax] * x0;
-        if (lane + 32 < m) p[u] += W[lane + 32 + (size_t)j * lmax] * x1;
+        if (lane < m) p[u] = ld_el(W + lane + (size_t)j * lmax, pol) * x0;
+        if (lane + 32 < m) p[u] += ld_el(W + lane + 32 + (size_t)j * lmax, pol) * x1;
       }
     }
 #pragma unroll
@@ -338,8 +429,15 @@ __device__ __forceinline__ void stage_load(const double* Tp, const int64_t* Toff
   const double* src = Tp + R.tb;
   const unsigned dst = (unsigned)__cvta_generic_to_shared(tbuf);
   const int nv = (int)(R.len >> 1);  // len is even
+#ifdef H2_MV_NOHINT
   for (int e = threadIdx.x; e < nv; e += blockDim.x)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + 16u * (unsigned)e), "l"(src + 2 * e));
+#else
+  const unsigned long long pol = el_policy();
+  for (int e = threadIdx.x; e < nv; e += blockDim.x)
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst + 16u * (unsigned)e),
+                 "l"(src + 2 * e), "l"(pol));
+#endif
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void stage_store(const StageRegs& R, double*) {
@@ -354,7 +452,7 @@ __device__ __forceinline__ void prefetch_top(const double* Tp, const int64_t* To
   const char* b = reinterpret_cast<const char*>(Tp + Toff[c]);
   const int64_t bytes = (Toff[c + 1] - Toff[c]) * 8;
   for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += (int64_t)blockDim.x * 128)
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(b + o));
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(b + o));
 }
 
 __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ MvArgs a) {
@@ -448,6 +546,7 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ 
     }
     __syncthreads();
   }
+  const unsigned long long pol = el_policy();
   for (int l = a.s_top_nlev - 1; l >= 0; --l) {
     const int qb = a.s_top_lptr[l], qe = a.s_top_lptr[l + 1];
     for (int i = qb + warp; i < qe; i += nw) {
@@ -473,11 +572,11 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_fwd_sub(const __grid_constant__ 
         double acc = 0.0;
         for (int q = 0; q < sk0; ++q) {
           const double xq = __shfl_sync(FULL, q < 32 ? xa0 : xa1, q & 31);
-          if (j < k) acc += F0[j + (size_t)q * k] * xq;
+          if (j < k) acc += ld_el(F0 + j + (size_t)q * k, pol) * xq;
         }
         for (int q = 0; q < sk1; ++q) {
           const double xq = __shfl_sync(FULL, q < 32 ? xb0 : xb1, q & 31);
-          if (j < k) acc += F1[j + (size_t)q * k] * xq;
+          if (j < k) acc += ld_el(F1 + j + (size_t)q * k, pol) * xq;
         }
         if (j < k) a.s_xh[(size_t)s * rcap + j] = acc;
       }
@@ -507,6 +606,7 @@ __device__ __forceinline__ void mv_couple_packed(const MvArgs& a, int t, int lan
   const int ig = TR ? lane : (kt >= 32 ? lane : lane % kt);
   const int g = TR ? 0 : (kt >= 32 ? 0 : lane / kt);
   const bool act = TR ? true : g < G;
+  const unsigned long long pol = el_policy();
   double acc0 = 0.0, acc1 = 0.0;
   for (int base = qb; base < qe; base += 32) {
     const int cnt = qe - base < 32 ? qe - base : 32;
@@ -520,7 +620,7 @@ __device__ __forceinline__ void mv_couple_packed(const MvArgs& a, int t, int lan
       // all blocks of the batch in flight at once: the walk below then hits L2
       const char* pb = reinterpret_cast<const char*>(a.Sp + d_off);
       const int bytes = kt * d_k * 8;
-      for (int o = 0; o < bytes; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + o));
+      for (int o = 0; o < bytes; o += 128) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(pb + o));
     }
     if (!TR) {
       // S_b: k_t x k_s, ld k_t; out[i] += sum_j S[i + j k_t] xhat_s[j].  Group g takes the blocks
@@ -539,8 +639,8 @@ __device__ __forceinline__ void mv_couple_packed(const MvArgs& a, int t, int lan
 #pragma unroll 4
           for (int j = 0; j < ks; ++j) {
             const double xj = __ldcg(xs + j);
-            if (ig < kt) acc0 = fma(Sa[ig + (size_t)j * kt], xj, acc0);
-            if (ig + 32 < kt) acc1 = fma(Sa[ig + 32 + (size_t)j * kt], xj, acc1);
+            if (ig < kt) acc0 = fma(ld_el(Sa + ig + (size_t)j * kt, pol), xj, acc0);
+            if (ig + 32 < kt) acc1 = fma(ld_el(Sa + ig + 32 + (size_t)j * kt, pol), xj, acc1);
           }
         }
       }
@@ -558,7 +658,7 @@ __device__ __forceinline__ void mv_couple_packed(const MvArgs& a, int t, int lan
           if (j < kt) {
             const double* Sj = Sa + (size_t)j * ks;
             double v = 0.0;
-            for (int i = 0; i < ks; ++i) v = fma(Sj[i], __ldcg(xs + i), v);
+            for (int i = 0; i < ks; ++i) v = fma(ld_el(Sj + i, pol), __ldcg(xs + i), v);
             if (q) acc1 += v;
             else acc0 += v;
           }
@@ -612,6 +712,7 @@ __global__ void __launch_bounds__(256, 4) k_mv_couple_top(const __grid_constant_
   __threadfence();
   stamp(a, 8);
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, rcap = a.rcap;
+  const unsigned long long pol = el_policy();
   for (int l = 1; l < a.d_top_nlev; ++l) {  // the root (level 0) keeps its coupling sum
     for (int i = a.d_top_lptr[l] + warp; i < a.d_top_lptr[l + 1]; i += nw) {
       const int c = a.d_top[i];
@@ -627,7 +728,7 @@ __global__ void __launch_bounds__(256, 4) k_mv_couple_top(const __grid_constant_
         double v = r < kc ? __ldcg(yc + r) : 0.0;
         for (int j = 0; j < kp; ++j) {
           const double yj = __shfl_sync(FULL, j < 32 ? yp0 : yp1, j & 31);
-          if (r < kc) v += E[r + (size_t)j * kc] * yj;
+          if (r < kc) v += ld_el(E + r + (size_t)j * kc, pol) * yj;
         }
         if (r < kc) yc[r] = v;
       }
@@ -671,6 +772,7 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_bwd_sub(const __grid_constant__ 
   const int64_t tb = staged ? SR.tb : 0;
   const double* tp = staged ? tbuf : a.d_Tp;
   __syncthreads();
+  const unsigned long long pol = el_policy();
   if (warp == 0 && pr >= 0) {
     const int kc = L.rk[0];
     const double* E = a.d_Tp + L.to[0];
@@ -679,7 +781,7 @@ __global__ void __launch_bounds__(SUBT, 1) k_mv_bwd_sub(const __grid_constant__ 
       double v = r < kc ? ys[r] : 0.0;
       for (int j = 0; j < kpr; ++j) {
         const double yj = __shfl_sync(FULL, j < 32 ? ypr0 : ypr1, j & 31);
-        if (r < kc) v += E[r + (size_t)j * kc] * yj;
+        if (r < kc) v += ld_el(E + r + (size_t)j * kc, pol) * yj;
       }
       if (r < kc) ys[r] = v;
     }
@@ -717,11 +819,12 @@ __global__ void __launch_bounds__(256) k_mv_leaf_bwd(const __grid_constant__ MvA
   const double yl0 = lane < kt ? __ldcg(yh + lane) : 0.0;
   const double yl1 = lane + 32 < kt ? __ldcg(yh + lane + 32) : 0.0;
   double a0 = 0.0, a1 = 0.0;
+  const unsigned long long pol = el_policy();
 #pragma unroll 4
   for (int j = 0; j < kt; ++j) {
     const double yj = __shfl_sync(FULL, j < 32 ? yl0 : yl1, j & 31);
-    if (lane < m) a0 += V[lane + (size_t)j * lmax] * yj;
-    if (lane + 32 < m) a1 += V[lane + 32 + (size_t)j * lmax] * yj;
+    if (lane < m) a0 += ld_el(V + lane + (size_t)j * lmax, pol) * yj;
+    if (lane + 32 < m) a1 += ld_el(V + lane + 32 + (size_t)j * lmax, pol) * yj;
   }
   if (lane < m) {
     double* yo = a.y + a.d_perm[lo + lane];
@@ -986,6 +1089,7 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
     if ((e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming))) return e;
     if ((e = cudaFuncSetAttribute(k_mv_fwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB_SMEM))) return e;
     if ((e = cudaFuncSetAttribute(k_mv_bwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB_SMEM))) return e;
+    if ((e = cudaFuncSetAttribute(k_matvec_near_s, cudaFuncAttributeMaxDynamicSharedMemorySize, NEAR_W * 16384))) return e;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
@@ -1000,8 +1104,17 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   static const int part = getenv("H2_MV_PART") ? atoi(getenv("H2_MV_PART")) : 0;
   static const int near_per_sm = getenv("H2_MV_NEARGRID") ? atoi(getenv("H2_MV_NEARGRID")) : 0;
   const int near_grid = near_per_sm > 0 ? std::min(cdiv(dst.nleaves, 8), near_per_sm * nsm) : cdiv(dst.nleaves, 8);
+  // the staged nearfield kernel (one small CTA per SM) only on request (H2_MV_NEAR_STAGED=1):
+  // measured 101 us alone against 66 us for the register-panel kernel at C2 (4 warps x 2 slots per
+  // SM do not cover the load latency; more slots do not fit beside the far field's shared memory)
+  static const bool staged_on = getenv("H2_MV_NEAR_STAGED") && atoi(getenv("H2_MV_NEAR_STAGED")) != 0;
+  const bool near_staged = staged_on && !transpose && M.lmax == 32;
   if (part == 2) {
-    H2_LAUNCH(K_MV, st, (transpose ? k_matvec_near_t : k_matvec_near)<<<near_grid, 256, 0, st>>>(a));
+    if (near_staged) {
+      H2_LAUNCH(K_MV, st, k_matvec_near_s<<<std::min(nsm, cdiv(dst.nleaves, NEAR_W)), NEAR_W * 32, NEAR_W * 16384, st>>>(a));
+    } else {
+      H2_LAUNCH(K_MV, st, (transpose ? k_matvec_near_t : k_matvec_near)<<<near_grid, 256, 0, st>>>(a));
+    }
     return cudaGetLastError();
   }
   static unsigned long long* dbg = nullptr;
@@ -1041,7 +1154,11 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   if (part == 5) return cudaGetLastError();
   if (part == 0) {
     if ((e = cudaEventRecord(ev_join, s2))) return e;
-    H2_LAUNCH(K_MV, st, (transpose ? k_matvec_near_t : k_matvec_near)<<<near_grid, 256, 0, st>>>(a));
+    if (near_staged) {
+      H2_LAUNCH(K_MV, st, k_matvec_near_s<<<std::min(nsm, cdiv(dst.nleaves, NEAR_W)), NEAR_W * 32, NEAR_W * 16384, st>>>(a));
+    } else {
+      H2_LAUNCH(K_MV, st, (transpose ? k_matvec_near_t : k_matvec_near)<<<near_grid, 256, 0, st>>>(a));
+    }
     if ((e = cudaStreamWaitEvent(st, ev_join, 0))) return e;
   }
   H2_LAUNCH(K_MV, st, k_mv_leaf_bwd<<<cdiv(dst.nleaves, 8), 256, 0, st>>>(a));
