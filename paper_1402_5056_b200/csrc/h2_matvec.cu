@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <unordered_map>
 
 #include "h2_internal.h"
@@ -1084,7 +1085,9 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   if (!s2) {
     int lo = 0, hi = 0, dev = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    if ((e = cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, hi))) return e;
+    // H2_MV_PRIO=equal: the far-field stream at the caller's (lowest) priority (A/B)
+    const bool equal = getenv("H2_MV_PRIO") && std::string(getenv("H2_MV_PRIO")) == "equal";
+    if ((e = cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, equal ? lo : hi))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming))) return e;
     if ((e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming))) return e;
     if ((e = cudaFuncSetAttribute(k_mv_fwd_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, SUB_SMEM))) return e;
@@ -1122,9 +1125,17 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   if (dbg_on && !dbg) cudaMalloc((void**)&dbg, 16 * sizeof(unsigned long long));
   a.dbg = dbg;
   cudaStream_t sf = part == 0 ? s2 : st;  // the far-field chain
+  static const bool near_first = getenv("H2_MV_ORDER") && std::string(getenv("H2_MV_ORDER")) == "near_first";  // A/B
   if (part == 0) {
     if ((e = cudaEventRecord(ev_fork, st))) return e;
     if ((e = cudaStreamWaitEvent(s2, ev_fork, 0))) return e;
+    if (near_first) {
+      if (near_staged) {
+        H2_LAUNCH(K_MV, st, k_matvec_near_s<<<std::min(nsm, cdiv(dst.nleaves, NEAR_W)), NEAR_W * 32, NEAR_W * 16384, st>>>(a));
+      } else {
+        H2_LAUNCH(K_MV, st, (transpose ? k_matvec_near_t : k_matvec_near)<<<near_grid, 256, 0, st>>>(a));
+      }
+    }
   }
   // the dependent kernels of the chain are launched programmatically (their prologues -- staging,
   // sublists, prefetches -- overlap the predecessor's tail); H2_MV_NOPDL=1: plain launches (A/B)
@@ -1154,7 +1165,8 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
   if (part == 5) return cudaGetLastError();
   if (part == 0) {
     if ((e = cudaEventRecord(ev_join, s2))) return e;
-    if (near_staged) {
+    if (near_first) {
+    } else if (near_staged) {
       H2_LAUNCH(K_MV, st, k_matvec_near_s<<<std::min(nsm, cdiv(dst.nleaves, NEAR_W)), NEAR_W * 32, NEAR_W * 16384, st>>>(a));
     } else {
       H2_LAUNCH(K_MV, st, (transpose ? k_matvec_near_t : k_matvec_near)<<<near_grid, 256, 0, st>>>(a));
