@@ -283,7 +283,8 @@ def run_table1(levels, dd=False, jump=False):
         del Z, Aop
 
 
-TABLE2 = {11: (1.2e-4, 1.6e-4, 0.8, 0.05, 3), 12: (6.1e-5, 1.9e-4, 0.8, 0.03, 3), 13: (3.1e-5, 2.1e-4, 0.8, 0.03, 3),
+TABLE2 = {17: (1.9e-6, 3.3e-4, 0.8, 0.02, 3), 18: (9.5e-7, 3.5e-4, 0.8, 0.01, 4),
+          11: (1.2e-4, 1.6e-4, 0.8, 0.05, 3), 12: (6.1e-5, 1.9e-4, 0.8, 0.03, 3), 13: (3.1e-5, 2.1e-4, 0.8, 0.03, 3),
           14: (1.5e-5, 2.4e-4, 0.8, 0.02, 3), 15: (7.6e-6, 2.6e-4, 0.8, 0.02, 3), 16: (3.8e-6, 3.0e-4, 0.8, 0.02, 3)}
 
 
