@@ -1,4 +1,4 @@
-"""Diagnostic (tools): oracle vs GPU Cholesky with the block-relative rule; prints rank statistics,
+"""Diagnostic (test infrastructure; run from the repo root as python tests/diag_...py): oracle vs GPU Cholesky with the block-relative rule; prints rank statistics,
 the first differing cluster and the device flags instead of asserting."""
 import sys
 

@@ -1,4 +1,4 @@
-"""Diagnostic (tools): the sequence of non-zero-rank local updates (t0, s0, k) of the GPU Cholesky
+"""Diagnostic (test infrastructure; run from the repo root as python tests/diag_...py): the sequence of non-zero-rank local updates (t0, s0, k) of the GPU Cholesky
 (H2_UPD_LOG) against the oracle's, on the DD tree; prints the first difference."""
 import os
 import sys

@@ -1,7 +1,7 @@
-"""One Cholesky parity check outside pytest (tools): oracle vs GPU on config NAME at side N and
+"""One Cholesky parity check outside pytest (test infrastructure): oracle vs GPU on config NAME at side N and
 truncation eps: ranks, device flags, non-zero update counts, operator difference on 16 probes.
 
-    python tools/parity_once.py NAME N eps [rank_cap]
+    python tests/parity_once.py NAME N eps [rank_cap]
 """
 import json
 import os
@@ -11,7 +11,7 @@ import time
 import numpy as np
 import torch
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # tests/ -> repo root
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import paper_1402_5056_b200 as P  # noqa: E402

@@ -91,7 +91,7 @@ def test_cholesky_blockwise_parity(name, N, eps, eta):
     block-relative factorization sits at the edge of a leaf breakdown on BOTH sides (the oracle
     itself breaks down at 5e-2, changes ranks under a 1e-15 relative perturbation of A at 1e-2,
     and the device breaks down at 9e-3 / 1e-2 / 2e-2 while matching bit for bit at 7e-3 / 1.1e-2:
-    tools/diag_blockwise.py, profiles/r02/blockwise_fragility.log)."""
+    tests/diag_blockwise.py, profiles/r02/blockwise_fragility.log)."""
     s = setup(name, N, lower=True, eta=eta)
     OZ, Z, A = s["OZ"], s["Z"], s["c"]["A"]
     ar = Arith(OZ, OTrunc(eps, blockwise=True))
@@ -129,7 +129,7 @@ def test_cholesky_parity_dd_tree(name, N, eps, bw, eta):
     # pure rounding noise (sigma_1 ~ 4e-18 in the oracle at C2-256) and the relative rule alone
     # would decide their rank on that noise (R5 covers only sigma_1 = 0 exactly), differently on
     # the two sides; the absolute floor 1e-13 -- far below every meaningful singular value -- makes
-    # them rank 0 on both (tools/diag_updlog.py shows the transient rank difference without it)
+    # them rank 0 on both (tests/diag_updlog.py shows the transient rank difference without it)
     ar = Arith(OZ, OTrunc(eps, abs_tol=1e-13, blockwise=bw))
     ar.chol()
     P.h2_lr_factor(Z, cholesky=True, trunc=P.Trunc(eps, abs_tol=1e-13, blockwise=bw))
