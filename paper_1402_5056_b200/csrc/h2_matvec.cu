@@ -1153,15 +1153,23 @@ cudaError_t launch_matvec(const h2_mat_* Zc, int transpose, double alpha, const 
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, a);
   };
+  // a failed launch would leave the forward epoch counters out of step with the host's epoch (the
+  // next product's coupling warps would wait forever): start over from zero
+  auto fail = [&](cudaError_t err) -> cudaError_t {
+    cudaStreamSynchronize(sf);
+    cudaMemset(src.mv_cnt, 0, 2 * sizeof(int32_t));
+    const_cast<DevSide&>(src).mv_epoch = 0;
+    return err;
+  };
   H2_LAUNCH(K_MV, sf, k_mv_leaf_fwd<<<cdiv(src.nleaves, 8), 256, 0, sf>>>(a));
   H2_LAUNCH(K_MV, sf, e = launch_dep(k_mv_fwd_sub, src.n_mv_roots, SUBT, smem));
-  if (e) return e;
+  if (e) return fail(e);
   if (part == 3) return cudaGetLastError();
   H2_LAUNCH(K_MV, sf, e = launch_dep(k_mv_couple_top, cdiv(dst.nclusters, 8), 256, 0));
-  if (e) return e;
+  if (e) return fail(e);
   if (part == 4) return cudaGetLastError();
   H2_LAUNCH(K_MV, sf, e = launch_dep(k_mv_bwd_sub, dst.n_mv_roots, SUBT, smem));
-  if (e) return e;
+  if (e) return fail(e);
   if (part == 5) return cudaGetLastError();
   if (part == 0) {
     if ((e = cudaEventRecord(ev_join, s2))) return e;
