@@ -146,7 +146,14 @@ h2_status h2_batch_begin(h2_stream stream);
 h2_status h2_batch_end(void);
 
 /* y <- alpha op(Z) x + beta y (op = transpose ? Z^T : Z), x/y device vectors in ORIGINAL order
- * (forward transform, couplings, backward transform, nearfield). */
+ * (forward transform, couplings, backward transform, nearfield).
+ * x and y: device, n doubles each, borrowed until the stream passes the call; y may not alias x.
+ * The first product after any call that changed Z (update, product, factorization, inversion)
+ * rebuilds Z's packed coupling / transfer copies: it reads the ranks back (one synchronisation of
+ * `stream`) and allocates device memory for them (H2_ERR_NOMEM / H2_ERR_CUDA); later products are
+ * stream-ordered without host synchronisation.  The far-field part runs on a library-owned side
+ * stream, forked from and joined to `stream` inside the call.  Not thread-safe per matrix
+ * (the transform coefficients are workspace of Z); different matrices may be used concurrently. */
 h2_status h2_matvec(h2_mat Z, int32_t transpose, double alpha, const double* x, double beta, double* y,
                     h2_stream stream);
 
